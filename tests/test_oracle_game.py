@@ -1,0 +1,240 @@
+"""Pins for oracle/game.py against the paper's printed facts, its closed-form
+propositions and independent mathematics (finite differences, fixed points)."""
+import numpy as np
+import pytest
+
+from oracle import estimators, game, linalg
+from synth import appendix_b_example, dense_gep_small, gaussian_init
+
+
+def _planted(d, k, seed):
+    a, b = dense_gep_small(seed, d)
+    w, V = linalg.generalized_eigh(a, b, k)
+    return a, b, w, V
+
+
+# --- §2 utilities ----------------------------------------------------------
+
+def test_fig1_utility_values():
+    """Fig. 1 caption: player 2 aligned with the top
+    eigenvector receives zero utility, aligned with the second eigenvector it
+    receives the second eigenvalue."""
+    a, b = appendix_b_example()
+    w, V = linalg.generalized_eigh(a, b)
+    at_top = np.stack([V[0], V[0]])
+    assert abs(game.utility(1, at_top, a, b)) < 1e-12 * w[0]
+    assert abs(game.utility(1, V, a, b) - w[1]) < 1e-10 * w[0]
+
+
+def test_utility_forms_agree_and_first_player_is_rayleigh():
+    rng = np.random.default_rng(0)
+    a, b = dense_gep_small(1, 8)
+    V = rng.standard_normal((4, 8))
+    for i in range(4):
+        assert np.isclose(game.utility(i, V, a, b), game.utility_y_form(i, V, a, b), rtol=1e-12)
+    assert np.isclose(game.utility(0, V, a, b), game.rayleigh(V[0], a, b), rtol=1e-14)
+
+
+def test_utility_simplex_form_lemma_well_posed():
+    """Lemma well_posed_utils: with exact parents,
+    u_i = sum_{j>=i} lambda_j z_j, z_j = w_j^2 <v_j,Bv_j> / sum_p w_p^2 <v_p,Bv_p>,
+    where v_hat_i = sum_p w_p v_p (expansion in the generalized eigenbasis)."""
+    a, b = dense_gep_small(2, 6)
+    lam, Vall = linalg.generalized_eigh(a, b)           # all 6 pairs
+    rng = np.random.default_rng(7)
+    for i in range(4):
+        vhat = rng.standard_normal(6)
+        vhat /= np.linalg.norm(vhat)
+        wcoef = np.linalg.solve(Vall.T, vhat)
+        bnorm = np.einsum("pi,ij,pj->p", Vall, b, Vall)
+        z = wcoef ** 2 * bnorm / np.sum(wcoef ** 2 * bnorm)
+        V = np.vstack([Vall[:i], vhat[None]])
+        assert np.isclose(game.utility(i, V, a, b), np.sum(lam[i:] * z[i:]), rtol=1e-7, atol=1e-10)
+
+
+def test_utility_gradient_is_half_true_gradient():
+    """Eq. eq:util_grad 'up to scaling factors' — it equals exactly 1/2 of the
+    gradient of Eq. util_new; checked by central finite differences."""
+    rng = np.random.default_rng(3)
+    a, b = dense_gep_small(3, 5)
+    V = rng.standard_normal((3, 5))
+    for i in range(3):
+        g = game.utility_gradient(i, V, a, b)
+        fd = np.zeros(5)
+        h = 1e-6
+        for c in range(5):
+            Vp, Vm = V.copy(), V.copy()
+            Vp[i, c] += h
+            Vm[i, c] -= h
+            fd[c] = (game.utility(i, Vp, a, b) - game.utility(i, Vm, a, b)) / (2 * h)
+        assert np.allclose(2 * g, fd, rtol=1e-6, atol=1e-8)
+
+
+# --- §3 update direction -----------------------------------------------------
+
+def test_direction_is_steepest_ascent_at_exact_parents():
+    """Prop.: with exact parents, Eq. eq:update equals
+    <v_i,Bv_i>^2 x Eq. eq:util_grad (relation (i)), i.e. a positive multiple
+    of the utility gradient."""
+    a, b, w, Vt = _planted(7, 4, 4)
+    rng = np.random.default_rng(4)
+    for i in range(1, 4):
+        V = Vt.copy()
+        V[i] = rng.standard_normal(7)
+        V[i] /= np.linalg.norm(V[i])
+        d1 = game.direction_alg1(i, V, a, b)
+        g = game.utility_gradient(i, V, a, b)
+        bii = V[i] @ b @ V[i]
+        assert np.allclose(d1, bii ** 2 * g, rtol=1e-8, atol=1e-8)
+        # same through Alg. 2 with exact estimates and exact aux
+        av, bv = estimators.dense_products(a, b, V)
+        d2 = game.direction_alg2(i, V, (b @ V.T).T, av, bv, rho=0.0)
+        assert np.allclose(d2, d1, rtol=1e-12, atol=1e-12)
+
+
+def test_equivalence_to_eigengame_unloaded_when_B_is_identity():
+    """Prop. 'Equivalence to EigenGame Unloaded': with
+    B = I the direction is (I - v_i v_i^T)[A v_i - sum_{j<i}(v_i^T A v_j) v_j]."""
+    rng = np.random.default_rng(5)
+    d, k = 9, 5
+    a = rng.standard_normal((d, d))
+    a = a + a.T
+    V = rng.standard_normal((k, d))
+    V /= np.linalg.norm(V, axis=1, keepdims=True)
+    av, bv = estimators.dense_products(a, np.eye(d), V)
+    for i in range(k):
+        mu = a @ V[i] - sum((V[i] @ a @ V[j]) * V[j] for j in range(i))
+        ref = mu - (V[i] @ mu) * V[i]
+        got = game.direction_alg2(i, V, V.copy(), av, bv, rho=0.5)
+        assert np.allclose(got, ref, atol=1e-12)
+
+
+def test_direction_tangent_to_sphere():
+    """Appendix D: the update already lives in the tangent
+    space, <grad_i, v_i> = 0, for any state and any symmetric estimates."""
+    rng = np.random.default_rng(6)
+    d, k = 11, 6
+    x, y = rng.standard_normal((40, 5)), rng.standard_normal((40, 6))
+    V = rng.standard_normal((k, d))
+    V /= np.linalg.norm(V, axis=1, keepdims=True)
+    aux = rng.standard_normal((k, d))
+    av, bv = estimators.cca_products(x, y, V)
+    for i in range(k):
+        g = game.direction_alg2(i, V, aux, av, bv, rho=0.1)
+        assert abs(g @ V[i]) <= 1e-12 * max(1.0, np.linalg.norm(g))
+
+
+def test_fixed_point_at_generalized_eigenvectors():
+    """Lemma lemma:right_fp: exact expectations, exact
+    auxiliaries [Bv]_j = B v_j, v_j = generalized eigenvectors => every
+    direction and every aux direction vanishes."""
+    a, b, w, Vt = _planted(10, 5, 6)
+    assert np.all(w > 0)
+    av, bv = estimators.dense_products(a, b, Vt)
+    aux = bv.copy()
+    scale = np.linalg.norm(a) * np.linalg.norm(b)
+    for i in range(5):
+        assert np.linalg.norm(game.direction_alg2(i, Vt, aux, av, bv, rho=1e-3)) < 1e-10 * scale
+        assert np.linalg.norm(game.aux_direction(i, aux, bv)) == 0.0
+    V2, A2 = game.step_alg2(Vt, aux, [(av, bv)], 0.1, 1.0, 1e-3)
+    assert np.allclose(V2, Vt, atol=1e-12) and np.allclose(A2, aux)
+
+
+def test_rho_clipping_branch():
+    """Alg. 2 line 8: denominators use max(<v_j,[Bv]_j>, rho)."""
+    v = np.array([1.0, 0.0])
+    assert game.clip_denominator(v, np.array([4.0, 0.0]), 0.0) == 2.0
+    assert game.clip_denominator(v, np.array([0.01, 0.0]), 0.5) == pytest.approx(np.sqrt(0.5))
+    assert game.clip_denominator(v, np.array([-3.0, 0.0]), 0.25) == pytest.approx(0.5)
+
+
+def test_step_alg2_sphere_and_aux_running_average():
+    """Sphere preservation (Alg. 2 lines 16-17) and the aux update being an
+    exact running average: with a frozen v and constant B_t, [Bv] -> B v at
+    rate (1 - gamma) per step."""
+    rng = np.random.default_rng(8)
+    a, b = dense_gep_small(0)
+    V, aux = game.init_state(gaussian_init(4, 16, 0))
+    av, bv = estimators.dense_products(a, b, V)
+    V2, aux2 = game.step_alg2(V, aux, [(av, bv)], 0.01, 0.3, 0.05)
+    assert np.allclose(np.linalg.norm(V2, axis=1), 1.0, atol=1e-14)
+    e0 = np.linalg.norm(aux - bv)
+    e = aux.copy()
+    for _ in range(10):
+        e = e + 0.3 * (bv - e)
+    assert np.isclose(np.linalg.norm(e - bv), 0.7 ** 10 * e0, rtol=1e-9)
+    assert np.allclose(aux2, aux + 0.3 * (bv - aux))
+
+
+def test_alg2_machine_average_and_appendix_f():
+    """Alg. 2 lines 14-17: directions averaged over M machines; Appendix F
+    aggregates products first.  With identical machines both reduce to M=1;
+    the M=4 mean equals the mean of two M=2 means."""
+    rng = np.random.default_rng(9)
+    d, k = 8, 3
+    V, aux = game.init_state(rng.standard_normal((k, d)))
+    ms = []
+    for _ in range(4):
+        x, y = rng.standard_normal((20, 4)), rng.standard_normal((20, 4))
+        ms.append(estimators.cca_products(x, y, V))
+    one = game.step_alg2(V, aux, [ms[0]], 0.1, 0.5, 0.01)
+    rep = game.step_alg2(V, aux, [ms[0]] * 3, 0.1, 0.5, 0.01)
+    assert np.allclose(one[0], rep[0]) and np.allclose(one[1], rep[1])
+    f = game.step_alg2_appendix_f(V, aux, [ms[0]] * 3, 0.1, 0.5, 0.01)
+    assert np.allclose(one[0], f[0])
+    g4 = [game.direction_alg2(1, V, aux, av, bv, 0.01) for av, bv in ms]
+    assert np.allclose(np.mean(g4, 0), 0.5 * (np.mean(g4[:2], 0) + np.mean(g4[2:], 0)))
+
+
+def test_alg2_reduces_to_alg1_direction_with_exact_aux():
+    """Appendix C: Alg. 2 subsumes Alg. 1 (rho=0, exact
+    estimates): with [Bv]_j = B v_j the two directions coincide."""
+    rng = np.random.default_rng(10)
+    a, b = dense_gep_small(1)
+    V, _ = game.init_state(rng.standard_normal((4, 16)))
+    av, bv = estimators.dense_products(a, b, V)
+    for i in range(4):
+        assert np.allclose(game.direction_alg2(i, V, bv, av, bv, 0.0),
+                           game.direction_alg1(i, V, a, b), atol=1e-12)
+
+
+# --- Alg. 3 (Appendix E) ----------------------------------------------------
+
+def test_alg3_bracket_and_stationarity():
+    rho, nu = 0.05, 20.0
+    for z in [-50.0, -2.0, 0.0, 3.0, 50.0]:
+        br = game.smooth_bracket(z, rho, nu)
+        assert rho * (1 - 1e-12) <= br <= nu * (1 + 1e-12)
+    assert np.isclose(game.smooth_bracket(0.0, rho, nu), np.sqrt(rho * nu))
+    # z-gradient vanishes when <v,[Bv]> equals the bracket
+    v = np.array([[1.0, 0.0]])
+    br = game.smooth_bracket(0.7, rho, nu)
+    aux = np.array([[br, 5.0]])
+    assert abs(game.z_direction(0, v, aux, [0.7], rho, nu)) < 1e-14
+    # ascent sign: bracket below target -> z increases
+    assert game.z_direction(0, v, np.array([[br * 2, 0.0]]), [0.7], rho, nu) > 0
+
+
+def test_alg3_tracks_alg2_on_exact_stream():
+    """With exact matrices the smooth variant converges to the same
+    solution as Alg. 2 (config 0 problem, rho < lambda_min(B) < lambda_max(B) < nu)."""
+    a, b = dense_gep_small(0)
+    ev = np.linalg.eigvalsh(b)
+    rho, nu = 0.5 * ev[0], 2 * ev[-1]
+    w, Vt = linalg.generalized_eigh(a, b, 3)
+    V, aux = game.init_state(gaussian_init(3, 16, 0))
+    z = np.zeros(3)
+    for _ in range(3000):
+        av, bv = estimators.dense_products(a, b, V)
+        V, aux, z = game.step_alg3(V, aux, z, [(av, bv)], 0.05, 0.5, rho, nu)
+    from oracle import metrics
+    assert np.all(metrics.per_vector_angles(V, Vt) < 1e-3)
+
+
+def test_adam_first_step():
+    v = np.zeros(3)
+    g = np.array([1.0, 0.0, -2.0])
+    v1, m, s = game.adam_ascent(v, g, np.zeros(3), np.zeros(3), 1, 0.1)
+    assert np.allclose(v1, 0.1 * np.sign(g), atol=1e-6)
+    v2, m2, s2 = game.adam_ascent(v, np.zeros(3), np.zeros(3), np.zeros(3), 1, 0.1)
+    assert np.allclose(v2, 0.0)
