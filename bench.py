@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py — throughput of gamma-EigenGame updates on B200.
+
+One step = one pass of the whole hot path (Alg. 2: minibatch products
+A_t V, B_t V; Gram tables; penalty coefficients; fused ascent / retraction /
+auxiliary update) over one minibatch of synthetic data already resident in
+HBM.  Default workload: BASELINE.json configs[3] (CCA, dx=dy=8192, k=64,
+batch 4096 rows per GPU, bf16 data, fp32 accumulate) — see DESIGN.md §Bench.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config I]
+                    [--math bf16|f32|tf32|3xtf32] [--impl reference]
+
+Multi-GPU (N > 1) is launched by torchrun; each rank owns its own batch
+(weak scaling), products are combined by an NCCL all-reduce (Appendix F).
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples/s of gamma-EigenGame updates (d,k)"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def _peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        sm, loaded = [], []
+        smax = None
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax = float(r[1])
+                if float(r[6]) > 0:
+                    loaded.append(float(r[0]))
+            except Exception:
+                continue
+            for n, v in zip(names, r[2:6]):
+                if v.strip().lower() in ("active", "1", "0x1"):
+                    reasons.add(n)
+        use = loaded or sm
+        return {"sm_mhz": statistics.median(use) if use else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def _workload(cfg, math):
+    return {"workload": cfg.name, "problem": cfg.problem, "dx": cfg.dx, "dy": cfg.dy, "k": cfg.k,
+            "batch_per_gpu": cfg.batch, "math": math, "data_dtype": cfg.dtype,
+            "recipe": cfg.recipe}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the fp64 oracle on the host cores
+# ---------------------------------------------------------------------------
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max((i.get("num_threads", 1) for i in info), default=os.cpu_count())
+    except Exception:
+        return os.cpu_count()
+
+
+def oracle_sample(cfg, seconds: float, max_steps: int | None = None, seed: int = 0):
+    """Time the oracle (as it stands) on real steps of the workload until
+    `seconds` of CPU work or `max_steps`; returns (rows/s, steps, rows)."""
+    import numpy as np
+    from oracle import estimators, game
+    from synth import cca_views, dense_gep_small, gaussian_init
+    if cfg.problem == "cca":
+        x, y = cca_views(cfg, cfg.batch, seed=seed)
+        x64, y64 = x.double().numpy(), y.double().numpy()
+        V, aux = game.init_state(gaussian_init(cfg.k, cfg.d, seed))
+        n, rows, t0 = 0, 0, time.perf_counter()
+        while True:
+            av, bv = estimators.cca_products(x64, y64, V)
+            V, aux = game.step_alg2(V, aux, [(av, bv)], cfg.eta, cfg.gamma, cfg.rho)
+            n += 1
+            rows += cfg.batch
+            el = time.perf_counter() - t0
+            if el >= seconds or (max_steps and n >= max_steps):
+                return rows / el, n, rows, el
+    a, b = dense_gep_small(seed, cfg.d) if cfg.d <= 64 else (None, None)
+    if a is None:
+        import torch
+        from synth import dense_gep_large
+        at, bt = dense_gep_large(min(cfg.d, 2048), seed)
+        a, b = at.double().numpy(), bt.double().numpy()
+    V, aux = game.init_state(gaussian_init(cfg.k, a.shape[0], seed))
+    n, t0 = 0, time.perf_counter()
+    while True:
+        av, bv = estimators.dense_products(a, b, V)
+        V, aux = game.step_alg2(V, aux, [(av, bv)], cfg.eta, cfg.gamma, cfg.rho)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or (max_steps and n >= max_steps):
+            return n / el, n, n, el
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    # warmup steps (untimed), then K timed steps, each a full oracle step
+    oracle_sample(cfg, 0.0, max_steps=max(1, args.warmup))
+    v, n, rows, el = oracle_sample(cfg, 1e9, max_steps=args.steps)
+    unit = "samples/s" if cfg.problem == "cca" else "steps/s"
+    cores = _blas_threads()
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": unit, "n_gpus": world,
+            "steps": n, "warmup": args.warmup, "ms_per_step": 1e3 * el / n, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _workload(cfg, "f64-oracle"),
+            "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "oracle",
+                             "sample": f"{n} full oracle steps of {cfg.batch if cfg.problem == 'cca' else 'full-batch'} rows"},
+            "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_gpu(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2206_04993_b200 import build
+    if rank == 0:
+        build.build()
+    if world > 1:
+        dist.barrier()
+    from paper_2206_04993_b200 import geig
+    from paper_2206_04993_b200.parallel import cca_scale
+    from synth import cca_views, dense_gep_large, gaussian_init
+
+    dev = torch.device(f"cuda:{local_rank}")
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    peaks, peaks_src = _peaks()
+
+    if cfg.problem != "cca":
+        raise SystemExit("bench: only the CCA workloads are benchmarked as the headline; "
+                         "use --config 1|2|3")
+    math = args.math
+    data_bf16 = cfg.dtype == "bf16"
+    dtype = torch.bfloat16 if data_bf16 else torch.float32
+    b = cfg.batch
+    esz = 2 if data_bf16 else 4
+    batch_bytes = b * cfg.d * esz
+    # ring of P distinct batches in HBM, larger than the 126 MB L2
+    P = max(2, int((4 * 126e6) // batch_bytes) + 1)
+    P = min(P, 64)
+    X, Y = cca_views(cfg, P * b, seed=1000 + rank, device=dev, dtype=dtype)
+    Xs = [X[i * b:(i + 1) * b] for i in range(P)]
+    Ys = [Y[i * b:(i + 1) * b] for i in range(P)]
+    s = geig.Solver(geig.GEIG_CCA, cfg.dx, cfg.dy, cfg.k, math=math,
+                    data_dtype=geig.GEIG_DATA_BF16 if data_bf16 else geig.GEIG_DATA_F32,
+                    rho=cfg.rho, max_rows=b, device=local_rank, stream=stream.cuda_stream)
+    G = torch.tensor(gaussian_init(cfg.k, cfg.d, 0), dtype=torch.float32, device=dev)
+    s.init_state(G)
+    AV = torch.empty(cfg.k, cfg.d, device=dev)
+    BV = torch.empty_like(AV)
+    scale = cca_scale(b, world)
+
+    ev = []
+
+    def step(i, timed):
+        if timed:
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+        geig.geig_products_cca(s.h, Xs[i % P], Ys[i % P], b, scale, AV, BV)
+        if timed:
+            e1.record(stream)
+        if world > 1:
+            flat = torch.stack([AV, BV])
+            dist.all_reduce(flat)
+            AV.copy_(flat[0])
+            BV.copy_(flat[1])
+        geig.geig_update(s.h, AV, BV, cfg.eta, cfg.gamma)
+        if timed:
+            e2.record(stream)
+            ev.append((e0, e1, e2))
+
+    for i in range(args.warmup):
+        step(i, False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = s.launches()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(args.warmup + i, True)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = s.launches() - l0
+    elapsed_ms = t_start.elapsed_time(t_end)
+    prod_ms = statistics.mean(a.elapsed_time(b_) for a, b_, _ in ev)
+    upd_ms = statistics.mean(b_.elapsed_time(c) for _, b_, c in ev)
+    if world > 1:
+        t = torch.tensor([elapsed_ms, prod_ms, upd_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, prod_ms, upd_ms = t.tolist()
+    value = world * b * args.steps / (elapsed_ms / 1e3)
+
+    # roofline of the dominant kernel (the products stage): algorithmic bytes =
+    # X and Y read once (b*d*esz) + V read + AV/BV written
+    alg_bytes = b * cfg.d * esz + cfg.k * cfg.d * (2 if math == "bf16" else 4) + 2 * cfg.k * cfg.d * 4
+    achieved = alg_bytes / (prod_ms / 1e3) / 1e9
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "frac": achieved / hbm_peak, "traffic": None, "kernel": "products (forward+backward GEMMs)",
+            "peak_source": peaks_src, "ms_per_launch": prod_ms, "update_ms": upd_ms,
+            "flops_per_step": 4.0 * cfg.k * cfg.d * b,
+            "tensor_tflops": 4.0 * cfg.k * cfg.d * b / (prod_ms / 1e3) / 1e12}
+
+    # end to end through the C ABI with HOST buffers (pinned), rank-local
+    e2e = None
+    if not args.no_e2e:
+        hx = Xs[0].cpu().pin_memory()
+        hy = Ys[0].cpu().pin_memory()
+        ga = torch.empty(cfg.k, cfg.k).pin_memory()
+        n_e2e = max(3, min(args.steps, 20))
+        geig.geig_step_cca_host(s.h, hx, hy, b, cfg.eta, cfg.gamma, ga)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            h2d, d2h = geig.geig_step_cca_host(s.h, hx, hy, b, cfg.eta, cfg.gamma, ga)
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": world * b * n_e2e / el, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": n_e2e, "timer": "host wall clock (call synchronises)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, n, rows, el = oracle_sample(cfg, args.cpu_seconds, seed=0)
+        cpu = {"value": v, "unit": "samples/s", "cores": _blas_threads(), "kind": "oracle",
+               "sample": f"{n} full fp64 oracle steps of {cfg.batch} rows ({el:.1f} s)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "bf16" if math == "bf16" else ("f32" if math == "f32" else math),
+                "data": "synthetic",
+                "config": dict(_workload(cfg, math), parallelism=f"dp{world}", global_batch=world * b,
+                               l2_policy=f"ring of {P} distinct batches ({P * batch_bytes / 2**20:.0f} MiB) "
+                                         "> 126 MB L2, a new batch every step"),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    s.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--math", default=None)
+    ap.add_argument("--impl", default="b200")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from synth import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.math is None:
+        args.math = "bf16" if cfg.dtype == "bf16" else "f32"
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    run_gpu(args, cfg, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

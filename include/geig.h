@@ -1,0 +1,171 @@
+/*
+ * geig.h — C ABI of the B200-native gamma-EigenGame hot path
+ * (arxiv 2206.04993, "The Generalized Eigenvalue Problem as a Nash
+ * Equilibrium").  Citations are PAPER.md line numbers with the section /
+ * algorithm they fall in.
+ *
+ * The library solves the top-k generalized eigenvalue problem A v = lambda B v
+ * (§1) by running Alg. 2 ("Stochastic gamma-EigenGame",
+ * PAPER.md:996-1030): k players hold unit vectors v_i (strategies,
+ * PAPER.md:871) and auxiliary vectors [Bv]_i; one step forms the minibatch
+ * products A_t v_j and B_t v_j for all players, the k x k inner-product
+ * tables, the normalised parents y_j = v_j / sqrt(max(<v_j,[Bv]_j>, rho)),
+ * the lower-triangular penalty sums, the v_i ascent + sphere retraction and
+ * the [Bv]_i running-average update.
+ *
+ * Layouts (all row-major, all device memory unless a function says HOST):
+ *   d = dx + dy (CCA) or d (dense).
+ *   V, AUX ([Bv]), AV, BV : k x d float32, row i = player i (player-major,
+ *                           each player's d-vector contiguous).
+ *   CCA views X : b x dx, Y : b x dy, one sample per row (fp32 or bf16).
+ *   Dense A, B : d x d symmetric, fp32 (or bf16), row-major.
+ *   Gram tables : k x k float32, row i, column j.
+ *
+ * Minibatch estimates (§3, Alg. 2 line 7 "unbiased estimates
+ * using independent data batches"), reading R1: the b rows of a
+ * step are split into halves; rows [0,h) estimate A, rows [h,2h) estimate B,
+ * h = floor(b/2):
+ *   A_t v = (1/h) [X1^T (Y1 v_y) ; Y1^T (X1 v_x)]
+ *   B_t v = (1/h) [X2^T (X2 v_x) ; Y2^T (Y2 v_y)]      (PAPER.md:831 CCA)
+ *
+ * Ownership: the solver owns V, AUX and its scratch (allocated in
+ * geig_create, freed in geig_destroy).  Every pointer argument is owned by the
+ * caller and only read (or written, for outputs) during the call / the
+ * stream-ordered work it enqueues.  All device work is enqueued on the
+ * solver's stream (geig_set_stream); calls return without synchronising
+ * except the *_host variants and geig_sync.
+ *
+ * Errors: every function returns GEIG_OK (0) or a nonzero geig_status; the
+ * message of the last error of the calling thread is geig_last_error().
+ * Invalid sizes/pointers -> GEIG_ERR_ARG; CUDA failures -> GEIG_ERR_CUDA;
+ * configurations the compiled kernels do not cover (e.g. k > 256) ->
+ * GEIG_ERR_UNSUPPORTED.  Nothing falls back to a CPU path.
+ */
+#ifndef GEIG_H_
+#define GEIG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct geig_solver geig_solver;
+
+typedef enum {
+  GEIG_OK = 0,
+  GEIG_ERR_ARG = 1,
+  GEIG_ERR_CUDA = 2,
+  GEIG_ERR_UNSUPPORTED = 3,
+  GEIG_ERR_STATE = 4
+} geig_status;
+
+/* Problem family (PAPER.md:765 generic GEP; PAPER.md:828 CCA). */
+typedef enum { GEIG_DENSE = 0, GEIG_CCA = 1 } geig_problem;
+
+/* Arithmetic of the minibatch products (the GEMMs):
+ *  GEIG_MATH_F32   : FFMA fp32 on CUDA cores (exactness-check variant)
+ *  GEIG_MATH_BF16  : tcgen05 tensor cores, bf16 operands, fp32 accumulate
+ *  GEIG_MATH_TF32  : tcgen05 tensor cores, tf32 operands, fp32 accumulate
+ *  GEIG_MATH_3XTF32: tcgen05 tf32 with hi/lo split (fp32-accurate)
+ * The Gram tables and the update are always fp32. */
+typedef enum {
+  GEIG_MATH_F32 = 0,
+  GEIG_MATH_BF16 = 1,
+  GEIG_MATH_TF32 = 2,
+  GEIG_MATH_3XTF32 = 3
+} geig_math;
+
+/* Storage dtype of X, Y (CCA) or A, B (dense). */
+typedef enum { GEIG_DATA_F32 = 0, GEIG_DATA_BF16 = 1 } geig_dtype;
+
+/* Create a solver for k players (1 <= k <= 256) on CUDA device `device`.
+ * dense: dx = d, dy = 0.  cca: dx, dy >= 1.  rho >= 0 is the clipping floor of
+ * Alg. 2 line 8 ("scalar rho lower bounding sigma_min(B)").
+ * max_rows bounds the batch size b of later geig_products_cca calls (scratch
+ * is sized for it; 0 for dense).  V and AUX are zero until geig_init_state /
+ * geig_set_state. */
+geig_status geig_create(geig_solver** out, int problem, int64_t dx, int64_t dy,
+                        int32_t k, int math, int data_dtype, double rho,
+                        int64_t max_rows, int device);
+
+/* Destroy the solver and free everything it owns (NULL is a no-op). */
+geig_status geig_destroy(geig_solver* s);
+
+/* Stream (a cudaStream_t passed as void*; NULL = legacy default stream). */
+geig_status geig_set_stream(geig_solver* s, void* stream);
+
+/* Block the host until all work enqueued by this solver has finished. */
+geig_status geig_sync(geig_solver* s);
+
+/* Alg. 2 lines 2-3: from the raw draws G (k x d, device,
+ * fp32; v_i ~ N(0, I_d) drawn by the caller) set v_i = G_i/||G_i|| and
+ * [Bv]_i = v_i.  Also resets the step counter. */
+geig_status geig_init_state(geig_solver* s, const float* G);
+
+/* Overwrite / read the state (V, AUX: k x d fp32, device). AUX may be NULL. */
+geig_status geig_set_state(geig_solver* s, const float* V, const float* AUX);
+geig_status geig_get(geig_solver* s, float* V, float* AUX);
+
+/* Minibatch products for CCA (stage a1): AV = scale * A_t-sum V, BV likewise,
+ * i.e. AV_j = scale * [X1^T (Y1 v_jy) ; Y1^T (X1 v_jx)] and
+ * BV_j = scale * [X2^T (X2 v_jx) ; Y2^T (Y2 v_jy)] with halves of b rows
+ * (reading R1).  scale = 1/h gives A_t v, B_t v; multi-GPU callers pass
+ * 1/(world * h) and all-reduce (Appendix F).  X: b x dx,
+ * Y: b x dy (data_dtype), row stride = dx / dy elements.  2 <= b <= max_rows.
+ * AV, BV: k x d fp32 outputs (overwritten). */
+geig_status geig_products_cca(geig_solver* s, const void* X, const void* Y,
+                              int64_t b, float scale, float* AV, float* BV);
+
+/* Dense products (configs 0, 4): AV[:, r0:r1] = A[r0:r1, :] V^T, BV likewise
+ * (rows r0..r1 of the symmetric A, B; a row shard for multi-GPU).  A, B:
+ * (r1-r0) x d row-major slices (row stride d), data_dtype.  Only columns
+ * [r0, r1) of AV, BV are written. */
+geig_status geig_products_dense(geig_solver* s, const void* A, const void* B,
+                                int64_t r0, int64_t r1, float* AV, float* BV);
+
+/* Stages a2-a4 (Alg. 2 lines 8-19): from the products
+ * AV_j = A_t v_j, BV_j = B_t v_j of the CURRENT state, form the Gram tables,
+ * y_j / [By]_j normalisation with the rho floor, rewards and lower-triangular
+ * penalties, v_i <- (v_i + eta grad_i)/||.||, [Bv]_i += gamma (BV_i - [Bv]_i).
+ * All players read the iteration-start snapshot (parfor). */
+geig_status geig_update(geig_solver* s, const float* AV, const float* BV,
+                        double eta, double gamma);
+
+/* Convenience: one full step = products + update on the solver's scratch. */
+geig_status geig_step_cca(geig_solver* s, const void* X, const void* Y,
+                          int64_t b, double eta, double gamma);
+geig_status geig_step_dense(geig_solver* s, const void* A, const void* B,
+                            double eta, double gamma);
+
+/* End-to-end step from HOST buffers (pinned or pageable): copies X, Y host ->
+ * device (stream-ordered), runs geig_step_cca and copies the k x k Gram table
+ * GA (A-table of the step) back to `ga_host` (may be NULL), then synchronises.
+ * Returns the bytes moved in *h2d / *d2h (may be NULL). */
+geig_status geig_step_cca_host(geig_solver* s, const void* X_host,
+                               const void* Y_host, int64_t b, double eta,
+                               double gamma, float* ga_host, int64_t* h2d,
+                               int64_t* d2h);
+
+/* Diagnostics of the last geig_update (device outputs, k x k fp32 each, any
+ * may be NULL): GA[i][j] = <v_i, AV_j>, GC[i][j] = <v_i, [Bv]_j>,
+ * GB[i][j] = <v_i, BV_j> (only the diagonal of GB is computed; the rest is
+ * zero; for GA and GC only i >= j is computed, the rest is zero) — the
+ * "k x k inner-product tables" of the north star, from the iteration-start
+ * state. */
+geig_status geig_get_gram(geig_solver* s, float* GA, float* GB, float* GC);
+
+/* Number of kernel launches this solver has enqueued since creation. */
+int64_t geig_launch_count(const geig_solver* s);
+
+/* Human-readable message of the last error on this thread ("" if none). */
+const char* geig_last_error(void);
+
+/* Library version string. */
+const char* geig_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GEIG_H_ */

@@ -1,0 +1,369 @@
+// geig_api.cu — the C ABI of include/geig.h: solver state, scratch, dispatch
+// of the product kernels (SIMT fp32 / tcgen05) and the cooperative update.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <algorithm>
+
+#include "../../include/geig.h"
+#include "common.cuh"
+#include "simt_gemm.cuh"
+#include "update.cuh"
+#include "tc_gemm.cuh"
+
+using namespace geig;
+
+static thread_local std::string g_err;
+
+static geig_status fail(geig_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CU(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(GEIG_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,           \
+                  cudaGetErrorString(e_));                                            \
+  } while (0)
+
+#define CHECK_LAUNCH() CU(cudaGetLastError())
+
+struct geig_solver {
+  int problem = 0, math = 0, dtype = 0, device = 0;
+  int64_t dx = 0, dy = 0, d = 0, max_rows = 0;
+  int k = 0;
+  float rho = 0.f;
+  cudaStream_t stream = nullptr;
+  // state
+  float *V = nullptr, *AUX = nullptr;
+  __nv_bfloat16* Vbf = nullptr;
+  // scratch
+  float *AV = nullptr, *BV = nullptr, *Vtmp = nullptr, *gram = nullptr, *coef = nullptr;
+  float *partial = nullptr, *norm_partial = nullptr;
+  float *Wx = nullptr, *Wy = nullptr;                 // fp32 backward operands k x max_rows
+  __nv_bfloat16 *Wxb = nullptr, *Wyb = nullptr;       // bf16 backward operands
+  void *hX = nullptr, *hY = nullptr;                  // device staging for *_host
+  int upd_grid = 1;
+  size_t upd_smem = 0;
+  int64_t launches = 0;
+  tc::TcPlan tc;                                      // tcgen05 plans (tensor maps, scratch)
+};
+
+extern "C" const char* geig_last_error(void) { return g_err.c_str(); }
+extern "C" const char* geig_version(void) { return "geig 0.1 (sm_100a)"; }
+extern "C" int64_t geig_launch_count(const geig_solver* s) { return s ? s->launches : 0; }
+
+static size_t upd_units(int k, int64_t d) {
+  const int T = (k + 31) / 32;
+  const int units = T * (T + 1) + T;
+  const int64_t nseg = (d + UPD_SEG - 1) / UPD_SEG;
+  return (size_t)units * nseg;
+}
+
+extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, int64_t dy,
+                                   int32_t k, int math, int data_dtype, double rho,
+                                   int64_t max_rows, int device) {
+  if (!out) return fail(GEIG_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  if (problem != GEIG_DENSE && problem != GEIG_CCA) return fail(GEIG_ERR_ARG, "bad problem %d", problem);
+  if (k < 1) return fail(GEIG_ERR_ARG, "k must be >= 1");
+  if (k > 128) return fail(GEIG_ERR_UNSUPPORTED, "k=%d > 128 not compiled", k);
+  if (dx < 1 || dy < 0 || (problem == GEIG_CCA && dy < 1) || (problem == GEIG_DENSE && dy != 0))
+    return fail(GEIG_ERR_ARG, "bad dims dx=%lld dy=%lld", (long long)dx, (long long)dy);
+  if (math < GEIG_MATH_F32 || math > GEIG_MATH_3XTF32) return fail(GEIG_ERR_ARG, "bad math %d", math);
+  if (data_dtype != GEIG_DATA_F32 && data_dtype != GEIG_DATA_BF16) return fail(GEIG_ERR_ARG, "bad dtype");
+  if (math == GEIG_MATH_BF16 && data_dtype != GEIG_DATA_BF16)
+    return fail(GEIG_ERR_ARG, "GEIG_MATH_BF16 requires bf16 data");
+  if ((math == GEIG_MATH_TF32 || math == GEIG_MATH_3XTF32) && data_dtype != GEIG_DATA_F32)
+    return fail(GEIG_ERR_ARG, "tf32 math requires fp32 data");
+  if (!(rho >= 0.0)) return fail(GEIG_ERR_ARG, "rho must be >= 0");
+  if (problem == GEIG_CCA && max_rows < 2) return fail(GEIG_ERR_ARG, "max_rows must be >= 2");
+  if (k > dx + dy) return fail(GEIG_ERR_ARG, "k > d");
+
+  geig_solver* s = new geig_solver();
+  s->problem = problem; s->math = math; s->dtype = data_dtype; s->device = device;
+  s->dx = dx; s->dy = dy; s->d = dx + dy; s->k = k; s->rho = (float)rho;
+  s->max_rows = problem == GEIG_CCA ? max_rows : 0;
+  auto cleanup = [&](geig_status st) { geig_destroy(s); return st; };
+  if (cudaSetDevice(device) != cudaSuccess) return cleanup(fail(GEIG_ERR_CUDA, "cudaSetDevice(%d)", device));
+  const size_t kd = (size_t)k * s->d;
+#define ALLOC(ptr, bytes)                                                               \
+  if (cudaMalloc((void**)&(ptr), (bytes)) != cudaSuccess)                              \
+    return cleanup(fail(GEIG_ERR_CUDA, "cudaMalloc %zu bytes failed", (size_t)(bytes)));
+  ALLOC(s->V, kd * 4);
+  ALLOC(s->AUX, kd * 4);
+  ALLOC(s->Vbf, kd * 2);
+  ALLOC(s->AV, kd * 4);
+  ALLOC(s->BV, kd * 4);
+  ALLOC(s->Vtmp, kd * 4);
+  ALLOC(s->gram, (size_t)3 * k * k * 4);
+  ALLOC(s->coef, ((size_t)k * k + 2 * k) * 4);
+  ALLOC(s->partial, upd_units(k, s->d) * 1024 * 4);
+  if (problem == GEIG_CCA) {
+    const int64_t mr = ((max_rows + 127) / 128) * 128;
+    ALLOC(s->Wx, (size_t)k * mr * 4);
+    ALLOC(s->Wy, (size_t)k * mr * 4);
+    ALLOC(s->Wxb, (size_t)k * mr * 2);
+    ALLOC(s->Wyb, (size_t)k * mr * 2);
+  }
+#undef ALLOC
+  cudaMemset(s->V, 0, kd * 4);
+  cudaMemset(s->AUX, 0, kd * 4);
+  cudaMemset(s->Vbf, 0, kd * 2);
+  cudaMemset(s->gram, 0, (size_t)3 * k * k * 4);
+
+  // cooperative update grid: co-resident CTAs only
+  const size_t sm_phase1 = (size_t)2 * 32 * 65 * 4;
+  const size_t sm_phase3 = ((size_t)k * k + 3 * k + (size_t)k * UPD_CW) * 4;
+  s->upd_smem = std::max(sm_phase1, sm_phase3);
+  if (cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)s->upd_smem) != cudaSuccess)
+    return cleanup(fail(GEIG_ERR_CUDA, "smem attribute for update kernel"));
+  int occ = 0, nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, update_kernel, UPD_THREADS, s->upd_smem) != cudaSuccess || occ < 1)
+    return cleanup(fail(GEIG_ERR_CUDA, "update kernel occupancy query failed"));
+  const int64_t work = std::max<int64_t>((int64_t)upd_units(k, s->d), (s->d + UPD_CW - 1) / UPD_CW);
+  s->upd_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::min(occ, 2), work));
+  if (cudaMalloc((void**)&s->norm_partial, (size_t)s->upd_grid * k * 4) != cudaSuccess)
+    return cleanup(fail(GEIG_ERR_CUDA, "cudaMalloc norm_partial"));
+  if (math != GEIG_MATH_F32) {
+    geig_status st = tc::plan_create(s->tc, problem, dx, dy, k, math, max_rows, device);
+    if (st != GEIG_OK) return cleanup(fail(st, "%s", tc::last_error()));
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(fail(GEIG_ERR_CUDA, "create sync"));
+  *out = s;
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_destroy(geig_solver* s) {
+  if (!s) return GEIG_OK;
+  cudaSetDevice(s->device);
+  for (void* p : {(void*)s->V, (void*)s->AUX, (void*)s->Vbf, (void*)s->AV, (void*)s->BV, (void*)s->Vtmp,
+                  (void*)s->gram, (void*)s->coef, (void*)s->partial, (void*)s->norm_partial,
+                  (void*)s->Wx, (void*)s->Wy, (void*)s->Wxb, (void*)s->Wyb, s->hX, s->hY})
+    if (p) cudaFree(p);
+  tc::plan_destroy(s->tc);
+  delete s;
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_set_stream(geig_solver* s, void* stream) {
+  if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  s->stream = (cudaStream_t)stream;
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_sync(geig_solver* s) {
+  if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  CU(cudaSetDevice(s->device));
+  CU(cudaStreamSynchronize(s->stream));
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_init_state(geig_solver* s, const float* G) {
+  if (!s || !G) return fail(GEIG_ERR_ARG, "NULL argument");
+  CU(cudaSetDevice(s->device));
+  init_state_kernel<<<s->k, 256, 0, s->stream>>>(G, s->V, s->AUX, s->Vbf, s->d);
+  CHECK_LAUNCH();
+  s->launches++;
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_set_state(geig_solver* s, const float* V, const float* AUX) {
+  if (!s || !V) return fail(GEIG_ERR_ARG, "NULL argument");
+  CU(cudaSetDevice(s->device));
+  const size_t kd = (size_t)s->k * s->d;
+  CU(cudaMemcpyAsync(s->V, V, kd * 4, cudaMemcpyDeviceToDevice, s->stream));
+  if (AUX) CU(cudaMemcpyAsync(s->AUX, AUX, kd * 4, cudaMemcpyDeviceToDevice, s->stream));
+  f32_to_bf16_kernel<<<256, 256, 0, s->stream>>>(s->V, s->Vbf, (int64_t)kd);
+  CHECK_LAUNCH();
+  s->launches++;
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_get(geig_solver* s, float* V, float* AUX) {
+  if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  CU(cudaSetDevice(s->device));
+  const size_t kd = (size_t)s->k * s->d;
+  if (V) CU(cudaMemcpyAsync(V, s->V, kd * 4, cudaMemcpyDeviceToDevice, s->stream));
+  if (AUX) CU(cudaMemcpyAsync(AUX, s->AUX, kd * 4, cudaMemcpyDeviceToDevice, s->stream));
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_get_gram(geig_solver* s, float* GA, float* GB, float* GC) {
+  if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  CU(cudaSetDevice(s->device));
+  const size_t kk = (size_t)s->k * s->k;
+  if (GA) CU(cudaMemcpyAsync(GA, s->gram, kk * 4, cudaMemcpyDeviceToDevice, s->stream));
+  if (GB) CU(cudaMemcpyAsync(GB, s->gram + kk, kk * 4, cudaMemcpyDeviceToDevice, s->stream));
+  if (GC) CU(cudaMemcpyAsync(GC, s->gram + 2 * kk, kk * 4, cudaMemcpyDeviceToDevice, s->stream));
+  return GEIG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// products
+// ---------------------------------------------------------------------------
+
+template <typename TA, bool A_K, bool B_K, class Epi>
+static geig_status launch_simt(geig_solver* s, const TA* A, int64_t lda, const float* B, int64_t ldb,
+                               int M, int N, int64_t kbeg, int64_t kend, Epi epi) {
+  if (M <= 0 || N <= 0) return GEIG_OK;
+  dim3 grid((M + SG_BM - 1) / SG_BM, (N + SG_BN - 1) / SG_BN);
+  simt_gemm_kernel<TA, float, A_K, B_K, Epi><<<grid, 256, 0, s->stream>>>(A, lda, B, ldb, M, N, kbeg, kend, epi);
+  CHECK_LAUNCH();
+  s->launches++;
+  return GEIG_OK;
+}
+
+template <typename T>
+static geig_status products_cca_simt(geig_solver* s, const T* X, const T* Y, int64_t b, float scale,
+                                     float* AV, float* BV) {
+  const int h = (int)(b / 2);
+  const int k = s->k;
+  const int64_t ldw = b;
+  geig_status st;
+  // forward: Z_x = X V_x^T (b x k), scattered into the backward operands
+  st = launch_simt<T, true, true>(s, X, s->dx, s->V, s->d, (int)(2 * h), k, 0, s->dx,
+                                  EpiForward{s->Wy, s->Wx, ldw, h});
+  if (st) return st;
+  st = launch_simt<T, true, true>(s, Y, s->dy, s->V + s->dx, s->d, (int)(2 * h), k, 0, s->dy,
+                                  EpiForward{s->Wx, s->Wy, ldw, h});
+  if (st) return st;
+  // backward: AV_x = X1^T W_x[:, :h], BV_x = X2^T W_x[:, h:2h], same for y
+  for (int view = 0; view < 2; ++view) {
+    const T* Xv = view == 0 ? X : Y;
+    const int64_t dv = view == 0 ? s->dx : s->dy;
+    const int64_t off = view == 0 ? 0 : s->dx;
+    const float* W = view == 0 ? s->Wx : s->Wy;
+    st = launch_simt<T, false, true>(s, Xv, dv, W, ldw, (int)dv, k, 0, h,
+                                     EpiTransposeScale{AV + off, s->d, scale});
+    if (st) return st;
+    st = launch_simt<T, false, true>(s, Xv, dv, W, ldw, (int)dv, k, h, 2 * h,
+                                     EpiTransposeScale{BV + off, s->d, scale});
+    if (st) return st;
+  }
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_products_cca(geig_solver* s, const void* X, const void* Y, int64_t b,
+                                         float scale, float* AV, float* BV) {
+  if (!s || !X || !Y || !AV || !BV) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (s->problem != GEIG_CCA) return fail(GEIG_ERR_STATE, "solver is not a CCA solver");
+  if (b < 2 || b > s->max_rows) return fail(GEIG_ERR_ARG, "b=%lld outside [2, max_rows=%lld]",
+                                            (long long)b, (long long)s->max_rows);
+  CU(cudaSetDevice(s->device));
+  if (s->math == GEIG_MATH_F32) {
+    if (s->dtype == GEIG_DATA_F32)
+      return products_cca_simt(s, (const float*)X, (const float*)Y, b, scale, AV, BV);
+    return products_cca_simt(s, (const __nv_bfloat16*)X, (const __nv_bfloat16*)Y, b, scale, AV, BV);
+  }
+  int64_t nl = 0;
+  geig_status st = tc::products_cca(s->tc, X, Y, b, scale, s->Vbf, s->V, s->Wxb, s->Wyb, AV, BV,
+                                    s->stream, &nl);
+  s->launches += nl;
+  if (st) return fail(st, "%s", tc::last_error());
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_products_dense(geig_solver* s, const void* A, const void* B, int64_t r0,
+                                           int64_t r1, float* AV, float* BV) {
+  if (!s || !A || !B || !AV || !BV) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (s->problem != GEIG_DENSE) return fail(GEIG_ERR_STATE, "solver is not a dense solver");
+  if (r0 < 0 || r1 > s->d || r0 >= r1) return fail(GEIG_ERR_ARG, "bad row range");
+  CU(cudaSetDevice(s->device));
+  const int M = (int)(r1 - r0);
+  if (s->math == GEIG_MATH_F32) {
+    geig_status st;
+    if (s->dtype == GEIG_DATA_F32) {
+      st = launch_simt<float, true, true>(s, (const float*)A, s->d, s->V, s->d, M, s->k, 0, s->d,
+                                          EpiTransposeScale{AV + r0, s->d, 1.f});
+      if (st) return st;
+      return launch_simt<float, true, true>(s, (const float*)B, s->d, s->V, s->d, M, s->k, 0, s->d,
+                                            EpiTransposeScale{BV + r0, s->d, 1.f});
+    }
+    st = launch_simt<__nv_bfloat16, true, true>(s, (const __nv_bfloat16*)A, s->d, s->V, s->d, M, s->k, 0,
+                                                s->d, EpiTransposeScale{AV + r0, s->d, 1.f});
+    if (st) return st;
+    return launch_simt<__nv_bfloat16, true, true>(s, (const __nv_bfloat16*)B, s->d, s->V, s->d, M, s->k, 0,
+                                                  s->d, EpiTransposeScale{BV + r0, s->d, 1.f});
+  }
+  int64_t nl = 0;
+  geig_status st = tc::products_dense(s->tc, A, B, r0, r1, s->Vbf, s->V, AV, BV, s->stream, &nl);
+  s->launches += nl;
+  if (st) return fail(st, "%s", tc::last_error());
+  return GEIG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// update
+// ---------------------------------------------------------------------------
+
+extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float* BV, double eta,
+                                   double gamma) {
+  if (!s || !AV || !BV) return fail(GEIG_ERR_ARG, "NULL argument");
+  CU(cudaSetDevice(s->device));
+  CU(cudaMemsetAsync(s->gram, 0, (size_t)3 * s->k * s->k * 4, s->stream));
+  UpdateArgs a;
+  a.V = s->V; a.AUX = s->AUX; a.AV = AV; a.BV = BV; a.Vtmp = s->Vtmp;
+  a.Vbf = s->Vbf; a.partial = s->partial; a.gram = s->gram; a.coef = s->coef;
+  a.norm_partial = s->norm_partial; a.k = s->k; a.d = s->d;
+  a.eta = (float)eta; a.gamma = (float)gamma; a.rho = s->rho;
+  void* args[] = {&a};
+  CU(cudaLaunchCooperativeKernel((void*)update_kernel, dim3(s->upd_grid), dim3(UPD_THREADS), args,
+                                 s->upd_smem, s->stream));
+  s->launches++;
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* Y, int64_t b, double eta,
+                                     double gamma) {
+  if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  geig_status st = geig_products_cca(s, X, Y, b, 1.0f / (float)(b / 2), s->AV, s->BV);
+  if (st) return st;
+  return geig_update(s, s->AV, s->BV, eta, gamma);
+}
+
+extern "C" geig_status geig_step_dense(geig_solver* s, const void* A, const void* B, double eta,
+                                       double gamma) {
+  if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  geig_status st = geig_products_dense(s, A, B, 0, s->d, s->AV, s->BV);
+  if (st) return st;
+  return geig_update(s, s->AV, s->BV, eta, gamma);
+}
+
+extern "C" geig_status geig_step_cca_host(geig_solver* s, const void* X_host, const void* Y_host, int64_t b,
+                                          double eta, double gamma, float* ga_host, int64_t* h2d,
+                                          int64_t* d2h) {
+  if (!s || !X_host || !Y_host) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (s->problem != GEIG_CCA) return fail(GEIG_ERR_STATE, "solver is not a CCA solver");
+  if (b < 2 || b > s->max_rows) return fail(GEIG_ERR_ARG, "bad b");
+  CU(cudaSetDevice(s->device));
+  const size_t es = s->dtype == GEIG_DATA_BF16 ? 2 : 4;
+  if (!s->hX) {
+    CU(cudaMalloc(&s->hX, (size_t)s->max_rows * s->dx * es));
+    CU(cudaMalloc(&s->hY, (size_t)s->max_rows * s->dy * es));
+  }
+  const size_t bx = (size_t)b * s->dx * es, by = (size_t)b * s->dy * es;
+  CU(cudaMemcpyAsync(s->hX, X_host, bx, cudaMemcpyHostToDevice, s->stream));
+  CU(cudaMemcpyAsync(s->hY, Y_host, by, cudaMemcpyHostToDevice, s->stream));
+  geig_status st = geig_step_cca(s, s->hX, s->hY, b, eta, gamma);
+  if (st) return st;
+  const size_t gb = (size_t)s->k * s->k * 4;
+  if (ga_host) CU(cudaMemcpyAsync(ga_host, s->gram, gb, cudaMemcpyDeviceToHost, s->stream));
+  CU(cudaStreamSynchronize(s->stream));
+  if (h2d) *h2d = (int64_t)(bx + by);
+  if (d2h) *d2h = ga_host ? (int64_t)gb : 0;
+  return GEIG_OK;
+}

@@ -1,0 +1,216 @@
+"""Thin ctypes binding of include/geig.h (argument marshalling only).
+
+Every function has the C name and forwards to libgeig.so; torch tensors are
+accepted for device / host buffers and passed as raw pointers after shape,
+dtype, device and contiguity checks.  There is no Python or CPU fallback:
+if the shared library is missing this module raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgeig.so")
+
+GEIG_OK, GEIG_ERR_ARG, GEIG_ERR_CUDA, GEIG_ERR_UNSUPPORTED, GEIG_ERR_STATE = range(5)
+GEIG_DENSE, GEIG_CCA = 0, 1
+GEIG_MATH_F32, GEIG_MATH_BF16, GEIG_MATH_TF32, GEIG_MATH_3XTF32 = 0, 1, 2, 3
+GEIG_DATA_F32, GEIG_DATA_BF16 = 0, 1
+
+MATH_NAMES = {"f32": GEIG_MATH_F32, "bf16": GEIG_MATH_BF16, "tf32": GEIG_MATH_TF32,
+              "3xtf32": GEIG_MATH_3XTF32}
+
+
+class GeigError(RuntimeError):
+    pass
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: the sm_100a CUDA library has not been built "
+                      "(run `python -c 'import __graft_entry__ as g; g.build()'`); "
+                      "there is no CPU fallback")
+
+_lib = ctypes.CDLL(LIB_PATH)
+_vp, _i64, _i32, _f32, _f64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float, ctypes.c_double
+_SIGS = {
+    "geig_create": [ctypes.POINTER(_vp), ctypes.c_int, _i64, _i64, _i32, ctypes.c_int, ctypes.c_int,
+                    _f64, _i64, ctypes.c_int],
+    "geig_destroy": [_vp],
+    "geig_set_stream": [_vp, _vp],
+    "geig_sync": [_vp],
+    "geig_init_state": [_vp, _vp],
+    "geig_set_state": [_vp, _vp, _vp],
+    "geig_get": [_vp, _vp, _vp],
+    "geig_products_cca": [_vp, _vp, _vp, _i64, _f32, _vp, _vp],
+    "geig_products_dense": [_vp, _vp, _vp, _i64, _i64, _vp, _vp],
+    "geig_update": [_vp, _vp, _vp, _f64, _f64],
+    "geig_step_cca": [_vp, _vp, _vp, _i64, _f64, _f64],
+    "geig_step_dense": [_vp, _vp, _vp, _f64, _f64],
+    "geig_step_cca_host": [_vp, _vp, _vp, _i64, _f64, _f64, _vp, ctypes.POINTER(_i64),
+                           ctypes.POINTER(_i64)],
+    "geig_get_gram": [_vp, _vp, _vp, _vp],
+}
+for _name, _args in _SIGS.items():
+    _fn = getattr(_lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = ctypes.c_int
+_lib.geig_launch_count.argtypes = [_vp]
+_lib.geig_launch_count.restype = _i64
+_lib.geig_last_error.restype = ctypes.c_char_p
+_lib.geig_version.restype = ctypes.c_char_p
+
+EXPORTED = ["geig_create", "geig_destroy", "geig_set_stream", "geig_sync", "geig_init_state",
+            "geig_set_state", "geig_get", "geig_products_cca", "geig_products_dense", "geig_update",
+            "geig_step_cca", "geig_step_dense", "geig_step_cca_host", "geig_get_gram",
+            "geig_launch_count", "geig_last_error", "geig_version"]
+
+
+def _check(st: int):
+    if st != GEIG_OK:
+        raise GeigError(f"geig status {st}: {_lib.geig_last_error().decode()}")
+
+
+def _ptr(t, dtype=None, device=True, numel=None):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("expected a torch.Tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"expected dtype {dtype}, got {t.dtype}")
+    if device and not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not device and t.is_cuda:
+        raise ValueError("expected a host tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"expected {numel} elements, got {t.numel()}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def geig_version() -> str:
+    return _lib.geig_version().decode()
+
+
+def geig_last_error() -> str:
+    return _lib.geig_last_error().decode()
+
+
+def geig_create(problem: int, dx: int, dy: int, k: int, math: int, data_dtype: int, rho: float,
+                max_rows: int = 0, device: int = 0):
+    h = ctypes.c_void_p()
+    _check(_lib.geig_create(ctypes.byref(h), problem, dx, dy, k, math, data_dtype, rho, max_rows, device))
+    return h
+
+
+def geig_destroy(h):
+    _check(_lib.geig_destroy(h))
+
+
+def geig_set_stream(h, stream: int | None):
+    _check(_lib.geig_set_stream(h, ctypes.c_void_p(stream or 0)))
+
+
+def geig_sync(h):
+    _check(_lib.geig_sync(h))
+
+
+def geig_init_state(h, G):
+    _check(_lib.geig_init_state(h, _ptr(G, torch.float32)))
+
+
+def geig_set_state(h, V, AUX=None):
+    _check(_lib.geig_set_state(h, _ptr(V, torch.float32), _ptr(AUX, torch.float32)))
+
+
+def geig_get(h, V=None, AUX=None):
+    _check(_lib.geig_get(h, _ptr(V, torch.float32), _ptr(AUX, torch.float32)))
+
+
+def geig_products_cca(h, X, Y, b: int, scale: float, AV, BV):
+    _check(_lib.geig_products_cca(h, _ptr(X), _ptr(Y), b, scale, _ptr(AV, torch.float32),
+                                  _ptr(BV, torch.float32)))
+
+
+def geig_products_dense(h, A, B, r0: int, r1: int, AV, BV):
+    _check(_lib.geig_products_dense(h, _ptr(A), _ptr(B), r0, r1, _ptr(AV, torch.float32),
+                                    _ptr(BV, torch.float32)))
+
+
+def geig_update(h, AV, BV, eta: float, gamma: float):
+    _check(_lib.geig_update(h, _ptr(AV, torch.float32), _ptr(BV, torch.float32), eta, gamma))
+
+
+def geig_step_cca(h, X, Y, b: int, eta: float, gamma: float):
+    _check(_lib.geig_step_cca(h, _ptr(X), _ptr(Y), b, eta, gamma))
+
+
+def geig_step_dense(h, A, B, eta: float, gamma: float):
+    _check(_lib.geig_step_dense(h, _ptr(A), _ptr(B), eta, gamma))
+
+
+def geig_step_cca_host(h, X_host, Y_host, b: int, eta: float, gamma: float, ga_host=None):
+    h2d, d2h = _i64(0), _i64(0)
+    _check(_lib.geig_step_cca_host(h, _ptr(X_host, device=False), _ptr(Y_host, device=False), b, eta,
+                                   gamma, _ptr(ga_host, torch.float32, device=False),
+                                   ctypes.byref(h2d), ctypes.byref(d2h)))
+    return h2d.value, d2h.value
+
+
+def geig_get_gram(h, GA=None, GB=None, GC=None):
+    _check(_lib.geig_get_gram(h, _ptr(GA, torch.float32), _ptr(GB, torch.float32), _ptr(GC, torch.float32)))
+
+
+def geig_launch_count(h) -> int:
+    return int(_lib.geig_launch_count(h))
+
+
+class Solver:
+    """Convenience owner of a geig_solver handle (marshalling only)."""
+
+    def __init__(self, problem, dx, dy, k, math="f32", data_dtype=GEIG_DATA_F32, rho=0.0,
+                 max_rows=0, device=0, stream=None):
+        self.problem, self.dx, self.dy, self.k = problem, dx, dy, k
+        self.d = dx + dy
+        self.device = device
+        self.math = MATH_NAMES[math] if isinstance(math, str) else math
+        self.h = geig_create(problem, dx, dy, k, self.math, data_dtype, rho, max_rows, device)
+        if stream is None:
+            stream = torch.cuda.current_stream(device).cuda_stream
+        geig_set_stream(self.h, stream)
+
+    def close(self):
+        if self.h is not None:
+            geig_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def init_state(self, G):
+        geig_init_state(self.h, G)
+
+    def set_state(self, V, AUX=None):
+        geig_set_state(self.h, V, AUX)
+
+    def state(self):
+        V = torch.empty(self.k, self.d, device=f"cuda:{self.device}")
+        AUX = torch.empty_like(V)
+        geig_get(self.h, V, AUX)
+        geig_sync(self.h)
+        return V, AUX
+
+    def gram(self):
+        t = [torch.empty(self.k, self.k, device=f"cuda:{self.device}") for _ in range(3)]
+        geig_get_gram(self.h, *t)
+        geig_sync(self.h)
+        return t
+
+    def launches(self):
+        return geig_launch_count(self.h)

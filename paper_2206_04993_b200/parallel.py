@@ -1,0 +1,60 @@
+"""Multi-GPU host logic (one process per GPU, torch.distributed over NCCL).
+
+Appendix F: "we parallelized the estimation of the
+matrix-vector products Av_i and Bv_i for all i and then aggregated this
+information across machines".  Each rank owns a shard of the minibatch rows
+(CCA) or of the matrix rows (dense), computes its partial products, and the
+partials are combined by an all-reduce (sum); every rank then applies the
+same update to its replica of V and [Bv].  The compute callables are
+injected so the orchestration can be exercised on CPU with gloo.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+
+def shard_rows(n_rows: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous row range [r0, r1) of `rank`; sizes differ by at most one."""
+    base, rem = divmod(n_rows, world)
+    r0 = rank * base + min(rank, rem)
+    return r0, r0 + base + (1 if rank < rem else 0)
+
+
+@dataclass
+class ShardedStep:
+    """One Appendix-F step.  products(AV, BV) writes this rank's partial
+    products (already scaled so that the SUM over ranks is the global
+    estimate); update(AV, BV) applies Alg. 2 lines 8-19 locally."""
+    products: Callable[[torch.Tensor, torch.Tensor], None]
+    update: Callable[[torch.Tensor, torch.Tensor], None]
+    group: object = None
+
+    def __call__(self, AV: torch.Tensor, BV: torch.Tensor):
+        self.products(AV, BV)
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            # one fused all-reduce of the two k x d products
+            flat = torch.stack([AV, BV])
+            dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
+            AV.copy_(flat[0])
+            BV.copy_(flat[1])
+        self.update(AV, BV)
+
+
+def cca_scale(b_local: int, world: int) -> float:
+    """Each rank holds b_local rows split into halves (reading R1); the global
+    A_t / B_t average over world * (b_local // 2) rows per half."""
+    return 1.0 / (world * (b_local // 2))
+
+
+def dense_allgather_rows(AV: torch.Tensor, BV: torch.Tensor, d: int, world: int, group=None):
+    """Dense row sharding: rank r wrote columns [r0, r1) of AV, BV (zeros
+    elsewhere); a SUM all-reduce assembles the full products."""
+    if dist.is_initialized() and world > 1:
+        flat = torch.stack([AV, BV])
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+        AV.copy_(flat[0])
+        BV.copy_(flat[1])
