@@ -8,6 +8,7 @@
 #include <cstring>
 #include <string>
 #include <algorithm>
+#include <initializer_list>
 
 #include "../../include/geig.h"
 #include "common.cuh"
@@ -270,8 +271,7 @@ extern "C" geig_status geig_products_cca(geig_solver* s, const void* X, const vo
     return products_cca_simt(s, (const __nv_bfloat16*)X, (const __nv_bfloat16*)Y, b, scale, AV, BV);
   }
   int64_t nl = 0;
-  geig_status st = tc::products_cca(s->tc, X, Y, b, scale, s->Vbf, s->V, s->Wxb, s->Wyb, AV, BV,
-                                    s->stream, &nl);
+  geig_status st = tc::products_cca(s->tc, X, Y, b, scale, s->Vbf, s->V, AV, BV, s->stream, &nl);
   s->launches += nl;
   if (st) return fail(st, "%s", tc::last_error());
   return GEIG_OK;

@@ -1,28 +1,537 @@
-// tc_gemm.cuh — tcgen05 / TMA tensor-core products (placeholder until the
-// sm_100a kernels land; every entry returns GEIG_ERR_UNSUPPORTED).
+// tc_gemm.cuh — tcgen05 / TMA tensor-core minibatch products for sm_100a.
+//
+// One warp-specialised kernel computes C[M x N] = sum_kk A(m,kk) B(n,kk) for
+// up to two "segments" (K ranges with their own operands and their own TMEM
+// accumulator), with
+//   * A staged by TMA (SWIZZLE_128B) either K-major (row-major [M][K]: the
+//     forward product X V^T, dense A V^T) or MN-major (row-major [K][M]: the
+//     backward product X^T W, read straight from the sample-major X without a
+//     transpose pass),
+//   * B staged by TMA K-major ([N][K]: V (k x d) or W^T (k x rows)),
+//   * tcgen05.mma (kind::f16 bf16 or kind::tf32) issued by ONE thread,
+//     accumulators in TMEM (fp32), 4-stage mbarrier ring TMA <-> MMA,
+//   * epilogue: tcgen05.ld 32x32b -> registers -> player-major output
+//     out[n*ldo + m] = scale*acc (plain store or fp32 red.add for split-K).
+// CTA = 128 threads: warp0 lane0 = TMA producer, warp1 lane0 = MMA issuer,
+// warp2 = TMEM allocator; all four warps run the epilogue (warp w owns TMEM
+// lanes 32w..32w+31 = output rows m0+32w..).
 #pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <stdint.h>
+#include <string>
 #include "../../include/geig.h"
 
 namespace geig { namespace tc {
 
-struct TcPlan { int ready = 0; };
+constexpr int TC_THREADS = 128;
+constexpr int TC_BM = 128;
+constexpr int TC_STAGES = 4;
 
-inline const char* last_error() { return "tcgen05 products not built in this version"; }
+// ----------------------------------------------------------------------------
+// PTX wrappers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TC_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TC_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-inline geig_status plan_create(TcPlan&, int, int64_t, int64_t, int, int, int64_t, int) {
-  return GEIG_ERR_UNSUPPORTED;
+template <int EB>
+__device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  if constexpr (EB == 2) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+  }
 }
-inline void plan_destroy(TcPlan&) {}
-inline geig_status products_cca(TcPlan&, const void*, const void*, int64_t, float, const __nv_bfloat16*,
-                                const float*, __nv_bfloat16*, __nv_bfloat16*, float*, float*,
-                                cudaStream_t, int64_t*) {
-  return GEIG_ERR_UNSUPPORTED;
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
 }
-inline geig_status products_dense(TcPlan&, const void*, const void*, int64_t, int64_t, const __nv_bfloat16*,
-                                  const float*, float*, float*, cudaStream_t, int64_t*) {
-  return GEIG_ERR_UNSUPPORTED;
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor, SWIZZLE_128B, sm_100 version bits = 1.
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// ----------------------------------------------------------------------------
+// kernel
+// ----------------------------------------------------------------------------
+struct TcMaps {
+  CUtensorMap a[4];   // index = group * 2 + segment
+  CUtensorMap b[4];
+};
+
+struct TcParams {
+  int M[2];            // valid rows per group
+  int N;               // valid columns (players)
+  int BN;              // MMA N (multiple of 16, <= 128)
+  int nseg;            // 1 or 2
+  int kblocks[2][2];   // [group][segment] K blocks
+  int splits;          // split-K factor (blockIdx.y)
+  float* out[2][2];    // [group][segment] output base (player-major)
+  int64_t ldo;
+  float scale;
+  int atomic;          // 1: red.add, 0: store
+  uint32_t idesc;
+};
+
+template <int EB, bool A_MN>
+__global__ void __launch_bounds__(TC_THREADS)
+tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
+  constexpr int ATOM = 128 / EB;           // elements per 128B row
+  constexpr int BK = ATOM;                 // K per stage
+  constexpr int UK = 32 / EB;              // K per MMA (16 bf16 / 8 tf32)
+  constexpr uint32_t A_BYTES = TC_BM * 128;
+  const int g = blockIdx.z;
+  const int m0 = blockIdx.x * TC_BM;
+  if (m0 >= p.M[g]) return;
+  const int BN = p.BN;
+  const uint32_t B_BYTES = (uint32_t)BN * 128;
+  const uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + TC_STAGES;
+  uint64_t* accum_bar = empty_bar + TC_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // per-segment K-block ranges of this split
+  int kb_beg[2], kb_cnt[2];
+  int total = 0;
+  for (int s = 0; s < 2; ++s) {
+    const int kb = s < p.nseg ? p.kblocks[g][s] : 0;
+    const int b0 = (int)((int64_t)kb * blockIdx.y / p.splits);
+    const int b1 = (int)((int64_t)kb * (blockIdx.y + 1) / p.splits);
+    kb_beg[s] = b0;
+    kb_cnt[s] = b1 - b0;
+    total += kb_cnt[s];
+  }
+  uint32_t ncols = 32;
+  while (ncols < (uint32_t)(p.nseg * BN)) ncols <<= 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(accum_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < p.nseg; ++s) {
+      tma_prefetch_desc(&maps.a[g * 2 + s]);
+      tma_prefetch_desc(&maps.b[g * 2 + s]);
+    }
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (total > 0) {
+    if (threadIdx.x == 0) {
+      // ---------------- TMA producer ----------------
+      int it = 0;
+      for (int s = 0; s < p.nseg; ++s) {
+        const CUtensorMap* ma = &maps.a[g * 2 + s];
+        const CUtensorMap* mb = &maps.b[g * 2 + s];
+        for (int j = 0; j < kb_cnt[s]; ++j, ++it) {
+          const int st = it % TC_STAGES;
+          if (it >= TC_STAGES) mbar_wait(&empty_bar[st], ((it / TC_STAGES) + 1) & 1);
+          uint8_t* sa = smem + st * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(&full_bar[st], STAGE_BYTES);
+          const int k0 = (kb_beg[s] + j) * BK;
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int q = 0; q < TC_BM / ATOM; ++q) tma_load_2d(sa + q * (BK * 128), ma, &full_bar[st], m0 + q * ATOM, k0);
+          } else {
+            tma_load_2d(sa, ma, &full_bar[st], k0, m0);
+          }
+          tma_load_2d(sb, mb, &full_bar[st], k0, 0);
+        }
+      }
+    } else if (threadIdx.x == 32) {
+      // ---------------- MMA issuer ----------------
+      int it = 0;
+      for (int s = 0; s < p.nseg; ++s) {
+        const uint32_t d_tmem = tmem_base + (uint32_t)(s * BN);
+        for (int j = 0; j < kb_cnt[s]; ++j, ++it) {
+          const int st = it % TC_STAGES;
+          mbar_wait(&full_bar[st], (it / TC_STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + st * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / UK; ++kk) {
+            uint64_t ad, bd;
+            if constexpr (A_MN) {
+              ad = make_sdesc(sa + kk * UK * 128, BK * 128, 1024);
+            } else {
+              ad = make_sdesc(sa + kk * 32, 16, 1024);
+            }
+            bd = make_sdesc(sb + kk * 32, 16, 1024);
+            umma<EB>(d_tmem, ad, bd, p.idesc, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[st]);
+        }
+      }
+      umma_commit(accum_bar);
+    }
+    // ---------------- epilogue (all 4 warps) ----------------
+    mbar_wait(accum_bar, 0);
+    tc_fence_after();
+    const int m = m0 + warp * 32 + lane;
+    const bool mok = m < p.M[g];
+    for (int s = 0; s < p.nseg; ++s) {
+      if (kb_cnt[s] == 0) continue;
+      float* out = p.out[g][s];
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(s * BN + c0), r);
+        if (mok) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = c0 + j;
+            if (n < p.N) {
+              float* dst = out + (int64_t)n * p.ldo + m;
+              const float v = p.scale * __uint_as_float(r[j]);
+              if (p.atomic) atomicAdd(dst, v); else *dst = v;
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
+  }
+}
+
+// Forward-product reshuffle: Zt[view] (k x ldz fp32, rows 0..2h) into the
+// four backward B operands Zb[view][half] (k x hpad, T) — reading R1:
+//   X backward: half0 (A_t) uses Z_y rows [0,h), half1 (B_t) uses Z_x rows [h,2h)
+//   Y backward: half0 uses Z_x rows [0,h), half1 uses Z_y rows [h,2h)
+// and re-zero Zt for the next step's split-K accumulation.
+template <typename T>
+__global__ void zshuffle_kernel(float* __restrict__ Zt, T* __restrict__ Zb, int k, int64_t ldz, int h,
+                                int64_t hpad) {
+  const int64_t per = (int64_t)k * h;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(e / h), r = (int)(e % h);
+    float* zx = Zt + (int64_t)n * ldz;
+    float* zy = Zt + (int64_t)k * ldz + (int64_t)n * ldz;
+    const float x0 = zx[r], x1 = zx[h + r], y0 = zy[r], y1 = zy[h + r];
+    const int64_t o = (int64_t)n * hpad + r;
+    const int64_t plane = (int64_t)k * hpad;
+    Zb[0 * plane + o] = (T)y0;     // view x, half 0
+    Zb[1 * plane + o] = (T)x1;     // view x, half 1
+    Zb[2 * plane + o] = (T)x0;     // view y, half 0
+    Zb[3 * plane + o] = (T)y1;     // view y, half 1
+    zx[r] = 0.f; zx[h + r] = 0.f; zy[r] = 0.f; zy[h + r] = 0.f;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// host side
+// ----------------------------------------------------------------------------
+struct TcPlan {
+  int ready = 0;
+  int problem = 0, math = 0, k = 0, BN = 0, device = 0, nsm = 148;
+  int64_t dx = 0, dy = 0, d = 0, max_rows = 0, ldz = 0, hpad = 0;
+  float* Zt = nullptr;     // 2 x k x ldz fp32 (CCA forward accumulators)
+  void* Zb = nullptr;      // 2 x 2 x k x hpad (bf16 or fp32)
+};
+
+inline std::string& err_str() {
+  static thread_local std::string e;
+  return e;
+}
+inline const char* last_error() { return err_str().c_str(); }
+inline geig_status tc_fail(geig_status st, const std::string& m) {
+  err_str() = m;
+  return st;
+}
+
+inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D row-major tensor [outer][inner] with row stride `stride_el` elements.
+inline bool make_map(CUtensorMap* m, const void* base, int eb, int64_t inner, int64_t outer, int64_t stride_el,
+                     int box_inner, int box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)(stride_el * eb)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, eb == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+inline uint32_t make_idesc(int eb, bool a_mn, int N, int M) {
+  const uint32_t fmt = eb == 2 ? 1u : 2u;  // BF16 : TF32
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((a_mn ? 1u : 0u) << 15) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+inline size_t smem_bytes(int BN) {
+  return 1024 + (size_t)TC_STAGES * (TC_BM * 128 + (size_t)BN * 128) + 256;
+}
+
+template <int EB, bool A_MN>
+inline geig_status launch(const TcMaps& maps, const TcParams& p, dim3 grid, cudaStream_t st) {
+  const size_t sm = smem_bytes(p.BN);
+  static bool attr_done = false;
+  if (!attr_done) {
+    if (cudaFuncSetAttribute(tc_gemm_kernel<EB, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_bytes(128)) != cudaSuccess)
+      return tc_fail(GEIG_ERR_CUDA, "cudaFuncSetAttribute(tc_gemm_kernel) failed");
+    attr_done = true;
+  }
+  tc_gemm_kernel<EB, A_MN><<<grid, TC_THREADS, sm, st>>>(maps, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("tc_gemm launch: ") + cudaGetErrorString(e));
+  return GEIG_OK;
+}
+
+inline int choose_splits(int ctas, int kblocks, int nsm) {
+  int s = 1;
+  while (ctas * (s * 2) <= 2 * nsm && s * 2 <= kblocks) s *= 2;
+  return s;
+}
+
+inline geig_status plan_create(TcPlan& t, int problem, int64_t dx, int64_t dy, int k, int math, int64_t max_rows,
+                               int device) {
+  if (math == GEIG_MATH_3XTF32) return tc_fail(GEIG_ERR_UNSUPPORTED, "3xTF32 products not built yet");
+  const int eb = math == GEIG_MATH_BF16 ? 2 : 4;
+  const int align = 16 / eb;
+  if (dx % align || dy % align)
+    return tc_fail(GEIG_ERR_UNSUPPORTED, "tensor-core path needs dx, dy multiples of " + std::to_string(align) +
+                                             " (TMA 16-byte strides); use GEIG_MATH_F32");
+  if (!encode_fn()) return tc_fail(GEIG_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  t.problem = problem; t.math = math; t.k = k; t.dx = dx; t.dy = dy; t.d = dx + dy; t.device = device;
+  t.max_rows = max_rows;
+  t.BN = ((k + 15) / 16) * 16;
+  cudaDeviceGetAttribute(&t.nsm, cudaDevAttrMultiProcessorCount, device);
+  if (problem == GEIG_CCA) {
+    t.ldz = ((max_rows + 3) / 4) * 4;
+    t.hpad = ((max_rows / 2 + 7) / 8) * 8;
+    if (cudaMalloc((void**)&t.Zt, (size_t)2 * k * t.ldz * 4) != cudaSuccess ||
+        cudaMalloc(&t.Zb, (size_t)4 * k * t.hpad * eb) != cudaSuccess)
+      return tc_fail(GEIG_ERR_CUDA, "cudaMalloc tc scratch");
+    cudaMemset(t.Zt, 0, (size_t)2 * k * t.ldz * 4);
+    cudaMemset(t.Zb, 0, (size_t)4 * k * t.hpad * eb);
+  }
+  t.ready = 1;
+  return GEIG_OK;
+}
+
+inline void plan_destroy(TcPlan& t) {
+  if (t.Zt) cudaFree(t.Zt);
+  if (t.Zb) cudaFree(t.Zb);
+  t.Zt = nullptr; t.Zb = nullptr; t.ready = 0;
+}
+
+// CCA products: forward (K-major X, V) -> Zt -> shuffle -> backward (MN-major X, Zb).
+inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t b, float scale,
+                                const __nv_bfloat16* Vbf, const float* V, float* AV, float* BV, cudaStream_t st,
+                                int64_t* nl) {
+  *nl = 0;
+  if (!t.ready) return tc_fail(GEIG_ERR_STATE, "tc plan not ready");
+  const int eb = t.math == GEIG_MATH_BF16 ? 2 : 4;
+  const int ATOM = 128 / eb;
+  const int h = (int)(b / 2);
+  const int rows = 2 * h;
+  const int k = t.k;
+  const void* Vop = eb == 2 ? (const void*)Vbf : (const void*)V;
+  const int64_t dv[2] = {t.dx, t.dy};
+  const void* Xv[2] = {X, Y};
+  // ---- forward: Z_v = X_v V_v^T, M = rows, K = d_v ----
+  {
+    TcMaps maps;
+    TcParams p{};
+    for (int v = 0; v < 2; ++v) {
+      const char* vb = (const char*)Vop + (v == 0 ? 0 : t.dx * eb);
+      if (!make_map(&maps.a[v * 2], Xv[v], eb, dv[v], rows, dv[v], ATOM, TC_BM) ||
+          !make_map(&maps.b[v * 2], vb, eb, dv[v], k, t.d, ATOM, t.BN))
+        return tc_fail(GEIG_ERR_CUDA, "tensor map encode (forward) failed");
+      maps.a[v * 2 + 1] = maps.a[v * 2];
+      maps.b[v * 2 + 1] = maps.b[v * 2];
+      p.M[v] = rows;
+      p.kblocks[v][0] = (int)((dv[v] + ATOM - 1) / ATOM);
+      p.kblocks[v][1] = 0;
+      p.out[v][0] = t.Zt + (int64_t)v * k * t.ldz;
+      p.out[v][1] = nullptr;
+    }
+    p.N = k; p.BN = t.BN; p.nseg = 1; p.ldo = t.ldz; p.scale = 1.f; p.atomic = 1;
+    p.idesc = make_idesc(eb, false, t.BN, TC_BM);
+    const int mt = (rows + TC_BM - 1) / TC_BM;
+    p.splits = choose_splits(2 * mt, std::min(p.kblocks[0][0], p.kblocks[1][0]), t.nsm);
+    dim3 grid(mt, p.splits, 2);
+    geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st) : launch<4, false>(maps, p, grid, st);
+    if (s) return s;
+    ++*nl;
+  }
+  // ---- shuffle Zt -> Zb halves (and zero Zt) ----
+  {
+    const int64_t per = (int64_t)k * h;
+    const int blocks = (int)std::min<int64_t>(1184, (per + 255) / 256);
+    if (eb == 2)
+      zshuffle_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(t.Zt, (__nv_bfloat16*)t.Zb, k, t.ldz, h, t.hpad);
+    else
+      zshuffle_kernel<float><<<blocks, 256, 0, st>>>(t.Zt, (float*)t.Zb, k, t.ldz, h, t.hpad);
+    if (cudaGetLastError() != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, "zshuffle launch failed");
+    ++*nl;
+  }
+  // ---- backward: AV_v = X_v[0:h]^T Zb[v][0], BV_v = X_v[h:2h]^T Zb[v][1] ----
+  {
+    TcMaps maps;
+    TcParams p{};
+    const int64_t plane = (int64_t)k * t.hpad;
+    for (int v = 0; v < 2; ++v) {
+      for (int s = 0; s < 2; ++s) {
+        const char* xb = (const char*)Xv[v] + (int64_t)s * h * dv[v] * eb;
+        const char* zb = (const char*)t.Zb + (int64_t)(v * 2 + s) * plane * eb;
+        if (!make_map(&maps.a[v * 2 + s], xb, eb, dv[v], h, dv[v], ATOM, ATOM) ||
+            !make_map(&maps.b[v * 2 + s], zb, eb, h, k, t.hpad, ATOM, t.BN))
+          return tc_fail(GEIG_ERR_CUDA, "tensor map encode (backward) failed");
+        p.kblocks[v][s] = (h + ATOM - 1) / ATOM;
+      }
+      p.M[v] = (int)dv[v];
+      const int64_t off = v == 0 ? 0 : t.dx;
+      p.out[v][0] = AV + off;
+      p.out[v][1] = BV + off;
+    }
+    p.N = k; p.BN = t.BN; p.nseg = 2; p.ldo = t.d; p.scale = scale;
+    p.idesc = make_idesc(eb, true, t.BN, TC_BM);
+    const int mt = (int)((std::max(t.dx, t.dy) + TC_BM - 1) / TC_BM);
+    const int mtot = (int)((t.dx + TC_BM - 1) / TC_BM + (t.dy + TC_BM - 1) / TC_BM);
+    p.splits = choose_splits(mtot, p.kblocks[0][0], t.nsm);
+    p.atomic = p.splits > 1;
+    if (p.atomic) {
+      if (cudaMemsetAsync(AV, 0, (size_t)k * t.d * 4, st) != cudaSuccess ||
+          cudaMemsetAsync(BV, 0, (size_t)k * t.d * 4, st) != cudaSuccess)
+        return tc_fail(GEIG_ERR_CUDA, "memset AV/BV failed");
+    }
+    dim3 grid(mt, p.splits, 2);
+    geig_status s = eb == 2 ? launch<2, true>(maps, p, grid, st) : launch<4, true>(maps, p, grid, st);
+    if (s) return s;
+    ++*nl;
+  }
+  return GEIG_OK;
+}
+
+// Dense products: AV[:, r0:r1] = A[r0:r1] V^T, BV likewise (K-major A rows, tf32 or bf16).
+inline geig_status products_dense(TcPlan& t, const void* A, const void* B, int64_t r0, int64_t r1,
+                                  const __nv_bfloat16* Vbf, const float* V, float* AV, float* BV, cudaStream_t st,
+                                  int64_t* nl) {
+  *nl = 0;
+  if (!t.ready) return tc_fail(GEIG_ERR_STATE, "tc plan not ready");
+  const int eb = t.math == GEIG_MATH_BF16 ? 2 : 4;
+  const int ATOM = 128 / eb;
+  const int k = t.k;
+  const int M = (int)(r1 - r0);
+  const void* Vop = eb == 2 ? (const void*)Vbf : (const void*)V;
+  TcMaps maps;
+  TcParams p{};
+  const void* mats[2] = {A, B};
+  float* outs[2] = {AV + r0, BV + r0};
+  for (int g = 0; g < 2; ++g) {
+    if (!make_map(&maps.a[g * 2], mats[g], eb, t.d, M, t.d, ATOM, TC_BM) ||
+        !make_map(&maps.b[g * 2], Vop, eb, t.d, k, t.d, ATOM, t.BN))
+      return tc_fail(GEIG_ERR_CUDA, "tensor map encode (dense) failed");
+    maps.a[g * 2 + 1] = maps.a[g * 2];
+    maps.b[g * 2 + 1] = maps.b[g * 2];
+    p.M[g] = M;
+    p.kblocks[g][0] = (int)((t.d + ATOM - 1) / ATOM);
+    p.out[g][0] = outs[g];
+  }
+  p.N = k; p.BN = t.BN; p.nseg = 1; p.ldo = t.d; p.scale = 1.f;
+  p.idesc = make_idesc(eb, false, t.BN, TC_BM);
+  const int mt = (M + TC_BM - 1) / TC_BM;
+  p.splits = choose_splits(2 * mt, p.kblocks[0][0], t.nsm);
+  p.atomic = p.splits > 1;
+  if (p.atomic) {
+    for (int g = 0; g < 2; ++g)
+      if (cudaMemset2DAsync(outs[g], (size_t)t.d * 4, 0, (size_t)M * 4, k, st) != cudaSuccess)
+        return tc_fail(GEIG_ERR_CUDA, "memset AV/BV rows failed");
+  }
+  dim3 grid(mt, p.splits, 2);
+  geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st) : launch<4, false>(maps, p, grid, st);
+  if (s) return s;
+  ++*nl;
+  return GEIG_OK;
 }
 
 }}  // namespace geig::tc
