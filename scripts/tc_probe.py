@@ -58,6 +58,11 @@ if which in ("all", "cca"):
     probe_cca(784, 784, 1024, 16, "bf16", torch.bfloat16)
     probe_cca(64, 64, 256, 8, "tf32", torch.float32)
     probe_cca(8192, 8192, 4096, 64, "bf16", torch.bfloat16)
+if which == "tf32":
+    probe_cca(64, 64, 256, 8, "bf16", torch.bfloat16)
+    probe_cca(64, 64, 256, 16, "tf32", torch.float32)
+    probe_cca(256, 128, 512, 32, "tf32", torch.float32)
+    probe_cca(8192, 8192, 4096, 64, "tf32", torch.float32)
 if which in ("all", "dense"):
     probe_dense(256, 16, "tf32")
     probe_dense(2048, 128, "tf32")
