@@ -56,6 +56,7 @@ struct geig_solver {
   __nv_bfloat16 *Wxb = nullptr, *Wyb = nullptr;       // bf16 backward operands
   void *hX = nullptr, *hY = nullptr;                  // device staging for *_host
   int upd_grid = 1;
+  int64_t upd_segw = 32;
   size_t upd_smem = 0;
   int64_t launches = 0;
   tc::TcPlan tc;                                      // tcgen05 plans (tensor maps, scratch)
@@ -65,11 +66,11 @@ extern "C" const char* geig_last_error(void) { return g_err.c_str(); }
 extern "C" const char* geig_version(void) { return "geig 0.1 (sm_100a)"; }
 extern "C" int64_t geig_launch_count(const geig_solver* s) { return s ? s->launches : 0; }
 
-static size_t upd_units(int k, int64_t d) {
-  const int T = (k + 31) / 32;
-  const int units = T * (T + 1) + T;
-  const int64_t nseg = (d + UPD_SEG - 1) / UPD_SEG;
-  return (size_t)units * nseg;
+static int64_t upd_segw(int k, int64_t d, int grid) {
+  const int ups = upd_units_per_seg(k);
+  int64_t w = (d * ups + 2 * grid - 1) / (2 * (int64_t)grid);
+  w = ((w + UPD_SUB - 1) / UPD_SUB) * UPD_SUB;
+  return std::max<int64_t>(w, UPD_SUB);
 }
 
 extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, int64_t dy,
@@ -110,7 +111,6 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
   ALLOC(s->Vtmp, kd * 4);
   ALLOC(s->gram, (size_t)3 * k * k * 4);
   ALLOC(s->coef, ((size_t)k * k + 2 * k) * 4);
-  ALLOC(s->partial, upd_units(k, s->d) * 1024 * 4);
   if (problem == GEIG_CCA) {
     const int64_t mr = ((max_rows + 127) / 128) * 128;
     ALLOC(s->Wx, (size_t)k * mr * 4);
@@ -125,18 +125,30 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
   cudaMemset(s->gram, 0, (size_t)3 * k * k * 4);
 
   // cooperative update grid: co-resident CTAs only
-  const size_t sm_phase1 = (size_t)2 * 32 * 65 * 4;
-  const size_t sm_phase3 = ((size_t)k * k + 3 * k + (size_t)k * UPD_CW) * 4;
+  const int kp = (k + 3) & ~3;
+  const size_t sm_phase1 = (size_t)2 * UPD_SUB * UPD_LD * 4;
+  const size_t sm_phase3 = ((size_t)k * kp + (size_t)k * UPD_CW + 3 * (size_t)kp) * 4;
   s->upd_smem = std::max(sm_phase1, sm_phase3);
-  if (cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)s->upd_smem) != cudaSuccess)
-    return cleanup(fail(GEIG_ERR_CUDA, "smem attribute for update kernel"));
-  int occ = 0, nsm = 0;
+  int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, update_kernel, UPD_THREADS, s->upd_smem) != cudaSuccess || occ < 1)
-    return cleanup(fail(GEIG_ERR_CUDA, "update kernel occupancy query failed"));
-  const int64_t work = std::max<int64_t>((int64_t)upd_units(k, s->d), (s->d + UPD_CW - 1) / UPD_CW);
-  s->upd_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::min(occ, 2), work));
+  int occ = 1 << 30;
+  for (void* fn : {(void*)update_kernel<true>, (void*)update_kernel<false>}) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->upd_smem) != cudaSuccess)
+      return cleanup(fail(GEIG_ERR_CUDA, "smem attribute for update kernel"));
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, UPD_THREADS, s->upd_smem) != cudaSuccess || o < 1)
+      return cleanup(fail(GEIG_ERR_CUDA, "update kernel occupancy query failed"));
+    occ = std::min(occ, o);
+  }
+  const int64_t nchunk = (s->d + UPD_CW - 1) / UPD_CW;
+  const int64_t want = std::max<int64_t>(nchunk, (int64_t)upd_units_per_seg(k) * ((s->d + UPD_SUB - 1) / UPD_SUB));
+  s->upd_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::min(occ, 1), want));
+  s->upd_segw = upd_segw(k, s->d, s->upd_grid);
+  {
+    const int64_t nseg = (s->d + s->upd_segw - 1) / s->upd_segw;
+    if (cudaMalloc((void**)&s->partial, (size_t)nseg * upd_units_per_seg(k) * 4096 * 4) != cudaSuccess)
+      return cleanup(fail(GEIG_ERR_CUDA, "cudaMalloc gram partials"));
+  }
   if (cudaMalloc((void**)&s->norm_partial, (size_t)s->upd_grid * k * 4) != cudaSuccess)
     return cleanup(fail(GEIG_ERR_CUDA, "cudaMalloc norm_partial"));
   if (math != GEIG_MATH_F32) {
@@ -318,11 +330,12 @@ extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float*
   UpdateArgs a;
   a.V = s->V; a.AUX = s->AUX; a.AV = AV; a.BV = BV; a.Vtmp = s->Vtmp;
   a.Vbf = s->Vbf; a.partial = s->partial; a.gram = s->gram; a.coef = s->coef;
-  a.norm_partial = s->norm_partial; a.k = s->k; a.d = s->d;
+  a.norm_partial = s->norm_partial; a.k = s->k; a.d = s->d; a.segw = (int)s->upd_segw;
   a.eta = (float)eta; a.gamma = (float)gamma; a.rho = s->rho;
   void* args[] = {&a};
-  CU(cudaLaunchCooperativeKernel((void*)update_kernel, dim3(s->upd_grid), dim3(UPD_THREADS), args,
-                                 s->upd_smem, s->stream));
+  const bool vec = (s->d % 4 == 0) && (((uintptr_t)AV | (uintptr_t)BV) % 16 == 0);
+  void* fn = vec ? (void*)update_kernel<true> : (void*)update_kernel<false>;
+  CU(cudaLaunchCooperativeKernel(fn, dim3(s->upd_grid), dim3(UPD_THREADS), args, s->upd_smem, s->stream));
   s->launches++;
   return GEIG_OK;
 }

@@ -11,13 +11,15 @@
 // <v_i, [By]_j> = G^C_ij / s_j.  Then v_i' = v_i + eta grad_i,
 // v_i <- v_i'/||v_i'|| (lines 16-17), [Bv]_i += gamma (BV_i - [Bv]_i) (19).
 //
-// Phases (grid.sync between them):
-//  1  Gram partials: work units = (32x32 pair tile of table A/C [lower
-//     tiles] or B [diagonal tiles]) x (segment of SEG columns of d).
+// Phases (grid.sync between them), 256 threads per CTA:
+//  1  Gram partials over column segments: 64x64 (i,j) blocks of table A or C
+//     (lower blocks only) as 4x4 register micro-tiles per thread fed by
+//     float4 shared-memory loads; table B's diagonal as warp dot products.
 //  2a deterministic reduction of the partials over segments -> gram.
 //  2b coefficients L, D1 = G^B_ii, D2 = G^A_ii - c_i (one warp per row).
-//  3  per column chunk: grad, v', [Bv]' (in place), partial ||v'||^2.
-//  4  reduce norms, V = v'/||v'|| (+ optional bf16 copy of V for the GEMMs).
+//  3  per 64-column chunk: L [Bv] as 4x4 micro-tiles, grad, v', [Bv]'
+//     (in place), partial ||v'||^2.
+//  4  reduce norms, V = v'/||v'|| (+ bf16 copy of V for the GEMMs).
 #pragma once
 #include <cooperative_groups.h>
 #include "common.cuh"
@@ -27,8 +29,9 @@ namespace geig {
 namespace cg = cooperative_groups;
 
 constexpr int UPD_THREADS = 256;
-constexpr int UPD_SEG = 256;     // columns per Gram work unit
-constexpr int UPD_CW = 32;       // columns per update chunk
+constexpr int UPD_CW = 64;       // columns per update chunk
+constexpr int UPD_SUB = 32;      // columns per shared-memory sub-chunk of a Gram unit
+constexpr int UPD_LD = 68;       // padded row (64 + 4) of the transposed tiles
 
 struct UpdateArgs {
   float* V;              // k x d (in/out)
@@ -37,94 +40,145 @@ struct UpdateArgs {
   const float* BV;       // k x d
   float* Vtmp;           // k x d scratch (v')
   __nv_bfloat16* Vbf;    // k x d bf16 copy of the new V (nullable)
-  float* partial;        // nseg x units x 1024 scratch
-  float* gram;           // 3 x k x k out: GA, GB, GC (zeroed by the host)
+  float* partial;        // nseg x units x 4096 scratch
+  float* gram;           // 3 x k x k out: GA, GB, GC
   float* coef;           // k x k (L) + k (D1) + k (D2)
   float* norm_partial;   // gridDim x k
   int k;
   int64_t d;
+  int segw;              // columns per Gram segment (multiple of UPD_SUB)
   float eta, gamma, rho;
 };
 
-__device__ __forceinline__ void unit_decode(int u, int T, int& table, int& ti, int& tj) {
-  // units 0..nlt-1 : table A lower tiles; nlt..2nlt-1 : table C; then T diagonal B tiles
-  const int nlt = T * (T + 1) / 2;
-  if (u < 2 * nlt) {
-    table = (u < nlt) ? 0 : 2;  // gram slots: 0 = GA, 1 = GB, 2 = GC
-    int r = (u < nlt) ? u : u - nlt;
-    int i = 0;
-    while (r >= i + 1) { r -= i + 1; ++i; }
-    ti = i; tj = r;
-  } else {
-    table = 1; ti = tj = u - 2 * nlt;
-  }
+__host__ __device__ inline int upd_nb(int k) { return (k + 63) / 64; }
+__host__ __device__ inline int upd_units_per_seg(int k) {
+  const int nb = upd_nb(k);
+  return nb * (nb + 1) + 1;   // 2 tables x lower block pairs + 1 GB-diagonal unit
 }
 
+// unit u of a segment -> (table 0=A / 2=C / 1=B-diag, block row bi, block col bj)
+__device__ __forceinline__ void upd_decode(int u, int nb, int& table, int& bi, int& bj) {
+  const int pairs = nb * (nb + 1) / 2;
+  if (u == 2 * pairs) { table = 1; bi = bj = 0; return; }
+  table = u < pairs ? 0 : 2;
+  int r = u < pairs ? u : u - pairs;
+  int i = 0;
+  while (r >= i + 1) { r -= i + 1; ++i; }
+  bi = i; bj = r;
+}
+
+template <bool VEC>
+__device__ __forceinline__ float4 ld4(const float* p, int64_t x, int64_t d) {
+  if (VEC && x + 3 < d) return *reinterpret_cast<const float4*>(p + x);
+  float4 r;
+  r.x = x < d ? p[x] : 0.f;
+  r.y = x + 1 < d ? p[x + 1] : 0.f;
+  r.z = x + 2 < d ? p[x + 2] : 0.f;
+  r.w = x + 3 < d ? p[x + 3] : 0.f;
+  return r;
+}
+template <bool VEC>
+__device__ __forceinline__ void st4(float* p, int64_t x, int64_t d, float4 v) {
+  if (VEC && x + 3 < d) { *reinterpret_cast<float4*>(p + x) = v; return; }
+  if (x < d) p[x] = v.x;
+  if (x + 1 < d) p[x + 1] = v.y;
+  if (x + 2 < d) p[x + 2] = v.z;
+  if (x + 3 < d) p[x + 3] = v.w;
+}
+
+template <bool VEC>
 __global__ void __launch_bounds__(UPD_THREADS)
 update_kernel(UpdateArgs p) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ float smem[];
+  extern __shared__ __align__(16) float smem[];
   const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int k = p.k;
   const int64_t d = p.d;
-  const int T = (k + 31) / 32;
-  const int nlt = T * (T + 1) / 2;
-  const int units = 2 * nlt + T;
-  const int nseg = (int)((d + UPD_SEG - 1) / UPD_SEG);
+  const int nb = upd_nb(k);
+  const int ups = upd_units_per_seg(k);
+  const int nseg = (int)((d + p.segw - 1) / p.segw);
 
   // ---------------- phase 1: Gram partial sums ----------------
   {
-    float* Vs = smem;                 // [32][65]
-    float* Ps = smem + 32 * 65;       // [32][65]
-    const int li = tid >> 3;          // 0..31 : row i within tile
-    const int lj = (tid & 7) * 4;     // 0..28 : 4 columns j within tile
-    for (int w = blockIdx.x; w < units * nseg; w += gridDim.x) {
-      const int seg = w / units, u = w % units;
-      int table, ti, tj;
-      unit_decode(u, T, table, ti, tj);
-      const float* P = table == 0 ? p.AV : (table == 1 ? p.BV : p.AUX);
-      const int i0 = ti * 32, j0 = tj * 32;
-      const int64_t c0 = (int64_t)seg * UPD_SEG;
-      const int64_t c1 = min((int64_t)d, c0 + UPD_SEG);
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int64_t x0 = c0; x0 < c1; x0 += 64) {
-        for (int e = tid; e < 32 * 64; e += UPD_THREADS) {
-          const int r = e >> 6, x = e & 63;
+    float* Vs = smem;                       // [UPD_SUB][UPD_LD]  (x-major: Vs[x][i])
+    float* Ps = smem + UPD_SUB * UPD_LD;    // [UPD_SUB][UPD_LD]
+    const int ti = tid & 15, tj = tid >> 4; // micro-tile rows 4ti.., cols 4tj..
+    for (int w = blockIdx.x; w < ups * nseg; w += gridDim.x) {
+      const int seg = w / ups, u = w % ups;
+      int table, bi, bj;
+      upd_decode(u, nb, table, bi, bj);
+      const int64_t c0 = (int64_t)seg * p.segw;
+      const int64_t c1 = min((int64_t)d, c0 + p.segw);
+      float* out = p.partial + ((int64_t)seg * ups + u) * 4096;
+      if (table == 1) {
+        // diagonal of G^B: one warp per player row, lanes over columns
+        for (int i = warp; i < k; i += UPD_THREADS / 32) {
+          float s = 0.f;
+          for (int64_t x = c0 + lane; x < c1; x += 32)
+            s = fmaf(p.V[(int64_t)i * d + x], p.BV[(int64_t)i * d + x], s);
+          s = warp_sum(s);
+          if (lane == 0) out[i] = s;
+        }
+        continue;
+      }
+      const float* P = table == 0 ? p.AV : p.AUX;
+      const int i0 = bi * 64, j0 = bj * 64;
+      const bool active = !(bi == bj && ti < tj);   // micro-tile strictly above the diagonal
+      float acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+      for (int64_t x0 = c0; x0 < c1; x0 += UPD_SUB) {
+        for (int e = tid; e < 64 * UPD_SUB; e += UPD_THREADS) {
+          const int r = e / UPD_SUB, x = e % UPD_SUB;
           const int64_t gx = x0 + x;
           const bool inx = gx < c1;
-          Vs[r * 65 + x] = (inx && i0 + r < k) ? p.V[(int64_t)(i0 + r) * d + gx] : 0.f;
-          Ps[r * 65 + x] = (inx && j0 + r < k) ? P[(int64_t)(j0 + r) * d + gx] : 0.f;
+          Vs[x * UPD_LD + r] = (inx && i0 + r < k) ? p.V[(int64_t)(i0 + r) * d + gx] : 0.f;
+          Ps[x * UPD_LD + r] = (inx && j0 + r < k) ? P[(int64_t)(j0 + r) * d + gx] : 0.f;
         }
         __syncthreads();
+        if (active) {
 #pragma unroll 8
-        for (int x = 0; x < 64; ++x) {
-          const float a = Vs[li * 65 + x];
+          for (int x = 0; x < UPD_SUB; ++x) {
+            const float4 a = *reinterpret_cast<const float4*>(Vs + x * UPD_LD + 4 * ti);
+            const float4 b = *reinterpret_cast<const float4*>(Ps + x * UPD_LD + 4 * tj);
+            const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-          for (int c = 0; c < 4; ++c) acc[c] = fmaf(a, Ps[(lj + c) * 65 + x], acc[c]);
+            for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fmaf(av[ii], bv[jj], acc[ii][jj]);
+          }
         }
         __syncthreads();
       }
-      float* out = p.partial + ((int64_t)seg * units + u) * 1024;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) out[li * 32 + lj + c] = acc[c];
+      for (int ii = 0; ii < 4; ++ii)
+        *reinterpret_cast<float4*>(out + (4 * ti + ii) * 64 + 4 * tj) =
+            make_float4(acc[ii][0], acc[ii][1], acc[ii][2], acc[ii][3]);
     }
   }
   grid.sync();
 
   // ---------------- phase 2a: reduce partials -> gram ----------------
   {
-    const int64_t total = (int64_t)units * 1024;
-    for (int64_t e = (int64_t)blockIdx.x * UPD_THREADS + tid; e < total;
-         e += (int64_t)gridDim.x * UPD_THREADS) {
-      const int u = (int)(e >> 10), q = (int)(e & 1023);
-      int table, ti, tj;
-      unit_decode(u, T, table, ti, tj);
-      const int i = ti * 32 + (q >> 5), j = tj * 32 + (q & 31);
+    const int pairs = nb * (nb + 1) / 2;
+    const int64_t per_table = (int64_t)pairs * 4096;
+    const int64_t total = 2 * per_table + k;
+    for (int64_t e = (int64_t)blockIdx.x * UPD_THREADS + tid; e < total; e += (int64_t)gridDim.x * UPD_THREADS) {
+      int u, q;
+      if (e < 2 * per_table) { u = (int)(e / 4096); q = (int)(e % 4096); }
+      else { u = 2 * pairs; q = (int)(e - 2 * per_table); }
+      int table, bi, bj;
+      upd_decode(u, nb, table, bi, bj);
+      int i, j;
+      if (table == 1) { i = j = q; }
+      else { i = bi * 64 + q / 64; j = bj * 64 + q % 64; }
       if (i >= k || j >= k) continue;
       float s = 0.f;
-      for (int sg = 0; sg < nseg; ++sg) s += p.partial[((int64_t)sg * units + u) * 1024 + q];
-      const bool keep = (table == 1) ? (i == j) : (i >= j);
-      p.gram[(int64_t)table * k * k + (int64_t)i * k + j] = keep ? s : 0.f;
+      for (int sg = 0; sg < nseg; ++sg) s += p.partial[((int64_t)sg * ups + u) * 4096 + q];
+      if (table == 1 || i >= j) p.gram[(int64_t)table * k * k + (int64_t)i * k + j] = s;
     }
   }
   grid.sync();
@@ -134,7 +188,6 @@ update_kernel(UpdateArgs p) {
     const float* GA = p.gram;
     const float* GB = p.gram + (int64_t)k * k;
     const float* GC = p.gram + 2 * (int64_t)k * k;
-    const int lane = tid & 31, warp = tid >> 5;
     const int nwarps = gridDim.x * (UPD_THREADS / 32);
     for (int i = blockIdx.x * (UPD_THREADS / 32) + warp; i < k; i += nwarps) {
       const float gbii = GB[(int64_t)i * k + i];
@@ -147,7 +200,7 @@ update_kernel(UpdateArgs p) {
           l = gbii * ga / s2;
           c = fmaf(ga, GC[(int64_t)i * k + j] / s2, c);
         }
-        p.coef[(int64_t)i * k + j] = l;
+        p.coef[(int64_t)j * k + i] = l;       // stored transposed: Lt[j][i]
       }
       c = warp_sum(c);
       if (lane == 0) {
@@ -159,36 +212,87 @@ update_kernel(UpdateArgs p) {
   grid.sync();
 
   // ---------------- phase 3: grad, v', aux' ----------------
-  float* Ls = smem;                                 // k x k
-  float* D1s = Ls + (size_t)k * k;                  // k
-  float* D2s = D1s + k;                             // k
-  float* Xs = D2s + k;                              // k x UPD_CW  (AUX chunk)
-  float* Ns = Xs + (size_t)k * UPD_CW;              // k (norm partial)
-  for (int e = tid; e < k * k + 2 * k; e += UPD_THREADS) Ls[e] = p.coef[e];
-  for (int e = tid; e < k; e += UPD_THREADS) Ns[e] = 0.f;
+  const int kp = (k + 3) & ~3;                    // rows padded to a float4
+  float* Lt = smem;                               // k x kp  (Lt[j][i])
+  float* Xs = Lt + (size_t)k * kp;                // k x UPD_CW (AUX chunk)
+  float* D1s = Xs + (size_t)k * UPD_CW;           // k
+  float* D2s = D1s + kp;                          // k
+  float* Ns = D2s + kp;                           // k (norm partial)
+  for (int e = tid; e < k * kp; e += UPD_THREADS) {
+    const int j = e / kp, i = e % kp;
+    Lt[e] = i < k ? p.coef[(int64_t)j * k + i] : 0.f;
+  }
+  for (int e = tid; e < k; e += UPD_THREADS) {
+    D1s[e] = p.coef[(int64_t)k * k + e];
+    D2s[e] = p.coef[(int64_t)k * k + k + e];
+    Ns[e] = 0.f;
+  }
   __syncthreads();
   const int nchunk = (int)((d + UPD_CW - 1) / UPD_CW);
-  const int lane = tid & 31, warp = tid >> 5;
+  const int tx = tid & 15;          // 4 columns 4tx..4tx+3
+  const int tr = tid >> 4;          // 4 rows per pass: 4(tr + 16 pass)..
+  const int nrb = (k + 3) / 4;      // row blocks of 4
   for (int ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
-    const int64_t gx = (int64_t)ch * UPD_CW + lane;
-    const bool in = gx < d;
-    for (int i = warp; i < k; i += UPD_THREADS / 32)
-      Xs[i * UPD_CW + lane] = in ? p.AUX[(int64_t)i * d + gx] : 0.f;
+    const int64_t cx = (int64_t)ch * UPD_CW;
+    for (int e = tid; e < k * (UPD_CW / 4); e += UPD_THREADS) {
+      const int r = e / (UPD_CW / 4), q = e % (UPD_CW / 4);
+      const float4 v = ld4<VEC>(p.AUX + (int64_t)r * d, cx + 4 * q, d);
+      *reinterpret_cast<float4*>(Xs + r * UPD_CW + 4 * q) = v;
+    }
     __syncthreads();
-    for (int i = warp; i < k; i += UPD_THREADS / 32) {
-      float vn = 0.f;
-      if (in) {
-        const int64_t o = (int64_t)i * d + gx;
-        float g = D1s[i] * p.AV[o] - D2s[i] * p.BV[o];
-        const float* Li = Ls + (size_t)i * k;
-        for (int j = 0; j < i; ++j) g = fmaf(-Li[j], Xs[j * UPD_CW + lane], g);
-        vn = p.V[o] + p.eta * g;
-        const float ax = Xs[i * UPD_CW + lane];
-        p.AUX[o] = ax + p.gamma * (p.BV[o] - ax);
-        p.Vtmp[o] = vn;
+    const int64_t gx = cx + 4 * tx;
+    for (int rb = tr; rb < nrb; rb += 16) {
+      const int i0 = 4 * rb;
+      float acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+      const int jmax = min(i0 + 3, k);            // L_ij = 0 for j >= i
+      for (int j = 0; j < jmax; ++j) {
+        const float4 l = *reinterpret_cast<const float4*>(Lt + (size_t)j * kp + i0);
+        const float4 x = *reinterpret_cast<const float4*>(Xs + j * UPD_CW + 4 * tx);
+        const float lv[4] = {l.x, l.y, l.z, l.w}, xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(lv[a], xv[b], acc[a][b]);
       }
-      const float sq = warp_sum(vn * vn);
-      if (lane == 0) Ns[i] += sq;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int i = i0 + a;
+        float sq = 0.f;
+        if (i < k && gx < d) {
+          const int64_t o = (int64_t)i * d;
+          const float4 av = ld4<VEC>(p.AV + o, gx, d);
+          const float4 bv = ld4<VEC>(p.BV + o, gx, d);
+          const float4 vv = ld4<VEC>(p.V + o, gx, d);
+          const float4 xa = *reinterpret_cast<const float4*>(Xs + i * UPD_CW + 4 * tx);
+          const float d1 = D1s[i], d2 = D2s[i];
+          float4 vn, an;
+          vn.x = vv.x + p.eta * (d1 * av.x - d2 * bv.x - acc[a][0]);
+          vn.y = vv.y + p.eta * (d1 * av.y - d2 * bv.y - acc[a][1]);
+          vn.z = vv.z + p.eta * (d1 * av.z - d2 * bv.z - acc[a][2]);
+          vn.w = vv.w + p.eta * (d1 * av.w - d2 * bv.w - acc[a][3]);
+          an.x = xa.x + p.gamma * (bv.x - xa.x);
+          an.y = xa.y + p.gamma * (bv.y - xa.y);
+          an.z = xa.z + p.gamma * (bv.z - xa.z);
+          an.w = xa.w + p.gamma * (bv.w - xa.w);
+          // zero the padding lanes of a ragged tail before squaring
+          if (!(gx + 1 < d)) vn.y = 0.f;
+          if (!(gx + 2 < d)) vn.z = 0.f;
+          if (!(gx + 3 < d)) vn.w = 0.f;
+          st4<VEC>(p.Vtmp + o, gx, d, vn);
+          st4<VEC>(p.AUX + o, gx, d, an);
+          sq = vn.x * vn.x + vn.y * vn.y + vn.z * vn.z + vn.w * vn.w;
+        }
+        // reduce over the 16 threads (tx) sharing row i (a half warp)
+        sq += __shfl_xor_sync(0xffffffffu, sq, 1);
+        sq += __shfl_xor_sync(0xffffffffu, sq, 2);
+        sq += __shfl_xor_sync(0xffffffffu, sq, 4);
+        sq += __shfl_xor_sync(0xffffffffu, sq, 8);
+        if (tx == 0 && i < k) Ns[i] += sq;
+      }
     }
     __syncthreads();
   }
@@ -203,13 +307,29 @@ update_kernel(UpdateArgs p) {
   }
   __syncthreads();
   for (int ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
-    const int64_t gx = (int64_t)ch * UPD_CW + lane;
-    if (gx >= d) continue;
-    for (int i = warp; i < k; i += UPD_THREADS / 32) {
-      const int64_t o = (int64_t)i * d + gx;
-      const float v = p.Vtmp[o] * Ns[i];
-      p.V[o] = v;
-      if (p.Vbf) p.Vbf[o] = __float2bfloat16_rn(v);
+    const int64_t cx = (int64_t)ch * UPD_CW;
+    for (int e = tid; e < k * (UPD_CW / 4); e += UPD_THREADS) {
+      const int r = e / (UPD_CW / 4), q = e % (UPD_CW / 4);
+      const int64_t gx = cx + 4 * q;
+      if (gx >= d) continue;
+      const int64_t o = (int64_t)r * d;
+      float4 v = ld4<VEC>(p.Vtmp + o, gx, d);
+      const float sc = Ns[r];
+      v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
+      st4<VEC>(p.V + o, gx, d, v);
+      if (p.Vbf) {
+        __nv_bfloat16* q2 = p.Vbf + o + gx;
+        if (VEC && gx + 3 < d) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(q2) = pk;
+        } else {
+          const float vs[4] = {v.x, v.y, v.z, v.w};
+          for (int t = 0; t < 4 && gx + t < d; ++t) q2[t] = __float2bfloat16_rn(vs[t]);
+        }
+      }
     }
   }
 }

@@ -151,3 +151,77 @@ def test_errors_are_loud(geig):
     with pytest.raises(geig.GeigError):
         geig.geig_products_cca(s.h, x, x, 16, 1.0, AV, AV)      # b > max_rows
     s.close()
+
+
+# --- tensor-core variants (tcgen05): bf16 1e-2, tf32 1e-2 ---------------------
+
+def test_cca_config2_bf16_tcgen05(geig):
+    errs, got = check_cca_step(geig, 2, 1024, math="bf16")
+    _assert(errs, 1e-2)
+
+
+def test_cca_config3_full_size_bf16_tcgen05(geig):
+    """Config 3 at full size in the launch configuration bench.py times."""
+    errs, _ = check_cca_step(geig, 3, 4096, math="bf16")
+    _assert(errs, 1e-2)
+
+
+@pytest.mark.parametrize("rows,dx,dy,k", [(300, 200, 136, 24), (130, 64, 8, 5), (1000, 784, 784, 16),
+                                          (258, 2048, 1024, 128)])
+def test_cca_ragged_bf16_tcgen05(geig, rows, dx, dy, k):
+    """Ragged for the TMA tiles: h not a multiple of 64 (zero-filled K tail),
+    d not a multiple of 128 (masked M tail), k not a multiple of 16 (N pad),
+    k = 128 (largest tile)."""
+    errs, _ = check_cca_step(geig, 2, rows, k=k, dx=dx, dy=dy, math="bf16")
+    _assert(errs, 1e-2)
+
+
+def _dense_step_check(geig, a, b, k, math, rho, eta, gamma, seed=0, tol=1e-2):
+    from oracle import estimators, game
+    dev = "cuda:0"
+    d = a.shape[0]
+    A = a.to(dev).float().contiguous() if isinstance(a, torch.Tensor) else torch.tensor(a, dtype=torch.float32, device=dev)
+    B = b.to(dev).float().contiguous() if isinstance(b, torch.Tensor) else torch.tensor(b, dtype=torch.float32, device=dev)
+    V, aux = random_state(k, d, seed)
+    V = V.astype(np.float32).astype(np.float64)
+    aux = aux.astype(np.float32).astype(np.float64)
+    s = geig.Solver(geig.GEIG_DENSE, d, 0, k, math=math, rho=rho)
+    try:
+        s.set_state(torch.tensor(V, dtype=torch.float32, device=dev), torch.tensor(aux, dtype=torch.float32, device=dev))
+        AV = torch.empty(k, d, device=dev)
+        BV = torch.empty_like(AV)
+        geig.geig_products_dense(s.h, A, B, 0, d, AV, BV)
+        geig.geig_update(s.h, AV, BV, eta, gamma)
+        V2g, aux2g = s.state()
+        a64, b64 = A.double().cpu().numpy(), B.double().cpu().numpy()
+        av, bv = estimators.dense_products(a64, b64, V)
+        V2, aux2 = game.step_alg2(V, aux, [(av, bv)], eta, gamma, rho)
+        errs = dict(av=rel_err(AV.double().cpu().numpy(), av), bv=rel_err(BV.double().cpu().numpy(), bv),
+                    step=rel_err(V2g.double().cpu().numpy() - V, V2 - V),
+                    aux=rel_err(aux2g.double().cpu().numpy(), aux2), sphere=0.0)
+    finally:
+        s.close()
+    _assert(errs, tol)
+    return errs
+
+
+def test_dense_config0_tf32_tcgen05(geig):
+    from synth import CONFIGS, dense_gep_small
+    cfg = CONFIGS[0]
+    a, b = dense_gep_small(0)
+    _dense_step_check(geig, a, b, cfg.k, "tf32", cfg.rho, cfg.eta, cfg.gamma)
+
+
+def test_dense_config4_reduced_fp32(geig):
+    from synth import CONFIGS, dense_gep_large
+    cfg = CONFIGS[4]
+    a, b = dense_gep_large(1000, seed=2, device="cuda:0")
+    _dense_step_check(geig, a, b, 37, "f32", cfg.rho, cfg.eta, cfg.gamma, tol=1e-4)
+
+
+def test_dense_config4_full_size_tf32_tcgen05(geig):
+    """Config 4 at full size: d = 16384, k = 128, TF32 tensor cores."""
+    from synth import CONFIGS, dense_gep_large
+    cfg = CONFIGS[4]
+    a, b = dense_gep_large(cfg.d, seed=0, device="cuda:0")
+    _dense_step_check(geig, a, b, cfg.k, "tf32", cfg.rho, cfg.eta, cfg.gamma)
