@@ -127,7 +127,7 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
   // cooperative update grid: co-resident CTAs only
   const int kp = (k + 3) & ~3;
   const size_t sm_phase1 = (size_t)2 * UPD_SUB * UPD_LD * 4;
-  const size_t sm_phase3 = ((size_t)k * kp + (size_t)k * UPD_CW + 3 * (size_t)kp) * 4;
+  const size_t sm_phase3 = ((size_t)k * kp + (size_t)k * UPD_CW + 3 * (size_t)kp + 256) * 4;
   s->upd_smem = std::max(sm_phase1, sm_phase3);
   int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);

@@ -162,23 +162,48 @@ update_kernel(UpdateArgs p) {
   grid.sync();
 
   // ---------------- phase 2a: reduce partials -> gram ----------------
+  // 32 consecutive entries per CTA iteration (lanes), the 8 warps split the
+  // segments, fixed-order combine through shared memory (deterministic).
   {
+    float* red = smem;                       // [8][32]
     const int pairs = nb * (nb + 1) / 2;
     const int64_t per_table = (int64_t)pairs * 4096;
     const int64_t total = 2 * per_table + k;
-    for (int64_t e = (int64_t)blockIdx.x * UPD_THREADS + tid; e < total; e += (int64_t)gridDim.x * UPD_THREADS) {
-      int u, q;
-      if (e < 2 * per_table) { u = (int)(e / 4096); q = (int)(e % 4096); }
-      else { u = 2 * pairs; q = (int)(e - 2 * per_table); }
-      int table, bi, bj;
-      upd_decode(u, nb, table, bi, bj);
-      int i, j;
-      if (table == 1) { i = j = q; }
-      else { i = bi * 64 + q / 64; j = bj * 64 + q % 64; }
-      if (i >= k || j >= k) continue;
-      float s = 0.f;
-      for (int sg = 0; sg < nseg; ++sg) s += p.partial[((int64_t)sg * ups + u) * 4096 + q];
-      if (table == 1 || i >= j) p.gram[(int64_t)table * k * k + (int64_t)i * k + j] = s;
+    const int64_t ngroups = (total + 31) / 32;
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+      const int64_t e = grp * 32 + lane;
+      int u = 0, q = 0;
+      const bool ok = e < total;
+      if (ok) {
+        if (e < 2 * per_table) { u = (int)(e / 4096); q = (int)(e % 4096); }
+        else { u = 2 * pairs; q = (int)(e - 2 * per_table); }
+      }
+      float s0 = 0.f, s1 = 0.f;
+      if (ok) {
+        const float* src = p.partial + (int64_t)u * 4096 + q;
+        const int64_t stride = (int64_t)ups * 4096;
+        int sg = warp;
+        for (; sg + 8 < nseg; sg += 16) {
+          s0 += src[(int64_t)sg * stride];
+          s1 += src[(int64_t)(sg + 8) * stride];
+        }
+        if (sg < nseg) s0 += src[(int64_t)sg * stride];
+      }
+      red[warp * 32 + lane] = s0 + s1;
+      __syncthreads();
+      if (warp == 0 && ok) {
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s += red[w * 32 + lane];
+        int table, bi, bj;
+        upd_decode(u, nb, table, bi, bj);
+        int i, j;
+        if (table == 1) { i = j = q; }
+        else { i = bi * 64 + q / 64; j = bj * 64 + q % 64; }
+        if (i < k && j < k && (table == 1 || i >= j))
+          p.gram[(int64_t)table * k * k + (int64_t)i * k + j] = s;
+      }
+      __syncthreads();
     }
   }
   grid.sync();
@@ -213,11 +238,12 @@ update_kernel(UpdateArgs p) {
 
   // ---------------- phase 3: grad, v', aux' ----------------
   const int kp = (k + 3) & ~3;                    // rows padded to a float4
-  float* Lt = smem;                               // k x kp  (Lt[j][i])
+  float* Ns = smem;                               // kp (norm partial)
+  float* red4 = Ns + kp;                          // 256 (phase-4 reduction scratch)
+  float* Lt = red4 + 256;                         // k x kp  (Lt[j][i])
   float* Xs = Lt + (size_t)k * kp;                // k x UPD_CW (AUX chunk)
   float* D1s = Xs + (size_t)k * UPD_CW;           // k
   float* D2s = D1s + kp;                          // k
-  float* Ns = D2s + kp;                           // k (norm partial)
   for (int e = tid; e < k * kp; e += UPD_THREADS) {
     const int j = e / kp, i = e % kp;
     Lt[e] = i < k ? p.coef[(int64_t)j * k + i] : 0.f;
@@ -241,14 +267,15 @@ update_kernel(UpdateArgs p) {
     }
     __syncthreads();
     const int64_t gx = cx + 4 * tx;
-    for (int rb = tr; rb < nrb; rb += 16) {
+    for (int rb0 = 0; rb0 < nrb; rb0 += 16) {
+      const int rb = rb0 + tr;               // every lane iterates (full-warp shuffles below)
       const int i0 = 4 * rb;
       float acc[4][4];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
-      const int jmax = min(i0 + 3, k);            // L_ij = 0 for j >= i
+      const int jmax = rb < nrb ? min(i0 + 3, k) : 0;   // L_ij = 0 for j >= i
       for (int j = 0; j < jmax; ++j) {
         const float4 l = *reinterpret_cast<const float4*>(Lt + (size_t)j * kp + i0);
         const float4 x = *reinterpret_cast<const float4*>(Xs + j * UPD_CW + 4 * tx);
@@ -300,12 +327,32 @@ update_kernel(UpdateArgs p) {
   grid.sync();
 
   // ---------------- phase 4: retraction v <- v'/||v'|| ----------------
-  for (int i = tid; i < k; i += UPD_THREADS) {
-    float s = 0.f;
-    for (int b = 0; b < (int)gridDim.x; ++b) s += p.norm_partial[(int64_t)b * k + i];
-    Ns[i] = rsqrtf(s);
+  // every CTA reduces the per-CTA norm partials: lanes over rows i, warps
+  // over the partial index, fixed-order combine (deterministic).
+  {
+    float* red = red4;                        // [8][32]
+    for (int i0 = 0; i0 < k; i0 += 32) {
+      const int i = i0 + lane;
+      float s0 = 0.f, s1 = 0.f;
+      if (i < k) {
+        int b = warp;
+        for (; b + 8 < (int)gridDim.x; b += 16) {
+          s0 += p.norm_partial[(int64_t)b * k + i];
+          s1 += p.norm_partial[(int64_t)(b + 8) * k + i];
+        }
+        if (b < (int)gridDim.x) s0 += p.norm_partial[(int64_t)b * k + i];
+      }
+      red[warp * 32 + lane] = s0 + s1;
+      __syncthreads();
+      if (warp == 0 && i < k) {
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s += red[w * 32 + lane];
+        Ns[i] = rsqrtf(s);
+      }
+      __syncthreads();
+    }
   }
-  __syncthreads();
   for (int ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
     const int64_t cx = (int64_t)ch * UPD_CW;
     for (int e = tid; e < k * (UPD_CW / 4); e += UPD_THREADS) {
