@@ -66,13 +66,6 @@ extern "C" const char* geig_last_error(void) { return g_err.c_str(); }
 extern "C" const char* geig_version(void) { return "geig 0.1 (sm_100a)"; }
 extern "C" int64_t geig_launch_count(const geig_solver* s) { return s ? s->launches : 0; }
 
-static int64_t upd_segw(int k, int64_t d, int grid) {
-  const int ups = upd_units_per_seg(k);
-  int64_t w = (d * ups + 2 * grid - 1) / (2 * (int64_t)grid);
-  w = ((w + UPD_SUB - 1) / UPD_SUB) * UPD_SUB;
-  return std::max<int64_t>(w, UPD_SUB);
-}
-
 extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, int64_t dy,
                                    int32_t k, int math, int data_dtype, double rho,
                                    int64_t max_rows, int device) {
@@ -124,29 +117,30 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
   cudaMemset(s->Vbf, 0, kd * 2);
   cudaMemset(s->gram, 0, (size_t)3 * k * k * 4);
 
-  // cooperative update grid: co-resident CTAs only
-  const int kp = (k + 3) & ~3;
-  const size_t sm_phase1 = (size_t)2 * UPD_SUB * UPD_LD * 4;
-  const size_t sm_phase3 = ((size_t)k * kp + (size_t)k * UPD_CW + 3 * (size_t)kp + 256) * 4;
-  s->upd_smem = std::max(sm_phase1, sm_phase3);
-  int nsm = 0;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-  int occ = 1 << 30;
-  for (void* fn : {(void*)update_kernel<true>, (void*)update_kernel<false>}) {
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->upd_smem) != cudaSuccess)
-      return cleanup(fail(GEIG_ERR_CUDA, "smem attribute for update kernel"));
-    int o = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, UPD_THREADS, s->upd_smem) != cudaSuccess || o < 1)
-      return cleanup(fail(GEIG_ERR_CUDA, "update kernel occupancy query failed"));
-    occ = std::min(occ, o);
-  }
-  const int64_t nchunk = (s->d + UPD_CW - 1) / UPD_CW;
-  const int64_t want = std::max<int64_t>(nchunk, (int64_t)upd_units_per_seg(k) * ((s->d + UPD_SUB - 1) / UPD_SUB));
-  s->upd_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::min(occ, 1), want));
-  s->upd_segw = upd_segw(k, s->d, s->upd_grid);
+  // cooperative update grid: one co-resident CTA per SM, contiguous column ranges
   {
-    const int64_t nseg = (s->d + s->upd_segw - 1) / s->upd_segw;
-    if (cudaMalloc((void**)&s->partial, (size_t)nseg * upd_units_per_seg(k) * 4096 * 4) != cudaSuccess)
+    const int NB = k <= 64 ? 1 : 2;
+    s->upd_smem = upd_smem_floats(NB) * 4;
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    void* fns[2] = {NB == 1 ? (void*)update_kernel<1, true> : (void*)update_kernel<2, true>,
+                    NB == 1 ? (void*)update_kernel<1, false> : (void*)update_kernel<2, false>};
+    for (void* fn : fns) {
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->upd_smem) != cudaSuccess)
+        return cleanup(fail(GEIG_ERR_CUDA, "smem attribute for update kernel"));
+      int o = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, UPD_THREADS, s->upd_smem) != cudaSuccess || o < 1)
+        return cleanup(fail(GEIG_ERR_CUDA, "update kernel cannot be co-resident"));
+    }
+    int64_t G = std::min<int64_t>(nsm, (s->d + UPD_XC - 1) / UPD_XC);
+    G = std::max<int64_t>(G, 1);
+    int64_t segw = (s->d + G - 1) / G;
+    segw = ((segw + 3) / 4) * 4;
+    G = (s->d + segw - 1) / segw;
+    s->upd_grid = (int)G;
+    s->upd_segw = segw;
+    const int KP = NB * 64;
+    if (cudaMalloc((void**)&s->partial, (size_t)G * (2 * KP * KP + KP) * 4) != cudaSuccess)
       return cleanup(fail(GEIG_ERR_CUDA, "cudaMalloc gram partials"));
   }
   if (cudaMalloc((void**)&s->norm_partial, (size_t)s->upd_grid * k * 4) != cudaSuccess)
@@ -330,11 +324,13 @@ extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float*
   UpdateArgs a;
   a.V = s->V; a.AUX = s->AUX; a.AV = AV; a.BV = BV; a.Vtmp = s->Vtmp;
   a.Vbf = s->Vbf; a.partial = s->partial; a.gram = s->gram; a.coef = s->coef;
-  a.norm_partial = s->norm_partial; a.k = s->k; a.d = s->d; a.segw = (int)s->upd_segw;
+  a.norm_partial = s->norm_partial; a.k = s->k; a.d = s->d; a.segw = s->upd_segw;
   a.eta = (float)eta; a.gamma = (float)gamma; a.rho = s->rho;
   void* args[] = {&a};
   const bool vec = (s->d % 4 == 0) && (((uintptr_t)AV | (uintptr_t)BV) % 16 == 0);
-  void* fn = vec ? (void*)update_kernel<true> : (void*)update_kernel<false>;
+  void* fn;
+  if (s->k <= 64) fn = vec ? (void*)update_kernel<1, true> : (void*)update_kernel<1, false>;
+  else fn = vec ? (void*)update_kernel<2, true> : (void*)update_kernel<2, false>;
   CU(cudaLaunchCooperativeKernel(fn, dim3(s->upd_grid), dim3(UPD_THREADS), args, s->upd_smem, s->stream));
   s->launches++;
   return GEIG_OK;

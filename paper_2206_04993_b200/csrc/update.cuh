@@ -11,15 +11,18 @@
 // <v_i, [By]_j> = G^C_ij / s_j.  Then v_i' = v_i + eta grad_i,
 // v_i <- v_i'/||v_i'|| (lines 16-17), [Bv]_i += gamma (BV_i - [Bv]_i) (19).
 //
-// Phases (grid.sync between them), 256 threads per CTA:
-//  1  Gram partials over column segments: 64x64 (i,j) blocks of table A or C
-//     (lower blocks only) as 4x4 register micro-tiles per thread fed by
-//     float4 shared-memory loads; table B's diagonal as warp dot products.
-//  2a deterministic reduction of the partials over segments -> gram.
-//  2b coefficients L, D1 = G^B_ii, D2 = G^A_ii - c_i (one warp per row).
-//  3  per 64-column chunk: L [Bv] as 4x4 micro-tiles, grad, v', [Bv]'
-//     (in place), partial ||v'||^2.
-//  4  reduce norms, V = v'/||v'|| (+ bf16 copy of V for the GEMMs).
+// One CTA (256 threads) per SM owns a contiguous column range of d; the
+// four k x range tiles (V, AV, [Bv], BV) stream through shared memory in
+// 32-column sub-chunks with double-buffered cp.async (16-byte, zero-fill
+// past the range).  Phases (grid.sync between them):
+//  1  per-CTA Gram partials: G^A, G^C as 4x4 register micro-tiles per
+//     thread (rows t, t+16, t+32, t+48 of each 64-row block: conflict-free
+//     LDS.128 with a 36-float row stride), lower 64-blocks only; diag G^B.
+//  2a deterministic reduction of the per-CTA partials -> gram.
+//  2b coefficients L (stored transposed), D1 = G^B_ii, D2 = G^A_ii - c_i.
+//  3  stream the tiles again: L [Bv] micro-tiles, grad, v' (to scratch),
+//     [Bv]' (to the state), per-CTA ||v'||^2 partials.
+//  4  reduce the norms, V = v'/||v'|| (+ bf16 copy of V for the GEMMs).
 #pragma once
 #include <cooperative_groups.h>
 #include "common.cuh"
@@ -29,9 +32,8 @@ namespace geig {
 namespace cg = cooperative_groups;
 
 constexpr int UPD_THREADS = 256;
-constexpr int UPD_CW = 64;       // columns per update chunk
-constexpr int UPD_SUB = 32;      // columns per shared-memory sub-chunk of a Gram unit
-constexpr int UPD_LD = 68;       // padded row (64 + 4) of the transposed tiles
+constexpr int UPD_XC = 32;             // columns per sub-chunk
+constexpr int UPD_S = UPD_XC + 4;      // smem row stride (36 == 4 mod 32)
 
 struct UpdateArgs {
   float* V;              // k x d (in/out)
@@ -40,168 +42,200 @@ struct UpdateArgs {
   const float* BV;       // k x d
   float* Vtmp;           // k x d scratch (v')
   __nv_bfloat16* Vbf;    // k x d bf16 copy of the new V (nullable)
-  float* partial;        // nseg x units x 4096 scratch
-  float* gram;           // 3 x k x k out: GA, GB, GC
-  float* coef;           // k x k (L) + k (D1) + k (D2)
+  float* partial;        // gridDim x (2*KP*KP + KP) scratch
+  float* gram;           // 3 x k x k out: GA, GB, GC (zeroed by the host)
+  float* coef;           // k x k (Lt, transposed L) + k (D1) + k (D2)
   float* norm_partial;   // gridDim x k
   int k;
   int64_t d;
-  int segw;              // columns per Gram segment (multiple of UPD_SUB)
+  int64_t segw;          // columns per CTA (multiple of 4)
   float eta, gamma, rho;
 };
 
-__host__ __device__ inline int upd_nb(int k) { return (k + 63) / 64; }
-__host__ __device__ inline int upd_units_per_seg(int k) {
-  const int nb = upd_nb(k);
-  return nb * (nb + 1) + 1;   // 2 tables x lower block pairs + 1 GB-diagonal unit
+__host__ __device__ constexpr size_t upd_smem_floats(int NB) {
+  // phase 1/3 double buffer of 4 tiles + phase-3 Lt + D1 + D2 + Ns + red
+  return (size_t)2 * 4 * (NB * 64) * UPD_S + (size_t)(NB * 64) * (NB * 64) + 3 * (NB * 64) + 256;
 }
 
-// unit u of a segment -> (table 0=A / 2=C / 1=B-diag, block row bi, block col bj)
-__device__ __forceinline__ void upd_decode(int u, int nb, int& table, int& bi, int& bj) {
-  const int pairs = nb * (nb + 1) / 2;
-  if (u == 2 * pairs) { table = 1; bi = bj = 0; return; }
-  table = u < pairs ? 0 : 2;
-  int r = u < pairs ? u : u - pairs;
-  int i = 0;
-  while (r >= i + 1) { r -= i + 1; ++i; }
-  bi = i; bj = r;
+__device__ __forceinline__ void cp_async16(float* dst, const float* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Stage rows [0, KP) x columns [x0, x0+32) of the four k x d arrays into
+// tiles[4][KP][UPD_S]; rows >= k and columns >= xend are zero-filled.
+template <int KP, bool VEC>
+__device__ __forceinline__ void stage_tiles(float* tiles, const float* const* src, int k, int64_t d, int64_t x0,
+                                            int64_t xend) {
+  if (VEC) {
+    constexpr int Q = UPD_XC / 4;                 // float4 per row
+    for (int e = threadIdx.x; e < 4 * KP * Q; e += UPD_THREADS) {
+      const int a = e / (KP * Q), rem = e % (KP * Q), r = rem / Q, q = rem % Q;
+      const int64_t gx = x0 + 4 * q;
+      const bool ok = r < k && gx < xend;
+      const float* s = ok ? src[a] + (int64_t)r * d + gx : src[a];
+      cp_async16(tiles + ((size_t)a * KP + r) * UPD_S + 4 * q, s, ok ? 16 : 0);
+    }
+  } else {
+    for (int e = threadIdx.x; e < 4 * KP * UPD_XC; e += UPD_THREADS) {
+      const int a = e / (KP * UPD_XC), rem = e % (KP * UPD_XC), r = rem / UPD_XC, x = rem % UPD_XC;
+      const int64_t gx = x0 + x;
+      const bool ok = r < k && gx < xend;
+      const float* s = ok ? src[a] + (int64_t)r * d + gx : src[a];
+      cp_async4(tiles + ((size_t)a * KP + r) * UPD_S + x, s, ok ? 4 : 0);
+    }
+  }
 }
 
-template <bool VEC>
-__device__ __forceinline__ float4 ld4(const float* p, int64_t x, int64_t d) {
-  if (VEC && x + 3 < d) return *reinterpret_cast<const float4*>(p + x);
-  float4 r;
-  r.x = x < d ? p[x] : 0.f;
-  r.y = x + 1 < d ? p[x + 1] : 0.f;
-  r.z = x + 2 < d ? p[x + 2] : 0.f;
-  r.w = x + 3 < d ? p[x + 3] : 0.f;
-  return r;
-}
-template <bool VEC>
-__device__ __forceinline__ void st4(float* p, int64_t x, int64_t d, float4 v) {
-  if (VEC && x + 3 < d) { *reinterpret_cast<float4*>(p + x) = v; return; }
-  if (x < d) p[x] = v.x;
-  if (x + 1 < d) p[x + 1] = v.y;
-  if (x + 2 < d) p[x + 2] = v.z;
-  if (x + 3 < d) p[x + 3] = v.w;
-}
-
-template <bool VEC>
-__global__ void __launch_bounds__(UPD_THREADS)
+template <int NB, bool VEC>
+__global__ void __launch_bounds__(UPD_THREADS, 1)
 update_kernel(UpdateArgs p) {
+  constexpr int KP = NB * 64;
+  constexpr int TILE = KP * UPD_S;               // floats per array tile
+  constexpr int NPAIR = NB * (NB + 1) / 2;       // lower 64-block pairs
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) float smem[];
+  float* buf0 = smem;                            // [4][KP][UPD_S]
+  float* buf1 = smem + 4 * TILE;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int k = p.k;
   const int64_t d = p.d;
-  const int nb = upd_nb(k);
-  const int ups = upd_units_per_seg(k);
-  const int nseg = (int)((d + p.segw - 1) / p.segw);
+  const int64_t c0 = (int64_t)blockIdx.x * p.segw;
+  const int64_t c1 = min(d, c0 + p.segw);
+  const int nsub = c1 > c0 ? (int)((c1 - c0 + UPD_XC - 1) / UPD_XC) : 0;
+  const float* src[4] = {p.V, p.AV, p.AUX, p.BV};   // tile order: 0 V, 1 AV, 2 AUX, 3 BV
 
-  // ---------------- phase 1: Gram partial sums ----------------
+  // ---------------- phase 1: Gram partial sums of this CTA's columns ----------------
   {
-    float* Vs = smem;                       // [UPD_SUB][UPD_LD]  (x-major: Vs[x][i])
-    float* Ps = smem + UPD_SUB * UPD_LD;    // [UPD_SUB][UPD_LD]
-    const int ti = tid & 15, tj = tid >> 4; // micro-tile rows 4ti.., cols 4tj..
-    for (int w = blockIdx.x; w < ups * nseg; w += gridDim.x) {
-      const int seg = w / ups, u = w % ups;
-      int table, bi, bj;
-      upd_decode(u, nb, table, bi, bj);
-      const int64_t c0 = (int64_t)seg * p.segw;
-      const int64_t c1 = min((int64_t)d, c0 + p.segw);
-      float* out = p.partial + ((int64_t)seg * ups + u) * 4096;
-      if (table == 1) {
-        // diagonal of G^B: one warp per player row, lanes over columns
-        for (int i = warp; i < k; i += UPD_THREADS / 32) {
-          float s = 0.f;
-          for (int64_t x = c0 + lane; x < c1; x += 32)
-            s = fmaf(p.V[(int64_t)i * d + x], p.BV[(int64_t)i * d + x], s);
-          s = warp_sum(s);
-          if (lane == 0) out[i] = s;
-        }
-        continue;
-      }
-      const float* P = table == 0 ? p.AV : p.AUX;
-      const int i0 = bi * 64, j0 = bj * 64;
-      const bool active = !(bi == bj && ti < tj);   // micro-tile strictly above the diagonal
-      float acc[4][4];
+    const int ti = tid & 15, tj = tid >> 4;
+    float accA[NPAIR][4][4], accC[NPAIR][4][4];
+#pragma unroll
+    for (int pr = 0; pr < NPAIR; ++pr)
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
-      for (int64_t x0 = c0; x0 < c1; x0 += UPD_SUB) {
-        for (int e = tid; e < 64 * UPD_SUB; e += UPD_THREADS) {
-          const int r = e / UPD_SUB, x = e % UPD_SUB;
-          const int64_t gx = x0 + x;
-          const bool inx = gx < c1;
-          Vs[x * UPD_LD + r] = (inx && i0 + r < k) ? p.V[(int64_t)(i0 + r) * d + gx] : 0.f;
-          Ps[x * UPD_LD + r] = (inx && j0 + r < k) ? P[(int64_t)(j0 + r) * d + gx] : 0.f;
-        }
-        __syncthreads();
-        if (active) {
-#pragma unroll 8
-          for (int x = 0; x < UPD_SUB; ++x) {
-            const float4 a = *reinterpret_cast<const float4*>(Vs + x * UPD_LD + 4 * ti);
-            const float4 b = *reinterpret_cast<const float4*>(Ps + x * UPD_LD + 4 * tj);
-            const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+        for (int b = 0; b < 4; ++b) accA[pr][a][b] = accC[pr][a][b] = 0.f;
+    float gb[KP / 8];
 #pragma unroll
-            for (int ii = 0; ii < 4; ++ii)
+    for (int q = 0; q < KP / 8; ++q) gb[q] = 0.f;
+
+    if (nsub > 0) { stage_tiles<KP, VEC>(buf0, src, k, d, c0, c1); }
+    cp_async_commit();
+    for (int sc = 0; sc < nsub; ++sc) {
+      float* cur = (sc & 1) ? buf1 : buf0;
+      float* nxt = (sc & 1) ? buf0 : buf1;
+      if (sc + 1 < nsub) stage_tiles<KP, VEC>(nxt, src, k, d, c0 + (int64_t)(sc + 1) * UPD_XC, c1);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncthreads();
+      const float* Vt = cur;
+      const float* At = cur + TILE;
+      const float* Ct = cur + 2 * TILE;
+      const float* Bt = cur + 3 * TILE;
+#pragma unroll 2
+      for (int xq = 0; xq < UPD_XC / 4; ++xq) {
+        int pr = 0;
 #pragma unroll
-              for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = fmaf(av[ii], bv[jj], acc[ii][jj]);
+        for (int bi = 0; bi < NB; ++bi) {
+          float4 va[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+            va[a] = *reinterpret_cast<const float4*>(Vt + (bi * 64 + ti + 16 * a) * UPD_S + 4 * xq);
+#pragma unroll
+          for (int bj = 0; bj <= bi; ++bj, ++pr) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int j = bj * 64 + tj + 16 * b;
+              const float4 pa = *reinterpret_cast<const float4*>(At + j * UPD_S + 4 * xq);
+              const float4 pc = *reinterpret_cast<const float4*>(Ct + j * UPD_S + 4 * xq);
+#pragma unroll
+              for (int a = 0; a < 4; ++a) {
+                accA[pr][a][b] = fmaf(va[a].x, pa.x, fmaf(va[a].y, pa.y, fmaf(va[a].z, pa.z, fmaf(va[a].w, pa.w, accA[pr][a][b]))));
+                accC[pr][a][b] = fmaf(va[a].x, pc.x, fmaf(va[a].y, pc.y, fmaf(va[a].z, pc.z, fmaf(va[a].w, pc.w, accC[pr][a][b]))));
+              }
+            }
           }
         }
-        __syncthreads();
       }
+      // diagonal of G^B: warp w owns rows w + 8q, lanes over the 32 columns
 #pragma unroll
-      for (int ii = 0; ii < 4; ++ii)
-        *reinterpret_cast<float4*>(out + (4 * ti + ii) * 64 + 4 * tj) =
-            make_float4(acc[ii][0], acc[ii][1], acc[ii][2], acc[ii][3]);
+      for (int q = 0; q < KP / 8; ++q) {
+        const int i = warp + 8 * q;
+        gb[q] = fmaf(Vt[i * UPD_S + lane], Bt[i * UPD_S + lane], gb[q]);
+      }
+      __syncthreads();
+    }
+    cp_async_wait<0>();
+    // write this CTA's partials: [2][KP][KP] (A, C) + [KP] (GB diag)
+    float* out = p.partial + (size_t)blockIdx.x * (2 * KP * KP + KP);
+    {
+      int pr = 0;
+#pragma unroll
+      for (int bi = 0; bi < NB; ++bi)
+#pragma unroll
+        for (int bj = 0; bj <= bi; ++bj, ++pr)
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int i = bi * 64 + ti + 16 * a, j = bj * 64 + tj + 16 * b;
+              out[i * KP + j] = accA[pr][a][b];
+              out[KP * KP + i * KP + j] = accC[pr][a][b];
+            }
+    }
+#pragma unroll
+    for (int q = 0; q < KP / 8; ++q) {
+      const float s = warp_sum(gb[q]);
+      if (lane == 0) out[2 * KP * KP + warp + 8 * q] = s;
     }
   }
   grid.sync();
 
-  // ---------------- phase 2a: reduce partials -> gram ----------------
-  // 32 consecutive entries per CTA iteration (lanes), the 8 warps split the
-  // segments, fixed-order combine through shared memory (deterministic).
+  // ---------------- phase 2a: reduce the per-CTA partials -> gram ----------------
   {
-    float* red = smem;                       // [8][32]
-    const int pairs = nb * (nb + 1) / 2;
-    const int64_t per_table = (int64_t)pairs * 4096;
-    const int64_t total = 2 * per_table + k;
-    const int64_t ngroups = (total + 31) / 32;
-    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-      const int64_t e = grp * 32 + lane;
-      int u = 0, q = 0;
-      const bool ok = e < total;
+    float* red = smem;                            // [8][32]
+    const int pstride = 2 * KP * KP + KP;
+    const int total = pstride;
+    const int ngroups = (total + 31) / 32;
+    const int G = gridDim.x;
+    for (int grp = blockIdx.x; grp < ngroups; grp += G) {
+      const int e = grp * 32 + lane;
+      int table = 0, i = 0, j = 0;
+      bool ok = e < total;
       if (ok) {
-        if (e < 2 * per_table) { u = (int)(e / 4096); q = (int)(e % 4096); }
-        else { u = 2 * pairs; q = (int)(e - 2 * per_table); }
+        if (e < 2 * KP * KP) { table = e < KP * KP ? 0 : 2; const int q = e % (KP * KP); i = q / KP; j = q % KP; }
+        else { table = 1; i = j = e - 2 * KP * KP; }
+        ok = i < k && j < k && i >= j;
       }
-      float s0 = 0.f, s1 = 0.f;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
       if (ok) {
-        const float* src = p.partial + (int64_t)u * 4096 + q;
-        const int64_t stride = (int64_t)ups * 4096;
-        int sg = warp;
-        for (; sg + 8 < nseg; sg += 16) {
-          s0 += src[(int64_t)sg * stride];
-          s1 += src[(int64_t)(sg + 8) * stride];
+        const float* srcp = p.partial + e;
+        int b = warp;
+        for (; b + 24 < G; b += 32) {
+          s0 += srcp[(size_t)b * pstride];
+          s1 += srcp[(size_t)(b + 8) * pstride];
+          s2 += srcp[(size_t)(b + 16) * pstride];
+          s3 += srcp[(size_t)(b + 24) * pstride];
         }
-        if (sg < nseg) s0 += src[(int64_t)sg * stride];
+        for (; b < G; b += 8) s0 += srcp[(size_t)b * pstride];
       }
-      red[warp * 32 + lane] = s0 + s1;
+      red[warp * 32 + lane] = (s0 + s1) + (s2 + s3);
       __syncthreads();
       if (warp == 0 && ok) {
         float s = 0.f;
 #pragma unroll
         for (int w = 0; w < 8; ++w) s += red[w * 32 + lane];
-        int table, bi, bj;
-        upd_decode(u, nb, table, bi, bj);
-        int i, j;
-        if (table == 1) { i = j = q; }
-        else { i = bi * 64 + q / 64; j = bj * 64 + q % 64; }
-        if (i < k && j < k && (table == 1 || i >= j))
-          p.gram[(int64_t)table * k * k + (int64_t)i * k + j] = s;
+        p.gram[(size_t)table * k * k + (size_t)i * k + j] = s;
       }
       __syncthreads();
     }
@@ -211,90 +245,91 @@ update_kernel(UpdateArgs p) {
   // ---------------- phase 2b: coefficients ----------------
   {
     const float* GA = p.gram;
-    const float* GB = p.gram + (int64_t)k * k;
-    const float* GC = p.gram + 2 * (int64_t)k * k;
+    const float* GB = p.gram + (size_t)k * k;
+    const float* GC = p.gram + 2 * (size_t)k * k;
     const int nwarps = gridDim.x * (UPD_THREADS / 32);
     for (int i = blockIdx.x * (UPD_THREADS / 32) + warp; i < k; i += nwarps) {
-      const float gbii = GB[(int64_t)i * k + i];
+      const float gbii = GB[(size_t)i * k + i];
       float c = 0.f;
       for (int j = lane; j < k; j += 32) {
         float l = 0.f;
         if (j < i) {
-          const float s2 = fmaxf(GC[(int64_t)j * k + j], p.rho);
-          const float ga = GA[(int64_t)i * k + j];
+          const float s2 = fmaxf(GC[(size_t)j * k + j], p.rho);
+          const float ga = GA[(size_t)i * k + j];
           l = gbii * ga / s2;
-          c = fmaf(ga, GC[(int64_t)i * k + j] / s2, c);
+          c = fmaf(ga, GC[(size_t)i * k + j] / s2, c);
         }
-        p.coef[(int64_t)j * k + i] = l;       // stored transposed: Lt[j][i]
+        p.coef[(size_t)j * k + i] = l;       // Lt[j][i]
       }
       c = warp_sum(c);
       if (lane == 0) {
-        p.coef[(int64_t)k * k + i] = gbii;                              // D1
-        p.coef[(int64_t)k * k + k + i] = GA[(int64_t)i * k + i] - c;    // D2
+        p.coef[(size_t)k * k + i] = gbii;                              // D1
+        p.coef[(size_t)k * k + k + i] = GA[(size_t)i * k + i] - c;     // D2
       }
     }
   }
   grid.sync();
 
   // ---------------- phase 3: grad, v', aux' ----------------
-  const int kp = (k + 3) & ~3;                    // rows padded to a float4
-  float* Ns = smem;                               // kp (norm partial)
-  float* red4 = Ns + kp;                          // 256 (phase-4 reduction scratch)
-  float* Lt = red4 + 256;                         // k x kp  (Lt[j][i])
-  float* Xs = Lt + (size_t)k * kp;                // k x UPD_CW (AUX chunk)
-  float* D1s = Xs + (size_t)k * UPD_CW;           // k
-  float* D2s = D1s + kp;                          // k
-  for (int e = tid; e < k * kp; e += UPD_THREADS) {
-    const int j = e / kp, i = e % kp;
-    Lt[e] = i < k ? p.coef[(int64_t)j * k + i] : 0.f;
+  float* Lt = smem + 8 * TILE;                   // [KP][KP]  Lt[j][i]
+  float* D1s = Lt + KP * KP;
+  float* D2s = D1s + KP;
+  float* Ns = D2s + KP;
+  float* red = Ns + KP;                          // [8][32]
+  for (int e = tid; e < KP * KP; e += UPD_THREADS) {
+    const int j = e / KP, i = e % KP;
+    Lt[e] = (i < k && j < k) ? p.coef[(size_t)j * k + i] : 0.f;
   }
-  for (int e = tid; e < k; e += UPD_THREADS) {
-    D1s[e] = p.coef[(int64_t)k * k + e];
-    D2s[e] = p.coef[(int64_t)k * k + k + e];
+  for (int e = tid; e < KP; e += UPD_THREADS) {
+    D1s[e] = e < k ? p.coef[(size_t)k * k + e] : 0.f;
+    D2s[e] = e < k ? p.coef[(size_t)k * k + k + e] : 0.f;
     Ns[e] = 0.f;
   }
   __syncthreads();
-  const int nchunk = (int)((d + UPD_CW - 1) / UPD_CW);
-  const int tx = tid & 15;          // 4 columns 4tx..4tx+3
-  const int tr = tid >> 4;          // 4 rows per pass: 4(tr + 16 pass)..
-  const int nrb = (k + 3) / 4;      // row blocks of 4
-  for (int ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
-    const int64_t cx = (int64_t)ch * UPD_CW;
-    for (int e = tid; e < k * (UPD_CW / 4); e += UPD_THREADS) {
-      const int r = e / (UPD_CW / 4), q = e % (UPD_CW / 4);
-      const float4 v = ld4<VEC>(p.AUX + (int64_t)r * d, cx + 4 * q, d);
-      *reinterpret_cast<float4*>(Xs + r * UPD_CW + 4 * q) = v;
-    }
-    __syncthreads();
-    const int64_t gx = cx + 4 * tx;
-    for (int rb0 = 0; rb0 < nrb; rb0 += 16) {
-      const int rb = rb0 + tr;               // every lane iterates (full-warp shuffles below)
-      const int i0 = 4 * rb;
+  {
+    const int tx = tid & 7;            // columns 4tx..4tx+3 of the sub-chunk
+    const int tr = tid >> 3;           // rows 4tr..4tr+3
+    const int i0 = 4 * tr;
+    if (nsub > 0) stage_tiles<KP, VEC>(buf0, src, k, d, c0, c1);
+    cp_async_commit();
+    for (int sc = 0; sc < nsub; ++sc) {
+      float* cur = (sc & 1) ? buf1 : buf0;
+      float* nxt = (sc & 1) ? buf0 : buf1;
+      if (sc + 1 < nsub) stage_tiles<KP, VEC>(nxt, src, k, d, c0 + (int64_t)(sc + 1) * UPD_XC, c1);
+      cp_async_commit();
+      cp_async_wait<1>();
+      __syncthreads();
+      const float* Vt = cur;
+      const float* At = cur + TILE;
+      const float* Ct = cur + 2 * TILE;
+      const float* Bt = cur + 3 * TILE;
       float acc[4][4];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
-      const int jmax = rb < nrb ? min(i0 + 3, k) : 0;   // L_ij = 0 for j >= i
-      for (int j = 0; j < jmax; ++j) {
-        const float4 l = *reinterpret_cast<const float4*>(Lt + (size_t)j * kp + i0);
-        const float4 x = *reinterpret_cast<const float4*>(Xs + j * UPD_CW + 4 * tx);
-        const float lv[4] = {l.x, l.y, l.z, l.w}, xv[4] = {x.x, x.y, x.z, x.w};
+      if (i0 < KP) {
+        const int jmax = min(i0 + 3, k);         // L_ij = 0 for j >= i
+        for (int j = 0; j < jmax; ++j) {
+          const float4 l = *reinterpret_cast<const float4*>(Lt + j * KP + i0);
+          const float4 x = *reinterpret_cast<const float4*>(Ct + j * UPD_S + 4 * tx);
+          const float lv[4] = {l.x, l.y, l.z, l.w}, xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+          for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(lv[a], xv[b], acc[a][b]);
+            for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(lv[a], xv[b], acc[a][b]);
+        }
       }
+      const int64_t gx = c0 + (int64_t)sc * UPD_XC + 4 * tx;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const int i = i0 + a;
         float sq = 0.f;
-        if (i < k && gx < d) {
-          const int64_t o = (int64_t)i * d;
-          const float4 av = ld4<VEC>(p.AV + o, gx, d);
-          const float4 bv = ld4<VEC>(p.BV + o, gx, d);
-          const float4 vv = ld4<VEC>(p.V + o, gx, d);
-          const float4 xa = *reinterpret_cast<const float4*>(Xs + i * UPD_CW + 4 * tx);
+        if (i < k && gx < c1) {
+          const float4 av = *reinterpret_cast<const float4*>(At + i * UPD_S + 4 * tx);
+          const float4 bv = *reinterpret_cast<const float4*>(Bt + i * UPD_S + 4 * tx);
+          const float4 vv = *reinterpret_cast<const float4*>(Vt + i * UPD_S + 4 * tx);
+          const float4 xa = *reinterpret_cast<const float4*>(Ct + i * UPD_S + 4 * tx);
           const float d1 = D1s[i], d2 = D2s[i];
           float4 vn, an;
           vn.x = vv.x + p.eta * (d1 * av.x - d2 * bv.x - acc[a][0]);
@@ -305,77 +340,79 @@ update_kernel(UpdateArgs p) {
           an.y = xa.y + p.gamma * (bv.y - xa.y);
           an.z = xa.z + p.gamma * (bv.z - xa.z);
           an.w = xa.w + p.gamma * (bv.w - xa.w);
-          // zero the padding lanes of a ragged tail before squaring
-          if (!(gx + 1 < d)) vn.y = 0.f;
-          if (!(gx + 2 < d)) vn.z = 0.f;
-          if (!(gx + 3 < d)) vn.w = 0.f;
-          st4<VEC>(p.Vtmp + o, gx, d, vn);
-          st4<VEC>(p.AUX + o, gx, d, an);
+          const size_t o = (size_t)i * d;
+          if (VEC && gx + 3 < c1) {
+            *reinterpret_cast<float4*>(p.Vtmp + o + gx) = vn;
+            *reinterpret_cast<float4*>(p.AUX + o + gx) = an;
+          } else {
+            const float vs[4] = {vn.x, vn.y, vn.z, vn.w}, as[4] = {an.x, an.y, an.z, an.w};
+            for (int t = 0; t < 4; ++t)
+              if (gx + t < c1) { p.Vtmp[o + gx + t] = vs[t]; p.AUX[o + gx + t] = as[t]; }
+          }
+          // zero-filled columns past the range give vn = 0 automatically
           sq = vn.x * vn.x + vn.y * vn.y + vn.z * vn.z + vn.w * vn.w;
         }
-        // reduce over the 16 threads (tx) sharing row i (a half warp)
         sq += __shfl_xor_sync(0xffffffffu, sq, 1);
         sq += __shfl_xor_sync(0xffffffffu, sq, 2);
         sq += __shfl_xor_sync(0xffffffffu, sq, 4);
-        sq += __shfl_xor_sync(0xffffffffu, sq, 8);
         if (tx == 0 && i < k) Ns[i] += sq;
       }
+      __syncthreads();
     }
-    __syncthreads();
+    cp_async_wait<0>();
   }
-  for (int e = tid; e < k; e += UPD_THREADS) p.norm_partial[(int64_t)blockIdx.x * k + e] = Ns[e];
+  for (int e = tid; e < k; e += UPD_THREADS) p.norm_partial[(size_t)blockIdx.x * k + e] = Ns[e];
   grid.sync();
 
   // ---------------- phase 4: retraction v <- v'/||v'|| ----------------
-  // every CTA reduces the per-CTA norm partials: lanes over rows i, warps
-  // over the partial index, fixed-order combine (deterministic).
-  {
-    float* red = red4;                        // [8][32]
-    for (int i0 = 0; i0 < k; i0 += 32) {
-      const int i = i0 + lane;
-      float s0 = 0.f, s1 = 0.f;
-      if (i < k) {
-        int b = warp;
-        for (; b + 8 < (int)gridDim.x; b += 16) {
-          s0 += p.norm_partial[(int64_t)b * k + i];
-          s1 += p.norm_partial[(int64_t)(b + 8) * k + i];
-        }
-        if (b < (int)gridDim.x) s0 += p.norm_partial[(int64_t)b * k + i];
+  for (int r0 = 0; r0 < k; r0 += 32) {
+    const int i = r0 + lane;
+    float s0 = 0.f, s1 = 0.f;
+    if (i < k) {
+      int b = warp;
+      for (; b + 8 < (int)gridDim.x; b += 16) {
+        s0 += p.norm_partial[(size_t)b * k + i];
+        s1 += p.norm_partial[(size_t)(b + 8) * k + i];
       }
-      red[warp * 32 + lane] = s0 + s1;
-      __syncthreads();
-      if (warp == 0 && i < k) {
-        float s = 0.f;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) s += red[w * 32 + lane];
-        Ns[i] = rsqrtf(s);
-      }
-      __syncthreads();
+      if (b < (int)gridDim.x) s0 += p.norm_partial[(size_t)b * k + i];
     }
+    red[warp * 32 + lane] = s0 + s1;
+    __syncthreads();
+    if (warp == 0 && i < k) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += red[w * 32 + lane];
+      Ns[i] = rsqrtf(s);
+    }
+    __syncthreads();
   }
-  for (int ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
-    const int64_t cx = (int64_t)ch * UPD_CW;
-    for (int e = tid; e < k * (UPD_CW / 4); e += UPD_THREADS) {
-      const int r = e / (UPD_CW / 4), q = e % (UPD_CW / 4);
-      const int64_t gx = cx + 4 * q;
-      if (gx >= d) continue;
-      const int64_t o = (int64_t)r * d;
-      float4 v = ld4<VEC>(p.Vtmp + o, gx, d);
-      const float sc = Ns[r];
-      v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
-      st4<VEC>(p.V + o, gx, d, v);
-      if (p.Vbf) {
-        __nv_bfloat16* q2 = p.Vbf + o + gx;
-        if (VEC && gx + 3 < d) {
+  if (c1 > c0) {
+    const int64_t w = c1 - c0;
+    if (VEC) {
+      const int64_t nq = w / 4;
+      for (int64_t e = tid; e < (int64_t)k * nq; e += UPD_THREADS) {
+        const int r = (int)(e / nq);
+        const int64_t gx = c0 + 4 * (e % nq);
+        const size_t o = (size_t)r * d + gx;
+        float4 v = *reinterpret_cast<const float4*>(p.Vtmp + o);
+        const float sc = Ns[r];
+        v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
+        *reinterpret_cast<float4*>(p.V + o) = v;
+        if (p.Vbf) {
           __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
           uint2 pk;
           pk.x = *reinterpret_cast<uint32_t*>(&lo);
           pk.y = *reinterpret_cast<uint32_t*>(&hi);
-          *reinterpret_cast<uint2*>(q2) = pk;
-        } else {
-          const float vs[4] = {v.x, v.y, v.z, v.w};
-          for (int t = 0; t < 4 && gx + t < d; ++t) q2[t] = __float2bfloat16_rn(vs[t]);
+          *reinterpret_cast<uint2*>(p.Vbf + o) = pk;
         }
+      }
+    } else {
+      for (int64_t e = tid; e < (int64_t)k * w; e += UPD_THREADS) {
+        const int r = (int)(e / w);
+        const size_t o = (size_t)r * d + c0 + (e % w);
+        const float v = p.Vtmp[o] * Ns[r];
+        p.V[o] = v;
+        if (p.Vbf) p.Vbf[o] = __float2bfloat16_rn(v);
       }
     }
   }
