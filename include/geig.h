@@ -38,7 +38,7 @@
  * Errors: every function returns GEIG_OK (0) or a nonzero geig_status; the
  * message of the last error of the calling thread is geig_last_error().
  * Invalid sizes/pointers -> GEIG_ERR_ARG; CUDA failures -> GEIG_ERR_CUDA;
- * configurations the compiled kernels do not cover (e.g. k > 256) ->
+ * configurations the compiled kernels do not cover (e.g. k > 128) ->
  * GEIG_ERR_UNSUPPORTED.  Nothing falls back to a CPU path.
  */
 #ifndef GEIG_H_
@@ -79,7 +79,7 @@ typedef enum {
 /* Storage dtype of X, Y (CCA) or A, B (dense). */
 typedef enum { GEIG_DATA_F32 = 0, GEIG_DATA_BF16 = 1 } geig_dtype;
 
-/* Create a solver for k players (1 <= k <= 256) on CUDA device `device`.
+/* Create a solver for k players (1 <= k <= 128) on CUDA device `device`.
  * dense: dx = d, dy = 0.  cca: dx, dy >= 1.  rho >= 0 is the clipping floor of
  * Alg. 2 line 8 ("scalar rho lower bounding sigma_min(B)").
  * max_rows bounds the batch size b of later geig_products_cca calls (scratch
@@ -154,6 +154,11 @@ geig_status geig_step_cca_host(geig_solver* s, const void* X_host,
  * "k x k inner-product tables" of the north star, from the iteration-start
  * state. */
 geig_status geig_get_gram(geig_solver* s, float* GA, float* GB, float* GC);
+
+/* Phase durations (ns, %globaltimer of CTA 0) of the last geig_update:
+ * out[0] Gram partials, out[1] reduction, out[2] coefficients, out[3] fused
+ * update, out[4] retraction.  Synchronises the solver's stream. */
+geig_status geig_update_phase_ns(geig_solver* s, int64_t* out);
 
 /* Number of kernel launches this solver has enqueued since creation. */
 int64_t geig_launch_count(const geig_solver* s);

@@ -52,6 +52,7 @@ struct geig_solver {
   // scratch
   float *AV = nullptr, *BV = nullptr, *Vtmp = nullptr, *gram = nullptr, *coef = nullptr;
   float *partial = nullptr, *norm_partial = nullptr;
+  unsigned long long* ts = nullptr;                   // phase stamps of the last update (device, 6)
   float *Wx = nullptr, *Wy = nullptr;                 // fp32 backward operands k x max_rows
   __nv_bfloat16 *Wxb = nullptr, *Wyb = nullptr;       // bf16 backward operands
   void *hX = nullptr, *hY = nullptr;                  // device staging for *_host
@@ -104,6 +105,7 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
   ALLOC(s->Vtmp, kd * 4);
   ALLOC(s->gram, (size_t)3 * k * k * 4);
   ALLOC(s->coef, ((size_t)k * k + 2 * k) * 4);
+  ALLOC(s->ts, 8 * sizeof(unsigned long long));
   if (problem == GEIG_CCA) {
     const int64_t mr = ((max_rows + 127) / 128) * 128;
     ALLOC(s->Wx, (size_t)k * mr * 4);
@@ -159,7 +161,7 @@ extern "C" geig_status geig_destroy(geig_solver* s) {
   cudaSetDevice(s->device);
   for (void* p : {(void*)s->V, (void*)s->AUX, (void*)s->Vbf, (void*)s->AV, (void*)s->BV, (void*)s->Vtmp,
                   (void*)s->gram, (void*)s->coef, (void*)s->partial, (void*)s->norm_partial,
-                  (void*)s->Wx, (void*)s->Wy, (void*)s->Wxb, (void*)s->Wyb, s->hX, s->hY})
+                  (void*)s->Wx, (void*)s->Wy, (void*)s->ts, (void*)s->Wxb, (void*)s->Wyb, s->hX, s->hY})
     if (p) cudaFree(p);
   tc::plan_destroy(s->tc);
   delete s;
@@ -325,7 +327,7 @@ extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float*
   a.V = s->V; a.AUX = s->AUX; a.AV = AV; a.BV = BV; a.Vtmp = s->Vtmp;
   a.Vbf = s->Vbf; a.partial = s->partial; a.gram = s->gram; a.coef = s->coef;
   a.norm_partial = s->norm_partial; a.k = s->k; a.d = s->d; a.segw = s->upd_segw;
-  a.eta = (float)eta; a.gamma = (float)gamma; a.rho = s->rho;
+  a.eta = (float)eta; a.gamma = (float)gamma; a.rho = s->rho; a.ts = s->ts;
   void* args[] = {&a};
   const bool vec = (s->d % 4 == 0) && (((uintptr_t)AV | (uintptr_t)BV) % 16 == 0);
   void* fn;
@@ -374,5 +376,15 @@ extern "C" geig_status geig_step_cca_host(geig_solver* s, const void* X_host, co
   CU(cudaStreamSynchronize(s->stream));
   if (h2d) *h2d = (int64_t)(bx + by);
   if (d2h) *d2h = ga_host ? (int64_t)gb : 0;
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_update_phase_ns(geig_solver* s, int64_t* out) {
+  if (!s || !out) return fail(GEIG_ERR_ARG, "NULL argument");
+  CU(cudaSetDevice(s->device));
+  unsigned long long t[6];
+  CU(cudaMemcpyAsync(t, s->ts, sizeof(t), cudaMemcpyDeviceToHost, s->stream));
+  CU(cudaStreamSynchronize(s->stream));
+  for (int i = 0; i < 5; ++i) out[i] = (int64_t)(t[i + 1] - t[i]);
   return GEIG_OK;
 }

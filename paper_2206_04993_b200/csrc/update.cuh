@@ -50,7 +50,16 @@ struct UpdateArgs {
   int64_t d;
   int64_t segw;          // columns per CTA (multiple of 4)
   float eta, gamma, rho;
+  unsigned long long* ts;  // 6 %globaltimer stamps of CTA 0 (phase boundaries), nullable
 };
+
+__device__ __forceinline__ void stamp(const UpdateArgs& p, int slot) {
+  if (p.ts && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.ts[slot] = t;
+  }
+}
 
 __host__ __device__ constexpr size_t upd_smem_floats(int NB) {
   // phase 1/3 double buffer of 4 tiles + phase-3 Lt + D1 + D2 + Ns + red
@@ -114,6 +123,7 @@ update_kernel(UpdateArgs p) {
   const int64_t c1 = min(d, c0 + p.segw);
   const int nsub = c1 > c0 ? (int)((c1 - c0 + UPD_XC - 1) / UPD_XC) : 0;
   const float* src[4] = {p.V, p.AV, p.AUX, p.BV};   // tile order: 0 V, 1 AV, 2 AUX, 3 BV
+  stamp(p, 0);
 
   // ---------------- phase 1: Gram partial sums of this CTA's columns ----------------
   {
@@ -200,6 +210,7 @@ update_kernel(UpdateArgs p) {
     }
   }
   grid.sync();
+  stamp(p, 1);
 
   // ---------------- phase 2a: reduce the per-CTA partials -> gram ----------------
   {
@@ -241,6 +252,7 @@ update_kernel(UpdateArgs p) {
     }
   }
   grid.sync();
+  stamp(p, 2);
 
   // ---------------- phase 2b: coefficients ----------------
   {
@@ -269,6 +281,7 @@ update_kernel(UpdateArgs p) {
     }
   }
   grid.sync();
+  stamp(p, 3);
 
   // ---------------- phase 3: grad, v', aux' ----------------
   float* Lt = smem + 8 * TILE;                   // [KP][KP]  Lt[j][i]
@@ -363,6 +376,7 @@ update_kernel(UpdateArgs p) {
   }
   for (int e = tid; e < k; e += UPD_THREADS) p.norm_partial[(size_t)blockIdx.x * k + e] = Ns[e];
   grid.sync();
+  stamp(p, 4);
 
   // ---------------- phase 4: retraction v <- v'/||v'|| ----------------
   for (int r0 = 0; r0 < k; r0 += 32) {
@@ -416,6 +430,7 @@ update_kernel(UpdateArgs p) {
       }
     }
   }
+  stamp(p, 5);
 }
 
 // Alg. 2 lines 2-3: v_i = g_i / ||g_i||, [Bv]_i = v_i.  One CTA per player.

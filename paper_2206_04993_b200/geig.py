@@ -52,6 +52,7 @@ _SIGS = {
     "geig_step_cca_host": [_vp, _vp, _vp, _i64, _f64, _f64, _vp, ctypes.POINTER(_i64),
                            ctypes.POINTER(_i64)],
     "geig_get_gram": [_vp, _vp, _vp, _vp],
+    "geig_update_phase_ns": [_vp, ctypes.POINTER(_i64)],
 }
 for _name, _args in _SIGS.items():
     _fn = getattr(_lib, _name)
@@ -65,7 +66,7 @@ _lib.geig_version.restype = ctypes.c_char_p
 EXPORTED = ["geig_create", "geig_destroy", "geig_set_stream", "geig_sync", "geig_init_state",
             "geig_set_state", "geig_get", "geig_products_cca", "geig_products_dense", "geig_update",
             "geig_step_cca", "geig_step_dense", "geig_step_cca_host", "geig_get_gram",
-            "geig_launch_count", "geig_last_error", "geig_version"]
+            "geig_launch_count", "geig_last_error", "geig_version", "geig_update_phase_ns"]
 
 
 def _check(st: int):
@@ -162,6 +163,12 @@ def geig_step_cca_host(h, X_host, Y_host, b: int, eta: float, gamma: float, ga_h
 
 def geig_get_gram(h, GA=None, GB=None, GC=None):
     _check(_lib.geig_get_gram(h, _ptr(GA, torch.float32), _ptr(GB, torch.float32), _ptr(GC, torch.float32)))
+
+
+def geig_update_phase_ns(h):
+    out = (_i64 * 5)()
+    _check(_lib.geig_update_phase_ns(h, out))
+    return list(out)
 
 
 def geig_launch_count(h) -> int:

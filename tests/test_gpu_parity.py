@@ -217,7 +217,10 @@ def test_dense_config4_reduced_fp32(geig):
     from synth import CONFIGS, dense_gep_large
     cfg = CONFIGS[4]
     a, b = dense_gep_large(1000, seed=2, device="cuda:0")
-    _dense_step_check(geig, a, b, 37, "f32", cfg.rho, cfg.eta, cfg.gamma, tol=1e-4)
+    # eta = 0.5 so that the step (eta ||grad|| ~ 2e-2 ||V||) is resolved by
+    # fp32 storage of V'; with the config's eta the fp32 rounding of V' alone
+    # is 1.6e-4 of the step
+    _dense_step_check(geig, a, b, 37, "f32", cfg.rho, 0.5, cfg.gamma, tol=1e-4)
 
 
 def test_dense_config4_full_size_tf32_tcgen05(geig):
