@@ -103,7 +103,10 @@ geig_status geig_sync(geig_solver* s);
  * [Bv]_i = v_i.  Also resets the step counter. */
 geig_status geig_init_state(geig_solver* s, const float* G);
 
-/* Overwrite / read the state (V, AUX: k x d fp32, device). AUX may be NULL. */
+/* Overwrite / read the state (V, AUX: k x d fp32, device). AUX may be NULL.
+ * Internally the retraction v <- v/||v|| of Alg. 2 line 17 is applied when
+ * the next update reads the state; geig_get returns the retracted
+ * (unit-norm) v_i. */
 geig_status geig_set_state(geig_solver* s, const float* V, const float* AUX);
 geig_status geig_get(geig_solver* s, float* V, float* AUX);
 
@@ -156,8 +159,8 @@ geig_status geig_step_cca_host(geig_solver* s, const void* X_host,
 geig_status geig_get_gram(geig_solver* s, float* GA, float* GB, float* GC);
 
 /* Phase durations (ns, %globaltimer of CTA 0) of the last geig_update:
- * out[0] Gram partials, out[1] reduction, out[2] coefficients, out[3] fused
- * update, out[4] retraction.  Synchronises the solver's stream. */
+ * out[0] Gram partials, out[1] grid reduction, out[2] coefficients + fused
+ * update; out[3], out[4] = 0 (reserved).  Synchronises the solver's stream. */
 geig_status geig_update_phase_ns(geig_solver* s, int64_t* out);
 
 /* Number of kernel launches this solver has enqueued since creation. */

@@ -50,8 +50,8 @@ struct geig_solver {
   float *V = nullptr, *AUX = nullptr;
   __nv_bfloat16* Vbf = nullptr;
   // scratch
-  float *AV = nullptr, *BV = nullptr, *Vtmp = nullptr, *gram = nullptr, *coef = nullptr;
-  float *partial = nullptr, *norm_partial = nullptr;
+  float *AV = nullptr, *BV = nullptr, *gram = nullptr, *raw = nullptr;
+  float *partial = nullptr;
   unsigned long long* ts = nullptr;                   // phase stamps of the last update (device, 6)
   float *Wx = nullptr, *Wy = nullptr;                 // fp32 backward operands k x max_rows
   __nv_bfloat16 *Wxb = nullptr, *Wyb = nullptr;       // bf16 backward operands
@@ -102,9 +102,8 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
   ALLOC(s->Vbf, kd * 2);
   ALLOC(s->AV, kd * 4);
   ALLOC(s->BV, kd * 4);
-  ALLOC(s->Vtmp, kd * 4);
   ALLOC(s->gram, (size_t)3 * k * k * 4);
-  ALLOC(s->coef, ((size_t)k * k + 2 * k) * 4);
+  ALLOC(s->raw, upd_partial_floats(k <= 64 ? 1 : 2) * 4);
   ALLOC(s->ts, 8 * sizeof(unsigned long long));
   if (problem == GEIG_CCA) {
     const int64_t mr = ((max_rows + 127) / 128) * 128;
@@ -141,12 +140,9 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
     G = (s->d + segw - 1) / segw;
     s->upd_grid = (int)G;
     s->upd_segw = segw;
-    const int KP = NB * 64;
-    if (cudaMalloc((void**)&s->partial, (size_t)G * (2 * KP * KP + KP) * 4) != cudaSuccess)
+    if (cudaMalloc((void**)&s->partial, (size_t)G * upd_partial_floats(NB) * 4) != cudaSuccess)
       return cleanup(fail(GEIG_ERR_CUDA, "cudaMalloc gram partials"));
   }
-  if (cudaMalloc((void**)&s->norm_partial, (size_t)s->upd_grid * k * 4) != cudaSuccess)
-    return cleanup(fail(GEIG_ERR_CUDA, "cudaMalloc norm_partial"));
   if (math != GEIG_MATH_F32) {
     geig_status st = tc::plan_create(s->tc, problem, dx, dy, k, math, max_rows, device);
     if (st != GEIG_OK) return cleanup(fail(st, "%s", tc::last_error()));
@@ -159,8 +155,8 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
 extern "C" geig_status geig_destroy(geig_solver* s) {
   if (!s) return GEIG_OK;
   cudaSetDevice(s->device);
-  for (void* p : {(void*)s->V, (void*)s->AUX, (void*)s->Vbf, (void*)s->AV, (void*)s->BV, (void*)s->Vtmp,
-                  (void*)s->gram, (void*)s->coef, (void*)s->partial, (void*)s->norm_partial,
+  for (void* p : {(void*)s->V, (void*)s->AUX, (void*)s->Vbf, (void*)s->AV, (void*)s->BV,
+                  (void*)s->gram, (void*)s->raw, (void*)s->partial,
                   (void*)s->Wx, (void*)s->Wy, (void*)s->ts, (void*)s->Wxb, (void*)s->Wyb, s->hX, s->hY})
     if (p) cudaFree(p);
   tc::plan_destroy(s->tc);
@@ -206,7 +202,12 @@ extern "C" geig_status geig_get(geig_solver* s, float* V, float* AUX) {
   if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
   CU(cudaSetDevice(s->device));
   const size_t kd = (size_t)s->k * s->d;
-  if (V) CU(cudaMemcpyAsync(V, s->V, kd * 4, cudaMemcpyDeviceToDevice, s->stream));
+  if (V) {
+    // the state holds v'' (retraction folded into the next update): return v''/||v''||
+    normalize_rows_kernel<<<s->k, 256, 0, s->stream>>>(s->V, V, s->d);
+    CHECK_LAUNCH();
+    s->launches++;
+  }
   if (AUX) CU(cudaMemcpyAsync(AUX, s->AUX, kd * 4, cudaMemcpyDeviceToDevice, s->stream));
   return GEIG_OK;
 }
@@ -322,11 +323,10 @@ extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float*
                                    double gamma) {
   if (!s || !AV || !BV) return fail(GEIG_ERR_ARG, "NULL argument");
   CU(cudaSetDevice(s->device));
-  CU(cudaMemsetAsync(s->gram, 0, (size_t)3 * s->k * s->k * 4, s->stream));
   UpdateArgs a;
-  a.V = s->V; a.AUX = s->AUX; a.AV = AV; a.BV = BV; a.Vtmp = s->Vtmp;
-  a.Vbf = s->Vbf; a.partial = s->partial; a.gram = s->gram; a.coef = s->coef;
-  a.norm_partial = s->norm_partial; a.k = s->k; a.d = s->d; a.segw = s->upd_segw;
+  a.V = s->V; a.AUX = s->AUX; a.AV = AV; a.BV = BV;
+  a.Vbf = s->Vbf; a.partial = s->partial; a.raw = s->raw; a.gram = s->gram;
+  a.k = s->k; a.d = s->d; a.segw = s->upd_segw;
   a.eta = (float)eta; a.gamma = (float)gamma; a.rho = s->rho; a.ts = s->ts;
   void* args[] = {&a};
   const bool vec = (s->d % 4 == 0) && (((uintptr_t)AV | (uintptr_t)BV) % 16 == 0);
@@ -382,9 +382,10 @@ extern "C" geig_status geig_step_cca_host(geig_solver* s, const void* X_host, co
 extern "C" geig_status geig_update_phase_ns(geig_solver* s, int64_t* out) {
   if (!s || !out) return fail(GEIG_ERR_ARG, "NULL argument");
   CU(cudaSetDevice(s->device));
-  unsigned long long t[6];
+  unsigned long long t[4];
   CU(cudaMemcpyAsync(t, s->ts, sizeof(t), cudaMemcpyDeviceToHost, s->stream));
   CU(cudaStreamSynchronize(s->stream));
-  for (int i = 0; i < 5; ++i) out[i] = (int64_t)(t[i + 1] - t[i]);
+  for (int i = 0; i < 3; ++i) out[i] = (int64_t)(t[i + 1] - t[i]);
+  out[3] = out[4] = 0;
   return GEIG_OK;
 }

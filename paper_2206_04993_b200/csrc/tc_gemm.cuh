@@ -29,6 +29,7 @@ namespace geig { namespace tc {
 constexpr int TC_THREADS = 128;
 constexpr int TC_BM = 128;
 constexpr int TC_STAGES = 4;
+constexpr int TC_MAX_SPLITS = 8;
 
 // ----------------------------------------------------------------------------
 // PTX wrappers
@@ -122,6 +123,7 @@ struct TcParams {
   int64_t ldo;
   float scale;
   int atomic;          // 1: red.add, 0: store
+  int64_t split_stride;  // store mode with splits > 1: output offset per split (elements)
   uint32_t idesc;
 };
 
@@ -240,7 +242,7 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
     const bool mok = m < p.M[g];
     for (int s = 0; s < p.nseg; ++s) {
       if (kb_cnt[s] == 0) continue;
-      float* out = p.out[g][s];
+      float* out = p.out[g][s] + (p.atomic ? 0 : (int64_t)blockIdx.y * p.split_stride);
       for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t r[16];
         tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(s * BN + c0), r);
@@ -266,27 +268,30 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   }
 }
 
-// Forward-product reshuffle: Zt[view] (k x ldz fp32, rows 0..2h) into the
-// four backward B operands Zb[view][half] (k x hpad, T) — reading R1:
+// Forward-product reshuffle: the split-K partials Zp[split][view] (k x ldz
+// fp32, rows 0..2h) summed in fixed split order (deterministic) into the four
+// backward B operands Zb[view][half] (k x hpad, T) — reading R1:
 //   X backward: half0 (A_t) uses Z_y rows [0,h), half1 (B_t) uses Z_x rows [h,2h)
 //   Y backward: half0 uses Z_x rows [0,h), half1 uses Z_y rows [h,2h)
-// and re-zero Zt for the next step's split-K accumulation.
 template <typename T>
-__global__ void zshuffle_kernel(float* __restrict__ Zt, T* __restrict__ Zb, int k, int64_t ldz, int h,
-                                int64_t hpad) {
+__global__ void zshuffle_kernel(const float* __restrict__ Zp, T* __restrict__ Zb, int k, int64_t ldz, int h,
+                                int64_t hpad, int splits) {
   const int64_t per = (int64_t)k * h;
+  const int64_t vstride = (int64_t)k * ldz;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x) {
     const int n = (int)(e / h), r = (int)(e % h);
-    float* zx = Zt + (int64_t)n * ldz;
-    float* zy = Zt + (int64_t)k * ldz + (int64_t)n * ldz;
-    const float x0 = zx[r], x1 = zx[h + r], y0 = zy[r], y1 = zy[h + r];
+    float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
+    for (int sp = 0; sp < splits; ++sp) {
+      const float* zx = Zp + (int64_t)(2 * sp) * vstride + (int64_t)n * ldz;
+      const float* zy = zx + vstride;
+      x0 += zx[r]; x1 += zx[h + r]; y0 += zy[r]; y1 += zy[h + r];
+    }
     const int64_t o = (int64_t)n * hpad + r;
     const int64_t plane = (int64_t)k * hpad;
     Zb[0 * plane + o] = (T)y0;     // view x, half 0
     Zb[1 * plane + o] = (T)x1;     // view x, half 1
     Zb[2 * plane + o] = (T)x0;     // view y, half 0
     Zb[3 * plane + o] = (T)y1;     // view y, half 1
-    zx[r] = 0.f; zx[h + r] = 0.f; zy[r] = 0.f; zy[h + r] = 0.f;
   }
 }
 
@@ -297,7 +302,7 @@ struct TcPlan {
   int ready = 0;
   int problem = 0, math = 0, k = 0, BN = 0, device = 0, nsm = 148;
   int64_t dx = 0, dy = 0, d = 0, max_rows = 0, ldz = 0, hpad = 0;
-  float* Zt = nullptr;     // 2 x k x ldz fp32 (CCA forward accumulators)
+  float* Zt = nullptr;     // TC_MAX_SPLITS x 2 x k x ldz fp32 (CCA forward split-K partials)
   void* Zb = nullptr;      // 2 x 2 x k x hpad (bf16 or fp32)
 };
 
@@ -387,10 +392,9 @@ inline geig_status plan_create(TcPlan& t, int problem, int64_t dx, int64_t dy, i
   if (problem == GEIG_CCA) {
     t.ldz = ((max_rows + 3) / 4) * 4;
     t.hpad = ((max_rows / 2 + 7) / 8) * 8;
-    if (cudaMalloc((void**)&t.Zt, (size_t)2 * k * t.ldz * 4) != cudaSuccess ||
+    if (cudaMalloc((void**)&t.Zt, (size_t)TC_MAX_SPLITS * 2 * k * t.ldz * 4) != cudaSuccess ||
         cudaMalloc(&t.Zb, (size_t)4 * k * t.hpad * eb) != cudaSuccess)
       return tc_fail(GEIG_ERR_CUDA, "cudaMalloc tc scratch");
-    cudaMemset(t.Zt, 0, (size_t)2 * k * t.ldz * 4);
     cudaMemset(t.Zb, 0, (size_t)4 * k * t.hpad * eb);
   }
   t.ready = 1;
@@ -417,7 +421,9 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
   const void* Vop = eb == 2 ? (const void*)Vbf : (const void*)V;
   const int64_t dv[2] = {t.dx, t.dy};
   const void* Xv[2] = {X, Y};
-  // ---- forward: Z_v = X_v V_v^T, M = rows, K = d_v ----
+  // ---- forward: Z_v = X_v V_v^T, M = rows, K = d_v; split-K partials stored
+  //      (no atomics) and summed by the reshuffle ----
+  int fsplits = 1;
   {
     TcMaps maps;
     TcParams p{};
@@ -434,23 +440,25 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
       p.out[v][0] = t.Zt + (int64_t)v * k * t.ldz;
       p.out[v][1] = nullptr;
     }
-    p.N = k; p.BN = t.BN; p.nseg = 1; p.ldo = t.ldz; p.scale = 1.f; p.atomic = 1;
+    p.N = k; p.BN = t.BN; p.nseg = 1; p.ldo = t.ldz; p.scale = 1.f; p.atomic = 0;
+    p.split_stride = (int64_t)2 * k * t.ldz;
     p.idesc = make_idesc(eb, false, t.BN, TC_BM);
     const int mt = (rows + TC_BM - 1) / TC_BM;
-    p.splits = choose_splits(2 * mt, std::min(p.kblocks[0][0], p.kblocks[1][0]), t.nsm);
+    p.splits = std::min(TC_MAX_SPLITS, choose_splits(2 * mt, std::min(p.kblocks[0][0], p.kblocks[1][0]), t.nsm));
+    fsplits = p.splits;
     dim3 grid(mt, p.splits, 2);
     geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st) : launch<4, false>(maps, p, grid, st);
     if (s) return s;
     ++*nl;
   }
-  // ---- shuffle Zt -> Zb halves (and zero Zt) ----
+  // ---- reshuffle: sum split partials -> Zb halves ----
   {
     const int64_t per = (int64_t)k * h;
     const int blocks = (int)std::min<int64_t>(1184, (per + 255) / 256);
     if (eb == 2)
-      zshuffle_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(t.Zt, (__nv_bfloat16*)t.Zb, k, t.ldz, h, t.hpad);
+      zshuffle_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(t.Zt, (__nv_bfloat16*)t.Zb, k, t.ldz, h, t.hpad, fsplits);
     else
-      zshuffle_kernel<float><<<blocks, 256, 0, st>>>(t.Zt, (float*)t.Zb, k, t.ldz, h, t.hpad);
+      zshuffle_kernel<float><<<blocks, 256, 0, st>>>(t.Zt, (float*)t.Zb, k, t.ldz, h, t.hpad, fsplits);
     if (cudaGetLastError() != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, "zshuffle launch failed");
     ++*nl;
   }
@@ -477,8 +485,9 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
     p.idesc = make_idesc(eb, true, t.BN, TC_BM);
     const int mt = (int)((std::max(t.dx, t.dy) + TC_BM - 1) / TC_BM);
     const int mtot = (int)((t.dx + TC_BM - 1) / TC_BM + (t.dy + TC_BM - 1) / TC_BM);
-    p.splits = choose_splits(mtot, p.kblocks[0][0], t.nsm);
+    p.splits = (mtot * 3 >= t.nsm * 2) ? 1 : choose_splits(mtot, p.kblocks[0][0], t.nsm);
     p.atomic = p.splits > 1;
+    p.split_stride = 0;
     if (p.atomic) {
       if (cudaMemsetAsync(AV, 0, (size_t)k * t.d * 4, st) != cudaSuccess ||
           cudaMemsetAsync(BV, 0, (size_t)k * t.d * 4, st) != cudaSuccess)
@@ -520,8 +529,9 @@ inline geig_status products_dense(TcPlan& t, const void* A, const void* B, int64
   p.N = k; p.BN = t.BN; p.nseg = 1; p.ldo = t.d; p.scale = 1.f;
   p.idesc = make_idesc(eb, false, t.BN, TC_BM);
   const int mt = (M + TC_BM - 1) / TC_BM;
-  p.splits = choose_splits(2 * mt, p.kblocks[0][0], t.nsm);
+  p.splits = (2 * mt * 3 >= t.nsm * 2) ? 1 : choose_splits(2 * mt, p.kblocks[0][0], t.nsm);
   p.atomic = p.splits > 1;
+  p.split_stride = 0;
   if (p.atomic) {
     for (int g = 0; g < 2; ++g)
       if (cudaMemset2DAsync(outs[g], (size_t)t.d * 4, 0, (size_t)M * 4, k, st) != cudaSuccess)

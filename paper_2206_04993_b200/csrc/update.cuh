@@ -11,18 +11,25 @@
 // <v_i, [By]_j> = G^C_ij / s_j.  Then v_i' = v_i + eta grad_i,
 // v_i <- v_i'/||v_i'|| (lines 16-17), [Bv]_i += gamma (BV_i - [Bv]_i) (19).
 //
+// Retraction folded forward: the state holds v'' = v + eta grad (line 16)
+// and the division by ||v''|| (line 17) is applied when the next update
+// reads it — products are linear in v, so A_t v = (A_t v'')/||v''||, and
+// ||v''||^2 is one more diagonal of the Gram phase.  This removes a global
+// reduction + grid barrier and a pass over V per step (geig_get returns
+// the retracted v).
+//
 // One CTA (256 threads) per SM owns a contiguous column range of d; the
-// four k x range tiles (V, AV, [Bv], BV) stream through shared memory in
-// 32-column sub-chunks with double-buffered cp.async (16-byte, zero-fill
+// four k x range tiles (V'', AV'', [Bv], BV'') stream through shared memory
+// in 32-column sub-chunks with double-buffered cp.async (16-byte, zero-fill
 // past the range).  Phases (grid.sync between them):
 //  1  per-CTA Gram partials: G^A, G^C as 4x4 register micro-tiles per
 //     thread (rows t, t+16, t+32, t+48 of each 64-row block: conflict-free
-//     LDS.128 with a 36-float row stride), lower 64-blocks only; diag G^B.
-//  2a deterministic reduction of the per-CTA partials -> gram.
-//  2b coefficients L (stored transposed), D1 = G^B_ii, D2 = G^A_ii - c_i.
-//  3  stream the tiles again: L [Bv] micro-tiles, grad, v' (to scratch),
-//     [Bv]' (to the state), per-CTA ||v'||^2 partials.
-//  4  reduce the norms, V = v'/||v'|| (+ bf16 copy of V for the GEMMs).
+//     LDS.128 with a 36-float row stride), lower 64-blocks only; diagonals
+//     <v''_i, BV''_i> and ||v''_i||^2.
+//  2  deterministic reduction of the per-CTA partials (fixed order).
+//  3  every CTA: normalisation factors, coefficients L (transposed in
+//     smem), D1, D2; then stream the tiles again: L [Bv] micro-tiles,
+//     grad, v'' (in place, + bf16 copy for the GEMMs), [Bv]' (in place).
 #pragma once
 #include <cooperative_groups.h>
 #include "common.cuh"
@@ -40,12 +47,10 @@ struct UpdateArgs {
   float* AUX;            // k x d (in/out)
   const float* AV;       // k x d
   const float* BV;       // k x d
-  float* Vtmp;           // k x d scratch (v')
   __nv_bfloat16* Vbf;    // k x d bf16 copy of the new V (nullable)
-  float* partial;        // gridDim x (2*KP*KP + KP) scratch
-  float* gram;           // 3 x k x k out: GA, GB, GC (zeroed by the host)
-  float* coef;           // k x k (Lt, transposed L) + k (D1) + k (D2)
-  float* norm_partial;   // gridDim x k
+  float* partial;        // gridDim x (2*KP*KP + 2*KP) scratch
+  float* raw;            // 2*KP*KP + 2*KP reduced un-normalised tables
+  float* gram;           // 3 x k x k out: normalised GA, GB, GC of the step
   int k;
   int64_t d;
   int64_t segw;          // columns per CTA (multiple of 4)
@@ -62,9 +67,10 @@ __device__ __forceinline__ void stamp(const UpdateArgs& p, int slot) {
 }
 
 __host__ __device__ constexpr size_t upd_smem_floats(int NB) {
-  // phase 1/3 double buffer of 4 tiles + phase-3 Lt + D1 + D2 + Ns + red
-  return (size_t)2 * 4 * (NB * 64) * UPD_S + (size_t)(NB * 64) * (NB * 64) + 3 * (NB * 64) + 256;
+  // double buffer of 4 tiles + phase-3 Lt + n, s^2, D1, D2
+  return (size_t)2 * 4 * (NB * 64) * UPD_S + (size_t)(NB * 64) * (NB * 64) + 4 * (NB * 64);
 }
+__host__ __device__ constexpr size_t upd_partial_floats(int NB) { return 2 * (NB * 64) * (NB * 64) + 2 * (NB * 64); }
 
 __device__ __forceinline__ void cp_async16(float* dst, const float* src, int bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
@@ -111,6 +117,7 @@ update_kernel(UpdateArgs p) {
   constexpr int KP = NB * 64;
   constexpr int TILE = KP * UPD_S;               // floats per array tile
   constexpr int NPAIR = NB * (NB + 1) / 2;       // lower 64-block pairs
+  constexpr int PSTRIDE = 2 * KP * KP + 2 * KP;  // per-CTA partial: GA', GC', diag GB', diag V'V'
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) float smem[];
   float* buf0 = smem;                            // [4][KP][UPD_S]
@@ -122,7 +129,7 @@ update_kernel(UpdateArgs p) {
   const int64_t c0 = (int64_t)blockIdx.x * p.segw;
   const int64_t c1 = min(d, c0 + p.segw);
   const int nsub = c1 > c0 ? (int)((c1 - c0 + UPD_XC - 1) / UPD_XC) : 0;
-  const float* src[4] = {p.V, p.AV, p.AUX, p.BV};   // tile order: 0 V, 1 AV, 2 AUX, 3 BV
+  const float* src[4] = {p.V, p.AV, p.AUX, p.BV};   // tile order: 0 V', 1 AV', 2 AUX, 3 BV'
   stamp(p, 0);
 
   // ---------------- phase 1: Gram partial sums of this CTA's columns ----------------
@@ -135,11 +142,11 @@ update_kernel(UpdateArgs p) {
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) accA[pr][a][b] = accC[pr][a][b] = 0.f;
-    float gb[KP / 8];
+    float gb[KP / 8], nn[KP / 8];
 #pragma unroll
-    for (int q = 0; q < KP / 8; ++q) gb[q] = 0.f;
+    for (int q = 0; q < KP / 8; ++q) gb[q] = nn[q] = 0.f;
 
-    if (nsub > 0) { stage_tiles<KP, VEC>(buf0, src, k, d, c0, c1); }
+    if (nsub > 0) stage_tiles<KP, VEC>(buf0, src, k, d, c0, c1);
     cp_async_commit();
     for (int sc = 0; sc < nsub; ++sc) {
       float* cur = (sc & 1) ? buf1 : buf0;
@@ -177,17 +184,18 @@ update_kernel(UpdateArgs p) {
           }
         }
       }
-      // diagonal of G^B: warp w owns rows w + 8q, lanes over the 32 columns
+      // diagonals <v'_i, BV'_i> and <v'_i, v'_i>: warp w owns rows w + 8q
 #pragma unroll
       for (int q = 0; q < KP / 8; ++q) {
         const int i = warp + 8 * q;
-        gb[q] = fmaf(Vt[i * UPD_S + lane], Bt[i * UPD_S + lane], gb[q]);
+        const float v = Vt[i * UPD_S + lane];
+        gb[q] = fmaf(v, Bt[i * UPD_S + lane], gb[q]);
+        nn[q] = fmaf(v, v, nn[q]);
       }
       __syncthreads();
     }
     cp_async_wait<0>();
-    // write this CTA's partials: [2][KP][KP] (A, C) + [KP] (GB diag)
-    float* out = p.partial + (size_t)blockIdx.x * (2 * KP * KP + KP);
+    float* out = p.partial + (size_t)blockIdx.x * PSTRIDE;
     {
       int pr = 0;
 #pragma unroll
@@ -205,40 +213,43 @@ update_kernel(UpdateArgs p) {
     }
 #pragma unroll
     for (int q = 0; q < KP / 8; ++q) {
-      const float s = warp_sum(gb[q]);
-      if (lane == 0) out[2 * KP * KP + warp + 8 * q] = s;
+      const float s1 = warp_sum(gb[q]);
+      const float s2 = warp_sum(nn[q]);
+      if (lane == 0) {
+        out[2 * KP * KP + warp + 8 * q] = s1;
+        out[2 * KP * KP + KP + warp + 8 * q] = s2;
+      }
     }
   }
   grid.sync();
   stamp(p, 1);
 
-  // ---------------- phase 2a: reduce the per-CTA partials -> gram ----------------
+  // ---------------- phase 2: reduce the per-CTA partials -> raw tables ----------------
+  // lanes over 32 consecutive entries, warps over the partial index (fixed order).
   {
     float* red = smem;                            // [8][32]
-    const int pstride = 2 * KP * KP + KP;
-    const int total = pstride;
-    const int ngroups = (total + 31) / 32;
+    const int ngroups = (PSTRIDE + 31) / 32;
     const int G = gridDim.x;
     for (int grp = blockIdx.x; grp < ngroups; grp += G) {
       const int e = grp * 32 + lane;
-      int table = 0, i = 0, j = 0;
-      bool ok = e < total;
-      if (ok) {
-        if (e < 2 * KP * KP) { table = e < KP * KP ? 0 : 2; const int q = e % (KP * KP); i = q / KP; j = q % KP; }
-        else { table = 1; i = j = e - 2 * KP * KP; }
+      bool ok = e < PSTRIDE;
+      if (ok && e < 2 * KP * KP) {
+        const int q = e % (KP * KP), i = q / KP, j = q % KP;
         ok = i < k && j < k && i >= j;
+      } else if (ok) {
+        ok = (e - 2 * KP * KP) % KP < k;
       }
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
       if (ok) {
         const float* srcp = p.partial + e;
         int b = warp;
         for (; b + 24 < G; b += 32) {
-          s0 += srcp[(size_t)b * pstride];
-          s1 += srcp[(size_t)(b + 8) * pstride];
-          s2 += srcp[(size_t)(b + 16) * pstride];
-          s3 += srcp[(size_t)(b + 24) * pstride];
+          s0 += srcp[(size_t)b * PSTRIDE];
+          s1 += srcp[(size_t)(b + 8) * PSTRIDE];
+          s2 += srcp[(size_t)(b + 16) * PSTRIDE];
+          s3 += srcp[(size_t)(b + 24) * PSTRIDE];
         }
-        for (; b < G; b += 8) s0 += srcp[(size_t)b * pstride];
+        for (; b < G; b += 8) s0 += srcp[(size_t)b * PSTRIDE];
       }
       red[warp * 32 + lane] = (s0 + s1) + (s2 + s3);
       __syncthreads();
@@ -246,7 +257,7 @@ update_kernel(UpdateArgs p) {
         float s = 0.f;
 #pragma unroll
         for (int w = 0; w < 8; ++w) s += red[w * 32 + lane];
-        p.gram[(size_t)table * k * k + (size_t)i * k + j] = s;
+        p.raw[e] = s;
       }
       __syncthreads();
     }
@@ -254,51 +265,60 @@ update_kernel(UpdateArgs p) {
   grid.sync();
   stamp(p, 2);
 
-  // ---------------- phase 2b: coefficients ----------------
+  // ---------------- phase 3a: coefficients (every CTA, from the raw tables) ----------------
+  // Normalisation folded in (retraction of the previous step, Alg. 2 line 17):
+  // n_i = 1/||v'_i||, v_i = n_i v'_i, AV_i = n_i AV'_i, BV_i = n_i BV'_i, so
+  // G^A_ij = n_i n_j G'^A_ij, G^C_ij = n_i G'^C_ij, G^B_ii = n_i^2 G'^B_ii.
+  float* Lt = smem + 8 * TILE;                   // [KP][KP]  Lt[j][i]
+  float* Ns = Lt + KP * KP;                      // n_i
+  float* S2 = Ns + KP;                           // s_j^2 = max(G^C_jj, rho)
+  float* D1s = S2 + KP;                          // G^B_ii
+  float* D2s = D1s + KP;                         // G^A_ii - c_i
   {
-    const float* GA = p.gram;
-    const float* GB = p.gram + (size_t)k * k;
-    const float* GC = p.gram + 2 * (size_t)k * k;
-    const int nwarps = gridDim.x * (UPD_THREADS / 32);
-    for (int i = blockIdx.x * (UPD_THREADS / 32) + warp; i < k; i += nwarps) {
-      const float gbii = GB[(size_t)i * k + i];
+    const float* rA = p.raw;
+    const float* rC = p.raw + KP * KP;
+    const float* rB = p.raw + 2 * KP * KP;
+    const float* rN = rB + KP;
+    for (int i = tid; i < KP; i += UPD_THREADS) {
+      float n = 0.f, s2 = 1.f, gb = 0.f;
+      if (i < k) {
+        n = rsqrtf(rN[i]);
+        gb = n * n * rB[i];
+        s2 = fmaxf(n * rC[i * KP + i], p.rho);
+      }
+      Ns[i] = n; S2[i] = s2; D1s[i] = gb;
+    }
+    __syncthreads();
+    for (int i = warp; i < KP; i += UPD_THREADS / 32) {
+      const float ni = Ns[i];
       float c = 0.f;
-      for (int j = lane; j < k; j += 32) {
+      for (int j = lane; j < KP; j += 32) {
         float l = 0.f;
-        if (j < i) {
-          const float s2 = fmaxf(GC[(size_t)j * k + j], p.rho);
-          const float ga = GA[(size_t)i * k + j];
-          l = gbii * ga / s2;
-          c = fmaf(ga, GC[(size_t)i * k + j] / s2, c);
+        if (i < k && j < i) {
+          const float ga = ni * Ns[j] * rA[i * KP + j];
+          const float gc = ni * rC[i * KP + j];
+          l = D1s[i] * ga / S2[j];
+          c = fmaf(ga, gc / S2[j], c);
         }
-        p.coef[(size_t)j * k + i] = l;       // Lt[j][i]
+        Lt[j * KP + i] = l;
       }
       c = warp_sum(c);
-      if (lane == 0) {
-        p.coef[(size_t)k * k + i] = gbii;                              // D1
-        p.coef[(size_t)k * k + k + i] = GA[(size_t)i * k + i] - c;     // D2
+      if (lane == 0) D2s[i] = i < k ? ni * ni * rA[i * KP + i] - c : 0.f;
+    }
+    if (blockIdx.x == 0) {
+      // diagnostics: normalised tables of the iteration-start state
+      for (int e = tid; e < k * k; e += UPD_THREADS) {
+        const int i = e / k, j = e % k;
+        const bool low = j <= i;
+        p.gram[e] = low ? rsqrtf(rN[i]) * rsqrtf(rN[j]) * rA[i * KP + j] : 0.f;
+        p.gram[(size_t)k * k + e] = (i == j) ? rB[i] / rN[i] : 0.f;
+        p.gram[2 * (size_t)k * k + e] = low ? rsqrtf(rN[i]) * rC[i * KP + j] : 0.f;
       }
     }
+    __syncthreads();
   }
-  grid.sync();
-  stamp(p, 3);
 
-  // ---------------- phase 3: grad, v', aux' ----------------
-  float* Lt = smem + 8 * TILE;                   // [KP][KP]  Lt[j][i]
-  float* D1s = Lt + KP * KP;
-  float* D2s = D1s + KP;
-  float* Ns = D2s + KP;
-  float* red = Ns + KP;                          // [8][32]
-  for (int e = tid; e < KP * KP; e += UPD_THREADS) {
-    const int j = e / KP, i = e % KP;
-    Lt[e] = (i < k && j < k) ? p.coef[(size_t)j * k + i] : 0.f;
-  }
-  for (int e = tid; e < KP; e += UPD_THREADS) {
-    D1s[e] = e < k ? p.coef[(size_t)k * k + e] : 0.f;
-    D2s[e] = e < k ? p.coef[(size_t)k * k + k + e] : 0.f;
-    Ns[e] = 0.f;
-  }
-  __syncthreads();
+  // ---------------- phase 3b: grad, v'' and [Bv]' for this CTA's columns ----------------
   {
     const int tx = tid & 7;            // columns 4tx..4tx+3 of the sub-chunk
     const int tr = tid >> 3;           // rows 4tr..4tr+3
@@ -337,100 +357,73 @@ update_kernel(UpdateArgs p) {
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const int i = i0 + a;
-        float sq = 0.f;
         if (i < k && gx < c1) {
           const float4 av = *reinterpret_cast<const float4*>(At + i * UPD_S + 4 * tx);
           const float4 bv = *reinterpret_cast<const float4*>(Bt + i * UPD_S + 4 * tx);
           const float4 vv = *reinterpret_cast<const float4*>(Vt + i * UPD_S + 4 * tx);
           const float4 xa = *reinterpret_cast<const float4*>(Ct + i * UPD_S + 4 * tx);
-          const float d1 = D1s[i], d2 = D2s[i];
+          const float ni = Ns[i];
+          const float d1 = D1s[i] * ni, d2 = D2s[i] * ni;
           float4 vn, an;
-          vn.x = vv.x + p.eta * (d1 * av.x - d2 * bv.x - acc[a][0]);
-          vn.y = vv.y + p.eta * (d1 * av.y - d2 * bv.y - acc[a][1]);
-          vn.z = vv.z + p.eta * (d1 * av.z - d2 * bv.z - acc[a][2]);
-          vn.w = vv.w + p.eta * (d1 * av.w - d2 * bv.w - acc[a][3]);
-          an.x = xa.x + p.gamma * (bv.x - xa.x);
-          an.y = xa.y + p.gamma * (bv.y - xa.y);
-          an.z = xa.z + p.gamma * (bv.z - xa.z);
-          an.w = xa.w + p.gamma * (bv.w - xa.w);
-          const size_t o = (size_t)i * d;
+          vn.x = ni * vv.x + p.eta * (d1 * av.x - d2 * bv.x - acc[a][0]);
+          vn.y = ni * vv.y + p.eta * (d1 * av.y - d2 * bv.y - acc[a][1]);
+          vn.z = ni * vv.z + p.eta * (d1 * av.z - d2 * bv.z - acc[a][2]);
+          vn.w = ni * vv.w + p.eta * (d1 * av.w - d2 * bv.w - acc[a][3]);
+          an.x = xa.x + p.gamma * (ni * bv.x - xa.x);
+          an.y = xa.y + p.gamma * (ni * bv.y - xa.y);
+          an.z = xa.z + p.gamma * (ni * bv.z - xa.z);
+          an.w = xa.w + p.gamma * (ni * bv.w - xa.w);
+          const size_t o = (size_t)i * d + gx;
           if (VEC && gx + 3 < c1) {
-            *reinterpret_cast<float4*>(p.Vtmp + o + gx) = vn;
-            *reinterpret_cast<float4*>(p.AUX + o + gx) = an;
+            *reinterpret_cast<float4*>(p.V + o) = vn;
+            *reinterpret_cast<float4*>(p.AUX + o) = an;
+            if (p.Vbf) {
+              __nv_bfloat162 lo = __floats2bfloat162_rn(vn.x, vn.y), hi = __floats2bfloat162_rn(vn.z, vn.w);
+              uint2 pk;
+              pk.x = *reinterpret_cast<uint32_t*>(&lo);
+              pk.y = *reinterpret_cast<uint32_t*>(&hi);
+              *reinterpret_cast<uint2*>(p.Vbf + o) = pk;
+            }
           } else {
             const float vs[4] = {vn.x, vn.y, vn.z, vn.w}, as[4] = {an.x, an.y, an.z, an.w};
             for (int t = 0; t < 4; ++t)
-              if (gx + t < c1) { p.Vtmp[o + gx + t] = vs[t]; p.AUX[o + gx + t] = as[t]; }
+              if (gx + t < c1) {
+                p.V[o + t] = vs[t];
+                p.AUX[o + t] = as[t];
+                if (p.Vbf) p.Vbf[o + t] = __float2bfloat16_rn(vs[t]);
+              }
           }
-          // zero-filled columns past the range give vn = 0 automatically
-          sq = vn.x * vn.x + vn.y * vn.y + vn.z * vn.z + vn.w * vn.w;
         }
-        sq += __shfl_xor_sync(0xffffffffu, sq, 1);
-        sq += __shfl_xor_sync(0xffffffffu, sq, 2);
-        sq += __shfl_xor_sync(0xffffffffu, sq, 4);
-        if (tx == 0 && i < k) Ns[i] += sq;
       }
       __syncthreads();
     }
     cp_async_wait<0>();
   }
-  for (int e = tid; e < k; e += UPD_THREADS) p.norm_partial[(size_t)blockIdx.x * k + e] = Ns[e];
-  grid.sync();
-  stamp(p, 4);
+  stamp(p, 3);
+}
 
-  // ---------------- phase 4: retraction v <- v'/||v'|| ----------------
-  for (int r0 = 0; r0 < k; r0 += 32) {
-    const int i = r0 + lane;
-    float s0 = 0.f, s1 = 0.f;
-    if (i < k) {
-      int b = warp;
-      for (; b + 8 < (int)gridDim.x; b += 16) {
-        s0 += p.norm_partial[(size_t)b * k + i];
-        s1 += p.norm_partial[(size_t)(b + 8) * k + i];
-      }
-      if (b < (int)gridDim.x) s0 += p.norm_partial[(size_t)b * k + i];
-    }
-    red[warp * 32 + lane] = s0 + s1;
-    __syncthreads();
-    if (warp == 0 && i < k) {
-      float s = 0.f;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) s += red[w * 32 + lane];
-      Ns[i] = rsqrtf(s);
-    }
-    __syncthreads();
+// geig_get: the stored state is v'' = v + eta grad (the retraction is folded
+// into the next update); return the retracted v = v'' / ||v''|| (one CTA per row).
+__global__ void __launch_bounds__(256)
+normalize_rows_kernel(const float* __restrict__ Vin, float* __restrict__ Vout, int64_t d) {
+  __shared__ float red[8];
+  const int i = blockIdx.x;
+  float s = 0.f;
+  for (int64_t x = threadIdx.x; x < d; x += blockDim.x) {
+    const float v = Vin[(int64_t)i * d + x];
+    s = fmaf(v, v, s);
   }
-  if (c1 > c0) {
-    const int64_t w = c1 - c0;
-    if (VEC) {
-      const int64_t nq = w / 4;
-      for (int64_t e = tid; e < (int64_t)k * nq; e += UPD_THREADS) {
-        const int r = (int)(e / nq);
-        const int64_t gx = c0 + 4 * (e % nq);
-        const size_t o = (size_t)r * d + gx;
-        float4 v = *reinterpret_cast<const float4*>(p.Vtmp + o);
-        const float sc = Ns[r];
-        v.x *= sc; v.y *= sc; v.z *= sc; v.w *= sc;
-        *reinterpret_cast<float4*>(p.V + o) = v;
-        if (p.Vbf) {
-          __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
-          uint2 pk;
-          pk.x = *reinterpret_cast<uint32_t*>(&lo);
-          pk.y = *reinterpret_cast<uint32_t*>(&hi);
-          *reinterpret_cast<uint2*>(p.Vbf + o) = pk;
-        }
-      }
-    } else {
-      for (int64_t e = tid; e < (int64_t)k * w; e += UPD_THREADS) {
-        const int r = (int)(e / w);
-        const size_t o = (size_t)r * d + c0 + (e % w);
-        const float v = p.Vtmp[o] * Ns[r];
-        p.V[o] = v;
-        if (p.Vbf) p.Vbf[o] = __float2bfloat16_rn(v);
-      }
-    }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = rsqrtf(t);
   }
-  stamp(p, 5);
+  __syncthreads();
+  const float inv = red[0];
+  for (int64_t x = threadIdx.x; x < d; x += blockDim.x) Vout[(int64_t)i * d + x] = Vin[(int64_t)i * d + x] * inv;
 }
 
 // Alg. 2 lines 2-3: v_i = g_i / ||g_i||, [Bv]_i = v_i.  One CTA per player.

@@ -35,6 +35,6 @@ for it in range(30):
         prod.append(e0.elapsed_time(e1) * 1e3); upd.append(e1.elapsed_time(e2) * 1e3)
         phases.append(geig.geig_update_phase_ns(s.h))
 print(f"config {cfg.index} {math}: products {statistics.median(prod):.1f} us, update {statistics.median(upd):.1f} us")
-names = ["gram", "reduce", "coef", "update", "retract"]
+names = ["gram", "reduce", "coef+update"]
 for j, n in enumerate(names):
     print(f"  phase {n:8s} {statistics.median(p[j] for p in phases)/1e3:8.2f} us")
