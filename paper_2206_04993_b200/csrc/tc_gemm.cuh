@@ -28,7 +28,7 @@ namespace geig { namespace tc {
 
 constexpr int TC_THREADS = 128;
 constexpr int TC_BM = 128;
-constexpr int TC_STAGES = 4;
+constexpr int TC_MAX_STAGES = 8;
 constexpr int TC_MAX_SPLITS = 8;
 
 // ----------------------------------------------------------------------------
@@ -127,7 +127,7 @@ struct TcParams {
   uint32_t idesc;
 };
 
-template <int EB, bool A_MN>
+template <int EB, bool A_MN, int TC_STAGES>
 __global__ void __launch_bounds__(TC_THREADS)
 tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   constexpr int ATOM = 128 / EB;           // elements per 128B row
@@ -350,24 +350,39 @@ inline uint32_t make_idesc(int eb, bool a_mn, int N, int M) {
          ((uint32_t)(M >> 4) << 24);
 }
 
-inline size_t smem_bytes(int BN) {
-  return 1024 + (size_t)TC_STAGES * (TC_BM * 128 + (size_t)BN * 128) + 256;
+inline size_t smem_bytes(int BN, int stages) {
+  return 1024 + (size_t)stages * (TC_BM * 128 + (size_t)BN * 128) + 256;
 }
 
+// Stage count: enough bytes in flight per SM to cover DRAM latency. One
+// resident CTA per SM (grid <= #SM) gets 8 stages, denser grids 4.
 template <int EB, bool A_MN>
-inline geig_status launch(const TcMaps& maps, const TcParams& p, dim3 grid, cudaStream_t st) {
-  const size_t sm = smem_bytes(p.BN);
-  static bool attr_done = false;
-  if (!attr_done) {
-    if (cudaFuncSetAttribute(tc_gemm_kernel<EB, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem_bytes(128)) != cudaSuccess)
-      return tc_fail(GEIG_ERR_CUDA, "cudaFuncSetAttribute(tc_gemm_kernel) failed");
-    attr_done = true;
+inline geig_status launch(const TcMaps& maps, const TcParams& p, dim3 grid, cudaStream_t st, int nsm) {
+  const int ctas = grid.x * grid.y * grid.z;
+  const bool deep = ctas <= nsm && smem_bytes(p.BN, 8) <= 227 * 1024;
+  static bool attr_done[2] = {false, false};
+  if (!attr_done[deep]) {
+    cudaError_t e = deep ? cudaFuncSetAttribute(tc_gemm_kernel<EB, A_MN, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem_bytes(128, 8) > 227 * 1024 ? 227 * 1024 : (int)smem_bytes(128, 8))
+                         : cudaFuncSetAttribute(tc_gemm_kernel<EB, A_MN, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)smem_bytes(128, 4));
+    if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, "cudaFuncSetAttribute(tc_gemm_kernel) failed");
+    attr_done[deep] = true;
   }
-  tc_gemm_kernel<EB, A_MN><<<grid, TC_THREADS, sm, st>>>(maps, p);
+  if (deep)
+    tc_gemm_kernel<EB, A_MN, 8><<<grid, TC_THREADS, smem_bytes(p.BN, 8), st>>>(maps, p);
+  else
+    tc_gemm_kernel<EB, A_MN, 4><<<grid, TC_THREADS, smem_bytes(p.BN, 4), st>>>(maps, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("tc_gemm launch: ") + cudaGetErrorString(e));
   return GEIG_OK;
+}
+
+// largest power-of-two split keeping the grid within one CTA per SM
+inline int choose_splits_deep(int ctas, int kblocks, int nsm) {
+  int s = 1;
+  while (ctas * (s * 2) <= nsm && s * 2 <= kblocks) s *= 2;
+  return s;
 }
 
 inline int choose_splits(int ctas, int kblocks, int nsm) {
@@ -444,10 +459,10 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
     p.split_stride = (int64_t)2 * k * t.ldz;
     p.idesc = make_idesc(eb, false, t.BN, TC_BM);
     const int mt = (rows + TC_BM - 1) / TC_BM;
-    p.splits = std::min(TC_MAX_SPLITS, choose_splits(2 * mt, std::min(p.kblocks[0][0], p.kblocks[1][0]), t.nsm));
+    p.splits = std::min(TC_MAX_SPLITS, choose_splits_deep(2 * mt, std::min(p.kblocks[0][0], p.kblocks[1][0]), t.nsm));
     fsplits = p.splits;
     dim3 grid(mt, p.splits, 2);
-    geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st) : launch<4, false>(maps, p, grid, st);
+    geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st, t.nsm) : launch<4, false>(maps, p, grid, st, t.nsm);
     if (s) return s;
     ++*nl;
   }
@@ -494,7 +509,7 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
         return tc_fail(GEIG_ERR_CUDA, "memset AV/BV failed");
     }
     dim3 grid(mt, p.splits, 2);
-    geig_status s = eb == 2 ? launch<2, true>(maps, p, grid, st) : launch<4, true>(maps, p, grid, st);
+    geig_status s = eb == 2 ? launch<2, true>(maps, p, grid, st, t.nsm) : launch<4, true>(maps, p, grid, st, t.nsm);
     if (s) return s;
     ++*nl;
   }
@@ -538,7 +553,7 @@ inline geig_status products_dense(TcPlan& t, const void* A, const void* B, int64
         return tc_fail(GEIG_ERR_CUDA, "memset AV/BV rows failed");
   }
   dim3 grid(mt, p.splits, 2);
-  geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st) : launch<4, false>(maps, p, grid, st);
+  geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st, t.nsm) : launch<4, false>(maps, p, grid, st, t.nsm);
   if (s) return s;
   ++*nl;
   return GEIG_OK;
