@@ -389,3 +389,8 @@ extern "C" geig_status geig_update_phase_ns(geig_solver* s, int64_t* out) {
   out[3] = out[4] = 0;
   return GEIG_OK;
 }
+
+// Developer hook (not part of the documented ABI): per-CTA %globaltimer stamps
+// of the tensor-core product kernels are written to `buf` (4 x uint64 per CTA,
+// launch after launch overwrite), NULL disables.
+extern "C" void geig_debug_set_tc_stamps(void* buf) { tc::dbg_ptr() = (unsigned long long*)buf; }

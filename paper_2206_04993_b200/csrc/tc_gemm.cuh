@@ -125,7 +125,14 @@ struct TcParams {
   int atomic;          // 1: red.add, 0: store
   int64_t split_stride;  // store mode with splits > 1: output offset per split (elements)
   uint32_t idesc;
+  unsigned long long* dbg; // optional per-CTA %globaltimer stamps (4 per CTA), nullable
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <int EB, bool A_MN, int TC_STAGES>
 __global__ void __launch_bounds__(TC_THREADS)
@@ -149,6 +156,8 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t cta_id = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  if (p.dbg && threadIdx.x == 0) p.dbg[cta_id * 4 + 0] = gtimer();
   // per-segment K-block ranges of this split
   int kb_beg[2], kb_cnt[2];
   int total = 0;
@@ -216,6 +225,7 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
         for (int j = 0; j < kb_cnt[s]; ++j, ++it) {
           const int st = it % TC_STAGES;
           mbar_wait(&full_bar[st], (it / TC_STAGES) & 1);
+          if (p.dbg && it == 0) p.dbg[cta_id * 4 + 1] = gtimer();
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + st * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
@@ -234,6 +244,7 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
         }
       }
       umma_commit(accum_bar);
+      if (p.dbg) p.dbg[cta_id * 4 + 2] = gtimer();
     }
     // ---------------- epilogue (all 4 warps) ----------------
     mbar_wait(accum_bar, 0);
@@ -262,6 +273,7 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   }
   tc_fence_before();
   __syncthreads();
+  if (p.dbg && threadIdx.x == 0) p.dbg[cta_id * 4 + 3] = gtimer();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
@@ -305,6 +317,11 @@ struct TcPlan {
   float* Zt = nullptr;     // TC_MAX_SPLITS x 2 x k x ldz fp32 (CCA forward split-K partials)
   void* Zb = nullptr;      // 2 x 2 x k x hpad (bf16 or fp32)
 };
+
+inline unsigned long long*& dbg_ptr() {
+  static unsigned long long* p = nullptr;
+  return p;
+}
 
 inline std::string& err_str() {
   static thread_local std::string e;
@@ -359,6 +376,7 @@ inline size_t smem_bytes(int BN, int stages) {
 template <int EB, bool A_MN>
 inline geig_status launch(const TcMaps& maps, const TcParams& p, dim3 grid, cudaStream_t st, int nsm) {
   const int ctas = grid.x * grid.y * grid.z;
+  const_cast<TcParams&>(p).dbg = dbg_ptr();
   const bool deep = ctas <= nsm && smem_bytes(p.BN, 8) <= 227 * 1024;
   static bool attr_done[2] = {false, false};
   if (!attr_done[deep]) {
