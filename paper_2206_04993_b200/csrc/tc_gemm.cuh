@@ -244,10 +244,10 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
         }
       }
       umma_commit(accum_bar);
-      if (p.dbg) p.dbg[cta_id * 4 + 2] = gtimer();
     }
     // ---------------- epilogue (all 4 warps) ----------------
     mbar_wait(accum_bar, 0);
+    if (p.dbg && threadIdx.x == 0) p.dbg[cta_id * 4 + 2] = gtimer();
     tc_fence_after();
     const int m = m0 + warp * 32 + lane;
     const bool mok = m < p.M[g];

@@ -31,6 +31,6 @@ for which in ("forward", "backward"):
     st = ((t - t0).double() / 1e3)
     print(f"last launch ({len(t)} CTAs): start [{st[:,0].min():.1f},{st[:,0].max():.1f}] "
           f"first-data med {statistics.median(st[:,1].tolist()):.1f} "
-          f"last-commit med {statistics.median(st[:,2].tolist()):.1f} max {st[:,2].max():.1f} "
+          f"accum-ready med {statistics.median(st[:,2].tolist()):.1f} max {st[:,2].max():.1f} "
           f"end med {statistics.median(st[:,3].tolist()):.1f} max {st[:,3].max():.1f} us")
     break
