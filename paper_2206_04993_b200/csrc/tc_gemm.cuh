@@ -377,6 +377,7 @@ template <int EB, bool A_MN>
 inline geig_status launch(const TcMaps& maps, const TcParams& p, dim3 grid, cudaStream_t st, int nsm) {
   const int ctas = grid.x * grid.y * grid.z;
   const_cast<TcParams&>(p).dbg = dbg_ptr();
+  if (dbg_ptr()) dbg_ptr() += (size_t)4 * ctas;   // next launch stamps after this one
   const bool deep = ctas <= nsm && smem_bytes(p.BN, 8) <= 227 * 1024;
   static bool attr_done[2] = {false, false};
   if (!attr_done[deep]) {

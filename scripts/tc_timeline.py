@@ -18,19 +18,19 @@ lib.geig_debug_set_tc_stamps.argtypes = [ctypes.c_void_p]
 for it in range(3):
     geig.geig_products_cca(s.h, X[:b], Y[:b], b, 1.0 / (b // 2), AV, BV)
 torch.cuda.synchronize()
-for which in ("forward", "backward"):
-    buf = torch.zeros(4 * 4096, dtype=torch.int64, device=dev)
-    lib.geig_debug_set_tc_stamps(ctypes.c_void_p(buf.data_ptr()))
-    # products = forward, shuffle, backward: capture both by running twice and reading after each
-    geig.geig_products_cca(s.h, X[b:2*b], Y[b:2*b], b, 1.0 / (b // 2), AV, BV)
-    torch.cuda.synchronize()
-    lib.geig_debug_set_tc_stamps(None)
-    t = buf.view(-1, 4).cpu()
-    t = t[t[:, 0] > 0]
-    t0 = t[:, 0].min().item()
-    st = ((t - t0).double() / 1e3)
-    print(f"last launch ({len(t)} CTAs): start [{st[:,0].min():.1f},{st[:,0].max():.1f}] "
+buf = torch.zeros(4 * 8192, dtype=torch.int64, device=dev)
+lib.geig_debug_set_tc_stamps(ctypes.c_void_p(buf.data_ptr()))
+geig.geig_products_cca(s.h, X[b:2*b], Y[b:2*b], b, 1.0 / (b // 2), AV, BV)
+torch.cuda.synchronize()
+lib.geig_debug_set_tc_stamps(None)
+t = buf.view(-1, 4).cpu()
+t0 = t[t[:, 0] > 0][:, 0].min().item()
+off = 0
+for name, n in (("forward", 128), ("backward", 128)):
+    tt = t[off:off + n]
+    off += n
+    st = ((tt - t0).double() / 1e3)
+    print(f"{name} ({n} CTAs): start [{st[:,0].min():.1f},{st[:,0].max():.1f}] "
           f"first-data med {statistics.median(st[:,1].tolist()):.1f} "
           f"accum-ready med {statistics.median(st[:,2].tolist()):.1f} max {st[:,2].max():.1f} "
           f"end med {statistics.median(st[:,3].tolist()):.1f} max {st[:,3].max():.1f} us")
-    break
