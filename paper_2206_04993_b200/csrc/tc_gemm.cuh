@@ -113,9 +113,9 @@ struct TcMaps {
 };
 
 struct TcParams {
-  int M[2];            // valid rows per group
-  int N;               // valid columns (players)
-  int BN;              // MMA N (multiple of 16, <= 128)
+  int M[2];            // valid rows per group (host-side arrays; the kernel
+  int N;               //   selects with blockIdx.z-uniform ternaries, never
+  int BN;              //   runtime-indexes the parameter block)
   int nseg;            // 1 or 2
   int kblocks[2][2];   // [group][segment] K blocks
   int splits;          // split-K factor (blockIdx.y)
@@ -143,7 +143,8 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   constexpr uint32_t A_BYTES = TC_BM * 128;
   const int g = blockIdx.z;
   const int m0 = blockIdx.x * TC_BM;
-  if (m0 >= p.M[g]) return;
+  const int Mg = g == 0 ? p.M[0] : p.M[1];
+  if (m0 >= Mg) return;
   const int BN = p.BN;
   const uint32_t B_BYTES = (uint32_t)BN * 128;
   const uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -162,7 +163,8 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   int kb_beg[2], kb_cnt[2];
   int total = 0;
   for (int s = 0; s < 2; ++s) {
-    const int kb = s < p.nseg ? p.kblocks[g][s] : 0;
+    const int kb = s >= p.nseg ? 0 : (g == 0 ? (s == 0 ? p.kblocks[0][0] : p.kblocks[0][1])
+                                             : (s == 0 ? p.kblocks[1][0] : p.kblocks[1][1]));
     const int b0 = (int)((int64_t)kb * blockIdx.y / p.splits);
     const int b1 = (int)((int64_t)kb * (blockIdx.y + 1) / p.splits);
     kb_beg[s] = b0;
@@ -246,29 +248,52 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
       umma_commit(accum_bar);
     }
     // ---------------- epilogue (all 4 warps) ----------------
+    // TMEM -> registers -> smem tile[n][m] (the idle pipeline buffers) ->
+    // coalesced 16-byte stores (or red.global.add.v4.f32 for split-K) of
+    // whole 512-byte output rows out[n][m0 .. m0+127].
     mbar_wait(accum_bar, 0);
     if (p.dbg && threadIdx.x == 0) p.dbg[cta_id * 4 + 2] = gtimer();
+    __syncwarp();
     tc_fence_after();
-    const int m = m0 + warp * 32 + lane;
-    const bool mok = m < p.M[g];
+    float* tile = reinterpret_cast<float*>(smem);          // [BN][TC_BM]
+    const float scale = p.scale;
+    const int N = p.N;
+    const int64_t ldo = p.ldo;
+    const bool atomic = p.atomic != 0;
+    const int64_t soff = atomic ? 0 : (int64_t)blockIdx.y * p.split_stride;
     for (int s = 0; s < p.nseg; ++s) {
       if (kb_cnt[s] == 0) continue;
-      float* out = p.out[g][s] + (p.atomic ? 0 : (int64_t)blockIdx.y * p.split_stride);
+      float* out = (g == 0 ? (s == 0 ? p.out[0][0] : p.out[0][1]) : (s == 0 ? p.out[1][0] : p.out[1][1])) + soff;
       for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t r[16];
         tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(s * BN + c0), r);
-        if (mok) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int n = c0 + j;
-            if (n < p.N) {
-              float* dst = out + (int64_t)n * p.ldo + m;
-              const float v = p.scale * __uint_as_float(r[j]);
-              if (p.atomic) atomicAdd(dst, v); else *dst = v;
+        for (int j = 0; j < 16; ++j) tile[(c0 + j) * TC_BM + warp * 32 + lane] = __uint_as_float(r[j]);
+      }
+      __syncthreads();
+      const int mm = m0 + 4 * lane;
+      const bool vec = ((ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+      for (int n = warp; n < N; n += 4) {
+        float4 v = *reinterpret_cast<const float4*>(tile + n * TC_BM + 4 * lane);
+        v.x *= scale; v.y *= scale; v.z *= scale; v.w *= scale;
+        float* dst = out + (int64_t)n * ldo + mm;
+        if (vec && mm + 3 < Mg) {
+          if (atomic)
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z),
+                         "f"(v.w)
+                         : "memory");
+          else
+            *reinterpret_cast<float4*>(dst) = v;
+        } else {
+          const float vs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (mm + q < Mg) {
+              if (atomic) atomicAdd(dst + q, vs[q]); else dst[q] = vs[q];
             }
-          }
         }
       }
+      __syncthreads();
     }
   }
   tc_fence_before();
