@@ -311,10 +311,51 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
 //   X backward: half0 (A_t) uses Z_y rows [0,h), half1 (B_t) uses Z_x rows [h,2h)
 //   Y backward: half0 uses Z_x rows [0,h), half1 uses Z_y rows [h,2h)
 template <typename T>
+__device__ __forceinline__ void store4(T* dst, float a, float b, float c, float d);
+template <>
+__device__ __forceinline__ void store4<float>(float* dst, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(dst) = make_float4(a, b, c, d);
+}
+template <>
+__device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* dst, float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 pk;
+  pk.x = *reinterpret_cast<uint32_t*>(&lo);
+  pk.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(dst) = pk;
+}
+
+template <typename T>
 __global__ void zshuffle_kernel(const float* __restrict__ Zp, T* __restrict__ Zb, int k, int64_t ldz, int h,
                                 int64_t hpad, int splits) {
-  const int64_t per = (int64_t)k * h;
   const int64_t vstride = (int64_t)k * ldz;
+  const int64_t plane = (int64_t)k * hpad;
+  const bool vec = ((h & 3) == 0) && ((ldz & 3) == 0) && ((hpad & 3) == 0);
+  if (vec) {
+    const int hq = h / 4;
+    const int64_t per = (int64_t)k * hq;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x) {
+      const int n = (int)(e / hq), r = 4 * (int)(e % hq);
+      float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0, y0 = x0, y1 = x0;
+      for (int sp = 0; sp < splits; ++sp) {
+        const float* zx = Zp + (int64_t)(2 * sp) * vstride + (int64_t)n * ldz;
+        const float* zy = zx + vstride;
+        const float4 a = *reinterpret_cast<const float4*>(zx + r), b = *reinterpret_cast<const float4*>(zx + h + r);
+        const float4 c = *reinterpret_cast<const float4*>(zy + r), d = *reinterpret_cast<const float4*>(zy + h + r);
+        x0.x += a.x; x0.y += a.y; x0.z += a.z; x0.w += a.w;
+        x1.x += b.x; x1.y += b.y; x1.z += b.z; x1.w += b.w;
+        y0.x += c.x; y0.y += c.y; y0.z += c.z; y0.w += c.w;
+        y1.x += d.x; y1.y += d.y; y1.z += d.z; y1.w += d.w;
+      }
+      const int64_t o = (int64_t)n * hpad + r;
+      store4<T>(Zb + 0 * plane + o, y0.x, y0.y, y0.z, y0.w);   // view x, half 0
+      store4<T>(Zb + 1 * plane + o, x1.x, x1.y, x1.z, x1.w);   // view x, half 1
+      store4<T>(Zb + 2 * plane + o, x0.x, x0.y, x0.z, x0.w);   // view y, half 0
+      store4<T>(Zb + 3 * plane + o, y1.x, y1.y, y1.z, y1.w);   // view y, half 1
+    }
+    return;
+  }
+  const int64_t per = (int64_t)k * h;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x) {
     const int n = (int)(e / h), r = (int)(e % h);
     float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
@@ -324,11 +365,10 @@ __global__ void zshuffle_kernel(const float* __restrict__ Zp, T* __restrict__ Zb
       x0 += zx[r]; x1 += zx[h + r]; y0 += zy[r]; y1 += zy[h + r];
     }
     const int64_t o = (int64_t)n * hpad + r;
-    const int64_t plane = (int64_t)k * hpad;
-    Zb[0 * plane + o] = (T)y0;     // view x, half 0
-    Zb[1 * plane + o] = (T)x1;     // view x, half 1
-    Zb[2 * plane + o] = (T)x0;     // view y, half 0
-    Zb[3 * plane + o] = (T)y1;     // view y, half 1
+    Zb[0 * plane + o] = (T)y0;
+    Zb[1 * plane + o] = (T)x1;
+    Zb[2 * plane + o] = (T)x0;
+    Zb[3 * plane + o] = (T)y1;
   }
 }
 
@@ -512,8 +552,8 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
   }
   // ---- reshuffle: sum split partials -> Zb halves ----
   {
-    const int64_t per = (int64_t)k * h;
-    const int blocks = (int)std::min<int64_t>(1184, (per + 255) / 256);
+    const int64_t per = (int64_t)k * h / 4 + 1;
+    const int blocks = (int)std::min<int64_t>(4 * t.nsm, (per + 255) / 256);
     if (eb == 2)
       zshuffle_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(t.Zt, (__nv_bfloat16*)t.Zb, k, t.ldz, h, t.hpad, fsplits);
     else
