@@ -1,0 +1,118 @@
+"""World-size-2 gloo tests of the multi-GPU host logic (parallel.py) on CPU:
+row sharding, the Appendix-F all-reduce of partial products and identical
+replicated updates.  The per-rank compute is injected (here: the oracle's
+product form), exactly where the product path injects the CUDA binding."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2206_04993_b200.parallel import ShardedStep, cca_scale, dense_allgather_rows, shard_rows
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, x, y, V, aux, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import estimators, game
+        b_local = x.shape[0] // world
+        xs = x[rank * b_local:(rank + 1) * b_local]
+        ys = y[rank * b_local:(rank + 1) * b_local]
+        h = b_local // 2
+        scale = cca_scale(b_local, world)
+        state = {"V": V.copy(), "aux": aux.copy()}
+
+        def products(AV, BV):
+            # per-rank partial sums, scaled so that the SUM over ranks is the estimate
+            av, bv = estimators.cca_products(xs.numpy(), ys.numpy(), state["V"])
+            AV.copy_(torch.from_numpy(av * h * scale))
+            BV.copy_(torch.from_numpy(bv * h * scale))
+
+        def update(AV, BV):
+            state["V"], state["aux"] = game.step_alg2(state["V"], state["aux"], [(AV.numpy(), BV.numpy())],
+                                                      0.1, 0.5, 1e-3)
+
+        step = ShardedStep(products, update)
+        AV = torch.zeros(V.shape, dtype=torch.float64)
+        BV = torch.zeros_like(AV)
+        step(AV, BV)
+        out_q.put((rank, AV.numpy().copy(), state["V"], state["aux"]))
+        # dense row sharding: each rank writes its columns, all-reduce assembles
+        d = 10
+        rng = np.random.default_rng(0)
+        A = rng.standard_normal((d, d)); A = A + A.T
+        W = rng.standard_normal((3, d))
+        r0, r1 = shard_rows(d, world, rank)
+        AVd = torch.zeros(3, d, dtype=torch.float64)
+        BVd = torch.zeros_like(AVd)
+        AVd[:, r0:r1] = torch.from_numpy((A[r0:r1] @ W.T).T)
+        BVd[:, r0:r1] = torch.from_numpy((2 * A[r0:r1] @ W.T).T)
+        dense_allgather_rows(AVd, BVd, d, world)
+        out_q.put((rank + 100, AVd.numpy(), (A @ W.T).T, None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_rows_partition():
+    for n in [1, 7, 16, 4097]:
+        for w in [1, 2, 3, 8]:
+            rs = [shard_rows(n, w, r) for r in range(w)]
+            assert rs[0][0] == 0 and rs[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+            sizes = [r1 - r0 for r0, r1 in rs]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_gloo_world2_allreduce_matches_global_batch():
+    from oracle import estimators, game
+    world = 2
+    rng = np.random.default_rng(3)
+    b_local, dx, dy, k = 40, 6, 5, 3
+    x = torch.from_numpy(rng.standard_normal((world * b_local, dx)))
+    y = torch.from_numpy(rng.standard_normal((world * b_local, dy)))
+    V, aux = game.init_state(rng.standard_normal((k, dx + dy)))
+    aux = aux + 0.1 * rng.standard_normal(aux.shape)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, x, y, V, aux, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2 * world):
+        r, a, b, c = q.get(timeout=120)
+        res[r] = (a, b, c)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # global reference: A-halves of both ranks form the A batch, B-halves the B batch (reading R1)
+    h = b_local // 2
+    xa = torch.cat([x[r * b_local:r * b_local + h] for r in range(world)])
+    xb = torch.cat([x[r * b_local + h:(r + 1) * b_local] for r in range(world)])
+    ya = torch.cat([y[r * b_local:r * b_local + h] for r in range(world)])
+    yb = torch.cat([y[r * b_local + h:(r + 1) * b_local] for r in range(world)])
+    xg = torch.cat([xa, xb]).numpy()
+    yg = torch.cat([ya, yb]).numpy()
+    av, bv = estimators.cca_products(xg, yg, V)
+    V2, aux2 = game.step_alg2(V, aux, [(av, bv)], 0.1, 0.5, 1e-3)
+    for r in range(world):
+        AVr, Vr, auxr = res[r]
+        assert np.allclose(AVr, av, atol=1e-12)
+        assert np.allclose(Vr, V2, atol=1e-12) and np.allclose(auxr, aux2, atol=1e-12)
+    assert np.array_equal(res[0][1], res[1][1])        # replicas identical
+    for r in range(world):
+        got, ref, _ = res[100 + r]
+        assert np.allclose(got, ref, atol=1e-12)
