@@ -268,8 +268,17 @@ def run_gpu(args, cfg, rank, world, local_rank):
     alg_bytes = b * cfg.d * esz + cfg.k * cfg.d * (2 if math == "bf16" else 4) + 2 * cfg.k * cfg.d * 4
     achieved = alg_bytes / (prod_ms / 1e3) / 1e9
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
+            tr = json.load(f)
+        if tr.get("workload") == cfg.name and tr.get("math") == math:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-            "frac": achieved / hbm_peak, "traffic": None, "kernel": "products (forward+backward GEMMs)",
+            "frac": achieved / hbm_peak, "traffic": traffic, "algorithmic_bytes": alg_bytes,
+            "kernel": "products stage (tc_gemm forward + zshuffle + tc_gemm backward)",
             "peak_source": peaks_src, "ms_per_launch": prod_ms, "update_ms": upd_ms,
             "flops_per_step": 4.0 * cfg.k * cfg.d * b,
             "tensor_tflops": 4.0 * cfg.k * cfg.d * b / (prod_ms / 1e3) / 1e12}
