@@ -57,6 +57,7 @@ struct geig_solver {
   __nv_bfloat16 *Wxb = nullptr, *Wyb = nullptr;       // bf16 backward operands
   void *hX = nullptr, *hY = nullptr;                  // device staging for *_host
   int upd_grid = 1;
+  bool upd_res = false;                               // resident (k <= 64) update kernel
   int64_t upd_segw = 32;
   size_t upd_smem = 0;
   int64_t launches = 0;
@@ -103,7 +104,6 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
   ALLOC(s->AV, kd * 4);
   ALLOC(s->BV, kd * 4);
   ALLOC(s->gram, (size_t)3 * k * k * 4);
-  ALLOC(s->raw, upd_partial_floats(k <= 64 ? 1 : 2) * 4);
   ALLOC(s->ts, 8 * sizeof(unsigned long long));
   if (problem == GEIG_CCA) {
     const int64_t mr = ((max_rows + 127) / 128) * 128;
@@ -120,12 +120,25 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
 
   // cooperative update grid: one co-resident CTA per SM, contiguous column ranges
   {
-    const int NB = k <= 64 ? 1 : 2;
-    s->upd_smem = upd_smem_floats(NB) * 4;
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-    void* fns[2] = {NB == 1 ? (void*)update_kernel<1, true> : (void*)update_kernel<2, true>,
-                    NB == 1 ? (void*)update_kernel<1, false> : (void*)update_kernel<2, false>};
+    int64_t G = std::min<int64_t>(nsm, (s->d + UPD_XC - 1) / UPD_XC);
+    G = std::max<int64_t>(G, 1);
+    int64_t segw = (s->d + G - 1) / G;
+    const bool res = k <= 64 && ((segw + 7) / 8) * 8 <= UPD_RES_WMAX;
+    segw = res ? ((segw + 7) / 8) * 8 : ((segw + 3) / 4) * 4;
+    G = (s->d + segw - 1) / segw;
+    s->upd_grid = (int)G;
+    s->upd_segw = segw;
+    s->upd_res = res;
+    const int NB = k <= 64 ? 1 : 2;
+    s->upd_smem = res ? upd_res_smem_floats((int)segw) * 4 : upd_smem_floats(NB) * 4;
+    void* fns[2];
+    if (res) { fns[0] = (void*)update_res_kernel<true>; fns[1] = (void*)update_res_kernel<false>; }
+    else {
+      fns[0] = NB == 1 ? (void*)update_kernel<1, true> : (void*)update_kernel<2, true>;
+      fns[1] = NB == 1 ? (void*)update_kernel<1, false> : (void*)update_kernel<2, false>;
+    }
     for (void* fn : fns) {
       if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->upd_smem) != cudaSuccess)
         return cleanup(fail(GEIG_ERR_CUDA, "smem attribute for update kernel"));
@@ -133,14 +146,9 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, UPD_THREADS, s->upd_smem) != cudaSuccess || o < 1)
         return cleanup(fail(GEIG_ERR_CUDA, "update kernel cannot be co-resident"));
     }
-    int64_t G = std::min<int64_t>(nsm, (s->d + UPD_XC - 1) / UPD_XC);
-    G = std::max<int64_t>(G, 1);
-    int64_t segw = (s->d + G - 1) / G;
-    segw = ((segw + 3) / 4) * 4;
-    G = (s->d + segw - 1) / segw;
-    s->upd_grid = (int)G;
-    s->upd_segw = segw;
-    if (cudaMalloc((void**)&s->partial, (size_t)G * upd_partial_floats(NB) * 4) != cudaSuccess)
+    const size_t pfl = res ? (size_t)upd_raw_floats_res(k) : upd_partial_floats(NB);
+    if (cudaMalloc((void**)&s->partial, (size_t)G * pfl * 4) != cudaSuccess ||
+        cudaMalloc((void**)&s->raw, pfl * 4) != cudaSuccess)
       return cleanup(fail(GEIG_ERR_CUDA, "cudaMalloc gram partials"));
   }
   if (math != GEIG_MATH_F32) {
@@ -331,7 +339,8 @@ extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float*
   void* args[] = {&a};
   const bool vec = (s->d % 4 == 0) && (((uintptr_t)AV | (uintptr_t)BV) % 16 == 0);
   void* fn;
-  if (s->k <= 64) fn = vec ? (void*)update_kernel<1, true> : (void*)update_kernel<1, false>;
+  if (s->upd_res) fn = vec ? (void*)update_res_kernel<true> : (void*)update_res_kernel<false>;
+  else if (s->k <= 64) fn = vec ? (void*)update_kernel<1, true> : (void*)update_kernel<1, false>;
   else fn = vec ? (void*)update_kernel<2, true> : (void*)update_kernel<2, false>;
   CU(cudaLaunchCooperativeKernel(fn, dim3(s->upd_grid), dim3(UPD_THREADS), args, s->upd_smem, s->stream));
   s->launches++;

@@ -402,6 +402,271 @@ update_kernel(UpdateArgs p) {
   stamp(p, 3);
 }
 
+// ============================================================================
+// Resident variant (k <= 64): every CTA loads its four k x W tiles ONCE
+// (one cp.async burst, maximal memory-level parallelism), computes the Gram
+// partials and, after the two grid barriers, the update from the same
+// shared-memory tiles.  Compact lower-triangular reduction: raw layout
+// [tri(A) | tri(C) | diag B | diag V'V'] with tri(i,j) = i(i+1)/2 + j.
+// ============================================================================
+constexpr int UPD_RES_WMAX = 192;   // max columns per CTA (smem: 4 x 64 x 196 x 4 B)
+
+__host__ __device__ constexpr size_t upd_res_smem_floats(int W) {
+  return (size_t)4 * 64 * (W + 4) + 64 * 64 + 4 * 64 + 8 * 32;
+}
+__host__ __device__ constexpr int upd_raw_floats_res(int k) { return k * (k + 1) + 2 * k; }
+
+__device__ __forceinline__ int tri_index(int i, int j) { return i * (i + 1) / 2 + j; }
+
+template <bool VEC>
+__global__ void __launch_bounds__(UPD_THREADS, 1)
+update_res_kernel(UpdateArgs p) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) float smem[];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int k = p.k;
+  const int64_t d = p.d;
+  const int W = (int)p.segw;                     // multiple of 8
+  const int S = W + 4;                           // S/4 odd: conflict-free LDS.128 below
+  const int64_t c0 = (int64_t)blockIdx.x * W;
+  const int64_t c1 = min(d, c0 + W);
+  float* Vt = smem;
+  float* At = Vt + 64 * S;
+  float* Ct = At + 64 * S;
+  float* Bt = Ct + 64 * S;
+  float* Lt = Bt + 64 * S;                       // [64][64] Lt[j][i]
+  float* Ns = Lt + 64 * 64;
+  float* S2 = Ns + 64;
+  float* D1s = S2 + 64;
+  float* D2s = D1s + 64;
+  float* red = D2s + 64;                         // [8][32]
+  const int ntri = k * (k + 1) / 2;
+  const int ntot = 2 * ntri + 2 * k;             // partial / raw length
+  stamp(p, 0);
+
+  // ---------------- stage the four tiles once ----------------
+  {
+    const float* src[4] = {p.V, p.AV, p.AUX, p.BV};
+    float* dst[4] = {Vt, At, Ct, Bt};
+    if (VEC) {
+      const int Q = W / 4;
+      for (int e = tid; e < 4 * 64 * Q; e += UPD_THREADS) {
+        const int a = e / (64 * Q), rem = e % (64 * Q), r = rem / Q, q = rem % Q;
+        const int64_t gx = c0 + 4 * q;
+        const bool ok = r < k && gx < c1;
+        cp_async16(dst[a] + r * S + 4 * q, ok ? src[a] + (int64_t)r * d + gx : src[a], ok ? 16 : 0);
+      }
+    } else {
+      for (int e = tid; e < 4 * 64 * W; e += UPD_THREADS) {
+        const int a = e / (64 * W), rem = e % (64 * W), r = rem / W, x = rem % W;
+        const int64_t gx = c0 + x;
+        const bool ok = r < k && gx < c1;
+        cp_async4(dst[a] + r * S + x, ok ? src[a] + (int64_t)r * d + gx : src[a], ok ? 4 : 0);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+
+  // ---------------- phase 1: Gram partials ----------------
+  {
+    const int ti = tid & 15, tj = tid >> 4;
+    float accA[4][4], accC[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) accA[a][b] = accC[a][b] = 0.f;
+    for (int xq = 0; xq < W / 4; ++xq) {
+      float4 va[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) va[a] = *reinterpret_cast<const float4*>(Vt + (ti + 16 * a) * S + 4 * xq);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int j = tj + 16 * b;
+        const float4 pa = *reinterpret_cast<const float4*>(At + j * S + 4 * xq);
+        const float4 pc = *reinterpret_cast<const float4*>(Ct + j * S + 4 * xq);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          accA[a][b] = fmaf(va[a].x, pa.x, fmaf(va[a].y, pa.y, fmaf(va[a].z, pa.z, fmaf(va[a].w, pa.w, accA[a][b]))));
+          accC[a][b] = fmaf(va[a].x, pc.x, fmaf(va[a].y, pc.y, fmaf(va[a].z, pc.z, fmaf(va[a].w, pc.w, accC[a][b]))));
+        }
+      }
+    }
+    float* out = p.partial + (size_t)blockIdx.x * ntot;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = ti + 16 * a, j = tj + 16 * b;
+        if (i < k && j <= i) {
+          out[tri_index(i, j)] = accA[a][b];
+          out[ntri + tri_index(i, j)] = accC[a][b];
+        }
+      }
+    for (int i = warp; i < k; i += UPD_THREADS / 32) {
+      float gb = 0.f, nn = 0.f;
+      for (int x = lane; x < W; x += 32) {
+        const float v = Vt[i * S + x];
+        gb = fmaf(v, Bt[i * S + x], gb);
+        nn = fmaf(v, v, nn);
+      }
+      gb = warp_sum(gb);
+      nn = warp_sum(nn);
+      if (lane == 0) { out[2 * ntri + i] = gb; out[2 * ntri + k + i] = nn; }
+    }
+  }
+  grid.sync();
+  stamp(p, 1);
+
+  // ---------------- phase 2: reduce partials (compact entries) ----------------
+  // a CTA owns a contiguous entry range; lanes over entries, warps over the
+  // partial index; all loads of a thread issued before the adds.
+  {
+    const int G = gridDim.x;
+    const int per = (ntot + G - 1) / G;
+    const int e0 = blockIdx.x * per, e1 = min(ntot, e0 + per);
+    for (int eb = e0; eb < e1; eb += 32) {
+      const int e = eb + lane;
+      float vals[24];
+#pragma unroll
+      for (int t = 0; t < 24; ++t) {
+        const int b = warp + 8 * t;
+        vals[t] = (e < e1 && b < G) ? p.partial[(size_t)b * ntot + e] : 0.f;
+      }
+      float s = 0.f;
+#pragma unroll
+      for (int t = 0; t < 24; ++t) s += vals[t];
+      for (int b = warp + 8 * 24; b < G; b += 8) s += (e < e1) ? p.partial[(size_t)b * ntot + e] : 0.f;
+      red[warp * 32 + lane] = s;
+      __syncthreads();
+      if (warp == 0 && e < e1) {
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += red[w * 32 + lane];
+        p.raw[e] = t;
+      }
+      __syncthreads();
+    }
+  }
+  grid.sync();
+  stamp(p, 2);
+
+  // ---------------- phase 3a: coefficients ----------------
+  {
+    const float* rA = p.raw;
+    const float* rC = p.raw + ntri;
+    const float* rB = p.raw + 2 * ntri;
+    const float* rN = rB + k;
+    for (int i = tid; i < 64; i += UPD_THREADS) {
+      float n = 0.f, s2 = 1.f, gb = 0.f;
+      if (i < k) {
+        n = rsqrtf(rN[i]);
+        gb = n * n * rB[i];
+        s2 = fmaxf(n * rC[tri_index(i, i)], p.rho);
+      }
+      Ns[i] = n; S2[i] = s2; D1s[i] = gb;
+    }
+    __syncthreads();
+    for (int i = warp; i < 64; i += UPD_THREADS / 32) {
+      const float ni = Ns[i];
+      float c = 0.f;
+      for (int j = lane; j < 64; j += 32) {
+        float l = 0.f;
+        if (i < k && j < i) {
+          const float ga = ni * Ns[j] * rA[tri_index(i, j)];
+          const float gc = ni * rC[tri_index(i, j)];
+          l = D1s[i] * ga / S2[j];
+          c = fmaf(ga, gc / S2[j], c);
+        }
+        Lt[j * 64 + i] = l;
+      }
+      c = warp_sum(c);
+      if (lane == 0) D2s[i] = i < k ? ni * ni * rA[tri_index(i, i)] - c : 0.f;
+    }
+    if (blockIdx.x == 0) {
+      for (int e = tid; e < k * k; e += UPD_THREADS) {
+        const int i = e / k, j = e % k;
+        const bool low = j <= i;
+        const float ni = rsqrtf(rN[i]);
+        p.gram[e] = low ? ni * rsqrtf(rN[j]) * rA[tri_index(i, low ? j : 0)] : 0.f;
+        p.gram[(size_t)k * k + e] = (i == j) ? rB[i] / rN[i] : 0.f;
+        p.gram[2 * (size_t)k * k + e] = low ? ni * rC[tri_index(i, low ? j : 0)] : 0.f;
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---------------- phase 3b: grad, v'' and [Bv]' from the resident tiles ----------------
+  {
+    const int tq = tid & 15;           // column quads tq, tq+16, ...
+    const int tr = tid >> 4;           // rows 4tr..4tr+3
+    const int i0 = 4 * tr;
+    const int nq = W / 4;
+    const int jmax = min(i0 + 3, k);   // L_ij = 0 for j >= i
+    for (int q = tq; q < nq; q += 16) {
+      float acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
+      for (int j = 0; j < jmax; ++j) {
+        const float4 l = *reinterpret_cast<const float4*>(Lt + j * 64 + i0);
+        const float4 x = *reinterpret_cast<const float4*>(Ct + j * S + 4 * q);
+        const float lv[4] = {l.x, l.y, l.z, l.w}, xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(lv[a], xv[b], acc[a][b]);
+      }
+      const int64_t gx = c0 + 4 * q;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int i = i0 + a;
+        if (i < k && gx < c1) {
+          const float4 av = *reinterpret_cast<const float4*>(At + i * S + 4 * q);
+          const float4 bv = *reinterpret_cast<const float4*>(Bt + i * S + 4 * q);
+          const float4 vv = *reinterpret_cast<const float4*>(Vt + i * S + 4 * q);
+          const float4 xa = *reinterpret_cast<const float4*>(Ct + i * S + 4 * q);
+          const float ni = Ns[i];
+          const float d1 = D1s[i] * ni, d2 = D2s[i] * ni;
+          float4 vn, an;
+          vn.x = ni * vv.x + p.eta * (d1 * av.x - d2 * bv.x - acc[a][0]);
+          vn.y = ni * vv.y + p.eta * (d1 * av.y - d2 * bv.y - acc[a][1]);
+          vn.z = ni * vv.z + p.eta * (d1 * av.z - d2 * bv.z - acc[a][2]);
+          vn.w = ni * vv.w + p.eta * (d1 * av.w - d2 * bv.w - acc[a][3]);
+          an.x = xa.x + p.gamma * (ni * bv.x - xa.x);
+          an.y = xa.y + p.gamma * (ni * bv.y - xa.y);
+          an.z = xa.z + p.gamma * (ni * bv.z - xa.z);
+          an.w = xa.w + p.gamma * (ni * bv.w - xa.w);
+          const size_t o = (size_t)i * d + gx;
+          if (VEC && gx + 3 < c1) {
+            *reinterpret_cast<float4*>(p.V + o) = vn;
+            *reinterpret_cast<float4*>(p.AUX + o) = an;
+            if (p.Vbf) {
+              __nv_bfloat162 lo = __floats2bfloat162_rn(vn.x, vn.y), hi = __floats2bfloat162_rn(vn.z, vn.w);
+              uint2 pk;
+              pk.x = *reinterpret_cast<uint32_t*>(&lo);
+              pk.y = *reinterpret_cast<uint32_t*>(&hi);
+              *reinterpret_cast<uint2*>(p.Vbf + o) = pk;
+            }
+          } else {
+            const float vs[4] = {vn.x, vn.y, vn.z, vn.w}, as[4] = {an.x, an.y, an.z, an.w};
+            for (int t = 0; t < 4; ++t)
+              if (gx + t < c1) {
+                p.V[o + t] = vs[t];
+                p.AUX[o + t] = as[t];
+                if (p.Vbf) p.Vbf[o + t] = __float2bfloat16_rn(vs[t]);
+              }
+          }
+        }
+      }
+    }
+  }
+  stamp(p, 3);
+}
+
 // geig_get: the stored state is v'' = v + eta grad (the retraction is folded
 // into the next update); return the retracted v = v'' / ||v''|| (one CTA per row).
 __global__ void __launch_bounds__(256)
