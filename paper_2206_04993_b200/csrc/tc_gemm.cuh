@@ -63,6 +63,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
+// Programmatic dependent launch: the prologue (barrier init, TMEM alloc,
+// descriptor prefetch) of a kernel overlaps the tail of its predecessor;
+// griddepcontrol.wait precedes the first read of predecessor outputs.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -144,6 +150,7 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   const int g = blockIdx.z;
   const int m0 = blockIdx.x * TC_BM;
   const int Mg = g == 0 ? p.M[0] : p.M[1];
+  pdl_trigger();
   if (m0 >= Mg) return;
   const int BN = p.BN;
   const uint32_t B_BYTES = (uint32_t)BN * 128;
@@ -195,6 +202,7 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
 
   if (total > 0) {
     if (threadIdx.x == 0) {
@@ -328,6 +336,8 @@ __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* dst, float 
 template <typename T>
 __global__ void zshuffle_kernel(const float* __restrict__ Zp, T* __restrict__ Zb, int k, int64_t ldz, int h,
                                 int64_t hpad, int splits) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t vstride = (int64_t)k * ldz;
   const int64_t plane = (int64_t)k * hpad;
   const bool vec = ((h & 3) == 0) && ((ldz & 3) == 0) && ((hpad & 3) == 0);
@@ -453,11 +463,19 @@ inline geig_status launch(const TcMaps& maps, const TcParams& p, dim3 grid, cuda
     if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, "cudaFuncSetAttribute(tc_gemm_kernel) failed");
     attr_done[deep] = true;
   }
-  if (deep)
-    tc_gemm_kernel<EB, A_MN, 8><<<grid, TC_THREADS, smem_bytes(p.BN, 8), st>>>(maps, p);
-  else
-    tc_gemm_kernel<EB, A_MN, 4><<<grid, TC_THREADS, smem_bytes(p.BN, 4), st>>>(maps, p);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = smem_bytes(p.BN, deep ? 8 : 4);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = deep ? cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EB, A_MN, 8>, maps, p)
+                       : cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EB, A_MN, 4>, maps, p);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("tc_gemm launch: ") + cudaGetErrorString(e));
   return GEIG_OK;
 }
@@ -554,10 +572,23 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
   {
     const int64_t per = (int64_t)k * h / 4 + 1;
     const int blocks = (int)std::min<int64_t>(4 * t.nsm, (per + 255) / 256);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t le;
     if (eb == 2)
-      zshuffle_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(t.Zt, (__nv_bfloat16*)t.Zb, k, t.ldz, h, t.hpad, fsplits);
+      le = cudaLaunchKernelEx(&cfg, zshuffle_kernel<__nv_bfloat16>, (const float*)t.Zt, (__nv_bfloat16*)t.Zb, k, t.ldz,
+                              h, t.hpad, fsplits);
     else
-      zshuffle_kernel<float><<<blocks, 256, 0, st>>>(t.Zt, (float*)t.Zb, k, t.ldz, h, t.hpad, fsplits);
+      le = cudaLaunchKernelEx(&cfg, zshuffle_kernel<float>, (const float*)t.Zt, (float*)t.Zb, k, t.ldz, h, t.hpad,
+                              fsplits);
+    if (le != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, "zshuffle launch failed");
     if (cudaGetLastError() != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, "zshuffle launch failed");
     ++*nl;
   }
