@@ -135,7 +135,10 @@ geig_status geig_products_dense(geig_solver* s, const void* A, const void* B,
 geig_status geig_update(geig_solver* s, const float* AV, const float* BV,
                         double eta, double gamma);
 
-/* Convenience: one full step = products + update on the solver's scratch. */
+/* One full step = products + update on the solver's scratch.  On the bf16
+ * tensor-core path with k <= 64 the whole step is ONE persistent cooperative
+ * kernel (forward GEMM, split-K reduction, backward GEMM, Gram tables and
+ * update separated by grid barriers); otherwise products then update. */
 geig_status geig_step_cca(geig_solver* s, const void* X, const void* Y,
                           int64_t b, double eta, double gamma);
 geig_status geig_step_dense(geig_solver* s, const void* A, const void* B,
@@ -158,9 +161,12 @@ geig_status geig_step_cca_host(geig_solver* s, const void* X_host,
  * state. */
 geig_status geig_get_gram(geig_solver* s, float* GA, float* GB, float* GC);
 
-/* Phase durations (ns, %globaltimer of CTA 0) of the last geig_update:
+/* Phase durations (ns, %globaltimer of CTA 0) of the last update:
  * out[0] Gram partials, out[1] grid reduction, out[2] coefficients + fused
- * update; out[3], out[4] = 0 (reserved).  Synchronises the solver's stream. */
+ * update; if the last step ran the fused single-launch kernel
+ * (geig_step_cca, bf16, k <= 64) out[3] = forward products phase and
+ * out[4] = reshuffle + backward products phases, else 0.  Synchronises the
+ * solver's stream. */
 geig_status geig_update_phase_ns(geig_solver* s, int64_t* out);
 
 /* Number of kernel launches this solver has enqueued since creation. */

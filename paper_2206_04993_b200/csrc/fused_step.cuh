@@ -1,0 +1,372 @@
+// fused_step.cuh — one persistent cooperative kernel per CCA step on the
+// tensor-core path: every stage of the hot path in a single launch.
+//
+//   phase F  forward products Z_v = X_v V_v^T (tcgen05, K-major TMA, split-K
+//            partials in fp32)                                    [row a1]
+//   phase S  sum the split-K partials, route the halves (reading R1) and cast
+//            the backward operands to bf16 (all threads, grid-stride)
+//   phase B  backward products AV = X_1^T Z, BV = X_2^T Z (tcgen05, MN-major
+//            TMA straight from the sample-major views, 2 TMEM accumulators)
+//   phase U  Gram tables, coefficients, fused update (update_res_phases)
+//                                                                  [rows a2-a4]
+// separated by grid barriers.  One CTA per SM (256 threads): warp 0 lane 0
+// issues TMA, warp 1 lane 0 issues tcgen05.mma, warp 2 owns TMEM, warps 4-7
+// drain the accumulators (tcgen05.ld -> registers -> coalesced stores); the
+// smem ring and its mbarrier phases persist across the work items of F and B,
+// so the producer runs ahead into the next item while the epilogue drains.
+// Removes, per step, 3 kernel launches, 2 TMEM allocations / pipeline
+// prologues and the separate reshuffle launch of the unfused path.
+#pragma once
+#include <cooperative_groups.h>
+#include "tc_gemm.cuh"
+#include "update.cuh"
+#include <algorithm>
+#include <string>
+
+namespace geig { namespace tc {
+
+namespace cg = cooperative_groups;
+
+constexpr int FS_THREADS = 256;
+
+struct FusedMaps {
+  CUtensorMap aF[2];   // forward A: X, Y (K-major, box {ATOM, 128})
+  CUtensorMap bF[2];   // forward B: V_x, V_y (K-major, box {ATOM, BN})
+  CUtensorMap aB[4];   // backward A: X[0:h], X[h:2h], Y[0:h], Y[h:2h] (MN-major, box {ATOM, ATOM})
+  CUtensorMap bB[4];   // backward B: Zb planes (K-major, box {ATOM, BN})
+};
+
+struct FusedParams {
+  int rows, h, k, BN, stages, splitsF, mtF, mtB[2];
+  int kbF[2], kbB;                 // K blocks: forward per view, backward per half
+  int64_t dv[2], d, ldz, hpad;
+  float scale;
+  uint32_t idescF, idescB;
+  float* Zt;                       // splitsF x 2 x k x ldz fp32 partials
+  __nv_bfloat16* Zb;               // 4 x k x hpad
+  float* AV;
+  float* BV;
+  UpdateArgs upd;
+};
+
+struct Item {
+  int nseg, m0, mbound;
+  int kb0[2], kbn[2];
+  const CUtensorMap* ma[2];
+  const CUtensorMap* mb[2];
+  float* out[2];
+  int64_t ldo;
+  float scale;
+};
+
+__device__ __forceinline__ void decode_forward(const FusedMaps& M, const FusedParams& p, int idx, Item& it) {
+  const int per_view = p.mtF * p.splitsF;
+  const int v = idx / per_view, r = idx % per_view;
+  const int mt = r / p.splitsF, sp = r % p.splitsF;
+  it.nseg = 1;
+  it.m0 = mt * TC_BM;
+  it.mbound = p.rows;
+  const int kb = v == 0 ? p.kbF[0] : p.kbF[1];
+  it.kb0[0] = (int)((int64_t)kb * sp / p.splitsF);
+  it.kbn[0] = (int)((int64_t)kb * (sp + 1) / p.splitsF) - it.kb0[0];
+  it.kb0[1] = it.kbn[1] = 0;
+  it.ma[0] = v == 0 ? &M.aF[0] : &M.aF[1];
+  it.mb[0] = v == 0 ? &M.bF[0] : &M.bF[1];
+  it.ma[1] = it.ma[0];
+  it.mb[1] = it.mb[0];
+  it.out[0] = p.Zt + ((int64_t)(2 * sp + v) * p.k) * p.ldz;
+  it.out[1] = nullptr;
+  it.ldo = p.ldz;
+  it.scale = 1.f;
+}
+
+__device__ __forceinline__ void decode_backward(const FusedMaps& M, const FusedParams& p, int idx, Item& it) {
+  const int v = idx < p.mtB[0] ? 0 : 1;
+  const int mt = v == 0 ? idx : idx - p.mtB[0];
+  it.nseg = 2;
+  it.m0 = mt * TC_BM;
+  it.mbound = (int)(v == 0 ? p.dv[0] : p.dv[1]);
+  it.kb0[0] = it.kb0[1] = 0;
+  it.kbn[0] = it.kbn[1] = p.kbB;
+  it.ma[0] = v == 0 ? &M.aB[0] : &M.aB[2];
+  it.ma[1] = v == 0 ? &M.aB[1] : &M.aB[3];
+  it.mb[0] = v == 0 ? &M.bB[0] : &M.bB[2];
+  it.mb[1] = v == 0 ? &M.bB[1] : &M.bB[3];
+  const int64_t off = v == 0 ? 0 : p.dv[0];
+  it.out[0] = p.AV + off;
+  it.out[1] = p.BV + off;
+  it.ldo = p.d;
+  it.scale = p.scale;
+}
+
+struct RingState {
+  int it_prod = 0, it_mma = 0, items = 0;   // per-role running counters (persist across phases)
+};
+
+// One GEMM phase over this CTA's items (idx = blockIdx.x, +gridDim.x, ...).
+template <int EB, bool A_MN>
+__device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams& p, int nitems, uint8_t* ring,
+                                           uint64_t* full_bar, uint64_t* empty_bar, uint64_t* accf_bar,
+                                           uint64_t* acce_bar, uint32_t tmem_base, RingState& rs) {
+  constexpr int ATOM = 128 / EB;
+  constexpr int BK = ATOM;
+  constexpr int UK = 32 / EB;
+  constexpr uint32_t A_BYTES = TC_BM * 128;
+  const uint32_t B_BYTES = (uint32_t)p.BN * 128;
+  const uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  const int S = p.stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t idesc = A_MN ? p.idescB : p.idescF;
+  Item it;
+  if (threadIdx.x == 0) {
+    // ---------------- TMA producer ----------------
+    for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
+      if (A_MN) decode_backward(M, p, idx, it); else decode_forward(M, p, idx, it);
+      for (int s = 0; s < it.nseg; ++s) {
+        for (int j = 0; j < it.kbn[s]; ++j, ++rs.it_prod) {
+          const int st = rs.it_prod % S;
+          if (rs.it_prod >= S) mbar_wait(&empty_bar[st], ((rs.it_prod / S) + 1) & 1);
+          uint8_t* sa = ring + st * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(&full_bar[st], STAGE_BYTES);
+          const int k0 = (it.kb0[s] + j) * BK;
+          if (A_MN) {
+#pragma unroll
+            for (int q = 0; q < TC_BM / ATOM; ++q)
+              tma_load_2d(sa + q * (BK * 128), it.ma[s], &full_bar[st], it.m0 + q * ATOM, k0);
+          } else {
+            tma_load_2d(sa, it.ma[s], &full_bar[st], k0, it.m0);
+          }
+          tma_load_2d(sb, it.mb[s], &full_bar[st], k0, 0);
+        }
+      }
+    }
+  } else if (threadIdx.x == 32) {
+    // ---------------- MMA issuer ----------------
+    for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++rs.items) {
+      if (A_MN) decode_backward(M, p, idx, it); else decode_forward(M, p, idx, it);
+      if (rs.items > 0) mbar_wait(acce_bar, (rs.items - 1) & 1);   // epilogue drained the accumulator
+      tc_fence_after();
+      for (int s = 0; s < it.nseg; ++s) {
+        const uint32_t d_tmem = tmem_base + (uint32_t)(s * p.BN);
+        for (int j = 0; j < it.kbn[s]; ++j, ++rs.it_mma) {
+          const int st = rs.it_mma % S;
+          mbar_wait(&full_bar[st], (rs.it_mma / S) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(ring + st * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / UK; ++kk) {
+            const uint64_t ad = A_MN ? make_sdesc(sa + kk * UK * 128, BK * 128, 1024) : make_sdesc(sa + kk * 32, 16, 1024);
+            const uint64_t bd = make_sdesc(sb + kk * 32, 16, 1024);
+            umma<EB>(d_tmem, ad, bd, idesc, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[st]);
+        }
+      }
+      umma_commit(accf_bar);
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue warps: TMEM -> registers -> global ----------------
+    const int ew = warp - 4;
+    for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++rs.items) {
+      if (A_MN) decode_backward(M, p, idx, it); else decode_forward(M, p, idx, it);
+      mbar_wait(accf_bar, rs.items & 1);
+      __syncwarp();
+      tc_fence_after();
+      const int m = it.m0 + ew * 32 + lane;
+      const bool mok = m < it.mbound;
+      for (int s = 0; s < it.nseg; ++s) {
+        float* out = it.out[s] + m;
+        for (int c0 = 0; c0 < p.BN; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(s * p.BN + c0), r);
+          if (mok) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (c0 + j < p.k) out[(int64_t)(c0 + j) * it.ldo] = it.scale * __uint_as_float(r[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(acce_bar);
+    }
+  }
+}
+
+template <int EB>
+__global__ void __launch_bounds__(FS_THREADS, 1)
+cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t STAGE_BYTES = TC_BM * 128 + (uint32_t)p.BN * 128;
+  uint8_t* ring = smem;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + p.stages * STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + TC_MAX_STAGES;
+  uint64_t* accf_bar = empty_bar + TC_MAX_STAGES;
+  uint64_t* acce_bar = accf_bar + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce_bar + 1);
+  const int warp = threadIdx.x >> 5;
+  constexpr uint32_t NCOLS = 256;   // >= 2 * BN (backward: A-half and B-half accumulators)
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(accf_bar, 1);
+    mbar_init(acce_bar, 128);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int v = 0; v < 2; ++v) { tma_prefetch_desc(&maps.aF[v]); tma_prefetch_desc(&maps.bF[v]); }
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(NCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  stamp(p.upd, 4);
+  RingState rs;
+
+  // ---- phase F: forward split-K partials ----
+  gemm_phase<EB, false>(maps, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
+  grid.sync();
+  stamp(p.upd, 5);
+
+  // ---- phase S: sum partials, route halves, cast to bf16 ----
+  {
+    const int64_t vstride = (int64_t)p.k * p.ldz;
+    const int64_t plane = (int64_t)p.k * p.hpad;
+    const int h = p.h;
+    const bool vec = ((h & 3) == 0) && ((p.ldz & 3) == 0) && ((p.hpad & 3) == 0);
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+    if (vec) {
+      const int hq = h / 4;
+      for (int64_t e = gtid; e < (int64_t)p.k * hq; e += gsz) {
+        const int n = (int)(e / hq), r = 4 * (int)(e % hq);
+        float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0, y0 = x0, y1 = x0;
+        for (int sp = 0; sp < p.splitsF; ++sp) {
+          const float* zx = p.Zt + (int64_t)(2 * sp) * vstride + (int64_t)n * p.ldz;
+          const float* zy = zx + vstride;
+          const float4 a = *reinterpret_cast<const float4*>(zx + r), b = *reinterpret_cast<const float4*>(zx + h + r);
+          const float4 c = *reinterpret_cast<const float4*>(zy + r), dd = *reinterpret_cast<const float4*>(zy + h + r);
+          x0.x += a.x; x0.y += a.y; x0.z += a.z; x0.w += a.w;
+          x1.x += b.x; x1.y += b.y; x1.z += b.z; x1.w += b.w;
+          y0.x += c.x; y0.y += c.y; y0.z += c.z; y0.w += c.w;
+          y1.x += dd.x; y1.y += dd.y; y1.z += dd.z; y1.w += dd.w;
+        }
+        const int64_t o = (int64_t)n * p.hpad + r;
+        store4<__nv_bfloat16>(p.Zb + 0 * plane + o, y0.x, y0.y, y0.z, y0.w);
+        store4<__nv_bfloat16>(p.Zb + 1 * plane + o, x1.x, x1.y, x1.z, x1.w);
+        store4<__nv_bfloat16>(p.Zb + 2 * plane + o, x0.x, x0.y, x0.z, x0.w);
+        store4<__nv_bfloat16>(p.Zb + 3 * plane + o, y1.x, y1.y, y1.z, y1.w);
+      }
+    } else {
+      for (int64_t e = gtid; e < (int64_t)p.k * h; e += gsz) {
+        const int n = (int)(e / h), r = (int)(e % h);
+        float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
+        for (int sp = 0; sp < p.splitsF; ++sp) {
+          const float* zx = p.Zt + (int64_t)(2 * sp) * vstride + (int64_t)n * p.ldz;
+          const float* zy = zx + vstride;
+          x0 += zx[r]; x1 += zx[h + r]; y0 += zy[r]; y1 += zy[h + r];
+        }
+        const int64_t o = (int64_t)n * p.hpad + r;
+        p.Zb[0 * plane + o] = __float2bfloat16_rn(y0);
+        p.Zb[1 * plane + o] = __float2bfloat16_rn(x1);
+        p.Zb[2 * plane + o] = __float2bfloat16_rn(x0);
+        p.Zb[3 * plane + o] = __float2bfloat16_rn(y1);
+      }
+    }
+    // generic-proxy writes consumed by the async proxy (TMA) after the barrier
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  grid.sync();
+  stamp(p.upd, 6);
+
+  // ---- phase B: backward products into AV, BV ----
+  if (threadIdx.x == 0)
+    for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&maps.aB[v]); tma_prefetch_desc(&maps.bB[v]); }
+  gemm_phase<EB, true>(maps, p, p.mtB[0] + p.mtB[1], ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
+  tc_fence_before();
+  grid.sync();
+  stamp(p.upd, 7);
+
+  // ---- release TMEM, then phase U: Gram tables + fused update ----
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NCOLS));
+  }
+  update_res_phases<true>(p.upd, reinterpret_cast<float*>(smem), grid);
+}
+
+
+// ----------------------------------------------------------------------------
+// host side
+// ----------------------------------------------------------------------------
+inline size_t fused_smem_bytes(int BN, int stages, size_t upd_bytes) {
+  const size_t ring = (size_t)stages * (TC_BM * 128 + (size_t)BN * 128) + (2 * TC_MAX_STAGES + 4) * 8;
+  return 1024 + std::max(ring, upd_bytes);
+}
+
+// Whole CCA step in one cooperative launch (bf16 tensor cores, k <= 64).
+// `upd` carries the update arguments (state, AV/BV scratch, eta, gamma...);
+// its grid partition (gridDim = G, segw) is reused by the GEMM phases.
+inline geig_status fused_cca_step(TcPlan& t, const void* X, const void* Y, int64_t b, float scale,
+                                  const __nv_bfloat16* Vbf, float* AV, float* BV, UpdateArgs upd, int grid_ctas,
+                                  size_t upd_bytes, cudaStream_t st) {
+  if (!t.ready || t.math != GEIG_MATH_BF16) return tc_fail(GEIG_ERR_STATE, "fused step needs the bf16 plan");
+  const int eb = 2, ATOM = 64;
+  const int h = (int)(b / 2), rows = 2 * h, k = t.k;
+  const int64_t dv[2] = {t.dx, t.dy};
+  const void* Xv[2] = {X, Y};
+  FusedMaps maps;
+  FusedParams p{};
+  for (int v = 0; v < 2; ++v) {
+    const char* vb = (const char*)Vbf + (v == 0 ? 0 : t.dx * eb);
+    if (!make_map(&maps.aF[v], Xv[v], eb, dv[v], rows, dv[v], ATOM, TC_BM) ||
+        !make_map(&maps.bF[v], vb, eb, dv[v], k, t.d, ATOM, t.BN))
+      return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused forward) failed");
+    for (int s = 0; s < 2; ++s) {
+      const char* xb = (const char*)Xv[v] + (int64_t)s * h * dv[v] * eb;
+      const char* zb = (const char*)t.Zb + (int64_t)(v * 2 + s) * k * t.hpad * eb;
+      if (!make_map(&maps.aB[v * 2 + s], xb, eb, dv[v], h, dv[v], ATOM, ATOM) ||
+          !make_map(&maps.bB[v * 2 + s], zb, eb, h, k, t.hpad, ATOM, t.BN))
+        return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused backward) failed");
+    }
+    p.dv[v] = dv[v];
+    p.kbF[v] = (int)((dv[v] + ATOM - 1) / ATOM);
+    p.mtB[v] = (int)((dv[v] + TC_BM - 1) / TC_BM);
+  }
+  p.rows = rows; p.h = h; p.k = k; p.BN = t.BN; p.d = t.d; p.ldz = t.ldz; p.hpad = t.hpad;
+  p.scale = scale;
+  p.mtF = (rows + TC_BM - 1) / TC_BM;
+  p.splitsF = std::min(TC_MAX_SPLITS, choose_splits_deep(2 * p.mtF, std::min(p.kbF[0], p.kbF[1]), grid_ctas));
+  p.kbB = (h + ATOM - 1) / ATOM;
+  p.idescF = make_idesc(eb, false, t.BN, TC_BM);
+  p.idescB = make_idesc(eb, true, t.BN, TC_BM);
+  p.Zt = t.Zt;
+  p.Zb = (__nv_bfloat16*)t.Zb;
+  p.AV = AV;
+  p.BV = BV;
+  p.upd = upd;
+  const size_t stage_bytes = TC_BM * 128 + (size_t)t.BN * 128;
+  p.stages = (int)std::min<size_t>(TC_MAX_STAGES, (200 * 1024) / stage_bytes);
+  const size_t smem = fused_smem_bytes(t.BN, p.stages, upd_bytes);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(cca_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+      return tc_fail(GEIG_ERR_CUDA, "cudaFuncSetAttribute(cca_step_kernel) failed");
+    attr = true;
+  }
+  void* args[] = {(void*)&maps, (void*)&p};
+  cudaError_t e = cudaLaunchCooperativeKernel((void*)cca_step_kernel<2>, dim3(grid_ctas), dim3(FS_THREADS), args, smem, st);
+  if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("cca_step_kernel launch: ") + cudaGetErrorString(e));
+  return GEIG_OK;
+}
+
+}}  // namespace geig::tc

@@ -15,6 +15,7 @@
 #include "simt_gemm.cuh"
 #include "update.cuh"
 #include "tc_gemm.cuh"
+#include "fused_step.cuh"
 
 using namespace geig;
 
@@ -58,6 +59,7 @@ struct geig_solver {
   void *hX = nullptr, *hY = nullptr;                  // device staging for *_host
   int upd_grid = 1;
   bool upd_res = false;                               // resident (k <= 64) update kernel
+  bool fused_last = false;                            // last step ran the fused cooperative kernel
   int64_t upd_segw = 32;
   size_t upd_smem = 0;
   int64_t launches = 0;
@@ -105,6 +107,7 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
   ALLOC(s->BV, kd * 4);
   ALLOC(s->gram, (size_t)3 * k * k * 4);
   ALLOC(s->ts, 8 * sizeof(unsigned long long));
+  cudaMemset(s->ts, 0, 8 * sizeof(unsigned long long));
   if (problem == GEIG_CCA) {
     const int64_t mr = ((max_rows + 127) / 128) * 128;
     ALLOC(s->Wx, (size_t)k * mr * 4);
@@ -347,11 +350,33 @@ extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float*
   return GEIG_OK;
 }
 
+static bool fused_ok(const geig_solver* s, const void* X, const void* Y) {
+  if (s->math != GEIG_MATH_BF16 || !s->upd_res || s->d % 4 != 0) return false;
+  if (getenv("GEIG_NO_FUSED")) return false;
+  return (((uintptr_t)X | (uintptr_t)Y) % 16) == 0;
+}
+
 extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* Y, int64_t b, double eta,
                                      double gamma) {
   if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  if (s->problem == GEIG_CCA && b >= 2 && b <= s->max_rows && X && Y && fused_ok(s, X, Y)) {
+    // whole step in one persistent cooperative launch (fused_step.cuh)
+    CU(cudaSetDevice(s->device));
+    UpdateArgs a;
+    a.V = s->V; a.AUX = s->AUX; a.AV = s->AV; a.BV = s->BV;
+    a.Vbf = s->Vbf; a.partial = s->partial; a.raw = s->raw; a.gram = s->gram;
+    a.k = s->k; a.d = s->d; a.segw = s->upd_segw;
+    a.eta = (float)eta; a.gamma = (float)gamma; a.rho = s->rho; a.ts = s->ts;
+    geig_status st = tc::fused_cca_step(s->tc, X, Y, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a,
+                                        s->upd_grid, s->upd_smem, s->stream);
+    if (st) return fail(st, "%s", tc::last_error());
+    s->launches++;
+    s->fused_last = true;
+    return GEIG_OK;
+  }
   geig_status st = geig_products_cca(s, X, Y, b, 1.0f / (float)(b / 2), s->AV, s->BV);
   if (st) return st;
+  s->fused_last = false;
   return geig_update(s, s->AV, s->BV, eta, gamma);
 }
 
@@ -391,11 +416,12 @@ extern "C" geig_status geig_step_cca_host(geig_solver* s, const void* X_host, co
 extern "C" geig_status geig_update_phase_ns(geig_solver* s, int64_t* out) {
   if (!s || !out) return fail(GEIG_ERR_ARG, "NULL argument");
   CU(cudaSetDevice(s->device));
-  unsigned long long t[4];
+  unsigned long long t[8];
   CU(cudaMemcpyAsync(t, s->ts, sizeof(t), cudaMemcpyDeviceToHost, s->stream));
   CU(cudaStreamSynchronize(s->stream));
   for (int i = 0; i < 3; ++i) out[i] = (int64_t)(t[i + 1] - t[i]);
-  out[3] = out[4] = 0;
+  out[3] = s->fused_last ? (int64_t)(t[5] - t[4]) : 0;      // fused: forward phase
+  out[4] = s->fused_last ? (int64_t)(t[7] - t[5]) : 0;      // fused: reshuffle + backward phases
   return GEIG_OK;
 }
 

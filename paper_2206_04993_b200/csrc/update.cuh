@@ -418,11 +418,11 @@ __host__ __device__ constexpr int upd_raw_floats_res(int k) { return k * (k + 1)
 
 __device__ __forceinline__ int tri_index(int i, int j) { return i * (i + 1) / 2 + j; }
 
+// The resident update as a device function over an explicit shared-memory
+// arena, so the fused step kernel (fused_step.cuh) can run it after its GEMM
+// phases inside the same cooperative launch.
 template <bool VEC>
-__global__ void __launch_bounds__(UPD_THREADS, 1)
-update_res_kernel(UpdateArgs p) {
-  cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) float smem[];
+__device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* smem, cg::grid_group& grid) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int k = p.k;
@@ -665,6 +665,14 @@ update_res_kernel(UpdateArgs p) {
     }
   }
   stamp(p, 3);
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(UPD_THREADS, 1)
+update_res_kernel(UpdateArgs p) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) float smem[];
+  update_res_phases<VEC>(p, smem, grid);
 }
 
 // geig_get: the stored state is v'' = v + eta grad (the retraction is folded

@@ -229,3 +229,25 @@ def test_dense_config4_full_size_tf32_tcgen05(geig):
     cfg = CONFIGS[4]
     a, b = dense_gep_large(cfg.d, seed=0, device="cuda:0")
     _dense_step_check(geig, a, b, cfg.k, "tf32", cfg.rho, cfg.eta, cfg.gamma)
+
+
+# --- the fused single-launch step (geig_step_cca on the bf16 path) -------------
+
+@pytest.mark.parametrize("cfg_idx,rows,k,dx,dy", [(3, 4096, None, None, None), (2, 1024, None, None, None),
+                                                  (2, 300, 24, 200, 136), (2, 130, 5, 64, 8),
+                                                  (3, 1000, 64, 8192, 4096)])
+def test_fused_step_bf16(geig, cfg_idx, rows, k, dx, dy):
+    """geig_step_cca runs forward GEMM, split-K reduction, backward GEMM, Gram
+    tables and the update in ONE cooperative kernel; the step must match the
+    oracle like the staged path (configs 2/3 full size + ragged shapes)."""
+    errs, _ = check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math="bf16", use_step=True)
+    _assert(errs, 1e-2)
+
+
+def test_fused_step_matches_staged_path(geig):
+    """Same inputs through the staged path (products + update) and the fused
+    kernel: the states agree to bf16-product rounding order."""
+    e1, g1 = check_cca_step(geig, 2, 1024, math="bf16", use_step=True)
+    e2, g2 = check_cca_step(geig, 2, 1024, math="bf16", use_step=False)
+    assert rel_err(g1["V"] - g2["V"] + 1.0, np.ones_like(g2["V"])) < 1e-3
+    assert rel_err(g1["aux"], g2["aux"]) < 1e-3
