@@ -217,19 +217,27 @@ def run_gpu(args, cfg, rank, world, local_rank):
 
     ev = []
 
+    fused = world == 1 and math == "bf16" and cfg.k <= 64 and not args.staged
+
     def step(i, timed):
         if timed:
             e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             e0.record(stream)
-        geig.geig_products_cca(s.h, Xs[i % P], Ys[i % P], b, scale, AV, BV)
-        if timed:
-            e1.record(stream)
-        if world > 1:
-            flat = torch.stack([AV, BV])
-            dist.all_reduce(flat)
-            AV.copy_(flat[0])
-            BV.copy_(flat[1])
-        geig.geig_update(s.h, AV, BV, cfg.eta, cfg.gamma)
+        if fused:
+            # one launch per step: forward GEMM, reshuffle, backward GEMM, Gram tables, update
+            geig.geig_step_cca(s.h, Xs[i % P], Ys[i % P], b, cfg.eta, cfg.gamma)
+            if timed:
+                e1.record(stream)
+        else:
+            geig.geig_products_cca(s.h, Xs[i % P], Ys[i % P], b, scale, AV, BV)
+            if timed:
+                e1.record(stream)
+            if world > 1:
+                flat = torch.stack([AV, BV])
+                dist.all_reduce(flat)
+                AV.copy_(flat[0])
+                BV.copy_(flat[1])
+            geig.geig_update(s.h, AV, BV, cfg.eta, cfg.gamma)
         if timed:
             e2.record(stream)
             ev.append((e0, e1, e2))
@@ -263,25 +271,38 @@ def run_gpu(args, cfg, rank, world, local_rank):
         elapsed_ms, prod_ms, upd_ms = t.tolist()
     value = world * b * args.steps / (elapsed_ms / 1e3)
 
-    # roofline of the dominant kernel (the products stage): algorithmic bytes =
-    # X and Y read once (b*d*esz) + V read + AV/BV written
-    alg_bytes = b * cfg.d * esz + cfg.k * cfg.d * (2 if math == "bf16" else 4) + 2 * cfg.k * cfg.d * 4
-    achieved = alg_bytes / (prod_ms / 1e3) / 1e9
+    # roofline of the dominant kernel.  Fused path: the single step kernel;
+    # algorithmic bytes = the batch read once + the state (V, [Bv]) read and
+    # written once + the bf16 shadow of V.  Staged path:
+    # the products stage, algorithmic bytes = batch + V read + AV/BV written.
+    kd = cfg.k * cfg.d
+    if fused:
+        alg_bytes = b * cfg.d * esz + 2 * kd * 4 + 2 * kd * 4 + kd * 2
+        kernel = "cca_step_kernel (fused: forward GEMM, reshuffle, backward GEMM, Gram, update)"
+        k_ms = prod_ms
+        ph = geig.geig_update_phase_ns(s.h)
+        phases = {"forward_us": ph[3] / 1e3, "reshuffle_backward_us": ph[4] / 1e3, "gram_us": ph[0] / 1e3,
+                  "reduce_us": ph[1] / 1e3, "coef_update_us": ph[2] / 1e3, "source": "%globaltimer, CTA 0, last step"}
+    else:
+        alg_bytes = b * cfg.d * esz + kd * (2 if math == "bf16" else 4) + 2 * kd * 4
+        kernel = "products stage (tc_gemm forward + zshuffle + tc_gemm backward)"
+        k_ms = prod_ms
+        phases = {"products_ms": prod_ms, "update_ms": upd_ms}
+    achieved = alg_bytes / (k_ms / 1e3) / 1e9
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
             tr = json.load(f)
-        if tr.get("workload") == cfg.name and tr.get("math") == math:
+        if tr.get("workload") == cfg.name and tr.get("math") == math and tr.get("fused", False) == fused:
             traffic = tr["dram_bytes_per_launch"]
     except Exception:
         pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved / hbm_peak, "traffic": traffic, "algorithmic_bytes": alg_bytes,
-            "kernel": "products stage (tc_gemm forward + zshuffle + tc_gemm backward)",
-            "peak_source": peaks_src, "ms_per_launch": prod_ms, "update_ms": upd_ms,
+            "kernel": kernel, "peak_source": peaks_src, "ms_per_launch": k_ms, "phases": phases,
             "flops_per_step": 4.0 * cfg.k * cfg.d * b,
-            "tensor_tflops": 4.0 * cfg.k * cfg.d * b / (prod_ms / 1e3) / 1e12}
+            "tensor_tflops": 4.0 * cfg.k * cfg.d * b / (k_ms / 1e3) / 1e12}
 
     # end to end through the C ABI with HOST buffers (pinned), rank-local
     e2e = None
@@ -336,6 +357,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--staged", action="store_true", help="products + update as separate launches")
     args = ap.parse_args()
     from synth import CONFIGS
     cfg = CONFIGS[args.config]

@@ -35,6 +35,20 @@ for it in range(30):
         prod.append(e0.elapsed_time(e1) * 1e3); upd.append(e1.elapsed_time(e2) * 1e3)
         phases.append(geig.geig_update_phase_ns(s.h))
 print(f"config {cfg.index} {math}: products {statistics.median(prod):.1f} us, update {statistics.median(upd):.1f} us")
+steps = []
+for it in range(30):
+    i = it % 4
+    e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+    e0.record(st)
+    geig.geig_step_cca(s.h, X[i*b:(i+1)*b], Y[i*b:(i+1)*b], b, cfg.eta, cfg.gamma)
+    e1.record(st)
+    torch.cuda.synchronize()
+    if it >= 5:
+        steps.append((e0.elapsed_time(e1) * 1e3, geig.geig_update_phase_ns(s.h)))
+print(f"  geig_step_cca: {statistics.median(t for t, _ in steps):.1f} us/step; fused phases: "
+      f"forward {statistics.median(p[3] for _, p in steps)/1e3:.1f} reshuffle+backward {statistics.median(p[4] for _, p in steps)/1e3:.1f} "
+      f"gram {statistics.median(p[0] for _, p in steps)/1e3:.1f} reduce {statistics.median(p[1] for _, p in steps)/1e3:.1f} "
+      f"coef+update {statistics.median(p[2] for _, p in steps)/1e3:.1f} us")
 names = ["gram", "reduce", "coef+update"]
 for j, n in enumerate(names):
     print(f"  phase {n:8s} {statistics.median(p[j] for p in phases)/1e3:8.2f} us")
