@@ -409,10 +409,11 @@ update_kernel(UpdateArgs p) {
 // shared-memory tiles.  Compact lower-triangular reduction: raw layout
 // [tri(A) | tri(C) | diag B | diag V'V'] with tri(i,j) = i(i+1)/2 + j.
 // ============================================================================
-constexpr int UPD_RES_WMAX = 192;   // max columns per CTA (smem: 4 x 64 x 196 x 4 B)
+constexpr int UPD_RES_WMAX = 168;   // max columns per CTA (smem: 4 x 64 x 172 x 4 B + tables)
 
 __host__ __device__ constexpr size_t upd_res_smem_floats(int W) {
-  return (size_t)4 * 64 * (W + 4) + 64 * 64 + 4 * 64 + 8 * 32;
+  // 4 tiles + Lt + n, s^2, D1, D2 + red + staged raw tables (64*65 + 128)
+  return (size_t)4 * 64 * (W + 4) + 64 * 64 + 4 * 64 + 8 * 32 + 64 * 65 + 128;
 }
 __host__ __device__ constexpr int upd_raw_floats_res(int k) { return k * (k + 1) + 2 * k; }
 
@@ -554,10 +555,15 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   stamp(p, 2);
 
   // ---------------- phase 3a: coefficients ----------------
+  // the reduced raw tables are first staged into shared memory by all threads
+  // (independent loads), then the coefficients are formed from smem.
   {
-    const float* rA = p.raw;
-    const float* rC = p.raw + ntri;
-    const float* rB = p.raw + 2 * ntri;
+    float* rs = red + 8 * 32;                    // [ntot] staged raw tables (<= 64*65 + 128 floats)
+    for (int e = tid; e < ntot; e += UPD_THREADS) rs[e] = p.raw[e];
+    __syncthreads();
+    const float* rA = rs;
+    const float* rC = rs + ntri;
+    const float* rB = rs + 2 * ntri;
     const float* rN = rB + k;
     for (int i = tid; i < 64; i += UPD_THREADS) {
       float n = 0.f, s2 = 1.f, gb = 0.f;
