@@ -59,15 +59,13 @@ struct Item {
   float scale;
 };
 
-// Forward item of half hh: rows [hh*h, (hh+1)*h) of view v, one 128-row tile,
-// one K split (all partial sums of a split land in their own Zt slice).
-__device__ __forceinline__ void decode_forward(const FusedMaps& M, const FusedParams& p, int hh, int idx, Item& it) {
+__device__ __forceinline__ void decode_forward(const FusedMaps& M, const FusedParams& p, int idx, Item& it) {
   const int per_view = p.mtF * p.splitsF;
   const int v = idx / per_view, r = idx % per_view;
   const int mt = r / p.splitsF, sp = r % p.splitsF;
   it.nseg = 1;
-  it.m0 = hh * p.h + mt * TC_BM;
-  it.mbound = (hh + 1) * p.h;
+  it.m0 = mt * TC_BM;
+  it.mbound = p.rows;
   const int kb = v == 0 ? p.kbF[0] : p.kbF[1];
   it.kb0[0] = (int)((int64_t)kb * sp / p.splitsF);
   it.kbn[0] = (int)((int64_t)kb * (sp + 1) / p.splitsF) - it.kb0[0];
@@ -82,25 +80,21 @@ __device__ __forceinline__ void decode_forward(const FusedMaps& M, const FusedPa
   it.scale = 1.f;
 }
 
-// Backward item of half hh (reading R1: hh = 0 -> A_t products, 1 -> B_t):
-// one 128-feature tile of view v, K = the h rows of the half (L2-resident,
-// just streamed by the forward phase of the same half).
-__device__ __forceinline__ void decode_backward(const FusedMaps& M, const FusedParams& p, int hh, int idx, Item& it) {
+__device__ __forceinline__ void decode_backward(const FusedMaps& M, const FusedParams& p, int idx, Item& it) {
   const int v = idx < p.mtB[0] ? 0 : 1;
   const int mt = v == 0 ? idx : idx - p.mtB[0];
-  it.nseg = 1;
+  it.nseg = 2;
   it.m0 = mt * TC_BM;
   it.mbound = (int)(v == 0 ? p.dv[0] : p.dv[1]);
   it.kb0[0] = it.kb0[1] = 0;
-  it.kbn[0] = p.kbB;
-  it.kbn[1] = 0;
-  it.ma[0] = &M.aB[v * 2 + hh];
-  it.mb[0] = &M.bB[v * 2 + hh];
-  it.ma[1] = it.ma[0];
-  it.mb[1] = it.mb[0];
+  it.kbn[0] = it.kbn[1] = p.kbB;
+  it.ma[0] = v == 0 ? &M.aB[0] : &M.aB[2];
+  it.ma[1] = v == 0 ? &M.aB[1] : &M.aB[3];
+  it.mb[0] = v == 0 ? &M.bB[0] : &M.bB[2];
+  it.mb[1] = v == 0 ? &M.bB[1] : &M.bB[3];
   const int64_t off = v == 0 ? 0 : p.dv[0];
-  it.out[0] = (hh == 0 ? p.AV : p.BV) + off;
-  it.out[1] = nullptr;
+  it.out[0] = p.AV + off;
+  it.out[1] = p.BV + off;
   it.ldo = p.d;
   it.scale = p.scale;
 }
@@ -111,7 +105,7 @@ struct RingState {
 
 // One GEMM phase over this CTA's items (idx = blockIdx.x, +gridDim.x, ...).
 template <int EB, bool A_MN>
-__device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams& p, int hh, int nitems, uint8_t* ring,
+__device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams& p, int nitems, uint8_t* ring,
                                            uint64_t* full_bar, uint64_t* empty_bar, uint64_t* accf_bar,
                                            uint64_t* acce_bar, uint32_t tmem_base, RingState& rs) {
   constexpr int ATOM = 128 / EB;
@@ -127,7 +121,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
   if (threadIdx.x == 0) {
     // ---------------- TMA producer ----------------
     for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
-      if (A_MN) decode_backward(M, p, hh, idx, it); else decode_forward(M, p, hh, idx, it);
+      if (A_MN) decode_backward(M, p, idx, it); else decode_forward(M, p, idx, it);
       for (int s = 0; s < it.nseg; ++s) {
         for (int j = 0; j < it.kbn[s]; ++j, ++rs.it_prod) {
           const int st = rs.it_prod % S;
@@ -150,7 +144,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
   } else if (threadIdx.x == 32) {
     // ---------------- MMA issuer ----------------
     for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++rs.items) {
-      if (A_MN) decode_backward(M, p, hh, idx, it); else decode_forward(M, p, hh, idx, it);
+      if (A_MN) decode_backward(M, p, idx, it); else decode_forward(M, p, idx, it);
       if (rs.items > 0) mbar_wait(acce_bar, (rs.items - 1) & 1);   // epilogue drained the accumulator
       tc_fence_after();
       for (int s = 0; s < it.nseg; ++s) {
@@ -176,7 +170,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
     // ---------------- epilogue warps: TMEM -> registers -> global ----------------
     const int ew = warp - 4;
     for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++rs.items) {
-      if (A_MN) decode_backward(M, p, hh, idx, it); else decode_forward(M, p, hh, idx, it);
+      if (A_MN) decode_backward(M, p, idx, it); else decode_forward(M, p, idx, it);
       mbar_wait(accf_bar, rs.items & 1);
       __syncwarp();
       tc_fence_after();
@@ -238,72 +232,68 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   stamp(p.upd, 4);
   RingState rs;
 
-  // Halves processed in turn so the backward pass of a half re-reads the
-  // rows the forward pass of that half has just brought into L2 (64 MiB at
-  // config 3, < 126 MB L2): F(0) S(0) B(0) F(1) S(1) B(1).
-  for (int hh = 0; hh < 2; ++hh) {
-    // ---- phase F: forward split-K partials of this half ----
-    gemm_phase<EB, false>(maps, p, hh, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar,
-                          tmem_base, rs);
-    grid.sync();
-    if (hh == 0) stamp(p.upd, 5);
+  // ---- phase F: forward split-K partials ----
+  gemm_phase<EB, false>(maps, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
+  grid.sync();
+  stamp(p.upd, 5);
 
-    // ---- phase S: sum partials of this half, route (reading R1), cast to bf16 ----
-    {
-      const int64_t vstride = (int64_t)p.k * p.ldz;
-      const int64_t plane = (int64_t)p.k * p.hpad;
-      const int h = p.h;
-      const int r0 = hh * h;
-      // half 0: X backward uses Z_y, Y backward uses Z_x; half 1: each view its own Z
-      __nv_bfloat16* dstx = p.Zb + (int64_t)(0 * 2 + hh) * plane;   // view x, half hh
-      __nv_bfloat16* dsty = p.Zb + (int64_t)(1 * 2 + hh) * plane;   // view y, half hh
-      const bool vec = ((h & 3) == 0) && ((p.ldz & 3) == 0) && ((p.hpad & 3) == 0);
-      const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-      const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
-      if (vec) {
-        const int hq = h / 4;
-        for (int64_t e = gtid; e < (int64_t)p.k * hq; e += gsz) {
-          const int n = (int)(e / hq), r = 4 * (int)(e % hq);
-          float4 zx = make_float4(0.f, 0.f, 0.f, 0.f), zy = zx;
-          for (int sp = 0; sp < p.splitsF; ++sp) {
-            const float* px = p.Zt + (int64_t)(2 * sp) * vstride + (int64_t)n * p.ldz + r0 + r;
-            const float4 a = *reinterpret_cast<const float4*>(px);
-            const float4 c = *reinterpret_cast<const float4*>(px + vstride);
-            zx.x += a.x; zx.y += a.y; zx.z += a.z; zx.w += a.w;
-            zy.x += c.x; zy.y += c.y; zy.z += c.z; zy.w += c.w;
-          }
-          const int64_t o = (int64_t)n * p.hpad + r;
-          const float4 fx = hh == 0 ? zy : zx, fy = hh == 0 ? zx : zy;
-          store4<__nv_bfloat16>(dstx + o, fx.x, fx.y, fx.z, fx.w);
-          store4<__nv_bfloat16>(dsty + o, fy.x, fy.y, fy.z, fy.w);
+  // ---- phase S: sum partials, route halves, cast to bf16 ----
+  {
+    const int64_t vstride = (int64_t)p.k * p.ldz;
+    const int64_t plane = (int64_t)p.k * p.hpad;
+    const int h = p.h;
+    const bool vec = ((h & 3) == 0) && ((p.ldz & 3) == 0) && ((p.hpad & 3) == 0);
+    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+    if (vec) {
+      const int hq = h / 4;
+      for (int64_t e = gtid; e < (int64_t)p.k * hq; e += gsz) {
+        const int n = (int)(e / hq), r = 4 * (int)(e % hq);
+        float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0, y0 = x0, y1 = x0;
+        for (int sp = 0; sp < p.splitsF; ++sp) {
+          const float* zx = p.Zt + (int64_t)(2 * sp) * vstride + (int64_t)n * p.ldz;
+          const float* zy = zx + vstride;
+          const float4 a = *reinterpret_cast<const float4*>(zx + r), b = *reinterpret_cast<const float4*>(zx + h + r);
+          const float4 c = *reinterpret_cast<const float4*>(zy + r), dd = *reinterpret_cast<const float4*>(zy + h + r);
+          x0.x += a.x; x0.y += a.y; x0.z += a.z; x0.w += a.w;
+          x1.x += b.x; x1.y += b.y; x1.z += b.z; x1.w += b.w;
+          y0.x += c.x; y0.y += c.y; y0.z += c.z; y0.w += c.w;
+          y1.x += dd.x; y1.y += dd.y; y1.z += dd.z; y1.w += dd.w;
         }
-      } else {
-        for (int64_t e = gtid; e < (int64_t)p.k * h; e += gsz) {
-          const int n = (int)(e / h), r = (int)(e % h);
-          float zx = 0.f, zy = 0.f;
-          for (int sp = 0; sp < p.splitsF; ++sp) {
-            const float* px = p.Zt + (int64_t)(2 * sp) * vstride + (int64_t)n * p.ldz + r0 + r;
-            zx += px[0];
-            zy += px[vstride];
-          }
-          const int64_t o = (int64_t)n * p.hpad + r;
-          dstx[o] = __float2bfloat16_rn(hh == 0 ? zy : zx);
-          dsty[o] = __float2bfloat16_rn(hh == 0 ? zx : zy);
-        }
+        const int64_t o = (int64_t)n * p.hpad + r;
+        store4<__nv_bfloat16>(p.Zb + 0 * plane + o, y0.x, y0.y, y0.z, y0.w);
+        store4<__nv_bfloat16>(p.Zb + 1 * plane + o, x1.x, x1.y, x1.z, x1.w);
+        store4<__nv_bfloat16>(p.Zb + 2 * plane + o, x0.x, x0.y, x0.z, x0.w);
+        store4<__nv_bfloat16>(p.Zb + 3 * plane + o, y1.x, y1.y, y1.z, y1.w);
       }
-      // generic-proxy writes consumed by the async proxy (TMA) after the barrier
-      asm volatile("fence.proxy.async.global;" ::: "memory");
+    } else {
+      for (int64_t e = gtid; e < (int64_t)p.k * h; e += gsz) {
+        const int n = (int)(e / h), r = (int)(e % h);
+        float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
+        for (int sp = 0; sp < p.splitsF; ++sp) {
+          const float* zx = p.Zt + (int64_t)(2 * sp) * vstride + (int64_t)n * p.ldz;
+          const float* zy = zx + vstride;
+          x0 += zx[r]; x1 += zx[h + r]; y0 += zy[r]; y1 += zy[h + r];
+        }
+        const int64_t o = (int64_t)n * p.hpad + r;
+        p.Zb[0 * plane + o] = __float2bfloat16_rn(y0);
+        p.Zb[1 * plane + o] = __float2bfloat16_rn(x1);
+        p.Zb[2 * plane + o] = __float2bfloat16_rn(x0);
+        p.Zb[3 * plane + o] = __float2bfloat16_rn(y1);
+      }
     }
-    grid.sync();
-
-    // ---- phase B: backward products of this half (AV for half 0, BV for half 1) ----
-    if (threadIdx.x == 0)
-      for (int v = 0; v < 2; ++v) { tma_prefetch_desc(&maps.aB[v * 2 + hh]); tma_prefetch_desc(&maps.bB[v * 2 + hh]); }
-    gemm_phase<EB, true>(maps, p, hh, p.mtB[0] + p.mtB[1], ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base,
-                         rs);
-    tc_fence_before();
-    grid.sync();
+    // generic-proxy writes consumed by the async proxy (TMA) after the barrier
+    asm volatile("fence.proxy.async.global;" ::: "memory");
   }
+  grid.sync();
+  stamp(p.upd, 6);
+
+  // ---- phase B: backward products into AV, BV ----
+  if (threadIdx.x == 0)
+    for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&maps.aB[v]); tma_prefetch_desc(&maps.bB[v]); }
+  gemm_phase<EB, true>(maps, p, p.mtB[0] + p.mtB[1], ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
+  tc_fence_before();
+  grid.sync();
   stamp(p.upd, 7);
 
   // ---- release TMEM, then phase U: Gram tables + fused update ----
@@ -324,7 +314,6 @@ inline size_t fused_smem_bytes(int BN, int stages, size_t upd_bytes) {
 }
 
 // Whole CCA step in one cooperative launch (bf16 tensor cores, k <= 64).
-// Zt must hold TC_MAX_SPLITS x 2 x k x ldz floats (ldz >= 2h).
 // `upd` carries the update arguments (state, AV/BV scratch, eta, gamma...);
 // its grid partition (gridDim = G, segw) is reused by the GEMM phases.
 inline geig_status fused_cca_step(TcPlan& t, const void* X, const void* Y, int64_t b, float scale,
@@ -355,7 +344,7 @@ inline geig_status fused_cca_step(TcPlan& t, const void* X, const void* Y, int64
   }
   p.rows = rows; p.h = h; p.k = k; p.BN = t.BN; p.d = t.d; p.ldz = t.ldz; p.hpad = t.hpad;
   p.scale = scale;
-  p.mtF = (h + TC_BM - 1) / TC_BM;      // row tiles per half
+  p.mtF = (rows + TC_BM - 1) / TC_BM;
   p.splitsF = std::min(TC_MAX_SPLITS, choose_splits_deep(2 * p.mtF, std::min(p.kbF[0], p.kbF[1]), grid_ctas));
   p.kbB = (h + ATOM - 1) / ATOM;
   p.idescF = make_idesc(eb, false, t.BN, TC_BM);
