@@ -16,6 +16,7 @@
 #include "update.cuh"
 #include "tc_gemm.cuh"
 #include "fused_step.cuh"
+#include "dataflow_step.cuh"
 
 using namespace geig;
 
@@ -64,6 +65,7 @@ struct geig_solver {
   size_t upd_smem = 0;
   int64_t launches = 0;
   tc::TcPlan tc;                                      // tcgen05 plans (tensor maps, scratch)
+  tc::DfPlan df;                                      // dataflow-step schedule + counters
 };
 
 extern "C" const char* geig_last_error(void) { return g_err.c_str(); }
@@ -170,6 +172,7 @@ extern "C" geig_status geig_destroy(geig_solver* s) {
                   (void*)s->gram, (void*)s->raw, (void*)s->partial,
                   (void*)s->Wx, (void*)s->Wy, (void*)s->ts, (void*)s->Wxb, (void*)s->Wyb, s->hX, s->hY})
     if (p) cudaFree(p);
+  tc::df_destroy(s->df);
   tc::plan_destroy(s->tc);
   delete s;
   return GEIG_OK;
@@ -367,8 +370,13 @@ extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* 
     a.Vbf = s->Vbf; a.partial = s->partial; a.raw = s->raw; a.gram = s->gram;
     a.k = s->k; a.d = s->d; a.segw = s->upd_segw;
     a.eta = (float)eta; a.gamma = (float)gamma; a.rho = s->rho; a.ts = s->ts;
-    geig_status st = tc::fused_cca_step(s->tc, X, Y, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a,
-                                        s->upd_grid, s->upd_smem, s->stream);
+    geig_status st;
+    if (!getenv("GEIG_NO_DATAFLOW") && tc::df_prepare(s->df, s->tc, b, s->upd_grid))
+      st = tc::df_cca_step(s->tc, s->df, X, Y, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a, s->upd_smem,
+                           s->stream);
+    else
+      st = tc::fused_cca_step(s->tc, X, Y, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a, s->upd_grid,
+                              s->upd_smem, s->stream);
     if (st) return fail(st, "%s", tc::last_error());
     s->launches++;
     s->fused_last = true;

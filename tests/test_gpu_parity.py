@@ -235,11 +235,13 @@ def test_dense_config4_full_size_tf32_tcgen05(geig):
 
 @pytest.mark.parametrize("cfg_idx,rows,k,dx,dy", [(3, 4096, None, None, None), (2, 1024, None, None, None),
                                                   (2, 300, 24, 200, 136), (2, 130, 5, 64, 8),
-                                                  (3, 1000, 64, 8192, 4096)])
+                                                  (3, 1000, 64, 8192, 4096), (3, 2048, 32, 1024, 512),
+                                                  (3, 1024, 64, 2048, 1024), (3, 512, 48, 256, 384)])
 def test_fused_step_bf16(geig, cfg_idx, rows, k, dx, dy):
     """geig_step_cca runs forward GEMM, split-K reduction, backward GEMM, Gram
-    tables and the update in ONE cooperative kernel; the step must match the
-    oracle like the staged path (configs 2/3 full size + ragged shapes)."""
+    tables and the update in ONE cooperative kernel (the dataflow schedule
+    when h % 128 == 0 and d_view % 128 == 0, else the phase-ordered one); the
+    step must match the oracle like the staged path."""
     errs, _ = check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math="bf16", use_step=True)
     _assert(errs, 1e-2)
 
