@@ -128,35 +128,48 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
   const uint32_t tmem_base = *tmem_slot;
   stamp(p.upd, 4);
 
+  // This CTA's F items (schedule entries that are not B) in schedule order.
+  // The producer issues them eagerly and slots in the CTA's backward chunk c
+  // as soon as ready[c] is complete (non-blocking probe between items), so a
+  // late chunk never stalls this SM's DRAM stream.  The order actually taken
+  // is published per stage (stage_meta) to the MMA issuer, and per forward
+  // accumulator slot (accF_item) to the epilogue warps.
+  volatile int* stage_meta = reinterpret_cast<volatile int*>(fix_flag + 1);   // [TC_MAX_STAGES]
+  volatile int* accF_item = stage_meta + TC_MAX_STAGES;                         // [2]
+  int nfm = 0, total_stages = 0;
+  for (int si = 0; si < nsched; ++si) {
+    const int e = my[1 + si];
+    if (!sched_is_b(e)) { ++nfm; total_stages += decode_f(p, sched_chunk(e), sched_item(e)).kbn; }
+  }
+  const int nbchunks = bt >= 0 ? p.nchunks : 0;
+  total_stages += nbchunks * (p.CH / BK);
+  // stage meta: F: (fidx << 8) | j  with bit 30 = last k-block ; B: bit 31 | half << 29 | first << 28
   if (threadIdx.x == 0) {
     // ======================= TMA producer =======================
-    int it = 0;
-    for (int si = 0; si < nsched; ++si) {
-      const int e = my[1 + si];
-      const int c = sched_chunk(e);
-      if (!sched_is_b(e)) {
-        const FItem f = decode_f(p, c, sched_item(e));
-        for (int j = 0; j < f.kbn; ++j, ++it) {
-          const int st = it % S;
-          if (it >= S) mbar_wait(&empty_bar[st], ((it / S) + 1) & 1);
-          uint8_t* sa = ring + st * STAGE_BYTES;
-          mbar_expect_tx(&full_bar[st], STAGE_BYTES);
-          const int k0 = (f.kb0 + j) * BK;
-          tma_load_2d(sa, &maps.aF[f.v], &full_bar[st], k0, f.row0);
-          tma_load_2d(sa + A_BYTES, &maps.bF[f.v], &full_bar[st], k0, 0);
+    int it = 0, fi = 0, si = 0, bc = 0;
+    const int need = 2 * p.RT;
+    while (fi < nfm || bc < nbchunks) {
+      bool doB = false;
+      if (bc < nbchunks) {
+        if (fi >= nfm) {
+          while (ld_acquire(&p.ready[bc]) < need) __nanosleep(64);
+          doB = true;
+        } else {
+          doB = ld_acquire(&p.ready[bc]) >= need;
         }
-      } else {
-        // wait until every row tile of chunk c is reduced (both views)
-        const int need = 2 * p.RT;
-        while (ld_acquire(&p.ready[c]) < need) __nanosleep(64);
+      }
+      if (doB) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
+        const int c = bc++;
         const int half = (c * p.CH) >= p.h ? 1 : 0;
-        const int r0 = c * p.CH;                    // absolute row of the chunk
-        const int rz = r0 - half * p.h;             // row within the half (Zb column)
+        const int r0 = c * p.CH;
+        const int rz = r0 - half * p.h;
+        const bool first_of_half = (c * p.CH) == half * p.h;
         const CUtensorMap* mb = &maps.bB[bview * 2 + half];
         for (int j = 0; j < p.CH / BK; ++j, ++it) {
           const int st = it % S;
           if (it >= S) mbar_wait(&empty_bar[st], ((it / S) + 1) & 1);
+          stage_meta[st] = (int)(0x80000000u | ((unsigned)half << 29) | ((first_of_half && j == 0) ? (1u << 28) : 0u));
           uint8_t* sa = ring + st * STAGE_BYTES;
           mbar_expect_tx(&full_bar[st], STAGE_BYTES);
 #pragma unroll
@@ -164,49 +177,60 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
             tma_load_2d(sa + q * (BK * 128), &maps.aB[bview], &full_bar[st], bm0 + q * ATOM, r0 + j * BK);
           tma_load_2d(sa + A_BYTES, mb, &full_bar[st], rz + j * BK, 0);
         }
+      } else {
+        // next F entry of the schedule
+        while (sched_is_b(my[1 + si])) ++si;
+        const int e = my[1 + si++];
+        const FItem f = decode_f(p, sched_chunk(e), sched_item(e));
+        ++fi;
+        for (int j = 0; j < f.kbn; ++j, ++it) {
+          const int st = it % S;
+          if (it >= S) mbar_wait(&empty_bar[st], ((it / S) + 1) & 1);
+          stage_meta[st] = ((si - 1) << 8) | j | (j == f.kbn - 1 ? (1 << 30) : 0);
+          uint8_t* sa = ring + st * STAGE_BYTES;
+          mbar_expect_tx(&full_bar[st], STAGE_BYTES);
+          const int k0 = (f.kb0 + j) * BK;
+          tma_load_2d(sa, &maps.aF[f.v], &full_bar[st], k0, f.row0);
+          tma_load_2d(sa + A_BYTES, &maps.bF[f.v], &full_bar[st], k0, 0);
+        }
       }
     }
   } else if (threadIdx.x == 32) {
     // ======================= MMA issuer =======================
-    int it = 0, nf = 0;
-    bool b_started[2] = {false, false};
-    for (int si = 0; si < nsched; ++si) {
-      const int e = my[1 + si];
-      const int c = sched_chunk(e);
-      if (!sched_is_b(e)) {
-        const FItem f = decode_f(p, c, sched_item(e));
-        const int slot = nf & 1;
-        if (nf >= 2) mbar_wait(&accF_empty[slot], ((nf >> 1) - 1) & 1);
-        tc_fence_after();
-        const uint32_t d = tmem_base + (uint32_t)(slot * 64);
-        for (int j = 0; j < f.kbn; ++j, ++it) {
-          const int st = it % S;
-          mbar_wait(&full_bar[st], (it / S) & 1);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(ring + st * STAGE_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < BK / UK; ++kk)
-            umma<2>(d, make_sdesc(sa + kk * 32, 16, 1024), make_sdesc(sa + A_BYTES + kk * 32, 16, 1024), p.idescF,
-                    (j > 0 || kk > 0) ? 1u : 0u);
-          umma_commit(&empty_bar[st]);
-        }
-        umma_commit(&accF_full[slot]);
-        ++nf;
-      } else {
-        const int half = (c * p.CH) >= p.h ? 1 : 0;
+    int nf = 0;
+    uint32_t dF = 0;
+    for (int it = 0; it < total_stages; ++it) {
+      const int st = it % S;
+      mbar_wait(&full_bar[st], (it / S) & 1);
+      const int meta = stage_meta[st];
+      tc_fence_after();
+      const uint32_t sa = smem_u32(ring + st * STAGE_BYTES);
+      if (meta < 0) {
+        const int half = (meta >> 29) & 1;
+        const bool first = (meta >> 28) & 1;
         const uint32_t d = tmem_base + 128u + (uint32_t)(half * 64);
-        for (int j = 0; j < p.CH / BK; ++j, ++it) {
-          const int st = it % S;
-          mbar_wait(&full_bar[st], (it / S) & 1);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(ring + st * STAGE_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < BK / UK; ++kk)
-            umma<2>(d, make_sdesc(sa + kk * UK * 128, BK * 128, 1024), make_sdesc(sa + A_BYTES + kk * 32, 16, 1024),
-                    p.idescB, (b_started[half] || j > 0 || kk > 0) ? 1u : 0u);
-          umma_commit(&empty_bar[st]);
+        for (int kk = 0; kk < BK / UK; ++kk)
+          umma<2>(d, make_sdesc(sa + kk * UK * 128, BK * 128, 1024), make_sdesc(sa + A_BYTES + kk * 32, 16, 1024),
+                  p.idescB, (!first || kk > 0) ? 1u : 0u);
+        umma_commit(&empty_bar[st]);
+      } else {
+        const int j = meta & 0xff;
+        const bool last = (meta >> 30) & 1;
+        const int slot = nf & 1;
+        if (j == 0) {
+          if (nf >= 2) mbar_wait(&accF_empty[slot], ((nf >> 1) - 1) & 1);
+          tc_fence_after();
+          accF_item[slot] = (meta >> 8) & 0x3fff;      // schedule position of the item
+          __threadfence_block();
+          dF = tmem_base + (uint32_t)(slot * 64);
         }
-        b_started[half] = true;
+#pragma unroll
+        for (int kk = 0; kk < BK / UK; ++kk)
+          umma<2>(dF, make_sdesc(sa + kk * 32, 16, 1024), make_sdesc(sa + A_BYTES + kk * 32, 16, 1024), p.idescF,
+                  (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(&empty_bar[st]);
+        if (last) { umma_commit(&accF_full[slot]); ++nf; }
       }
     }
     if (bt >= 0) umma_commit(accB_full);
@@ -214,16 +238,14 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
     // ======================= epilogue warps =======================
     const int ew = warp - 4;
     const int et = threadIdx.x - 128;         // 0..127
-    int nf = 0;
-    for (int si = 0; si < nsched; ++si) {
-      const int e = my[1 + si];
-      if (sched_is_b(e)) continue;
-      const int c = sched_chunk(e);
-      const FItem f = decode_f(p, c, sched_item(e));
+    for (int nf = 0; nf < nfm; ++nf) {
       const int slot = nf & 1;
       mbar_wait(&accF_full[slot], (nf >> 1) & 1);
       __syncwarp();
       tc_fence_after();
+      const int e = my[1 + accF_item[slot]];
+      const int c = sched_chunk(e);
+      const FItem f = decode_f(p, c, sched_item(e));
       // partial Z of this split: Zp[sp][v][n][row]
       {
         const int row = f.row0 + ew * 32 + lane;
@@ -240,21 +262,19 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
       }
       tc_fence_before();
       mbar_arrive(&accF_empty[slot]);
-      ++nf;
       // ---- split-K fix-up: the last arriving split of this row tile reduces it ----
       __threadfence();
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (et == 0) {
         int* cnt = p.tile_cnt + f.v * (p.rows / TC_BM) + (f.row0 / TC_BM);
         const int old = atomicAdd(cnt, 1);
-        const bool last = old == p.SPL - 1;
-        if (last) *cnt = 0;                     // self-reset for the next step
-        *fix_flag = last ? 1 : 0;
+        const bool lastsp = old == p.SPL - 1;
+        if (lastsp) *cnt = 0;                   // self-reset for the next step
+        *fix_flag = lastsp ? 1 : 0;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (*fix_flag) {
         __threadfence();
-        // rows f.row0 .. +127 of view v: sum SPL partials, cast, route (reading R1)
         const int half = f.row0 >= p.h ? 1 : 0;
         // half 0: Z_x feeds the Y backward, Z_y the X backward; half 1: own view
         const int dview = half == 0 ? 1 - f.v : f.v;
@@ -432,7 +452,7 @@ inline geig_status df_cca_step(TcPlan& t, DfPlan& q, const void* X, const void* 
   p.AV = AV; p.BV = BV; p.upd = upd;
   const size_t stage_bytes = TC_BM * 128 + (size_t)t.BN * 128;
   p.stages = (int)std::min<size_t>(TC_MAX_STAGES, (196 * 1024) / stage_bytes);
-  const size_t ring = (size_t)p.stages * stage_bytes + (2 * TC_MAX_STAGES + 8) * 8 + 16;
+  const size_t ring = (size_t)p.stages * stage_bytes + (2 * TC_MAX_STAGES + 8) * 8 + 16 + (TC_MAX_STAGES + 4) * 4;
   const size_t smem = 1024 + std::max(ring, upd_bytes);
   static bool attr = false;
   if (!attr) {
