@@ -55,6 +55,7 @@ struct DfParams {
   float* AV;
   float* BV;
   UpdateArgs upd;
+  unsigned long long* dbg;   // optional per-CTA stamps: [start, producer done, MMA done, epilogue done, F done]
 };
 
 // schedule entry: bit 31 = B item; F: chunk << 16 | item-in-chunk ; B: chunk
@@ -127,6 +128,7 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   stamp(p.upd, 4);
+  if (p.dbg && threadIdx.x == 0) p.dbg[blockIdx.x * 8 + 0] = gtimer();
 
   // This CTA's F items (schedule entries that are not B) in schedule order.
   // The producer issues them eagerly and slots in the CTA's backward chunk c
@@ -193,8 +195,10 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
           tma_load_2d(sa, &maps.aF[f.v], &full_bar[st], k0, f.row0);
           tma_load_2d(sa + A_BYTES, &maps.bF[f.v], &full_bar[st], k0, 0);
         }
+        if (p.dbg && fi == nfm) p.dbg[blockIdx.x * 8 + 4] = gtimer();
       }
     }
+    if (p.dbg) p.dbg[blockIdx.x * 8 + 1] = gtimer();
   } else if (threadIdx.x == 32) {
     // ======================= MMA issuer =======================
     int nf = 0;
@@ -234,6 +238,7 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
       }
     }
     if (bt >= 0) umma_commit(accB_full);
+    if (p.dbg) p.dbg[blockIdx.x * 8 + 2] = gtimer();
   } else if (warp >= 4) {
     // ======================= epilogue warps =======================
     const int ew = warp - 4;
@@ -299,6 +304,7 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
         if (et == 0) atomicAdd(p.ready + c, 1);
       }
     }
+    if (p.dbg && et == 0) p.dbg[blockIdx.x * 8 + 5] = gtimer();
     // ---- backward accumulators of the owned feature tile -> AV, BV ----
     if (bt >= 0) {
       mbar_wait(accB_full, 0);
@@ -321,6 +327,7 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
       }
     }
   }
+  if (p.dbg && threadIdx.x == 128) p.dbg[blockIdx.x * 8 + 3] = gtimer();
   tc_fence_before();
   grid.sync();
   stamp(p.upd, 7);
@@ -449,7 +456,7 @@ inline geig_status df_cca_step(TcPlan& t, DfPlan& q, const void* X, const void* 
   p.idescB = make_idesc(eb, true, t.BN, TC_BM);
   p.sched = q.d_sched; p.btile = q.d_btile; p.mtB0 = q.mtB0;
   p.Zp = q.d_Zp; p.Zb = (__nv_bfloat16*)t.Zb; p.tile_cnt = q.d_tile_cnt; p.ready = q.d_ready;
-  p.AV = AV; p.BV = BV; p.upd = upd;
+  p.AV = AV; p.BV = BV; p.upd = upd; p.dbg = dbg_ptr();
   const size_t stage_bytes = TC_BM * 128 + (size_t)t.BN * 128;
   p.stages = (int)std::min<size_t>(TC_MAX_STAGES, (196 * 1024) / stage_bytes);
   const size_t ring = (size_t)p.stages * stage_bytes + (2 * TC_MAX_STAGES + 8) * 8 + 16 + (TC_MAX_STAGES + 4) * 4;
