@@ -32,3 +32,6 @@ for j, n in enumerate(names):
     col = col[t[:, j] > 0]
     if len(col):
         print(f"{n:14s} min {col.min():7.1f} med {statistics.median(col.tolist()):7.1f} max {col.max():7.1f} us (n={len(col)})")
+order = sorted(range(len(t)), key=lambda i: -st[i, 5].item())
+print("slowest F-drained CTAs:", [(i, round(st[i, 5].item(), 1), round(st[i, 4].item(), 1)) for i in order[:12]])
+print("fastest:", [(i, round(st[i, 5].item(), 1)) for i in order[-5:]])
