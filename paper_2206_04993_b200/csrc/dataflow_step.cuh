@@ -393,16 +393,13 @@ inline bool df_prepare(DfPlan& q, const TcPlan& t, int64_t b, int G) {
   const int nF = 2 * RT * SPL;                // F items per chunk
   const int Fk = std::min(kbx, kby) / SPL;    // ~stages per F item
   const int Bk = CH / 64;                     // stages per B(c)
-  // F items of every chunk are dealt round-robin over a rotation in which the
-  // CTAs that own no backward tile appear twice (they have no L2-fed B work),
-  // so each chunk's forward work is spread over many SMs and completes early.
+  // F items of every chunk are dealt round-robin over all CTAs (the DRAM
+  // stream is the bottleneck; the L2-fed backward chunks fill the gaps), so
+  // each chunk's forward work is spread over many SMs and completes early.
   std::vector<int> btile(G, -1);
   for (int f = 0; f < mtB; ++f) btile[f] = f;
   std::vector<int> rot;
-  for (int g = 0; g < G; ++g) {
-    rot.push_back(g);
-    if (btile[g] < 0) rot.push_back(g);
-  }
+  for (int g = 0; g < G; ++g) rot.push_back(g);
   (void)Fk; (void)Bk;
   std::vector<std::vector<std::vector<int>>> per_chunk(G, std::vector<std::vector<int>>(nchunks));
   size_t ptr = 0;
