@@ -244,6 +244,7 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
     // ======================= epilogue warps =======================
     const int ew = warp - 4;
     const int et = threadIdx.x - 128;         // 0..127
+    unsigned long long t_red_acc = 0, t_fix_acc = 0;
     for (int nf = 0; nf < nfm; ++nf) {
       const int slot = nf & 1;
       mbar_wait(&accF_full[slot], (nf >> 1) & 1);
@@ -252,6 +253,7 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
       const int e = my[1 + accF_item[slot]];
       const int c = sched_chunk(e);
       const FItem f = decode_f(p, c, sched_item(e));
+      unsigned long long t_red0 = (p.dbg && et == 0) ? gtimer() : 0ull;
       // accumulate this split into Z_acc[v][n][row] (fp32 red.add at L2)
       {
         const int row = f.row0 + ew * 32 + lane;
@@ -274,6 +276,7 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
       // ---- the last arriving split of this row tile converts it (fix-up) ----
       __threadfence();
       asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (p.dbg && et == 0) { t_red_acc += gtimer() - t_red0; t_red0 = gtimer(); }
       if (et == 0) {
         int* cnt = p.tile_cnt + f.v * (p.rows / TC_BM) + (f.row0 / TC_BM);
         const int old = atomicAdd(cnt, 1);
@@ -314,8 +317,10 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
         __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (et == 0) atomicAdd(p.ready + c, 1);
+        if (p.dbg && et == 0) t_fix_acc += gtimer() - t_red0;
       }
     }
+    if (p.dbg && et == 0) { p.dbg[blockIdx.x * 8 + 6] = t_red_acc; p.dbg[blockIdx.x * 8 + 7] = t_fix_acc; }
     if (p.dbg && et == 0) p.dbg[blockIdx.x * 8 + 5] = gtimer();
     // ---- backward accumulators of the owned feature tile -> AV, BV ----
     if (bt >= 0) {

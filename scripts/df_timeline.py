@@ -35,3 +35,7 @@ for j, n in enumerate(names):
 order = sorted(range(len(t)), key=lambda i: -st[i, 5].item())
 print("slowest F-drained CTAs:", [(i, round(st[i, 5].item(), 1), round(st[i, 4].item(), 1)) for i in order[:12]])
 print("fastest:", [(i, round(st[i, 5].item(), 1)) for i in order[-5:]])
+
+red = t[:, 6].double() / 1e3
+fix = t[:, 7].double() / 1e3
+print(f"epilogue red-phase total per CTA: med {statistics.median(red.tolist()):.1f} max {red.max():.1f} us; fix-up total: med {statistics.median(fix.tolist()):.1f} max {fix.max():.1f} us")
