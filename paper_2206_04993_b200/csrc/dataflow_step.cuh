@@ -15,8 +15,7 @@
 // LAST finishing item of a row tile ("fix-up": per-tile arrival counter),
 // which writes the bf16 backward operand and bumps the chunk's ready counter;
 // the TMA producer of a B(c) item polls that counter (acquire) before its
-// loads.  Splits accumulate with red.global.add into an fp32 Z tile that the
-// fix-up converts (and re-zeroes).  The two TMEM accumulators of the forward items are double-buffered
+// loads.  The two TMEM accumulators of the forward items are double-buffered
 // so the MMA issuer never waits for the epilogue drain.  After all items a
 // grid barrier hands over to the Gram / update phases (update_res_phases).
 #pragma once
@@ -49,7 +48,7 @@ struct DfParams {
   const int* sched;      // [G][1 + DF_MAXSCHED]: count, then entries
   const int* btile;      // [G]: feature tile owned for the backward (-1: none)
   int mtB0;              // feature tiles of view x (tiles >= mtB0 belong to view y)
-  float* Zp;             // 2 x k x ldz fp32 split-K accumulators (red.add; re-zeroed by the fix-up)
+  float* Zp;             // SPL x 2 x k x ldz fp32 split-K partials (player-major)
   __nv_bfloat16* Zb;     // 4 x k x hpad
   int* tile_cnt;         // [2][rows/128] arrival counters (self-resetting)
   int* ready;            // [nchunks] reduced row tiles per chunk (reset at the end)
@@ -254,69 +253,82 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
       const int c = sched_chunk(e);
       const FItem f = decode_f(p, c, sched_item(e));
       unsigned long long t_red0 = (p.dbg && et == 0) ? gtimer() : 0ull;
-      // accumulate this split into Z_acc[v][n][row] (fp32 red.add at L2)
+      // partial Z of this split -> Zp[sp][v][n][row] (plain coalesced stores)
       {
         const int row = f.row0 + ew * 32 + lane;
-        float* out = p.Zp + ((int64_t)f.v * p.k) * p.ldz + row;
+        float* out = p.Zp + ((int64_t)(2 * f.sp + f.v) * p.k) * p.ldz + row;
         for (int c0 = 0; c0 < p.BN; c0 += 16) {
           uint32_t r[16];
           tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(slot * 64 + c0), r);
           if (row < p.rows) {
 #pragma unroll
             for (int jn = 0; jn < 16; ++jn)
-              if (c0 + jn < p.k)
-                asm volatile("red.global.add.f32 [%0], %1;" ::"l"(out + (int64_t)(c0 + jn) * p.ldz),
-                             "f"(__uint_as_float(r[jn]))
-                             : "memory");
+              if (c0 + jn < p.k) out[(int64_t)(c0 + jn) * p.ldz] = __uint_as_float(r[jn]);
           }
         }
       }
       tc_fence_before();
       mbar_arrive(&accF_empty[slot]);
-      // ---- the last arriving split of this row tile converts it (fix-up) ----
-      __threadfence();
+      // ---- the last arriving split of this row tile reduces it (fix-up) ----
+      // bar.sync makes the 128 threads' stores visible to thread 0, whose
+      // gpu-scope fence is cumulative over them before the arrival count.
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (p.dbg && et == 0) { t_red_acc += gtimer() - t_red0; t_red0 = gtimer(); }
       if (et == 0) {
+        __threadfence();
         int* cnt = p.tile_cnt + f.v * (p.rows / TC_BM) + (f.row0 / TC_BM);
         const int old = atomicAdd(cnt, 1);
         const bool lastsp = old == p.SPL - 1;
-        if (lastsp) *cnt = 0;                   // self-reset for the next step
+        if (lastsp) { *cnt = 0; __threadfence(); }   // self-reset for the next step
         *fix_flag = lastsp ? 1 : 0;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (p.dbg && et == 0) { t_red_acc += gtimer() - t_red0; t_red0 = gtimer(); }
       if (*fix_flag) {
-        __threadfence();
         const int half = f.row0 >= p.h ? 1 : 0;
         // half 0: Z_x feeds the Y backward, Z_y the X backward; half 1: own view
         const int dview = half == 0 ? 1 - f.v : f.v;
         __nv_bfloat16* dst = p.Zb + (int64_t)(dview * 2 + half) * p.k * p.hpad;
         const int rbase = f.row0 - half * p.h;
-        float* zacc = p.Zp + ((int64_t)f.v * p.k) * p.ldz;
-        constexpr int Q = TC_BM / 4;            // float4 per row-tile row of one player
-        float4 vals[16];
-        int idxs[16];
+        const int64_t vstride = (int64_t)p.k * p.ldz;
+        const float* zsrc = p.Zp + (int64_t)f.v * vstride;
+        constexpr int Q = TC_BM / 4;            // float4 per player row of the tile
+        for (int u0 = 0; u0 < 16; u0 += 4) {    // 16 x 128 = 2048 = 64 players x 32 quads (k <= 64)
+          float4 acc[4];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int idx = et + 128 * u;         // 16 x 128 = 2048 = 64 players x 32 quads (k <= 64)
-          idxs[u] = idx;
-          const int n = idx / Q, q = 4 * (idx % Q);
-          const bool ok = n < p.k && f.row0 + q < p.rows;
-          vals[u] = ok ? *reinterpret_cast<const float4*>(zacc + (int64_t)n * p.ldz + f.row0 + q)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+          for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int n = idxs[u] / Q, q = 4 * (idxs[u] % Q);
-          if (n < p.k && f.row0 + q < p.rows) {
-            store4<__nv_bfloat16>(dst + (int64_t)n * p.hpad + rbase + q, vals[u].x, vals[u].y, vals[u].z, vals[u].w);
-            *reinterpret_cast<float4*>(zacc + (int64_t)n * p.ldz + f.row0 + q) = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int sp = 0; sp < TC_MAX_SPLITS; ++sp) {
+            if (sp < p.SPL) {
+              float4 v4[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int idx = et + 128 * (u0 + u);
+                const int n = idx / Q, q = 4 * (idx % Q);
+                const bool ok = n < p.k && f.row0 + q < p.rows;
+                v4[u] = ok ? *reinterpret_cast<const float4*>(zsrc + (int64_t)(2 * sp) * vstride + (int64_t)n * p.ldz +
+                                                              f.row0 + q)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                acc[u].x += v4[u].x; acc[u].y += v4[u].y; acc[u].z += v4[u].z; acc[u].w += v4[u].w;
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int idx = et + 128 * (u0 + u);
+            const int n = idx / Q, q = 4 * (idx % Q);
+            if (n < p.k && f.row0 + q < p.rows)
+              store4<__nv_bfloat16>(dst + (int64_t)n * p.hpad + rbase + q, acc[u].x, acc[u].y, acc[u].z, acc[u].w);
           }
         }
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        __threadfence();
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (et == 0) atomicAdd(p.ready + c, 1);
+        if (et == 0) {
+          __threadfence();
+          atomicAdd(p.ready + c, 1);
+        }
         if (p.dbg && et == 0) t_fix_acc += gtimer() - t_red0;
       }
     }
@@ -428,7 +440,7 @@ inline bool df_prepare(DfPlan& q, const TcPlan& t, int64_t b, int G) {
   if (cudaMalloc(&q.d_sched, sched.size() * 4) != cudaSuccess || cudaMalloc(&q.d_btile, G * 4) != cudaSuccess ||
       cudaMalloc(&q.d_tile_cnt, 2 * (rows / TC_BM) * 4) != cudaSuccess ||
       cudaMalloc(&q.d_ready, nchunks * 4) != cudaSuccess ||
-      cudaMalloc(&q.d_Zp, (size_t)2 * t.k * t.ldz * 4) != cudaSuccess) {
+      cudaMalloc(&q.d_Zp, (size_t)SPL * 2 * t.k * t.ldz * 4) != cudaSuccess) {
     df_destroy(q);
     return false;
   }
@@ -436,7 +448,7 @@ inline bool df_prepare(DfPlan& q, const TcPlan& t, int64_t b, int G) {
   cudaMemcpy(q.d_btile, btile.data(), G * 4, cudaMemcpyHostToDevice);
   cudaMemset(q.d_tile_cnt, 0, 2 * (rows / TC_BM) * 4);
   cudaMemset(q.d_ready, 0, nchunks * 4);
-  cudaMemset(q.d_Zp, 0, (size_t)2 * t.k * t.ldz * 4);
+
   q.G = G; q.CH = CH; q.nchunks = nchunks; q.RT = RT; q.SPL = SPL; q.mtB = mtB; q.mtB0 = mtx; q.b = b;
   q.ready = true;
   return true;
