@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <string>
+#include <cstdlib>
 #include "../../include/geig.h"
 
 namespace geig { namespace tc {
@@ -565,6 +566,7 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
     p.idesc = make_idesc(eb, false, t.BN, TC_BM);
     const int mt = (rows + TC_BM - 1) / TC_BM;
     p.splits = std::min(TC_MAX_SPLITS, choose_splits_deep(2 * mt, std::min(p.kblocks[0][0], p.kblocks[1][0]), t.nsm));
+    if (const char* e = getenv("GEIG_FWD_SPLITS")) p.splits = std::max(1, std::min(TC_MAX_SPLITS, atoi(e)));
     fsplits = p.splits;
     dim3 grid(mt, p.splits, 2);
     geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st, t.nsm) : launch<4, false>(maps, p, grid, st, t.nsm);
