@@ -371,7 +371,10 @@ extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* 
     a.k = s->k; a.d = s->d; a.segw = s->upd_segw;
     a.eta = (float)eta; a.gamma = (float)gamma; a.rho = s->rho; a.ts = s->ts;
     geig_status st;
-    if (!getenv("GEIG_NO_DATAFLOW") && tc::df_prepare(s->df, s->tc, b, s->upd_grid))
+    // The dataflow schedule (dataflow_step.cuh) is correct but, measured on
+    // B200, not yet faster than the phase-ordered kernel (its split-K fix-ups
+    // sit on the critical path under full-DRAM load); opt-in via GEIG_DATAFLOW=1.
+    if (getenv("GEIG_DATAFLOW") && tc::df_prepare(s->df, s->tc, b, s->upd_grid))
       st = tc::df_cca_step(s->tc, s->df, X, Y, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a, s->upd_smem,
                            s->stream);
     else

@@ -253,3 +253,11 @@ def test_fused_step_matches_staged_path(geig):
     e2, g2 = check_cca_step(geig, 2, 1024, math="bf16", use_step=False)
     assert rel_err(g1["V"] - g2["V"] + 1.0, np.ones_like(g2["V"])) < 1e-3
     assert rel_err(g1["aux"], g2["aux"]) < 1e-3
+
+
+def test_dataflow_step_bf16(geig, monkeypatch):
+    """The opt-in dataflow schedule (GEIG_DATAFLOW=1) matches the oracle too."""
+    monkeypatch.setenv("GEIG_DATAFLOW", "1")
+    for cfg_idx, rows, k, dx, dy in [(3, 4096, None, None, None), (3, 1024, 64, 2048, 1024)]:
+        errs, _ = check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math="bf16", use_step=True)
+        _assert(errs, 1e-2)
