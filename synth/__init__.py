@@ -16,4 +16,5 @@ from .workloads import (  # noqa: F401
     cca_views,
     gaussian_init,
     appendix_b_example,
+    planted_cca_views,
 )

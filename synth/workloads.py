@@ -183,3 +183,25 @@ def appendix_b_example():
     a = np.array([[0.77759061, 0.26842584], [0.26842584, 0.87788983]])
     b = np.array([[0.2325605, 0.06042127], [0.06042127, 0.03241424]])
     return a, b
+
+
+def planted_cca_views(n: int, dx: int, dy: int, corrs, seed: int = 0, device="cpu",
+                      dtype: torch.dtype = torch.float32):
+    """Paired views with planted canonical correlations `corrs` and identity
+    population covariances: coordinates i < r of x are z_i, of y are
+    c_i z_i + sqrt(1-c_i^2) e_i, the rest independent N(0,1); each view is then
+    rotated by a seeded Haar matrix.  Population generalized eigenvalues of
+    the CCA GEP are +-c_i (and 0).  Used by convergence tests."""
+    r = len(corrs)
+    rng = _np_rng(31 * seed + 5)
+    qx = torch.tensor(haar_orthogonal(dx, rng), dtype=torch.float32, device=device)
+    qy = torch.tensor(haar_orthogonal(dy, rng), dtype=torch.float32, device=device)
+    g = torch.Generator(device=device)
+    g.manual_seed(97 * seed + 13)
+    z = torch.randn(n, r, generator=g, device=device)
+    x = torch.randn(n, dx, generator=g, device=device)
+    y = torch.randn(n, dy, generator=g, device=device)
+    c = torch.tensor(list(corrs), dtype=torch.float32, device=device)
+    x[:, :r] = z
+    y[:, :r] = c * z + torch.sqrt(1 - c * c) * y[:, :r]
+    return (x @ qx).to(dtype).contiguous(), (y @ qy).to(dtype).contiguous()

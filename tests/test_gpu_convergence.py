@@ -1,0 +1,80 @@
+"""GPU convergence (north star): iterating the GPU step reaches the exact
+generalized eigenvectors.  A fixed batch makes the step deterministic, so the
+target is the exact GEP of that batch's (A_t, B_t) (reading R1 halves),
+solved in fp64 by the oracle; the mean per-vector angle (reading R9) and the
+Appendix A subspace error are checked."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+CORRS = [0.95, 0.9, 0.85, 0.8, 0.75, 0.7, 0.65, 0.6]
+
+
+@pytest.fixture(scope="module")
+def geig():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2206_04993_b200 import build
+    build.build()
+    from paper_2206_04993_b200 import geig as g
+    return g
+
+
+def _run_cca(geig, math, dtype, steps=1500, eta=0.5, k=4, dv=128, b=8192):
+    from oracle import estimators, linalg, metrics
+    from synth import gaussian_init, planted_cca_views
+    x, y = planted_cca_views(b, dv, dv, CORRS, seed=1, dtype=dtype)
+    dev = "cuda:0"
+    s = geig.Solver(geig.GEIG_CCA, dv, dv, k, math=math,
+                    data_dtype=geig.GEIG_DATA_BF16 if dtype == torch.bfloat16 else geig.GEIG_DATA_F32,
+                    rho=0.1, max_rows=b)
+    try:
+        s.init_state(torch.tensor(gaussian_init(k, 2 * dv, 0), dtype=torch.float32, device=dev))
+        xd, yd = x.to(dev), y.to(dev)
+        for _ in range(steps):
+            geig.geig_step_cca(s.h, xd, yd, b, eta, 1.0)
+        V, _ = s.state()
+    finally:
+        s.close()
+    a_t, b_t = estimators.cca_minibatch_matrices(x.double().numpy(), y.double().numpy())
+    w, Vt = linalg.generalized_eigh(a_t, b_t, k)
+    Vg = V.double().cpu().numpy()
+    ang = metrics.per_vector_angles(Vg, Vt)
+    return ang, metrics.subspace_error(Vg, a_t, b_t)
+
+
+def test_converges_fp32_variant(geig):
+    ang, se = _run_cca(geig, "f32", torch.float32)
+    print("fp32 FFMA variant: angles", ang, "subspace error", se)
+    assert ang.mean() < 1e-3 and se < 1e-6
+
+
+def test_converges_bf16_variant(geig):
+    """bf16 tensor-core variant (fused single-launch step): V is rounded to
+    bf16 for the products, so the fixed point moves by O(bf16 eps / gap)."""
+    ang, se = _run_cca(geig, "bf16", torch.bfloat16)
+    print("bf16 tcgen05 variant: angles", ang, "mean", ang.mean(), "subspace error", se)
+    assert ang.mean() < 1e-2 and se < 1e-3
+
+
+def test_converges_tf32_dense_config0(geig):
+    from oracle import linalg, metrics
+    from synth import CONFIGS, dense_gep_small, gaussian_init
+    cfg = CONFIGS[0]
+    a, b = dense_gep_small(0)
+    dev = "cuda:0"
+    A = torch.tensor(a, dtype=torch.float32, device=dev)
+    B = torch.tensor(b, dtype=torch.float32, device=dev)
+    w, Vt = linalg.generalized_eigh(A.double().cpu().numpy(), B.double().cpu().numpy(), cfg.k)
+    s = geig.Solver(geig.GEIG_DENSE, cfg.d, 0, cfg.k, math="tf32", rho=cfg.rho)
+    try:
+        s.init_state(torch.tensor(gaussian_init(cfg.k, cfg.d, 0), dtype=torch.float32, device=dev))
+        for _ in range(cfg.steps):
+            geig.geig_step_dense(s.h, A, B, cfg.eta, cfg.gamma)
+        V, _ = s.state()
+    finally:
+        s.close()
+    ang = metrics.per_vector_angles(V.double().cpu().numpy(), Vt)
+    print("tf32 dense config 0: angles", ang)
+    assert ang.mean() < 1e-2
