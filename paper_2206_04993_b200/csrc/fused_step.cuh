@@ -34,10 +34,12 @@ struct FusedMaps {
   CUtensorMap bF[2];   // forward B: V_x, V_y (K-major, box {ATOM, BN})
   CUtensorMap aB[4];   // backward A: X[0:h], X[h:2h], Y[0:h], Y[h:2h] (MN-major, box {ATOM, ATOM})
   CUtensorMap bB[4];   // backward B: Zb planes (K-major, box {ATOM, BN})
+  CUtensorMap bFlo[2]; // bf16x2: low halves of V_x, V_y
+  CUtensorMap bBlo[4]; // bf16x2: low halves of the Zb planes
 };
 
 struct FusedParams {
-  int rows, h, k, BN, stages, splitsF, mtF, mtB[2];
+  int rows, h, k, BN, stages, splitsF, mtF, mtB[2], split;
   int kbF[2], kbB;                 // K blocks: forward per view, backward per half
   int64_t dv[2], d, ldz, hpad;
   float scale;
@@ -54,6 +56,7 @@ struct Item {
   int kb0[2], kbn[2];
   const CUtensorMap* ma[2];
   const CUtensorMap* mb[2];
+  const CUtensorMap* mblo[2];
   float* out[2];
   int64_t ldo;
   float scale;
@@ -74,6 +77,7 @@ __device__ __forceinline__ void decode_forward(const FusedMaps& M, const FusedPa
   it.mb[0] = v == 0 ? &M.bF[0] : &M.bF[1];
   it.ma[1] = it.ma[0];
   it.mb[1] = it.mb[0];
+  it.mblo[0] = it.mblo[1] = v == 0 ? &M.bFlo[0] : &M.bFlo[1];
   it.out[0] = p.Zt + ((int64_t)(2 * sp + v) * p.k) * p.ldz;
   it.out[1] = nullptr;
   it.ldo = p.ldz;
@@ -92,6 +96,8 @@ __device__ __forceinline__ void decode_backward(const FusedMaps& M, const FusedP
   it.ma[1] = v == 0 ? &M.aB[1] : &M.aB[3];
   it.mb[0] = v == 0 ? &M.bB[0] : &M.bB[2];
   it.mb[1] = v == 0 ? &M.bB[1] : &M.bB[3];
+  it.mblo[0] = v == 0 ? &M.bBlo[0] : &M.bBlo[2];
+  it.mblo[1] = v == 0 ? &M.bBlo[1] : &M.bBlo[3];
   const int64_t off = v == 0 ? 0 : p.dv[0];
   it.out[0] = p.AV + off;
   it.out[1] = p.BV + off;
@@ -113,7 +119,8 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
   constexpr int UK = 32 / EB;
   constexpr uint32_t A_BYTES = TC_BM * 128;
   const uint32_t B_BYTES = (uint32_t)p.BN * 128;
-  const uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  const bool split = p.split != 0;
+  const uint32_t STAGE_BYTES = A_BYTES + B_BYTES * (split ? 2 : 1);
   const int S = p.stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t idesc = A_MN ? p.idescB : p.idescF;
@@ -138,6 +145,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
             tma_load_2d(sa, it.ma[s], &full_bar[st], k0, it.m0);
           }
           tma_load_2d(sb, it.mb[s], &full_bar[st], k0, 0);
+          if (split) tma_load_2d(sb + B_BYTES, it.mblo[s], &full_bar[st], k0, 0);
         }
       }
     }
@@ -160,6 +168,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
             const uint64_t ad = A_MN ? make_sdesc(sa + kk * UK * 128, BK * 128, 1024) : make_sdesc(sa + kk * 32, 16, 1024);
             const uint64_t bd = make_sdesc(sb + kk * 32, 16, 1024);
             umma<EB>(d_tmem, ad, bd, idesc, (j > 0 || kk > 0) ? 1u : 0u);
+            if (split) umma<EB>(d_tmem, ad, make_sdesc(sb + B_BYTES + kk * 32, 16, 1024), idesc, 1u);
           }
           umma_commit(&empty_bar[st]);
         }
@@ -200,7 +209,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t STAGE_BYTES = TC_BM * 128 + (uint32_t)p.BN * 128;
+  const uint32_t STAGE_BYTES = TC_BM * 128 + (uint32_t)p.BN * 128 * (p.split ? 2 : 1);
   uint8_t* ring = smem;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + p.stages * STAGE_BYTES);
   uint64_t* empty_bar = full_bar + TC_MAX_STAGES;
@@ -265,6 +274,12 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
         store4<__nv_bfloat16>(p.Zb + 1 * plane + o, x1.x, x1.y, x1.z, x1.w);
         store4<__nv_bfloat16>(p.Zb + 2 * plane + o, x0.x, x0.y, x0.z, x0.w);
         store4<__nv_bfloat16>(p.Zb + 3 * plane + o, y1.x, y1.y, y1.z, y1.w);
+        if (p.split) {
+          store4_lo<__nv_bfloat16>(p.Zb + 4 * plane + o, y0.x, y0.y, y0.z, y0.w);
+          store4_lo<__nv_bfloat16>(p.Zb + 5 * plane + o, x1.x, x1.y, x1.z, x1.w);
+          store4_lo<__nv_bfloat16>(p.Zb + 6 * plane + o, x0.x, x0.y, x0.z, x0.w);
+          store4_lo<__nv_bfloat16>(p.Zb + 7 * plane + o, y1.x, y1.y, y1.z, y1.w);
+        }
       }
     } else {
       for (int64_t e = gtid; e < (int64_t)p.k * h; e += gsz) {
@@ -276,10 +291,12 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
           x0 += zx[r]; x1 += zx[h + r]; y0 += zy[r]; y1 += zy[h + r];
         }
         const int64_t o = (int64_t)n * p.hpad + r;
-        p.Zb[0 * plane + o] = __float2bfloat16_rn(y0);
-        p.Zb[1 * plane + o] = __float2bfloat16_rn(x1);
-        p.Zb[2 * plane + o] = __float2bfloat16_rn(x0);
-        p.Zb[3 * plane + o] = __float2bfloat16_rn(y1);
+        const float zv[4] = {y0, x1, x0, y1};
+        for (int q = 0; q < 4; ++q) {
+          const __nv_bfloat16 hv = __float2bfloat16_rn(zv[q]);
+          p.Zb[q * plane + o] = hv;
+          if (p.split) p.Zb[(4 + q) * plane + o] = __float2bfloat16_rn(zv[q] - __bfloat162float(hv));
+        }
       }
     }
     // generic-proxy writes consumed by the async proxy (TMA) after the barrier
@@ -308,10 +325,6 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
 // ----------------------------------------------------------------------------
 // host side
 // ----------------------------------------------------------------------------
-inline size_t fused_smem_bytes(int BN, int stages, size_t upd_bytes) {
-  const size_t ring = (size_t)stages * (TC_BM * 128 + (size_t)BN * 128) + (2 * TC_MAX_STAGES + 4) * 8;
-  return 1024 + std::max(ring, upd_bytes);
-}
 
 // Whole CCA step in one cooperative launch (bf16 tensor cores, k <= 64).
 // `upd` carries the update arguments (state, AV/BV scratch, eta, gamma...);
@@ -320,6 +333,7 @@ inline geig_status fused_cca_step(TcPlan& t, const void* X, const void* Y, int64
                                   const __nv_bfloat16* Vbf, float* AV, float* BV, UpdateArgs upd, int grid_ctas,
                                   size_t upd_bytes, cudaStream_t st) {
   if (!t.ready || t.math != GEIG_MATH_BF16) return tc_fail(GEIG_ERR_STATE, "fused step needs the bf16 plan");
+  // (t.math is BF16 for both GEIG_MATH_BF16 and GEIG_MATH_BF16X2; t.splitb selects hi+lo operands)
   const int eb = 2, ATOM = 64;
   const int h = (int)(b / 2), rows = 2 * h, k = t.k;
   const int64_t dv[2] = {t.dx, t.dy};
@@ -331,12 +345,16 @@ inline geig_status fused_cca_step(TcPlan& t, const void* X, const void* Y, int64
     if (!make_map(&maps.aF[v], Xv[v], eb, dv[v], rows, dv[v], ATOM, TC_BM) ||
         !make_map(&maps.bF[v], vb, eb, dv[v], k, t.d, ATOM, t.BN))
       return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused forward) failed");
+    if (t.splitb && !make_map(&maps.bFlo[v], vb + (int64_t)k * t.d * eb, eb, dv[v], k, t.d, ATOM, t.BN))
+      return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused forward lo) failed");
     for (int s = 0; s < 2; ++s) {
       const char* xb = (const char*)Xv[v] + (int64_t)s * h * dv[v] * eb;
       const char* zb = (const char*)t.Zb + (int64_t)(v * 2 + s) * k * t.hpad * eb;
       if (!make_map(&maps.aB[v * 2 + s], xb, eb, dv[v], h, dv[v], ATOM, ATOM) ||
           !make_map(&maps.bB[v * 2 + s], zb, eb, h, k, t.hpad, ATOM, t.BN))
         return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused backward) failed");
+      if (t.splitb && !make_map(&maps.bBlo[v * 2 + s], zb + (int64_t)4 * k * t.hpad * eb, eb, h, k, t.hpad, ATOM, t.BN))
+        return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused backward lo) failed");
     }
     p.dv[v] = dv[v];
     p.kbF[v] = (int)((dv[v] + ATOM - 1) / ATOM);
@@ -354,9 +372,10 @@ inline geig_status fused_cca_step(TcPlan& t, const void* X, const void* Y, int64
   p.AV = AV;
   p.BV = BV;
   p.upd = upd;
-  const size_t stage_bytes = TC_BM * 128 + (size_t)t.BN * 128;
+  p.split = t.splitb;
+  const size_t stage_bytes = TC_BM * 128 + (size_t)t.BN * 128 * (t.splitb ? 2 : 1);
   p.stages = (int)std::min<size_t>(TC_MAX_STAGES, (200 * 1024) / stage_bytes);
-  const size_t smem = fused_smem_bytes(t.BN, p.stages, upd_bytes);
+  const size_t smem = 1024 + std::max((size_t)p.stages * stage_bytes + (2 * TC_MAX_STAGES + 4) * 8, upd_bytes);
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(cca_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)

@@ -82,10 +82,10 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
   if (k > 128) return fail(GEIG_ERR_UNSUPPORTED, "k=%d > 128 not compiled", k);
   if (dx < 1 || dy < 0 || (problem == GEIG_CCA && dy < 1) || (problem == GEIG_DENSE && dy != 0))
     return fail(GEIG_ERR_ARG, "bad dims dx=%lld dy=%lld", (long long)dx, (long long)dy);
-  if (math < GEIG_MATH_F32 || math > GEIG_MATH_3XTF32) return fail(GEIG_ERR_ARG, "bad math %d", math);
+  if (math < GEIG_MATH_F32 || math > GEIG_MATH_BF16X2) return fail(GEIG_ERR_ARG, "bad math %d", math);
   if (data_dtype != GEIG_DATA_F32 && data_dtype != GEIG_DATA_BF16) return fail(GEIG_ERR_ARG, "bad dtype");
-  if (math == GEIG_MATH_BF16 && data_dtype != GEIG_DATA_BF16)
-    return fail(GEIG_ERR_ARG, "GEIG_MATH_BF16 requires bf16 data");
+  if ((math == GEIG_MATH_BF16 || math == GEIG_MATH_BF16X2) && data_dtype != GEIG_DATA_BF16)
+    return fail(GEIG_ERR_ARG, "GEIG_MATH_BF16/BF16X2 require bf16 data");
   if ((math == GEIG_MATH_TF32 || math == GEIG_MATH_3XTF32) && data_dtype != GEIG_DATA_F32)
     return fail(GEIG_ERR_ARG, "tf32 math requires fp32 data");
   if (!(rho >= 0.0)) return fail(GEIG_ERR_ARG, "rho must be >= 0");
@@ -104,7 +104,7 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
     return cleanup(fail(GEIG_ERR_CUDA, "cudaMalloc %zu bytes failed", (size_t)(bytes)));
   ALLOC(s->V, kd * 4);
   ALLOC(s->AUX, kd * 4);
-  ALLOC(s->Vbf, kd * 2);
+  ALLOC(s->Vbf, kd * 2 * 2);      // hi + lo planes
   ALLOC(s->AV, kd * 4);
   ALLOC(s->BV, kd * 4);
   ALLOC(s->gram, (size_t)3 * k * k * 4);
@@ -120,7 +120,7 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
 #undef ALLOC
   cudaMemset(s->V, 0, kd * 4);
   cudaMemset(s->AUX, 0, kd * 4);
-  cudaMemset(s->Vbf, 0, kd * 2);
+  cudaMemset(s->Vbf, 0, kd * 2 * 2);
   cudaMemset(s->gram, 0, (size_t)3 * k * k * 4);
 
   // cooperative update grid: one co-resident CTA per SM, contiguous column ranges
@@ -206,7 +206,7 @@ extern "C" geig_status geig_set_state(geig_solver* s, const float* V, const floa
   const size_t kd = (size_t)s->k * s->d;
   CU(cudaMemcpyAsync(s->V, V, kd * 4, cudaMemcpyDeviceToDevice, s->stream));
   if (AUX) CU(cudaMemcpyAsync(s->AUX, AUX, kd * 4, cudaMemcpyDeviceToDevice, s->stream));
-  f32_to_bf16_kernel<<<256, 256, 0, s->stream>>>(s->V, s->Vbf, (int64_t)kd);
+  f32_to_bf16_kernel<<<256, 256, 0, s->stream>>>(s->V, s->Vbf, (int64_t)kd);   // hi + lo planes
   CHECK_LAUNCH();
   s->launches++;
   return GEIG_OK;
@@ -354,7 +354,7 @@ extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float*
 }
 
 static bool fused_ok(const geig_solver* s, const void* X, const void* Y) {
-  if (s->math != GEIG_MATH_BF16 || !s->upd_res || s->d % 4 != 0) return false;
+  if ((s->math != GEIG_MATH_BF16 && s->math != GEIG_MATH_BF16X2) || !s->upd_res || s->d % 4 != 0) return false;
   if (getenv("GEIG_NO_FUSED")) return false;
   return (((uintptr_t)X | (uintptr_t)Y) % 16) == 0;
 }
@@ -374,7 +374,7 @@ extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* 
     // The dataflow schedule (dataflow_step.cuh) is correct but, measured on
     // B200, not yet faster than the phase-ordered kernel (its split-K fix-ups
     // sit on the critical path under full-DRAM load); opt-in via GEIG_DATAFLOW=1.
-    if (getenv("GEIG_DATAFLOW") && tc::df_prepare(s->df, s->tc, b, s->upd_grid))
+    if (getenv("GEIG_DATAFLOW") && !s->tc.splitb && tc::df_prepare(s->df, s->tc, b, s->upd_grid))
       st = tc::df_cca_step(s->tc, s->df, X, Y, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a, s->upd_smem,
                            s->stream);
     else

@@ -120,6 +120,7 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
 struct TcMaps {
   CUtensorMap a[4];   // index = group * 2 + segment
   CUtensorMap b[4];
+  CUtensorMap blo[4]; // bf16x2: low halves of the B operands (bf16(x - bf16(x)))
 };
 
 struct TcParams {
@@ -144,7 +145,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-template <int EB, bool A_MN, int TC_STAGES>
+template <int EB, bool A_MN, int TC_STAGES, bool SPLIT>
 __global__ void __launch_bounds__(TC_THREADS)
 tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   constexpr int ATOM = 128 / EB;           // elements per 128B row
@@ -158,7 +159,7 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   if (m0 >= Mg) return;
   const int BN = p.BN;
   const uint32_t B_BYTES = (uint32_t)BN * 128;
-  const uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  const uint32_t STAGE_BYTES = A_BYTES + B_BYTES * (SPLIT ? 2 : 1);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -229,6 +230,7 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
             tma_load_2d(sa, ma, &full_bar[st], k0, m0);
           }
           tma_load_2d(sb, mb, &full_bar[st], k0, 0);
+          if constexpr (SPLIT) tma_load_2d(sb + B_BYTES, &maps.blo[g * 2 + s], &full_bar[st], k0, 0);
         }
       }
     } else if (threadIdx.x == 32) {
@@ -253,6 +255,7 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
             }
             bd = make_sdesc(sb + kk * 32, 16, 1024);
             umma<EB>(d_tmem, ad, bd, p.idesc, (j > 0 || kk > 0) ? 1u : 0u);
+            if constexpr (SPLIT) umma<EB>(d_tmem, ad, make_sdesc(sb + B_BYTES + kk * 32, 16, 1024), p.idesc, 1u);
           }
           umma_commit(&empty_bar[st]);
         }
@@ -338,8 +341,17 @@ __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* dst, float 
 }
 
 template <typename T>
+__device__ __forceinline__ void store4_lo(T* dst, float a, float b, float c, float d) {}
+template <>
+__device__ __forceinline__ void store4_lo<__nv_bfloat16>(__nv_bfloat16* dst, float a, float b, float c, float d) {
+  const float ha = __bfloat162float(__float2bfloat16_rn(a)), hb = __bfloat162float(__float2bfloat16_rn(b));
+  const float hc = __bfloat162float(__float2bfloat16_rn(c)), hd = __bfloat162float(__float2bfloat16_rn(d));
+  store4<__nv_bfloat16>(dst, a - ha, b - hb, c - hc, d - hd);
+}
+
+template <typename T>
 __global__ void zshuffle_kernel(const float* __restrict__ Zp, T* __restrict__ Zb, int k, int64_t ldz, int h,
-                                int64_t hpad, int splits) {
+                                int64_t hpad, int splits, int lo) {
   pdl_trigger();
   pdl_wait();
   const int64_t vstride = (int64_t)k * ldz;
@@ -366,6 +378,12 @@ __global__ void zshuffle_kernel(const float* __restrict__ Zp, T* __restrict__ Zb
       store4<T>(Zb + 1 * plane + o, x1.x, x1.y, x1.z, x1.w);   // view x, half 1
       store4<T>(Zb + 2 * plane + o, x0.x, x0.y, x0.z, x0.w);   // view y, half 0
       store4<T>(Zb + 3 * plane + o, y1.x, y1.y, y1.z, y1.w);   // view y, half 1
+      if (lo) {                                                 // bf16x2 low halves
+        store4_lo<T>(Zb + 4 * plane + o, y0.x, y0.y, y0.z, y0.w);
+        store4_lo<T>(Zb + 5 * plane + o, x1.x, x1.y, x1.z, x1.w);
+        store4_lo<T>(Zb + 6 * plane + o, x0.x, x0.y, x0.z, x0.w);
+        store4_lo<T>(Zb + 7 * plane + o, y1.x, y1.y, y1.z, y1.w);
+      }
     }
     return;
   }
@@ -383,6 +401,10 @@ __global__ void zshuffle_kernel(const float* __restrict__ Zp, T* __restrict__ Zb
     Zb[1 * plane + o] = (T)x1;
     Zb[2 * plane + o] = (T)x0;
     Zb[3 * plane + o] = (T)y1;
+    if (lo) {
+      const float v4[4] = {y0, x1, x0, y1};
+      for (int q = 0; q < 4; ++q) Zb[(4 + q) * plane + o] = (T)(v4[q] - (float)(T)v4[q]);
+    }
   }
 }
 
@@ -391,6 +413,7 @@ __global__ void zshuffle_kernel(const float* __restrict__ Zp, T* __restrict__ Zb
 // ----------------------------------------------------------------------------
 struct TcPlan {
   int ready = 0;
+  int splitb = 0;          // bf16x2: B operands as hi + lo bf16 (V and Z), 2 MMAs per K step
   int problem = 0, math = 0, k = 0, BN = 0, device = 0, nsm = 148;
   int64_t dx = 0, dy = 0, d = 0, max_rows = 0, ldz = 0, hpad = 0;
   float* Zt = nullptr;     // TC_MAX_SPLITS x 2 x k x ldz fp32 (CCA forward split-K partials)
@@ -446,40 +469,52 @@ inline uint32_t make_idesc(int eb, bool a_mn, int N, int M) {
          ((uint32_t)(M >> 4) << 24);
 }
 
-inline size_t smem_bytes(int BN, int stages) {
-  return 1024 + (size_t)stages * (TC_BM * 128 + (size_t)BN * 128) + 256;
+inline size_t smem_bytes(int BN, int stages, bool split = false) {
+  return 1024 + (size_t)stages * (TC_BM * 128 + (size_t)BN * 128 * (split ? 2 : 1)) + 256;
 }
 
 // Stage count: enough bytes in flight per SM to cover DRAM latency. One
-// resident CTA per SM (grid <= #SM) gets 8 stages, denser grids 4.
-template <int EB, bool A_MN>
-inline geig_status launch(const TcMaps& maps, const TcParams& p, dim3 grid, cudaStream_t st, int nsm) {
-  const int ctas = grid.x * grid.y * grid.z;
-  const_cast<TcParams&>(p).dbg = dbg_ptr();
-  if (dbg_ptr()) dbg_ptr() += (size_t)4 * ctas;   // next launch stamps after this one
-  const bool deep = ctas <= nsm && smem_bytes(p.BN, 8) <= 227 * 1024;
-  static bool attr_done[2] = {false, false};
-  if (!attr_done[deep]) {
-    cudaError_t e = deep ? cudaFuncSetAttribute(tc_gemm_kernel<EB, A_MN, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)smem_bytes(128, 8) > 227 * 1024 ? 227 * 1024 : (int)smem_bytes(128, 8))
-                         : cudaFuncSetAttribute(tc_gemm_kernel<EB, A_MN, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)smem_bytes(128, 4));
-    if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, "cudaFuncSetAttribute(tc_gemm_kernel) failed");
-    attr_done[deep] = true;
+// resident CTA per SM (grid <= #SM) gets the deep ring, denser grids 4 stages.
+template <int EB, bool A_MN, int ST, bool SPLIT>
+inline cudaError_t launch_one(const TcMaps& maps, const TcParams& p, dim3 grid, cudaStream_t st) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    const size_t mx = std::min<size_t>(227 * 1024, smem_bytes(128, ST, SPLIT));
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<EB, A_MN, ST, SPLIT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = smem_bytes(p.BN, deep ? 8 : 4);
+  cfg.dynamicSmemBytes = smem_bytes(p.BN, ST, SPLIT);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = deep ? cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EB, A_MN, 8>, maps, p)
-                       : cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EB, A_MN, 4>, maps, p);
-  if (e == cudaSuccess) e = cudaGetLastError();
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EB, A_MN, ST, SPLIT>, maps, p);
+  return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
+template <int EB, bool A_MN>
+inline geig_status launch(const TcMaps& maps, const TcParams& p, dim3 grid, cudaStream_t st, int nsm,
+                          bool split = false) {
+  const int ctas = grid.x * grid.y * grid.z;
+  const_cast<TcParams&>(p).dbg = dbg_ptr();
+  if (dbg_ptr()) dbg_ptr() += (size_t)4 * ctas;   // next launch stamps after this one
+  const bool one_per_sm = ctas <= nsm;
+  cudaError_t e;
+  if (split) {
+    // bf16x2 stage = A + 2 B: 6 stages fit one CTA per SM
+    if (one_per_sm && smem_bytes(p.BN, 6, true) <= 227 * 1024) e = launch_one<EB, A_MN, 6, true>(maps, p, grid, st);
+    else e = launch_one<EB, A_MN, 3, true>(maps, p, grid, st);
+  } else {
+    if (one_per_sm && smem_bytes(p.BN, 8) <= 227 * 1024) e = launch_one<EB, A_MN, 8, false>(maps, p, grid, st);
+    else e = launch_one<EB, A_MN, 4, false>(maps, p, grid, st);
+  }
   if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("tc_gemm launch: ") + cudaGetErrorString(e));
   return GEIG_OK;
 }
@@ -500,6 +535,8 @@ inline int choose_splits(int ctas, int kblocks, int nsm) {
 inline geig_status plan_create(TcPlan& t, int problem, int64_t dx, int64_t dy, int k, int math, int64_t max_rows,
                                int device) {
   if (math == GEIG_MATH_3XTF32) return tc_fail(GEIG_ERR_UNSUPPORTED, "3xTF32 products not built yet");
+  t.splitb = math == GEIG_MATH_BF16X2 ? 1 : 0;
+  if (t.splitb) math = GEIG_MATH_BF16;
   const int eb = math == GEIG_MATH_BF16 ? 2 : 4;
   const int align = 16 / eb;
   if (dx % align || dy % align)
@@ -514,9 +551,9 @@ inline geig_status plan_create(TcPlan& t, int problem, int64_t dx, int64_t dy, i
     t.ldz = ((max_rows + 3) / 4) * 4;
     t.hpad = ((max_rows / 2 + 7) / 8) * 8;
     if (cudaMalloc((void**)&t.Zt, (size_t)TC_MAX_SPLITS * 2 * k * t.ldz * 4) != cudaSuccess ||
-        cudaMalloc(&t.Zb, (size_t)4 * k * t.hpad * eb) != cudaSuccess)
+        cudaMalloc(&t.Zb, (size_t)8 * k * t.hpad * eb) != cudaSuccess)
       return tc_fail(GEIG_ERR_CUDA, "cudaMalloc tc scratch");
-    cudaMemset(t.Zb, 0, (size_t)4 * k * t.hpad * eb);
+    cudaMemset(t.Zb, 0, (size_t)8 * k * t.hpad * eb);
   }
   t.ready = 1;
   return GEIG_OK;
@@ -553,8 +590,11 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
       if (!make_map(&maps.a[v * 2], Xv[v], eb, dv[v], rows, dv[v], ATOM, TC_BM) ||
           !make_map(&maps.b[v * 2], vb, eb, dv[v], k, t.d, ATOM, t.BN))
         return tc_fail(GEIG_ERR_CUDA, "tensor map encode (forward) failed");
+      if (t.splitb && !make_map(&maps.blo[v * 2], vb + (int64_t)k * t.d * eb, eb, dv[v], k, t.d, ATOM, t.BN))
+        return tc_fail(GEIG_ERR_CUDA, "tensor map encode (forward lo) failed");
       maps.a[v * 2 + 1] = maps.a[v * 2];
       maps.b[v * 2 + 1] = maps.b[v * 2];
+      maps.blo[v * 2 + 1] = maps.blo[v * 2];
       p.M[v] = rows;
       p.kblocks[v][0] = (int)((dv[v] + ATOM - 1) / ATOM);
       p.kblocks[v][1] = 0;
@@ -569,7 +609,7 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
     if (const char* e = getenv("GEIG_FWD_SPLITS")) p.splits = std::max(1, std::min(TC_MAX_SPLITS, atoi(e)));
     fsplits = p.splits;
     dim3 grid(mt, p.splits, 2);
-    geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st, t.nsm) : launch<4, false>(maps, p, grid, st, t.nsm);
+    geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st, t.nsm, t.splitb) : launch<4, false>(maps, p, grid, st, t.nsm);
     if (s) return s;
     ++*nl;
   }
@@ -589,10 +629,10 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
     cudaError_t le;
     if (eb == 2)
       le = cudaLaunchKernelEx(&cfg, zshuffle_kernel<__nv_bfloat16>, (const float*)t.Zt, (__nv_bfloat16*)t.Zb, k, t.ldz,
-                              h, t.hpad, fsplits);
+                              h, t.hpad, fsplits, t.splitb);
     else
       le = cudaLaunchKernelEx(&cfg, zshuffle_kernel<float>, (const float*)t.Zt, (float*)t.Zb, k, t.ldz, h, t.hpad,
-                              fsplits);
+                              fsplits, 0);
     if (le != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, "zshuffle launch failed");
     if (cudaGetLastError() != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, "zshuffle launch failed");
     ++*nl;
@@ -609,6 +649,8 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
         if (!make_map(&maps.a[v * 2 + s], xb, eb, dv[v], h, dv[v], ATOM, ATOM) ||
             !make_map(&maps.b[v * 2 + s], zb, eb, h, k, t.hpad, ATOM, t.BN))
           return tc_fail(GEIG_ERR_CUDA, "tensor map encode (backward) failed");
+        if (t.splitb && !make_map(&maps.blo[v * 2 + s], zb + 4 * plane * eb, eb, h, k, t.hpad, ATOM, t.BN))
+          return tc_fail(GEIG_ERR_CUDA, "tensor map encode (backward lo) failed");
         p.kblocks[v][s] = (h + ATOM - 1) / ATOM;
       }
       p.M[v] = (int)dv[v];
@@ -629,7 +671,7 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
         return tc_fail(GEIG_ERR_CUDA, "memset AV/BV failed");
     }
     dim3 grid(mt, p.splits, 2);
-    geig_status s = eb == 2 ? launch<2, true>(maps, p, grid, st, t.nsm) : launch<4, true>(maps, p, grid, st, t.nsm);
+    geig_status s = eb == 2 ? launch<2, true>(maps, p, grid, st, t.nsm, t.splitb) : launch<4, true>(maps, p, grid, st, t.nsm);
     if (s) return s;
     ++*nl;
   }

@@ -47,7 +47,7 @@ struct UpdateArgs {
   float* AUX;            // k x d (in/out)
   const float* AV;       // k x d
   const float* BV;       // k x d
-  __nv_bfloat16* Vbf;    // k x d bf16 copy of the new V (nullable)
+  __nv_bfloat16* Vbf;    // 2 x k x d bf16 shadow of the new V: hi plane, then lo = bf16(v - hi) (nullable)
   float* partial;        // gridDim x (2*KP*KP + 2*KP) scratch
   float* raw;            // 2*KP*KP + 2*KP reduced un-normalised tables
   float* gram;           // 3 x k x k out: normalised GA, GB, GC of the step
@@ -57,6 +57,24 @@ struct UpdateArgs {
   float eta, gamma, rho;
   unsigned long long* ts;  // 6 %globaltimer stamps of CTA 0 (phase boundaries), nullable
 };
+
+// bf16 "x2" shadow of v: hi = bf16(v), lo = bf16(v - hi); the products may
+// use hi alone (bf16) or hi + lo (bf16x2, ~fp32-accurate operand).
+__device__ __forceinline__ void store_vbf4(__nv_bfloat16* hi, int64_t lo_off, size_t o, float4 v) {
+  const __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y), h1 = __floats2bfloat162_rn(v.z, v.w);
+  const float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
+  const __nv_bfloat162 l0 = __floats2bfloat162_rn(v.x - f0.x, v.y - f0.y), l1 = __floats2bfloat162_rn(v.z - f1.x, v.w - f1.y);
+  uint2 ph, pl;
+  ph.x = *reinterpret_cast<const uint32_t*>(&h0); ph.y = *reinterpret_cast<const uint32_t*>(&h1);
+  pl.x = *reinterpret_cast<const uint32_t*>(&l0); pl.y = *reinterpret_cast<const uint32_t*>(&l1);
+  *reinterpret_cast<uint2*>(hi + o) = ph;
+  *reinterpret_cast<uint2*>(hi + lo_off + o) = pl;
+}
+__device__ __forceinline__ void store_vbf1(__nv_bfloat16* hi, int64_t lo_off, size_t o, float v) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  hi[o] = h;
+  hi[lo_off + o] = __float2bfloat16_rn(v - __bfloat162float(h));
+}
 
 __device__ __forceinline__ void stamp(const UpdateArgs& p, int slot) {
   if (p.ts && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -377,20 +395,14 @@ update_kernel(UpdateArgs p) {
           if (VEC && gx + 3 < c1) {
             *reinterpret_cast<float4*>(p.V + o) = vn;
             *reinterpret_cast<float4*>(p.AUX + o) = an;
-            if (p.Vbf) {
-              __nv_bfloat162 lo = __floats2bfloat162_rn(vn.x, vn.y), hi = __floats2bfloat162_rn(vn.z, vn.w);
-              uint2 pk;
-              pk.x = *reinterpret_cast<uint32_t*>(&lo);
-              pk.y = *reinterpret_cast<uint32_t*>(&hi);
-              *reinterpret_cast<uint2*>(p.Vbf + o) = pk;
-            }
+            if (p.Vbf) store_vbf4(p.Vbf, (int64_t)k * d, o, vn);
           } else {
             const float vs[4] = {vn.x, vn.y, vn.z, vn.w}, as[4] = {an.x, an.y, an.z, an.w};
             for (int t = 0; t < 4; ++t)
               if (gx + t < c1) {
                 p.V[o + t] = vs[t];
                 p.AUX[o + t] = as[t];
-                if (p.Vbf) p.Vbf[o + t] = __float2bfloat16_rn(vs[t]);
+                if (p.Vbf) store_vbf1(p.Vbf, (int64_t)k * d, o + t, vs[t]);
               }
           }
         }
@@ -650,20 +662,14 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
           if (VEC && gx + 3 < c1) {
             *reinterpret_cast<float4*>(p.V + o) = vn;
             *reinterpret_cast<float4*>(p.AUX + o) = an;
-            if (p.Vbf) {
-              __nv_bfloat162 lo = __floats2bfloat162_rn(vn.x, vn.y), hi = __floats2bfloat162_rn(vn.z, vn.w);
-              uint2 pk;
-              pk.x = *reinterpret_cast<uint32_t*>(&lo);
-              pk.y = *reinterpret_cast<uint32_t*>(&hi);
-              *reinterpret_cast<uint2*>(p.Vbf + o) = pk;
-            }
+            if (p.Vbf) store_vbf4(p.Vbf, (int64_t)k * d, o, vn);
           } else {
             const float vs[4] = {vn.x, vn.y, vn.z, vn.w}, as[4] = {an.x, an.y, an.z, an.w};
             for (int t = 0; t < 4; ++t)
               if (gx + t < c1) {
                 p.V[o + t] = vs[t];
                 p.AUX[o + t] = as[t];
-                if (p.Vbf) p.Vbf[o + t] = __float2bfloat16_rn(vs[t]);
+                if (p.Vbf) store_vbf1(p.Vbf, (int64_t)k * d, o + t, vs[t]);
               }
           }
         }
@@ -729,13 +735,14 @@ init_state_kernel(const float* __restrict__ G, float* V, float* AUX, __nv_bfloat
     const float v = G[(int64_t)i * d + x] * inv;
     V[(int64_t)i * d + x] = v;
     AUX[(int64_t)i * d + x] = v;
-    if (Vbf) Vbf[(int64_t)i * d + x] = __float2bfloat16_rn(v);
+    if (Vbf) store_vbf1(Vbf, (int64_t)gridDim.x * d, (size_t)i * d + x, v);
   }
 }
 
+// hi/lo bf16 shadow of an fp32 array (dst holds 2 x n: hi plane, lo plane)
 __global__ void f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* dst, int64_t n) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
-    dst[e] = __float2bfloat16_rn(src[e]);
+    store_vbf1(dst, n, (size_t)e, src[e]);
 }
 
 }  // namespace geig

@@ -17,11 +17,11 @@ LIB_PATH = os.path.join(_HERE, "libgeig.so")
 
 GEIG_OK, GEIG_ERR_ARG, GEIG_ERR_CUDA, GEIG_ERR_UNSUPPORTED, GEIG_ERR_STATE = range(5)
 GEIG_DENSE, GEIG_CCA = 0, 1
-GEIG_MATH_F32, GEIG_MATH_BF16, GEIG_MATH_TF32, GEIG_MATH_3XTF32 = 0, 1, 2, 3
+GEIG_MATH_F32, GEIG_MATH_BF16, GEIG_MATH_TF32, GEIG_MATH_3XTF32, GEIG_MATH_BF16X2 = 0, 1, 2, 3, 4
 GEIG_DATA_F32, GEIG_DATA_BF16 = 0, 1
 
 MATH_NAMES = {"f32": GEIG_MATH_F32, "bf16": GEIG_MATH_BF16, "tf32": GEIG_MATH_TF32,
-              "3xtf32": GEIG_MATH_3XTF32}
+              "3xtf32": GEIG_MATH_3XTF32, "bf16x2": GEIG_MATH_BF16X2}
 
 
 class GeigError(RuntimeError):

@@ -58,6 +58,13 @@ def test_converges_bf16_variant(geig):
     assert ang.mean() < 1e-2 and se < 1e-3
 
 
+def test_converges_bf16x2_variant(geig):
+    """bf16 data, tensor cores, hi+lo bf16 operands: meets the 1e-3 rad bar."""
+    ang, se = _run_cca(geig, "bf16x2", torch.bfloat16)
+    print("bf16x2 tcgen05 variant: angles", ang, "mean", ang.mean(), "subspace error", se)
+    assert ang.mean() < 1e-3 and se < 1e-6
+
+
 def test_converges_tf32_dense_config0(geig):
     from oracle import linalg, metrics
     from synth import CONFIGS, dense_gep_small, gaussian_init

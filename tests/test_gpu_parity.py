@@ -261,3 +261,17 @@ def test_dataflow_step_bf16(geig, monkeypatch):
     for cfg_idx, rows, k, dx, dy in [(3, 4096, None, None, None), (3, 1024, 64, 2048, 1024)]:
         errs, _ = check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math="bf16", use_step=True)
         _assert(errs, 1e-2)
+
+
+# --- bf16x2: V and Z split into hi + lo bf16 operands (exact bf16 data) ------
+
+@pytest.mark.parametrize("cfg_idx,rows,k,dx,dy,use_step", [(3, 4096, None, None, None, False),
+                                                           (3, 4096, None, None, None, True),
+                                                           (2, 1024, None, None, None, True),
+                                                           (2, 300, 24, 200, 136, False)])
+def test_bf16x2_fp32_level_parity(geig, cfg_idx, rows, k, dx, dy, use_step):
+    """With the bf16 data exact and the V / Z operands carried as hi+lo bf16
+    pairs, the tensor-core products reach the fp32 exactness-variant bar
+    (1e-4)."""
+    errs, _ = check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math="bf16x2", use_step=use_step)
+    _assert(errs, 1e-4)
