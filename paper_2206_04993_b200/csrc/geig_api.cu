@@ -51,6 +51,8 @@ struct geig_solver {
   // state
   float *V = nullptr, *AUX = nullptr;
   __nv_bfloat16* Vbf = nullptr;
+  char* arena = nullptr;                              // V | AUX | AV | BV | Vbf (one allocation)
+  size_t arena_bytes = 0;
   // scratch
   float *AV = nullptr, *BV = nullptr, *gram = nullptr, *raw = nullptr;
   float *partial = nullptr;
@@ -102,11 +104,22 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
 #define ALLOC(ptr, bytes)                                                               \
   if (cudaMalloc((void**)&(ptr), (bytes)) != cudaSuccess)                              \
     return cleanup(fail(GEIG_ERR_CUDA, "cudaMalloc %zu bytes failed", (size_t)(bytes)));
-  ALLOC(s->V, kd * 4);
-  ALLOC(s->AUX, kd * 4);
-  ALLOC(s->Vbf, kd * 2 * 2);      // hi + lo planes
-  ALLOC(s->AV, kd * 4);
-  ALLOC(s->BV, kd * 4);
+  // One arena for the per-step state (V, [Bv], bf16 shadow, AV, BV: 18 B per
+  // k x d element) so a single L2 persistence window can pin it while the
+  // minibatch streams through L2 (see set_l2_window).
+  {
+    const size_t arena = kd * (4 + 4 + 4 + 4 + 4);
+    char* base = nullptr;
+    if (cudaMalloc((void**)&base, arena) != cudaSuccess)
+      return cleanup(fail(GEIG_ERR_CUDA, "cudaMalloc state arena %zu bytes failed", arena));
+    s->arena = base;
+    s->arena_bytes = arena;
+    s->V = (float*)base;
+    s->AUX = (float*)(base + kd * 4);
+    s->AV = (float*)(base + kd * 8);
+    s->BV = (float*)(base + kd * 12);
+    s->Vbf = (__nv_bfloat16*)(base + kd * 16);      // hi + lo planes
+  }
   ALLOC(s->gram, (size_t)3 * k * k * 4);
   ALLOC(s->ts, 8 * sizeof(unsigned long long));
   cudaMemset(s->ts, 0, 8 * sizeof(unsigned long long));
@@ -168,7 +181,7 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
 extern "C" geig_status geig_destroy(geig_solver* s) {
   if (!s) return GEIG_OK;
   cudaSetDevice(s->device);
-  for (void* p : {(void*)s->V, (void*)s->AUX, (void*)s->Vbf, (void*)s->AV, (void*)s->BV,
+  for (void* p : {(void*)s->arena,
                   (void*)s->gram, (void*)s->raw, (void*)s->partial,
                   (void*)s->Wx, (void*)s->Wy, (void*)s->ts, (void*)s->Wxb, (void*)s->Wyb, s->hX, s->hY})
     if (p) cudaFree(p);
@@ -178,9 +191,31 @@ extern "C" geig_status geig_destroy(geig_solver* s) {
   return GEIG_OK;
 }
 
+// Pin the state arena in L2 (persisting access policy on the solver's stream)
+// so the update phases find V, [Bv], AV, BV in L2 after the products have
+// streamed the minibatch (> L2) through it.  Best effort: ignored on failure.
+static void set_l2_window(geig_solver* s) {
+  if (getenv("GEIG_NO_L2_PERSIST")) return;
+  int max_persist = 0, max_window = 0;
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, s->device);
+  cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, s->device);
+  if (max_persist <= 0 || max_window <= 0) return;
+  const size_t want = std::min<size_t>(s->arena_bytes, (size_t)max_persist);
+  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+  cudaStreamAttrValue v = {};
+  v.accessPolicyWindow.base_ptr = s->arena;
+  v.accessPolicyWindow.num_bytes = std::min<size_t>(s->arena_bytes, (size_t)max_window);
+  v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)want / (float)v.accessPolicyWindow.num_bytes);
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cudaStreamSetAttribute(s->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+  cudaGetLastError();   // best effort
+}
+
 extern "C" geig_status geig_set_stream(geig_solver* s, void* stream) {
   if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
   s->stream = (cudaStream_t)stream;
+  if (s->stream) set_l2_window(s);
   return GEIG_OK;
 }
 
