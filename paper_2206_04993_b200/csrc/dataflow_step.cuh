@@ -91,7 +91,10 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
   constexpr uint32_t A_BYTES = TC_BM * 128;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned view of the dynamic smem that stays in the shared
+  // address space (integer pointer round-trips would turn every later smem
+  // access into a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t STAGE_BYTES = A_BYTES + (uint32_t)p.BN * 128;
   const int S = p.stages;
   uint8_t* ring = smem;
@@ -358,6 +361,7 @@ cca_step_df_kernel(const __grid_constant__ DfMaps maps, const DfParams p) {
   }
   if (p.dbg && threadIdx.x == 128) p.dbg[blockIdx.x * 8 + 3] = gtimer();
   tc_fence_before();
+  __syncwarp();   // reconverge the role lanes before the CTA barrier inside grid.sync
   grid.sync();
   stamp(p.upd, 7);
   if (blockIdx.x == 0)

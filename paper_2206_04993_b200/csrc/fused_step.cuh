@@ -36,10 +36,11 @@ struct FusedMaps {
   CUtensorMap bB[4];   // backward B: Zb planes (K-major, box {ATOM, BN})
   CUtensorMap bFlo[2]; // bf16x2: low halves of V_x, V_y
   CUtensorMap bBlo[4]; // bf16x2: low halves of the Zb planes
+  UpdMaps um;          // phase U: fp32 state tiles (V'', AV, [Bv], BV)
 };
 
 struct FusedParams {
-  int rows, h, k, BN, stages, splitsF, mtF, mtB[2], split;
+  int rows, h, k, BN, stages, splitsF, mtF, mtB[2], split, bwd_y_first, dbg_nostore, dbg_mode;
   int kbF[2], kbB;                 // K blocks: forward per view, backward per half
   int64_t dv[2], d, ldz, hpad;
   float scale;
@@ -85,8 +86,10 @@ __device__ __forceinline__ void decode_forward(const FusedMaps& M, const FusedPa
 }
 
 __device__ __forceinline__ void decode_backward(const FusedMaps& M, const FusedParams& p, int idx, Item& it) {
-  const int v = idx < p.mtB[0] ? 0 : 1;
-  const int mt = v == 0 ? idx : idx - p.mtB[0];
+  // view Y first: phase F streamed Y last, so part of it is still in L2
+  const int first = p.bwd_y_first ? 1 : 0;
+  const int v = idx < p.mtB[first] ? first : 1 - first;
+  const int mt = v == first ? idx : idx - p.mtB[first];
   it.nseg = 2;
   it.m0 = mt * TC_BM;
   it.mbound = (int)(v == 0 ? p.dv[0] : p.dv[1]);
@@ -135,7 +138,8 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
           if (rs.it_prod >= S) mbar_wait(&empty_bar[st], ((rs.it_prod / S) + 1) & 1);
           uint8_t* sa = ring + st * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(&full_bar[st], STAGE_BYTES);
+          const bool nob = (p.dbg_mode & 2) != 0;
+          mbar_expect_tx(&full_bar[st], nob ? A_BYTES : STAGE_BYTES);
           const int k0 = (it.kb0[s] + j) * BK;
           if (A_MN) {
 #pragma unroll
@@ -144,8 +148,10 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
           } else {
             tma_load_2d(sa, it.ma[s], &full_bar[st], k0, it.m0);
           }
-          tma_load_2d(sb, it.mb[s], &full_bar[st], k0, 0);
-          if (split) tma_load_2d(sb + B_BYTES, it.mblo[s], &full_bar[st], k0, 0);
+          if (!nob) {
+            tma_load_2d(sb, it.mb[s], &full_bar[st], k0, 0);
+            if (split) tma_load_2d(sb + B_BYTES, it.mblo[s], &full_bar[st], k0, 0);
+          }
         }
       }
     }
@@ -165,6 +171,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
           const uint32_t sb = sa + A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / UK; ++kk) {
+            if (p.dbg_mode & 1) break;
             const uint64_t ad = A_MN ? make_sdesc(sa + kk * UK * 128, BK * 128, 1024) : make_sdesc(sa + kk * 32, 16, 1024);
             const uint64_t bd = make_sdesc(sb + kk * 32, 16, 1024);
             umma<EB>(d_tmem, ad, bd, idesc, (j > 0 || kk > 0) ? 1u : 0u);
@@ -190,7 +197,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
         for (int c0 = 0; c0 < p.BN; c0 += 16) {
           uint32_t r[16];
           tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(s * p.BN + c0), r);
-          if (mok) {
+          if (mok && !p.dbg_nostore) {
 #pragma unroll
             for (int j = 0; j < 16; ++j)
               if (c0 + j < p.k) out[(int64_t)(c0 + j) * it.ldo] = it.scale * __uint_as_float(r[j]);
@@ -201,14 +208,22 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
       mbar_arrive(acce_bar);
     }
   }
+  // Reconverge warps 0/1 (lane 0 ran a role, lanes 1-31 did not) before any
+  // CTA barrier: bar.sync counts whole warps, so a divergent warp arriving
+  // early would release the barrier before the epilogue warps finished.
+  __syncwarp();
 }
 
 template <int EB>
 __global__ void __launch_bounds__(FS_THREADS, 1)
 cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   cg::grid_group grid = cg::this_grid();
+  dstamp(p.upd, 0);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned view of the dynamic smem that stays in the shared
+  // address space (integer pointer round-trips would turn every later smem
+  // access into a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t STAGE_BYTES = TC_BM * 128 + (uint32_t)p.BN * 128 * (p.split ? 2 : 1);
   uint8_t* ring = smem;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + p.stages * STAGE_BYTES);
@@ -239,12 +254,17 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   stamp(p.upd, 4);
+  dstamp(p.upd, 1);
   RingState rs;
 
   // ---- phase F: forward split-K partials ----
-  gemm_phase<EB, false>(maps, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
+  if (!(p.dbg_mode & 8))
+    gemm_phase<EB, false>(maps, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
+  __syncthreads();
+  dstamp(p.upd, 2);
   grid.sync();
   stamp(p.upd, 5);
+  dstamp(p.upd, 3);
 
   // ---- phase S: sum partials, route halves, cast to bf16 ----
   {
@@ -252,6 +272,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     const int64_t plane = (int64_t)p.k * p.hpad;
     const int h = p.h;
     const bool vec = ((h & 3) == 0) && ((p.ldz & 3) == 0) && ((p.hpad & 3) == 0);
+    if (!(p.dbg_mode & 16)) {
     const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
     if (vec) {
@@ -299,26 +320,53 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
         }
       }
     }
+    }
     // generic-proxy writes consumed by the async proxy (TMA) after the barrier
     asm volatile("fence.proxy.async.global;" ::: "memory");
   }
+  __syncthreads();
+  dstamp(p.upd, 4);
   grid.sync();
   stamp(p.upd, 6);
+  dstamp(p.upd, 5);
 
   // ---- phase B: backward products into AV, BV ----
   if (threadIdx.x == 0)
     for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&maps.aB[v]); tma_prefetch_desc(&maps.bB[v]); }
-  gemm_phase<EB, true>(maps, p, p.mtB[0] + p.mtB[1], ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
+  if (!(p.dbg_mode & 32))
+    gemm_phase<EB, true>(maps, p, p.mtB[0] + p.mtB[1], ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
   tc_fence_before();
+  if (p.upd.dbg && threadIdx.x >= 128) {
+    if (threadIdx.x == 128) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) :: "memory");
+      p.upd.dbg[(size_t)blockIdx.x * 64 + 17] = t;
+      p.upd.dbg[(size_t)blockIdx.x * 64 + 49] = clock64();
+    }
+    __threadfence();
+    if (threadIdx.x == 128) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) :: "memory");
+      p.upd.dbg[(size_t)blockIdx.x * 64 + 16] = t;
+      p.upd.dbg[(size_t)blockIdx.x * 64 + 48] = clock64();
+    }
+  }
+  __syncthreads();
+  dstamp(p.upd, 6);
+  if (p.upd.dbg && threadIdx.x == 0) {
+    p.upd.dbg[(size_t)blockIdx.x * 64 + 18] = *(volatile unsigned long long*)&p.upd.dbg[(size_t)blockIdx.x * 64 + 17];
+    __threadfence(); dstamp(p.upd, 15);
+  }
   grid.sync();
   stamp(p.upd, 7);
+  dstamp(p.upd, 7);
 
   // ---- release TMEM, then phase U: Gram tables + fused update ----
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NCOLS));
   }
-  update_res_phases<true>(p.upd, reinterpret_cast<float*>(smem), grid);
+  if (!(p.dbg_mode & 64)) update_res_phases<true>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um);
 }
 
 
@@ -360,6 +408,12 @@ inline geig_status fused_cca_step(TcPlan& t, const void* X, const void* Y, int64
     p.kbF[v] = (int)((dv[v] + ATOM - 1) / ATOM);
     p.mtB[v] = (int)((dv[v] + TC_BM - 1) / TC_BM);
   }
+  {
+    const float* src[4] = {upd.V, AV, upd.AUX, BV};
+    for (int a = 0; a < 4; ++a)
+      if (!make_map(&maps.um.t[a], src[a], 4, t.d, k, t.d, (int)upd.segw + 4, 64, false))
+        return tc_fail(GEIG_ERR_CUDA, "tensor map encode (update tiles) failed");
+  }
   p.rows = rows; p.h = h; p.k = k; p.BN = t.BN; p.d = t.d; p.ldz = t.ldz; p.hpad = t.hpad;
   p.scale = scale;
   p.mtF = (rows + TC_BM - 1) / TC_BM;
@@ -372,7 +426,11 @@ inline geig_status fused_cca_step(TcPlan& t, const void* X, const void* Y, int64
   p.AV = AV;
   p.BV = BV;
   p.upd = upd;
+  p.upd.dbg = dbg_ptr();
   p.split = t.splitb;
+  p.bwd_y_first = getenv("GEIG_BWD_X_FIRST") ? 0 : 1;
+  p.dbg_nostore = getenv("GEIG_DBG_NOSTORE") ? 1 : 0;   // developer: drop GEMM epilogue stores (timing only)
+  p.dbg_mode = getenv("GEIG_DBG_MODE") ? atoi(getenv("GEIG_DBG_MODE")) : 0;   // developer timing knobs (wrong results)
   const size_t stage_bytes = TC_BM * 128 + (size_t)t.BN * 128 * (t.splitb ? 2 : 1);
   p.stages = (int)std::min<size_t>(TC_MAX_STAGES, (200 * 1024) / stage_bytes);
   const size_t smem = 1024 + std::max((size_t)p.stages * stage_bytes + (2 * TC_MAX_STAGES + 4) * 8, upd_bytes);

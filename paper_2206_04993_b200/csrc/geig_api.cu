@@ -372,7 +372,7 @@ extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float*
                                    double gamma) {
   if (!s || !AV || !BV) return fail(GEIG_ERR_ARG, "NULL argument");
   CU(cudaSetDevice(s->device));
-  UpdateArgs a;
+  UpdateArgs a{};
   a.V = s->V; a.AUX = s->AUX; a.AV = AV; a.BV = BV;
   a.Vbf = s->Vbf; a.partial = s->partial; a.raw = s->raw; a.gram = s->gram;
   a.k = s->k; a.d = s->d; a.segw = s->upd_segw;
@@ -400,7 +400,7 @@ extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* 
   if (s->problem == GEIG_CCA && b >= 2 && b <= s->max_rows && X && Y && fused_ok(s, X, Y)) {
     // whole step in one persistent cooperative launch (fused_step.cuh)
     CU(cudaSetDevice(s->device));
-    UpdateArgs a;
+    UpdateArgs a{};
     a.V = s->V; a.AUX = s->AUX; a.AV = s->AV; a.BV = s->BV;
     a.Vbf = s->Vbf; a.partial = s->partial; a.raw = s->raw; a.gram = s->gram;
     a.k = s->k; a.d = s->d; a.segw = s->upd_segw;

@@ -162,7 +162,10 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   const uint32_t STAGE_BYTES = A_BYTES + B_BYTES * (SPLIT ? 2 : 1);
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned view of the dynamic smem that stays in the shared
+  // address space (integer pointer round-trips would turn every later smem
+  // access into a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES);
   uint64_t* empty_bar = full_bar + TC_STAGES;
   uint64_t* accum_bar = empty_bar + TC_STAGES;
@@ -449,7 +452,7 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D row-major tensor [outer][inner] with row stride `stride_el` elements.
 inline bool make_map(CUtensorMap* m, const void* base, int eb, int64_t inner, int64_t outer, int64_t stride_el,
-                     int box_inner, int box_outer) {
+                     int box_inner, int box_outer, bool swizzle = true) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
@@ -458,7 +461,7 @@ inline bool make_map(CUtensorMap* m, const void* base, int eb, int64_t inner, in
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(m, eb == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                   const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

@@ -33,6 +33,7 @@
 #pragma once
 #include <cooperative_groups.h>
 #include "common.cuh"
+#include "tc_gemm.cuh"
 
 namespace geig {
 
@@ -56,7 +57,18 @@ struct UpdateArgs {
   int64_t segw;          // columns per CTA (multiple of 4)
   float eta, gamma, rho;
   unsigned long long* ts;  // 6 %globaltimer stamps of CTA 0 (phase boundaries), nullable
+  unsigned long long* dbg; // developer: 64 stamps per CTA (%globaltimer, then clock64) (fused step), nullable
 };
+
+// developer timeline stamp: slot `slot` of this CTA (thread 0 only)
+__device__ __forceinline__ void dstamp(const UpdateArgs& p, int slot) {
+  if (p.dbg && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) :: "memory");
+    p.dbg[(size_t)blockIdx.x * 64 + slot] = t;
+    p.dbg[(size_t)blockIdx.x * 64 + 32 + slot] = clock64();
+  }
+}
 
 // bf16 "x2" shadow of v: hi = bf16(v), lo = bf16(v - hi); the products may
 // use hi alone (bf16) or hi + lo (bf16x2, ~fp32-accurate operand).
@@ -79,7 +91,7 @@ __device__ __forceinline__ void store_vbf1(__nv_bfloat16* hi, int64_t lo_off, si
 __device__ __forceinline__ void stamp(const UpdateArgs& p, int slot) {
   if (p.ts && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) :: "memory");
     p.ts[slot] = t;
   }
 }
@@ -280,8 +292,10 @@ update_kernel(UpdateArgs p) {
       __syncthreads();
     }
   }
+  dstamp(p, 11);
   grid.sync();
   stamp(p, 2);
+  dstamp(p, 12);
 
   // ---------------- phase 3a: coefficients (every CTA, from the raw tables) ----------------
   // Normalisation folded in (retraction of the previous step, Alg. 2 line 17):
@@ -422,20 +436,33 @@ update_kernel(UpdateArgs p) {
 // [tri(A) | tri(C) | diag B | diag V'V'] with tri(i,j) = i(i+1)/2 + j.
 // ============================================================================
 constexpr int UPD_RES_WMAX = 168;   // max columns per CTA (smem: 4 x 64 x 172 x 4 B + tables)
+constexpr int UPD_GT = 72;          // 8x4 lower-triangle Gram tiles of a 64 x 64 table
+constexpr int UPD_GS = 3;           // column slices of the Gram phase (UPD_GT * UPD_GS <= UPD_THREADS)
+constexpr int UPD_AUXF = 64 * 64 + 4 * 64 + 8 * 32 + 64 * 65 + 128;   // Lt | N, 1/s^2, D1, D2 | red | raw
+constexpr int UPD_GREDF = (UPD_GS - 1) * UPD_GT * 64;                // Gram slice partials (aliases the above)
 
 __host__ __device__ constexpr size_t upd_res_smem_floats(int W) {
-  // 4 tiles + Lt + n, s^2, D1, D2 + red + staged raw tables (64*65 + 128)
-  return (size_t)4 * 64 * (W + 4) + 64 * 64 + 4 * 64 + 8 * 32 + 64 * 65 + 128;
+  // 4 tiles + max(tables, Gram slice buffer) + TMA mbarrier (16 B)
+  return (size_t)4 * 64 * (W + 4) + (UPD_AUXF > UPD_GREDF ? UPD_AUXF : UPD_GREDF) + 4;
 }
 __host__ __device__ constexpr int upd_raw_floats_res(int k) { return k * (k + 1) + 2 * k; }
 
 __device__ __forceinline__ int tri_index(int i, int j) { return i * (i + 1) / 2 + j; }
 
+// fp32 k x d state arrays as TMA tensors (box = one CTA's W+4 columns x 64
+// rows, no swizzle; rows >= k and columns >= d are zero-filled by the TMA
+// unit).  Order: V'', AV, [Bv], BV — the smem tile order.
+struct UpdMaps {
+  CUtensorMap t[4];
+};
+
 // The resident update as a device function over an explicit shared-memory
 // arena, so the fused step kernel (fused_step.cuh) can run it after its GEMM
-// phases inside the same cooperative launch.
+// phases inside the same cooperative launch.  `um` (param-space tensor maps)
+// selects TMA staging of the tiles; nullptr stages them with cp.async.
 template <bool VEC>
-__device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* smem, cg::grid_group& grid) {
+__device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* smem, cg::grid_group& grid,
+                                                  const UpdMaps* um = nullptr) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int k = p.k;
@@ -450,88 +477,156 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   float* Bt = Ct + 64 * S;
   float* Lt = Bt + 64 * S;                       // [64][64] Lt[j][i]
   float* Ns = Lt + 64 * 64;
-  float* S2 = Ns + 64;
-  float* D1s = S2 + 64;
+  float* IS2 = Ns + 64;                          // 1 / s_j^2
+  float* D1s = IS2 + 64;
   float* D2s = D1s + 64;
   float* red = D2s + 64;                         // [8][32]
+  float* rs = red + 8 * 32;                      // staged raw tables
+  float* gred = Lt;                              // phase 1 only: Gram slice partials
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(Lt + (UPD_AUXF > UPD_GREDF ? UPD_AUXF : UPD_GREDF));
   const int ntri = k * (k + 1) / 2;
   const int ntot = 2 * ntri + 2 * k;             // partial / raw length
   stamp(p, 0);
 
   // ---------------- stage the four tiles once ----------------
-  {
-    const float* src[4] = {p.V, p.AV, p.AUX, p.BV};
-    float* dst[4] = {Vt, At, Ct, Bt};
-    if (VEC) {
-      const int Q = W / 4;
-      for (int e = tid; e < 4 * 64 * Q; e += UPD_THREADS) {
-        const int a = e / (64 * Q), rem = e % (64 * Q), r = rem / Q, q = rem % Q;
-        const int64_t gx = c0 + 4 * q;
-        const bool ok = r < k && gx < c1;
-        cp_async16(dst[a] + r * S + 4 * q, ok ? src[a] + (int64_t)r * d + gx : src[a], ok ? 16 : 0);
-      }
-    } else {
-      for (int e = tid; e < 4 * 64 * W; e += UPD_THREADS) {
-        const int a = e / (64 * W), rem = e % (64 * W), r = rem / W, x = rem % W;
-        const int64_t gx = c0 + x;
-        const bool ok = r < k && gx < c1;
-        cp_async4(dst[a] + r * S + x, ok ? src[a] + (int64_t)r * d + gx : src[a], ok ? 4 : 0);
-      }
+  if (um) {
+    if (tid == 0) {
+      tc::mbar_init(tbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      // smem last written through the async proxy (GEMM ring) or generic
+      // stores of a previous use: order them before the TMA writes below
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc::mbar_expect_tx(tbar, (uint32_t)(4 * 64 * S * 4));
+      float* dst[4] = {Vt, At, Ct, Bt};
+#pragma unroll
+      for (int a = 0; a < 4; ++a) tc::tma_load_2d(dst[a], &um->t[a], tbar, (int)c0, 0);
     }
+    __syncthreads();
+    tc::mbar_wait(tbar, 0);
+  } else {
+    auto stage = [&](float* dst, const float* src) {
+      if (VEC) {
+        const int Q = W / 4;
+        for (int e = tid; e < 64 * Q; e += UPD_THREADS) {
+          const int r = e / Q, q = e - r * Q;
+          const int64_t gx = c0 + 4 * q;
+          const bool ok = r < k && gx < c1;
+          cp_async16(dst + r * S + 4 * q, ok ? src + (int64_t)r * d + gx : src, ok ? 16 : 0);
+        }
+      } else {
+        for (int e = tid; e < 64 * W; e += UPD_THREADS) {
+          const int r = e / W, x = e - r * W;
+          const int64_t gx = c0 + x;
+          const bool ok = r < k && gx < c1;
+          cp_async4(dst + r * S + x, ok ? src + (int64_t)r * d + gx : src, ok ? 4 : 0);
+        }
+      }
+    };
+    stage(Vt, p.V);
+    stage(At, p.AV);
+    stage(Ct, p.AUX);
+    stage(Bt, p.BV);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
   }
+  dstamp(p, 8);
 
   // ---------------- phase 1: Gram partials ----------------
+  // G^A_ij = <v''_i, AV''_j>, G^C_ij = <v''_i, [Bv]_j> for j <= i only:
+  // 72 register tiles of 8 rows (i) x 4 rows (j) cover the lower triangle of
+  // the 64 x 64 tables; threads 0..215 = 72 tiles x 3 column slices, slices
+  // 1-2 hand their sums to slice 0 through smem.  Threads 216..255 compute
+  // the diagonals <v''_i, BV''_i> and ||v''_i||^2 meanwhile.
   {
-    const int ti = tid & 15, tj = tid >> 4;
-    float accA[4][4], accC[4][4];
+    float* out = p.partial + (size_t)blockIdx.x * ntot;
+    const bool gt = tid < UPD_GT * UPD_GS;       // warp 6 straddles the two roles: no barrier inside them
+    const int sl = gt ? tid / UPD_GT : 0, t = gt ? tid - sl * UPD_GT : 0;
+    int I = 0;
+    while ((I + 1) * (I + 2) <= t) ++I;            // t = I(I+1) + J, J < 2I+2
+    const int J = t - I * (I + 1);
+    float accA[8][4], accC[8][4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 8; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) accA[a][b] = accC[a][b] = 0.f;
-    for (int xq = 0; xq < W / 4; ++xq) {
-      float4 va[4];
+    if (gt) {
+      const int nq = W / 4;
+      const int q0 = sl * nq / UPD_GS, q1 = (sl + 1) * nq / UPD_GS;
+      const float* vb = Vt + (8 * I) * S;
+      const float* ab = At + (4 * J) * S;
+      const float* cb = Ct + (4 * J) * S;
+      for (int q = q0; q < q1; ++q) {
+        float4 pa[4], pc[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) va[a] = *reinterpret_cast<const float4*>(Vt + (ti + 16 * a) * S + 4 * xq);
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int j = tj + 16 * b;
-        const float4 pa = *reinterpret_cast<const float4*>(At + j * S + 4 * xq);
-        const float4 pc = *reinterpret_cast<const float4*>(Ct + j * S + 4 * xq);
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          accA[a][b] = fmaf(va[a].x, pa.x, fmaf(va[a].y, pa.y, fmaf(va[a].z, pa.z, fmaf(va[a].w, pa.w, accA[a][b]))));
-          accC[a][b] = fmaf(va[a].x, pc.x, fmaf(va[a].y, pc.y, fmaf(va[a].z, pc.z, fmaf(va[a].w, pc.w, accC[a][b]))));
+        for (int b = 0; b < 4; ++b) {
+          pa[b] = *reinterpret_cast<const float4*>(ab + b * S + 4 * q);
+          pc[b] = *reinterpret_cast<const float4*>(cb + b * S + 4 * q);
         }
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          const float4 v = *reinterpret_cast<const float4*>(vb + a * S + 4 * q);
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            accA[a][b] = fmaf(v.x, pa[b].x, accA[a][b]);
+            accA[a][b] = fmaf(v.y, pa[b].y, accA[a][b]);
+            accA[a][b] = fmaf(v.z, pa[b].z, accA[a][b]);
+            accA[a][b] = fmaf(v.w, pa[b].w, accA[a][b]);
+            accC[a][b] = fmaf(v.x, pc[b].x, accC[a][b]);
+            accC[a][b] = fmaf(v.y, pc[b].y, accC[a][b]);
+            accC[a][b] = fmaf(v.z, pc[b].z, accC[a][b]);
+            accC[a][b] = fmaf(v.w, pc[b].w, accC[a][b]);
+          }
+        }
+      }
+      if (sl > 0) {
+        float* g = gred + (size_t)(sl - 1) * UPD_GT * 64 + t;
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            g[(a * 4 + b) * UPD_GT] = accA[a][b];
+            g[(32 + a * 4 + b) * UPD_GT] = accC[a][b];
+          }
+      }
+    } else {
+      // diagonals: rows i = tid - 216, tid - 216 + 40
+      for (int i = tid - UPD_GT * UPD_GS; i < k; i += UPD_THREADS - UPD_GT * UPD_GS) {
+        float gb = 0.f, nn = 0.f;
+        for (int q = 0; q < W / 4; ++q) {
+          const float4 v = *reinterpret_cast<const float4*>(Vt + i * S + 4 * q);
+          const float4 bb = *reinterpret_cast<const float4*>(Bt + i * S + 4 * q);
+          gb = fmaf(v.x, bb.x, fmaf(v.y, bb.y, fmaf(v.z, bb.z, fmaf(v.w, bb.w, gb))));
+          nn = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, nn))));
+        }
+        out[2 * ntri + i] = gb;
+        out[2 * ntri + k + i] = nn;
       }
     }
-    float* out = p.partial + (size_t)blockIdx.x * ntot;
+    __syncthreads();
+    if (gt && sl == 0) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 8; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int i = ti + 16 * a, j = tj + 16 * b;
-        if (i < k && j <= i) {
-          out[tri_index(i, j)] = accA[a][b];
-          out[ntri + tri_index(i, j)] = accC[a][b];
+        for (int b = 0; b < 4; ++b) {
+          float sa = accA[a][b], sc = accC[a][b];
+#pragma unroll
+          for (int s2 = 0; s2 < UPD_GS - 1; ++s2) {
+            sa += gred[(size_t)s2 * UPD_GT * 64 + (a * 4 + b) * UPD_GT + t];
+            sc += gred[(size_t)s2 * UPD_GT * 64 + (32 + a * 4 + b) * UPD_GT + t];
+          }
+          const int i = 8 * I + a, j = 4 * J + b;
+          if (i < k && j <= i) {
+            out[tri_index(i, j)] = sa;
+            out[ntri + tri_index(i, j)] = sc;
+          }
         }
-      }
-    for (int i = warp; i < k; i += UPD_THREADS / 32) {
-      float gb = 0.f, nn = 0.f;
-      for (int x = lane; x < W; x += 32) {
-        const float v = Vt[i * S + x];
-        gb = fmaf(v, Bt[i * S + x], gb);
-        nn = fmaf(v, v, nn);
-      }
-      gb = warp_sum(gb);
-      nn = warp_sum(nn);
-      if (lane == 0) { out[2 * ntri + i] = gb; out[2 * ntri + k + i] = nn; }
     }
   }
+  dstamp(p, 9);
   grid.sync();
   stamp(p, 1);
+  dstamp(p, 10);
 
   // ---------------- phase 2: reduce partials (compact entries) ----------------
   // a CTA owns a contiguous entry range; lanes over entries, warps over the
@@ -563,58 +658,76 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
       __syncthreads();
     }
   }
+  dstamp(p, 11);
   grid.sync();
   stamp(p, 2);
+  dstamp(p, 12);
 
   // ---------------- phase 3a: coefficients ----------------
-  // the reduced raw tables are first staged into shared memory by all threads
-  // (independent loads), then the coefficients are formed from smem.
+  // the reduced raw tables are staged into shared memory with one burst of
+  // independent 16-byte async copies, then the coefficients are formed from smem.
   {
-    float* rs = red + 8 * 32;                    // [ntot] staged raw tables (<= 64*65 + 128 floats)
-    for (int e = tid; e < ntot; e += UPD_THREADS) rs[e] = p.raw[e];
+    for (int e = 4 * tid; e < ntot; e += 4 * UPD_THREADS) {
+      const int nb = min(4, ntot - e) * 4;
+      cp_async16(rs + e, p.raw + e, nb);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
+    dstamp(p, 19);
     const float* rA = rs;
     const float* rC = rs + ntri;
     const float* rB = rs + 2 * ntri;
     const float* rN = rB + k;
-    for (int i = tid; i < 64; i += UPD_THREADS) {
-      float n = 0.f, s2 = 1.f, gb = 0.f;
+    if (tid < 64) {
+      const int i = tid;
+      float n = 0.f, is2 = 0.f, gb = 0.f;
       if (i < k) {
         n = rsqrtf(rN[i]);
         gb = n * n * rB[i];
-        s2 = fmaxf(n * rC[tri_index(i, i)], p.rho);
+        is2 = 1.f / fmaxf(n * rC[tri_index(i, i)], p.rho);
       }
-      Ns[i] = n; S2[i] = s2; D1s[i] = gb;
+      Ns[i] = n; IS2[i] = is2; D1s[i] = gb;
     }
     __syncthreads();
-    for (int i = warp; i < 64; i += UPD_THREADS / 32) {
-      const float ni = Ns[i];
-      float c = 0.f;
-      for (int j = lane; j < 64; j += 32) {
-        float l = 0.f;
-        if (i < k && j < i) {
-          const float ga = ni * Ns[j] * rA[tri_index(i, j)];
-          const float gc = ni * rC[tri_index(i, j)];
-          l = D1s[i] * ga / S2[j];
-          c = fmaf(ga, gc / S2[j], c);
-        }
-        Lt[j * 64 + i] = l;
-      }
-      c = warp_sum(c);
-      if (lane == 0) D2s[i] = i < k ? ni * ni * rA[tri_index(i, i)] - c : 0.f;
+    dstamp(p, 20);
+    // L_ij = G^B_ii G^A_ij / s_j^2 (j < i), transposed: Lt[j][i]; lanes over i
+    for (int e = tid; e < 64 * 64; e += UPD_THREADS) {
+      const int j = e >> 6, i = e & 63;
+      float l = 0.f;
+      if (i < k && j < i) l = D1s[i] * (Ns[i] * Ns[j] * rA[tri_index(i, j)]) * IS2[j];
+      Lt[e] = l;
     }
-    if (blockIdx.x == 0) {
-      for (int e = tid; e < k * k; e += UPD_THREADS) {
-        const int i = e / k, j = e % k;
+    // c_i = sum_{j<i} G^A_ij G^C_ij / s_j^2 (4 threads per i), D2_i = G^A_ii - c_i
+    {
+      const int i = tid >> 2, q = tid & 3;
+      float c = 0.f;
+      if (i < k) {
+        const float ni = Ns[i];
+        for (int j = q; j < i; j += 4)
+          c = fmaf(ni * Ns[j] * rA[tri_index(i, j)], ni * rC[tri_index(i, j)] * IS2[j], c);
+      }
+      c += __shfl_xor_sync(0xffffffffu, c, 1);
+      c += __shfl_xor_sync(0xffffffffu, c, 2);
+      if (q == 0) D2s[i] = i < k ? Ns[i] * Ns[i] * rA[tri_index(i, i)] - c : 0.f;
+    }
+    // the step's normalised tables (geig_get_gram), written by all CTAs in slices
+    {
+      const int G = gridDim.x, kk = k * k;
+      const int per = (kk + G - 1) / G;
+      const int e1 = min(kk, (int)(blockIdx.x + 1) * per);
+      for (int e = blockIdx.x * per + tid; e < e1; e += UPD_THREADS) {
+        const int i = e / k, j = e - (e / k) * k;
         const bool low = j <= i;
-        const float ni = rsqrtf(rN[i]);
-        p.gram[e] = low ? ni * rsqrtf(rN[j]) * rA[tri_index(i, low ? j : 0)] : 0.f;
-        p.gram[(size_t)k * k + e] = (i == j) ? rB[i] / rN[i] : 0.f;
-        p.gram[2 * (size_t)k * k + e] = low ? ni * rC[tri_index(i, low ? j : 0)] : 0.f;
+        const int tij = tri_index(i, low ? j : 0);
+        p.gram[e] = low ? Ns[i] * Ns[j] * rA[tij] : 0.f;
+        p.gram[(size_t)kk + e] = (i == j) ? D1s[i] : 0.f;
+        p.gram[2 * (size_t)kk + e] = low ? Ns[i] * rC[tij] : 0.f;
       }
     }
     __syncthreads();
   }
+  dstamp(p, 13);
 
   // ---------------- phase 3b: grad, v'' and [Bv]' from the resident tiles ----------------
   {
@@ -677,6 +790,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
     }
   }
   stamp(p, 3);
+  dstamp(p, 14);
 }
 
 template <bool VEC>

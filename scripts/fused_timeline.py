@@ -1,0 +1,41 @@
+"""Per-CTA timeline of the fused CCA step kernel (developer tool): per CTA,
+%globaltimer (cross-CTA) and clock64 (intra-CTA intervals) stamps written
+through geig_debug_set_tc_stamps (64 slots per CTA)."""
+import ctypes, os, sys, statistics
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2206_04993_b200 import build
+build.build()
+from paper_2206_04993_b200 import geig
+from synth import CONFIGS, cca_views, gaussian_init
+cfg = CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 3]
+math = sys.argv[2] if len(sys.argv) > 2 else "bf16x2"
+MHZ = float(os.environ.get("SM_MHZ", "1965"))
+dev = "cuda:0"
+b = cfg.batch
+X, Y = cca_views(cfg, 2 * b, seed=5, device=dev, dtype=torch.bfloat16)
+s = geig.Solver(geig.GEIG_CCA, cfg.dx, cfg.dy, cfg.k, math=math, data_dtype=geig.GEIG_DATA_BF16, rho=cfg.rho, max_rows=b)
+s.init_state(torch.tensor(gaussian_init(cfg.k, cfg.d, 0), dtype=torch.float32, device=dev))
+lib = geig._lib
+lib.geig_debug_set_tc_stamps.argtypes = [ctypes.c_void_p]
+names = {0: "launch", 1: "setup", 2: "F done", 3: "F sync", 4: "S done", 5: "S sync", 6: "B done", 7: "B sync",
+         8: "U staged", 9: "U gram", 10: "U sync1", 11: "U reduce", 12: "U sync2", 13: "U coef", 14: "U update",
+         15: "B fence0", 16: "B epi fence", 17: "B epi end", 19: "coef raw", 20: "coef N", 21: "coef L"}
+for it in range(50):
+    geig.geig_step_cca(s.h, X[:b], Y[:b], b, cfg.eta, cfg.gamma)
+torch.cuda.synchronize()
+buf = torch.zeros(64 * 1024, dtype=torch.int64, device=dev)
+buf.zero_()
+lib.geig_debug_set_tc_stamps(ctypes.c_void_p(buf.data_ptr()))
+geig.geig_step_cca(s.h, X[b:], Y[b:], b, cfg.eta, cfg.gamma)
+lib.geig_debug_set_tc_stamps(None)
+geig.geig_step_cca(s.h, X[:b], Y[:b], b, cfg.eta, cfg.gamma)
+torch.cuda.synchronize()
+t = buf.view(-1, 64).cpu()
+t = t[t[:, 0] > 0]
+t0 = t[:, 0].min().item()
+print(f"{t.shape[0]} CTAs; globaltimer us from first CTA start (min / median / max) | clock64 us since slot 0 (median)")
+for j, nm in names.items():
+    col = ((t[:, j] - t0).double() / 1e3).tolist()
+    ck = ((t[:, 32 + j] - t[:, 32]).double() / MHZ).tolist() if j != 15 else [0]
+    print(f"  {j:2d} {nm:12s} {min(col):7.2f} {statistics.median(col):7.2f} {max(col):7.2f} | {statistics.median(ck):7.2f}")

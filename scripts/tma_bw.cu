@@ -58,7 +58,8 @@ void run(const void* X, int R, int C, unsigned long long* sink) {
   CUtensorMap map, mapb;
   if (!make_map(&map, X, 2, C, R, C, 64, BH)) { printf("map failed\n"); return; }
   if (!make_map(&mapb, X, 2, C, 64, C, 64, BROWS ? BROWS : 64)) { printf("map failed\n"); return; }
-  const size_t sm = 1024 + (size_t)S * (128 * BH * NB + 128 * BROWS * NB) + 256;
+  size_t sm = 1024 + (size_t)S * (128 * BH * NB + 128 * BROWS * NB) + 256;
+  if (getenv("ONE_CTA_PER_SM")) sm = 200 * 1024;
   cudaFuncSetAttribute(stream_kernel<BH, NB, S, ORDER, SPLIT, BROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int grid = (ORDER == 0 ? R / BH : C / (64 * NB)) * SPLIT;
   cudaEvent_t e0, e1;
@@ -72,24 +73,33 @@ void run(const void* X, int R, int C, unsigned long long* sink) {
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   const double bytes = (double)R * C * 2;
-  printf("B %3d order %d split %d box 64x%-3d x%d stages %d grid %4d smem %6zu : %7.1f GB/s (%.1f us)\n", ORDER, SPLIT, BH, NB, S, grid, sm,
-         bytes / (ms / reps * 1e-3) / 1e9, ms / reps * 1e3);
+  printf("order %d split %d box 64x%-3d x%d stages %2d grid %4d smem %6zu : %7.1f GB/s (%.1f us)\n", ORDER, SPLIT, BH, NB, S,
+         grid, sm, bytes / (ms / reps * 1e-3) / 1e9, ms / reps * 1e3);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) printf("err %s\n", cudaGetErrorString(e));
 }
 
 int main() {
-  const int R = 8192, C = 8192;   // 128 MiB bf16, > L2
+  const int R = 8192, C = 8192;   // 128 MiB bf16 (X and Y of config 3 stacked), > L2
   void* X;
   cudaMalloc(&X, (size_t)R * C * 2);
   cudaMemset(X, 1, (size_t)R * C * 2);
   unsigned long long* sink;
   cudaMalloc(&sink, 8);
-  run<128, 1, 4, 0, 4>(X, R, C, sink);
-  run<128, 1, 4, 0, 4, 64>(X, R, C, sink);
-  run<128, 1, 6, 0, 4, 64>(X, R, C, sink);
-  run<128, 2, 4, 0, 4, 64>(X, R, C, sink);
-  run<256, 1, 4, 0, 4, 64>(X, R, C, sink);
-  run<128, 1, 4, 0, 4, 128>(X, R, C, sink);
+  // forward-phase pattern: 64 row strips x split 2 = 128 CTAs
+  run<128, 1, 6, 0, 2>(X, R, C, sink);
+  run<128, 1, 12, 0, 2>(X, R, C, sink);
+  run<128, 2, 6, 0, 2>(X, R, C, sink);
+  run<128, 4, 3, 0, 2>(X, R, C, sink);
+  run<128, 2, 3, 0, 2>(X, R, C, sink);
+  // 256 CTAs (2 waves / 2 per SM if smem allows)
+  run<128, 1, 6, 0, 4>(X, R, C, sink);
+  run<128, 2, 6, 0, 4>(X, R, C, sink);
+  run<64, 2, 6, 0, 2>(X, R, C, sink);
+  run<64, 4, 6, 0, 2>(X, R, C, sink);
+  // backward-like: CTA walks rows of a column strip (128 strips of 64 cols)
+  run<64, 2, 6, 1, 1>(X, R, C, sink);
+  run<128, 2, 6, 1, 1>(X, R, C, sink);
+  run<64, 1, 12, 1, 1>(X, R, C, sink);
   return 0;
 }
