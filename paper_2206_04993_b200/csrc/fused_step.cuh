@@ -40,7 +40,7 @@ struct FusedMaps {
 };
 
 struct FusedParams {
-  int rows, h, k, BN, stages, splitsF, mtF, mtB[2], split, bwd_y_first, dbg_nostore, dbg_mode;
+  int rows, h, k, BN, stages, splitsF, mtF, mtB[2], split, bwd_y_first, dbg_nostore, dbg_mode, l2_keep;
   int kbF[2], kbB;                 // K blocks: forward per view, backward per half
   int64_t dv[2], d, ldz, hpad;
   float scale;
@@ -61,6 +61,7 @@ struct Item {
   float* out[2];
   int64_t ldo;
   float scale;
+  bool keep_a;        // A operand (a view of the batch) is read again in phase B: keep it in L2
 };
 
 __device__ __forceinline__ void decode_forward(const FusedMaps& M, const FusedParams& p, int idx, Item& it) {
@@ -79,6 +80,7 @@ __device__ __forceinline__ void decode_forward(const FusedMaps& M, const FusedPa
   it.ma[1] = it.ma[0];
   it.mb[1] = it.mb[0];
   it.mblo[0] = it.mblo[1] = v == 0 ? &M.bFlo[0] : &M.bFlo[1];
+  it.keep_a = p.l2_keep && v == 1;    // view Y is streamed last in F and first in B
   it.out[0] = p.Zt + ((int64_t)(2 * sp + v) * p.k) * p.ldz;
   it.out[1] = nullptr;
   it.ldo = p.ldz;
@@ -102,6 +104,7 @@ __device__ __forceinline__ void decode_backward(const FusedMaps& M, const FusedP
   it.mblo[0] = v == 0 ? &M.bBlo[0] : &M.bBlo[2];
   it.mblo[1] = v == 0 ? &M.bBlo[1] : &M.bBlo[3];
   const int64_t off = v == 0 ? 0 : p.dv[0];
+  it.keep_a = false;
   it.out[0] = p.AV + off;
   it.out[1] = p.BV + off;
   it.ldo = p.d;
@@ -130,6 +133,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
   Item it;
   if (threadIdx.x == 0) {
     // ---------------- TMA producer ----------------
+    const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
     for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
       if (A_MN) decode_backward(M, p, idx, it); else decode_forward(M, p, idx, it);
       for (int s = 0; s < it.nseg; ++s) {
@@ -141,16 +145,17 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
           const bool nob = (p.dbg_mode & 2) != 0;
           mbar_expect_tx(&full_bar[st], nob ? A_BYTES : STAGE_BYTES);
           const int k0 = (it.kb0[s] + j) * BK;
+          const uint64_t pa = it.keep_a ? pol_keep : pol_stream;
           if (A_MN) {
 #pragma unroll
             for (int q = 0; q < TC_BM / ATOM; ++q)
-              tma_load_2d(sa + q * (BK * 128), it.ma[s], &full_bar[st], it.m0 + q * ATOM, k0);
+              tma_load_2d_hint(sa + q * (BK * 128), it.ma[s], &full_bar[st], it.m0 + q * ATOM, k0, pa);
           } else {
-            tma_load_2d(sa, it.ma[s], &full_bar[st], k0, it.m0);
+            tma_load_2d_hint(sa, it.ma[s], &full_bar[st], k0, it.m0, pa);
           }
-          if (!nob) {
-            tma_load_2d(sb, it.mb[s], &full_bar[st], k0, 0);
-            if (split) tma_load_2d(sb + B_BYTES, it.mblo[s], &full_bar[st], k0, 0);
+          if (!nob) {   // V / Z tiles: small, re-read by every CTA
+            tma_load_2d_hint(sb, it.mb[s], &full_bar[st], k0, 0, pol_keep);
+            if (split) tma_load_2d_hint(sb + B_BYTES, it.mblo[s], &full_bar[st], k0, 0, pol_keep);
           }
         }
       }
@@ -161,8 +166,13 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
       if (A_MN) decode_backward(M, p, idx, it); else decode_forward(M, p, idx, it);
       if (rs.items > 0) mbar_wait(acce_bar, (rs.items - 1) & 1);   // epilogue drained the accumulator
       tc_fence_after();
+      // bf16x2: the hi and lo tiles of the B operand sit back to back in smem
+      // and form ONE N = 2 BN operand, so each K step is a single MMA whose
+      // accumulator holds A.B_hi^T in columns [0, BN) and A.B_lo^T in [BN, 2BN)
+      // (summed by the epilogue): half the MMA issues and A-operand smem reads
+      // of two N = BN MMAs.
       for (int s = 0; s < it.nseg; ++s) {
-        const uint32_t d_tmem = tmem_base + (uint32_t)(s * p.BN);
+        const uint32_t d_tmem = tmem_base + (uint32_t)(s * p.BN * (split ? 2 : 1));
         for (int j = 0; j < it.kbn[s]; ++j, ++rs.it_mma) {
           const int st = rs.it_mma % S;
           mbar_wait(&full_bar[st], (rs.it_mma / S) & 1);
@@ -175,7 +185,6 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
             const uint64_t ad = A_MN ? make_sdesc(sa + kk * UK * 128, BK * 128, 1024) : make_sdesc(sa + kk * 32, 16, 1024);
             const uint64_t bd = make_sdesc(sb + kk * 32, 16, 1024);
             umma<EB>(d_tmem, ad, bd, idesc, (j > 0 || kk > 0) ? 1u : 0u);
-            if (split) umma<EB>(d_tmem, ad, make_sdesc(sb + B_BYTES + kk * 32, 16, 1024), idesc, 1u);
           }
           umma_commit(&empty_bar[st]);
         }
@@ -192,15 +201,20 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
       tc_fence_after();
       const int m = it.m0 + ew * 32 + lane;
       const bool mok = m < it.mbound;
+      const int acols = p.BN * (p.split ? 2 : 1);
       for (int s = 0; s < it.nseg; ++s) {
         float* out = it.out[s] + m;
+        const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(s * acols);
         for (int c0 = 0; c0 < p.BN; c0 += 16) {
-          uint32_t r[16];
-          tmem_ld16(tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(s * p.BN + c0), r);
+          uint32_t r[16], rl[16];
+          tmem_ld16(tb + (uint32_t)c0, r);
+          if (p.split) tmem_ld16(tb + (uint32_t)(p.BN + c0), rl);
           if (mok && !p.dbg_nostore) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (c0 + j < p.k) out[(int64_t)(c0 + j) * it.ldo] = it.scale * __uint_as_float(r[j]);
+            for (int j = 0; j < 16; ++j) {
+              const float v = p.split ? __uint_as_float(r[j]) + __uint_as_float(rl[j]) : __uint_as_float(r[j]);
+              if (c0 + j < p.k) out[(int64_t)(c0 + j) * it.ldo] = it.scale * v;
+            }
           }
         }
       }
@@ -266,62 +280,145 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   stamp(p.upd, 5);
   dstamp(p.upd, 3);
 
-  // ---- phase S: sum partials, route halves, cast to bf16 ----
-  {
+  // ---- phase S: sum partials, route halves, cast to bf16; Gram tables G^A, G^B ----
+  // CTA c owns a contiguous range of sample rows of each half.  For every
+  // row it sums the split-K partials of z = X_v v''^T (both views, both
+  // halves), routes the halves (reading R1) and writes the bf16 (hi, lo)
+  // backward operands.  From the same fp32 z it accumulates, by linearity
+  // (reading R3), the Gram tables that the update would otherwise form from
+  // AV and BV over all d columns:
+  //   <v''_i, AV''_j> = scale (zx1_i . zy1_j + zy1_i . zx1_j)     (rows [0,h))
+  //   <v''_i, BV''_i> = scale (|zx2_i|^2 + |zy2_i|^2)             (rows [h,2h))
+  // (zx1 = X[0:h] v''_x, zy2 = Y[h:2h] v''_y, ...), i.e. k^2 h instead of
+  // k^2 d multiply-adds.  The CTA's sums go to the first half of its Gram
+  // partial row; the update phase adds G^C and ||v''||^2 and reduces.
+  if (!(p.dbg_mode & 16)) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // ring smem: async-proxy writes before
     const int64_t vstride = (int64_t)p.k * p.ldz;
     const int64_t plane = (int64_t)p.k * p.hpad;
-    const int h = p.h;
+    const int h = p.h, k = p.k;
+    const int tid = threadIdx.x;
     const bool vec = ((h & 3) == 0) && ((p.ldz & 3) == 0) && ((p.hpad & 3) == 0);
-    if (!(p.dbg_mode & 16)) {
-    const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
-    if (vec) {
-      const int hq = h / 4;
-      for (int64_t e = gtid; e < (int64_t)p.k * hq; e += gsz) {
-        const int n = (int)(e / hq), r = 4 * (int)(e % hq);
-        float4 x0 = make_float4(0.f, 0.f, 0.f, 0.f), x1 = x0, y0 = x0, y1 = x0;
+    const int U = vec ? 4 : 1;                               // rows per work unit
+    const int nu = h / U;
+    const int ua = (int)((int64_t)nu * blockIdx.x / gridDim.x), ub = (int)((int64_t)nu * (blockIdx.x + 1) / gridDim.x);
+    constexpr int ZR = 16;                                   // rows per chunk
+    float* zs = reinterpret_cast<float*>(smem);              // [4 planes: x1, x2, y1, y2][ZR][64]
+    float* Ps = zs + 4 * ZR * 64;                            // [64][65]
+    float* pst = Ps + 64 * 65;                               // [hA]
+    const int ntri = k * (k + 1) / 2;
+    const int hA = (ntri + k + 3) & ~3;
+    for (int e = tid; e < 4 * ZR * 64; e += FS_THREADS) zs[e] = 0.f;
+    const int ib = tid & 15, jb = tid >> 4;                  // P tile rows 4ib.., cols 4jb..
+    float P[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) P[a][c] = 0.f;
+    float gB = 0.f;
+    __syncthreads();
+    dstamp(p.upd, 23);
+    for (int u0 = ua; u0 < ub; u0 += ZR / U) {
+      const int nuc = min(ZR / U, ub - u0);
+      for (int e = tid; e < k * nuc; e += FS_THREADS) {
+        const int n = e / nuc, uu = e - n * nuc;
+        const int r = (u0 + uu) * U;
+        float z[4][4];                                       // [plane][row]
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int w = 0; w < 4; ++w) z[q][w] = 0.f;
         for (int sp = 0; sp < p.splitsF; ++sp) {
           const float* zx = p.Zt + (int64_t)(2 * sp) * vstride + (int64_t)n * p.ldz;
           const float* zy = zx + vstride;
-          const float4 a = *reinterpret_cast<const float4*>(zx + r), b = *reinterpret_cast<const float4*>(zx + h + r);
-          const float4 c = *reinterpret_cast<const float4*>(zy + r), dd = *reinterpret_cast<const float4*>(zy + h + r);
-          x0.x += a.x; x0.y += a.y; x0.z += a.z; x0.w += a.w;
-          x1.x += b.x; x1.y += b.y; x1.z += b.z; x1.w += b.w;
-          y0.x += c.x; y0.y += c.y; y0.z += c.z; y0.w += c.w;
-          y1.x += dd.x; y1.y += dd.y; y1.z += dd.z; y1.w += dd.w;
+          if (vec) {
+            const float4 a0 = *reinterpret_cast<const float4*>(zx + r), a1 = *reinterpret_cast<const float4*>(zx + h + r);
+            const float4 c0 = *reinterpret_cast<const float4*>(zy + r), c1 = *reinterpret_cast<const float4*>(zy + h + r);
+            z[0][0] += a0.x; z[0][1] += a0.y; z[0][2] += a0.z; z[0][3] += a0.w;
+            z[1][0] += a1.x; z[1][1] += a1.y; z[1][2] += a1.z; z[1][3] += a1.w;
+            z[2][0] += c0.x; z[2][1] += c0.y; z[2][2] += c0.z; z[2][3] += c0.w;
+            z[3][0] += c1.x; z[3][1] += c1.y; z[3][2] += c1.z; z[3][3] += c1.w;
+          } else {
+            z[0][0] += zx[r]; z[1][0] += zx[h + r]; z[2][0] += zy[r]; z[3][0] += zy[h + r];
+          }
         }
+        // Zb planes: 0 = y1 (-> AV_x), 1 = x2 (-> BV_x), 2 = x1 (-> AV_y), 3 = y2 (-> BV_y)
         const int64_t o = (int64_t)n * p.hpad + r;
-        store4<__nv_bfloat16>(p.Zb + 0 * plane + o, y0.x, y0.y, y0.z, y0.w);
-        store4<__nv_bfloat16>(p.Zb + 1 * plane + o, x1.x, x1.y, x1.z, x1.w);
-        store4<__nv_bfloat16>(p.Zb + 2 * plane + o, x0.x, x0.y, x0.z, x0.w);
-        store4<__nv_bfloat16>(p.Zb + 3 * plane + o, y1.x, y1.y, y1.z, y1.w);
-        if (p.split) {
-          store4_lo<__nv_bfloat16>(p.Zb + 4 * plane + o, y0.x, y0.y, y0.z, y0.w);
-          store4_lo<__nv_bfloat16>(p.Zb + 5 * plane + o, x1.x, x1.y, x1.z, x1.w);
-          store4_lo<__nv_bfloat16>(p.Zb + 6 * plane + o, x0.x, x0.y, x0.z, x0.w);
-          store4_lo<__nv_bfloat16>(p.Zb + 7 * plane + o, y1.x, y1.y, y1.z, y1.w);
+        if (vec) {
+          store4<__nv_bfloat16>(p.Zb + 0 * plane + o, z[2][0], z[2][1], z[2][2], z[2][3]);
+          store4<__nv_bfloat16>(p.Zb + 1 * plane + o, z[1][0], z[1][1], z[1][2], z[1][3]);
+          store4<__nv_bfloat16>(p.Zb + 2 * plane + o, z[0][0], z[0][1], z[0][2], z[0][3]);
+          store4<__nv_bfloat16>(p.Zb + 3 * plane + o, z[3][0], z[3][1], z[3][2], z[3][3]);
+          if (p.split) {
+            store4_lo<__nv_bfloat16>(p.Zb + 4 * plane + o, z[2][0], z[2][1], z[2][2], z[2][3]);
+            store4_lo<__nv_bfloat16>(p.Zb + 5 * plane + o, z[1][0], z[1][1], z[1][2], z[1][3]);
+            store4_lo<__nv_bfloat16>(p.Zb + 6 * plane + o, z[0][0], z[0][1], z[0][2], z[0][3]);
+            store4_lo<__nv_bfloat16>(p.Zb + 7 * plane + o, z[3][0], z[3][1], z[3][2], z[3][3]);
+          }
+        } else {
+          const float zv[4] = {z[2][0], z[1][0], z[0][0], z[3][0]};
+          for (int q = 0; q < 4; ++q) {
+            const __nv_bfloat16 hv = __float2bfloat16_rn(zv[q]);
+            p.Zb[q * plane + o] = hv;
+            if (p.split) p.Zb[(4 + q) * plane + o] = __float2bfloat16_rn(zv[q] - __bfloat162float(hv));
+          }
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int w = 0; w < 4; ++w)
+            if (w < U) zs[(q * ZR + uu * U + w) * 64 + n] = z[q][w];
       }
-    } else {
-      for (int64_t e = gtid; e < (int64_t)p.k * h; e += gsz) {
-        const int n = (int)(e / h), r = (int)(e % h);
-        float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
-        for (int sp = 0; sp < p.splitsF; ++sp) {
-          const float* zx = p.Zt + (int64_t)(2 * sp) * vstride + (int64_t)n * p.ldz;
-          const float* zy = zx + vstride;
-          x0 += zx[r]; x1 += zx[h + r]; y0 += zy[r]; y1 += zy[h + r];
-        }
-        const int64_t o = (int64_t)n * p.hpad + r;
-        const float zv[4] = {y0, x1, x0, y1};
-        for (int q = 0; q < 4; ++q) {
-          const __nv_bfloat16 hv = __float2bfloat16_rn(zv[q]);
-          p.Zb[q * plane + o] = hv;
-          if (p.split) p.Zb[(4 + q) * plane + o] = __float2bfloat16_rn(zv[q] - __bfloat162float(hv));
-        }
+      __syncthreads();
+      dstamp(p.upd, 24);
+      const int nr = nuc * U;
+      for (int r = 0; r < nr; ++r) {
+        const float4 xi = *reinterpret_cast<const float4*>(zs + (0 * ZR + r) * 64 + 4 * ib);
+        const float4 yi = *reinterpret_cast<const float4*>(zs + (2 * ZR + r) * 64 + 4 * ib);
+        const float4 xj = *reinterpret_cast<const float4*>(zs + (0 * ZR + r) * 64 + 4 * jb);
+        const float4 yj = *reinterpret_cast<const float4*>(zs + (2 * ZR + r) * 64 + 4 * jb);
+        const float xa[4] = {xi.x, xi.y, xi.z, xi.w}, ya[4] = {yi.x, yi.y, yi.z, yi.w};
+        const float xb[4] = {xj.x, xj.y, xj.z, xj.w}, yb[4] = {yj.x, yj.y, yj.z, yj.w};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) P[a][c] = fmaf(xa[a], yb[c], fmaf(ya[a], xb[c], P[a][c]));
       }
+      if (tid < 64)
+        for (int r = 0; r < nr; ++r) {
+          const float x2 = zs[(1 * ZR + r) * 64 + tid], y2 = zs[(3 * ZR + r) * 64 + tid];
+          gB = fmaf(x2, x2, fmaf(y2, y2, gB));
+        }
+      __syncthreads();
+      dstamp(p.upd, 25);
     }
+    // first half of this CTA's Gram partial row: [tri(G^A) | diag(G^B) | pad]
+    {
+      float* pr = pst;
+      const float sc = p.scale;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) Ps[(4 * ib + a) * 65 + 4 * jb + c] = P[a][c];
+      __syncthreads();
+      for (int e = tid; e < ntri; e += FS_THREADS) {   // e = i(i+1)/2 + j, j <= i
+        int i = (int)((sqrtf(8.f * (float)e + 1.f) - 1.f) * 0.5f);
+        if ((i + 1) * (i + 2) / 2 <= e) ++i;
+        if (i * (i + 1) / 2 > e) --i;
+        const int j = e - i * (i + 1) / 2;
+        pr[e] = sc * Ps[i * 65 + j];
+      }
+      if (tid < k) pr[ntri + tid] = sc * gB;
+      for (int e = ntri + k + tid; e < hA; e += FS_THREADS) pr[e] = 0.f;
+      __syncthreads();
+      dstamp(p.upd, 26);
+      float* out = p.upd.partial + (size_t)blockIdx.x * (2 * hA);
+      for (int e = 4 * tid; e < hA; e += 4 * FS_THREADS)
+        *reinterpret_cast<float4*>(out + e) = *reinterpret_cast<const float4*>(pr + e);
     }
-    // generic-proxy writes consumed by the async proxy (TMA) after the barrier
+    // generic smem writes before the next TMA writes into the ring; generic
+    // global writes (Zb) consumed by the async proxy (TMA) after the barrier
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("fence.proxy.async.global;" ::: "memory");
   }
   __syncthreads();
@@ -419,16 +516,19 @@ inline geig_status fused_cca_step(TcPlan& t, const void* X, const void* Y, int64
   p.mtF = (rows + TC_BM - 1) / TC_BM;
   p.splitsF = std::min(TC_MAX_SPLITS, choose_splits_deep(2 * p.mtF, std::min(p.kbF[0], p.kbF[1]), grid_ctas));
   p.kbB = (h + ATOM - 1) / ATOM;
-  p.idescF = make_idesc(eb, false, t.BN, TC_BM);
-  p.idescB = make_idesc(eb, true, t.BN, TC_BM);
+  p.idescF = make_idesc(eb, false, t.BN * (t.splitb ? 2 : 1), TC_BM);
+  p.idescB = make_idesc(eb, true, t.BN * (t.splitb ? 2 : 1), TC_BM);
   p.Zt = t.Zt;
   p.Zb = (__nv_bfloat16*)t.Zb;
   p.AV = AV;
   p.BV = BV;
   p.upd = upd;
   p.upd.dbg = dbg_ptr();
+  p.upd.dbg_mode = getenv("GEIG_DBG_MODE") ? atoi(getenv("GEIG_DBG_MODE")) : 0;
+  p.upd.ga_done = (p.upd.dbg_mode & 16) ? 0 : 1;    // phase S forms G^A, G^B from z
   p.split = t.splitb;
   p.bwd_y_first = getenv("GEIG_BWD_X_FIRST") ? 0 : 1;
+  p.l2_keep = getenv("GEIG_NO_L2_KEEP") ? 0 : 1;
   p.dbg_nostore = getenv("GEIG_DBG_NOSTORE") ? 1 : 0;   // developer: drop GEMM epilogue stores (timing only)
   p.dbg_mode = getenv("GEIG_DBG_MODE") ? atoi(getenv("GEIG_DBG_MODE")) : 0;   // developer timing knobs (wrong results)
   const size_t stage_bytes = TC_BM * 128 + (size_t)t.BN * 128 * (t.splitb ? 2 : 1);

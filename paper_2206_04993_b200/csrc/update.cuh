@@ -58,6 +58,8 @@ struct UpdateArgs {
   float eta, gamma, rho;
   unsigned long long* ts;  // 6 %globaltimer stamps of CTA 0 (phase boundaries), nullable
   unsigned long long* dbg; // developer: 64 stamps per CTA (%globaltimer, then clock64) (fused step), nullable
+  int dbg_mode;            // developer timing knobs (results wrong when set)
+  int ga_done;             // fused step: phase S wrote tri(G^A), diag(G^B) of the partial rows
 };
 
 // developer timeline stamp: slot `slot` of this CTA (thread 0 only)
@@ -445,7 +447,7 @@ __host__ __device__ constexpr size_t upd_res_smem_floats(int W) {
   // 4 tiles + max(tables, Gram slice buffer) + TMA mbarrier (16 B)
   return (size_t)4 * 64 * (W + 4) + (UPD_AUXF > UPD_GREDF ? UPD_AUXF : UPD_GREDF) + 4;
 }
-__host__ __device__ constexpr int upd_raw_floats_res(int k) { return k * (k + 1) + 2 * k; }
+__host__ __device__ constexpr int upd_raw_floats_res(int k) { return 2 * ((k * (k + 1) / 2 + k + 3) & ~3); }   // 2 padded halves
 
 __device__ __forceinline__ int tri_index(int i, int j) { return i * (i + 1) / 2 + j; }
 
@@ -485,7 +487,8 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   float* gred = Lt;                              // phase 1 only: Gram slice partials
   uint64_t* tbar = reinterpret_cast<uint64_t*>(Lt + (UPD_AUXF > UPD_GREDF ? UPD_AUXF : UPD_GREDF));
   const int ntri = k * (k + 1) / 2;
-  const int ntot = 2 * ntri + 2 * k;             // partial / raw length
+  const int hA = (ntri + k + 3) & ~3;            // half row: [tri | diag | pad]
+  const int pstride = 2 * hA;                    // per-CTA partial row (16-byte multiple)
   stamp(p, 0);
 
   // ---------------- stage the four tiles once ----------------
@@ -533,94 +536,182 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   dstamp(p, 8);
 
   // ---------------- phase 1: Gram partials ----------------
-  // G^A_ij = <v''_i, AV''_j>, G^C_ij = <v''_i, [Bv]_j> for j <= i only:
-  // 72 register tiles of 8 rows (i) x 4 rows (j) cover the lower triangle of
-  // the 64 x 64 tables; threads 0..215 = 72 tiles x 3 column slices, slices
-  // 1-2 hand their sums to slice 0 through smem.  Threads 216..255 compute
-  // the diagonals <v''_i, BV''_i> and ||v''_i||^2 meanwhile.
+  // Partial row layout (pstride = 2 hA floats):
+  //   [tri(G^A) | diag(G^B) | pad][tri(G^C) | diag ||v''||^2 | pad].
+  // With p.ga_done the fused step's phase S has already written the first
+  // half from the forward products z (reading R3); only G^C and ||v''||^2
+  // are formed here.
   {
-    float* out = p.partial + (size_t)blockIdx.x * ntot;
-    const bool gt = tid < UPD_GT * UPD_GS;       // warp 6 straddles the two roles: no barrier inside them
-    const int sl = gt ? tid / UPD_GT : 0, t = gt ? tid - sl * UPD_GT : 0;
-    int I = 0;
-    while ((I + 1) * (I + 2) <= t) ++I;            // t = I(I+1) + J, J < 2I+2
-    const int J = t - I * (I + 1);
-    float accA[8][4], accC[8][4];
+    float* out = p.partial + (size_t)blockIdx.x * pstride;
+    float* pst = gred;                              // compact partial row, written after the slice reduction
+    const int nq = W / 4;
+    if (p.ga_done) {
+      // G^C_ij = <v''_i, [Bv]_j>, j <= i: 64 tiles (I, J) = (t & 7, t >> 3)
+      // of rows i = I + 8a, j = J + 8b (a, b < 8, pairs b <= a: 36 sums),
+      // 4 column slices (sl = tid >> 6).  Quarter-warps read 8 consecutive
+      // V rows (conflict-free) and one broadcast [Bv] row.
+      const int sl = tid >> 6, t = tid & 63;
+      const int I = t & 7, J = t >> 3;
+      float acc[36];
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) accA[a][b] = accC[a][b] = 0.f;
-    if (gt) {
-      const int nq = W / 4;
-      const int q0 = sl * nq / UPD_GS, q1 = (sl + 1) * nq / UPD_GS;
-      const float* vb = Vt + (8 * I) * S;
-      const float* ab = At + (4 * J) * S;
-      const float* cb = Ct + (4 * J) * S;
+      for (int e = 0; e < 36; ++e) acc[e] = 0.f;
+      const int q0 = sl * nq / 4, q1 = (p.dbg_mode & 128) ? q0 : (sl + 1) * nq / 4;
       for (int q = q0; q < q1; ++q) {
-        float4 pa[4], pc[4];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          pa[b] = *reinterpret_cast<const float4*>(ab + b * S + 4 * q);
-          pc[b] = *reinterpret_cast<const float4*>(cb + b * S + 4 * q);
-        }
+        float4 va[8], pc[8];
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
-          const float4 v = *reinterpret_cast<const float4*>(vb + a * S + 4 * q);
+          va[a] = *reinterpret_cast<const float4*>(Vt + (I + 8 * a) * S + 4 * q);
+          pc[a] = *reinterpret_cast<const float4*>(Ct + (J + 8 * a) * S + 4 * q);
+        }
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+          for (int b = 0; b <= a; ++b) {
+            float& c = acc[a * (a + 1) / 2 + b];
+            c = fmaf(va[a].x, pc[b].x, c);
+            c = fmaf(va[a].y, pc[b].y, c);
+            c = fmaf(va[a].z, pc[b].z, c);
+            c = fmaf(va[a].w, pc[b].w, c);
+          }
+      }
+      // ||v''_i||^2: 4 threads per row
+      float nn = 0.f;
+      {
+        const int i = tid >> 2, part = tid & 3;
+        for (int q = part; q < nq; q += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(Vt + i * S + 4 * q);
+          nn = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, nn))));
+        }
+        nn += __shfl_xor_sync(0xffffffffu, nn, 1);
+        nn += __shfl_xor_sync(0xffffffffu, nn, 2);
+      }
+      if (p.dbg) { __syncthreads(); dstamp(p, 27); }
+      if (sl > 0) {
+#pragma unroll
+        for (int e = 0; e < 36; ++e) gred[(size_t)(sl - 1) * 36 * 64 + e * 64 + t] = acc[e];
+      }
+      __syncthreads();
+      if (sl == 0) {
+#pragma unroll
+        for (int e = 0; e < 36; ++e)
+#pragma unroll
+          for (int s2 = 0; s2 < 3; ++s2) acc[e] += gred[(size_t)s2 * 36 * 64 + e * 64 + t];
+      }
+      __syncthreads();
+      if (sl == 0) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+          for (int b = 0; b <= a; ++b) {
+            const int i = I + 8 * a, j = J + 8 * b;
+            if (i < k && j <= i) pst[hA + tri_index(i, j)] = acc[a * (a + 1) / 2 + b];
+          }
+      }
+      if ((tid & 3) == 0 && (tid >> 2) < k) pst[hA + ntri + (tid >> 2)] = nn;
+      for (int e = hA + ntri + k + tid; e < pstride; e += UPD_THREADS) pst[e] = 0.f;
+      __syncthreads();
+      dstamp(p, 28);
+      for (int e = hA + 4 * tid; e < pstride; e += 4 * UPD_THREADS)
+        *reinterpret_cast<float4*>(out + e) = *reinterpret_cast<const float4*>(pst + e);
+    } else {
+      // G^A and G^C together: 72 register tiles of 8 rows (i) x 4 rows (j)
+      // over the lower triangle, 3 column slices (threads 0..215); threads
+      // 216..255 form the diagonals <v''_i, BV''_i> and ||v''_i||^2.
+      const bool gt = tid < UPD_GT * UPD_GS;     // warp 6 straddles the two roles: no barrier inside them
+      const int sl = gt ? tid / UPD_GT : 0, t = gt ? tid - sl * UPD_GT : 0;
+      int I = 0;
+      while ((I + 1) * (I + 2) <= t) ++I;          // t = I(I+1) + J, J < 2I+2
+      const int J = t - I * (I + 1);
+      float accA[8][4], accC[8][4];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) accA[a][b] = accC[a][b] = 0.f;
+      if (gt) {
+        const int q0 = sl * nq / UPD_GS, q1 = (sl + 1) * nq / UPD_GS;
+        const float* vb = Vt + (8 * I) * S;
+        const float* ab = At + (4 * J) * S;
+        const float* cb = Ct + (4 * J) * S;
+        for (int q = q0; q < q1; ++q) {
+          float4 va[8], pa[4], pc[4];
+#pragma unroll
+          for (int a = 0; a < 8; ++a) va[a] = *reinterpret_cast<const float4*>(vb + a * S + 4 * q);
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
-            accA[a][b] = fmaf(v.x, pa[b].x, accA[a][b]);
-            accA[a][b] = fmaf(v.y, pa[b].y, accA[a][b]);
-            accA[a][b] = fmaf(v.z, pa[b].z, accA[a][b]);
-            accA[a][b] = fmaf(v.w, pa[b].w, accA[a][b]);
-            accC[a][b] = fmaf(v.x, pc[b].x, accC[a][b]);
-            accC[a][b] = fmaf(v.y, pc[b].y, accC[a][b]);
-            accC[a][b] = fmaf(v.z, pc[b].z, accC[a][b]);
-            accC[a][b] = fmaf(v.w, pc[b].w, accC[a][b]);
+            pa[b] = *reinterpret_cast<const float4*>(ab + b * S + 4 * q);
+            pc[b] = *reinterpret_cast<const float4*>(cb + b * S + 4 * q);
           }
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              accA[a][b] = fmaf(va[a].x, pa[b].x, fmaf(va[a].y, pa[b].y, fmaf(va[a].z, pa[b].z, fmaf(va[a].w, pa[b].w, accA[a][b]))));
+              accC[a][b] = fmaf(va[a].x, pc[b].x, fmaf(va[a].y, pc[b].y, fmaf(va[a].z, pc[b].z, fmaf(va[a].w, pc[b].w, accC[a][b]))));
+            }
+        }
+        if (sl > 0) {
+          float* g = gred + (size_t)(sl - 1) * UPD_GT * 64 + t;
+#pragma unroll
+          for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              g[(a * 4 + b) * UPD_GT] = accA[a][b];
+              g[(32 + a * 4 + b) * UPD_GT] = accC[a][b];
+            }
+        }
+      } else {
+        for (int r = 0; r < 2; ++r) {
+          const int i = tid - UPD_GT * UPD_GS + r * (UPD_THREADS - UPD_GT * UPD_GS);
+          if (i >= k) break;
+          float gb = 0.f, nn = 0.f;
+          for (int q = 0; q < nq; ++q) {
+            const float4 v = *reinterpret_cast<const float4*>(Vt + i * S + 4 * q);
+            const float4 bb = *reinterpret_cast<const float4*>(Bt + i * S + 4 * q);
+            gb = fmaf(v.x, bb.x, fmaf(v.y, bb.y, fmaf(v.z, bb.z, fmaf(v.w, bb.w, gb))));
+            nn = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, nn))));
+          }
+          accA[0][r] = gb;
+          accC[0][r] = nn;
         }
       }
-      if (sl > 0) {
-        float* g = gred + (size_t)(sl - 1) * UPD_GT * 64 + t;
+      __syncthreads();
+      if (gt && sl == 0) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int s2 = 0; s2 < UPD_GS - 1; ++s2) {
+              accA[a][b] += gred[(size_t)s2 * UPD_GT * 64 + (a * 4 + b) * UPD_GT + t];
+              accC[a][b] += gred[(size_t)s2 * UPD_GT * 64 + (32 + a * 4 + b) * UPD_GT + t];
+            }
+      }
+      __syncthreads();
+      if (gt && sl == 0) {
 #pragma unroll
         for (int a = 0; a < 8; ++a)
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
-            g[(a * 4 + b) * UPD_GT] = accA[a][b];
-            g[(32 + a * 4 + b) * UPD_GT] = accC[a][b];
+            const int i = 8 * I + a, j = 4 * J + b;
+            if (i < k && j <= i) {
+              pst[tri_index(i, j)] = accA[a][b];
+              pst[hA + tri_index(i, j)] = accC[a][b];
+            }
           }
-      }
-    } else {
-      // diagonals: rows i = tid - 216, tid - 216 + 40
-      for (int i = tid - UPD_GT * UPD_GS; i < k; i += UPD_THREADS - UPD_GT * UPD_GS) {
-        float gb = 0.f, nn = 0.f;
-        for (int q = 0; q < W / 4; ++q) {
-          const float4 v = *reinterpret_cast<const float4*>(Vt + i * S + 4 * q);
-          const float4 bb = *reinterpret_cast<const float4*>(Bt + i * S + 4 * q);
-          gb = fmaf(v.x, bb.x, fmaf(v.y, bb.y, fmaf(v.z, bb.z, fmaf(v.w, bb.w, gb))));
-          nn = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, nn))));
-        }
-        out[2 * ntri + i] = gb;
-        out[2 * ntri + k + i] = nn;
-      }
-    }
-    __syncthreads();
-    if (gt && sl == 0) {
-#pragma unroll
-      for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          float sa = accA[a][b], sc = accC[a][b];
-#pragma unroll
-          for (int s2 = 0; s2 < UPD_GS - 1; ++s2) {
-            sa += gred[(size_t)s2 * UPD_GT * 64 + (a * 4 + b) * UPD_GT + t];
-            sc += gred[(size_t)s2 * UPD_GT * 64 + (32 + a * 4 + b) * UPD_GT + t];
-          }
-          const int i = 8 * I + a, j = 4 * J + b;
-          if (i < k && j <= i) {
-            out[tri_index(i, j)] = sa;
-            out[ntri + tri_index(i, j)] = sc;
+      } else if (!gt) {
+        for (int r = 0; r < 2; ++r) {
+          const int i = tid - UPD_GT * UPD_GS + r * (UPD_THREADS - UPD_GT * UPD_GS);
+          if (i < k) {
+            pst[ntri + i] = accA[0][r];
+            pst[hA + ntri + i] = accC[0][r];
           }
         }
+      }
+      for (int e = ntri + k + tid; e < hA; e += UPD_THREADS) pst[e] = 0.f;
+      for (int e = hA + ntri + k + tid; e < pstride; e += UPD_THREADS) pst[e] = 0.f;
+      __syncthreads();
+      for (int e = 4 * tid; e < pstride; e += 4 * UPD_THREADS)
+        *reinterpret_cast<float4*>(out + e) = *reinterpret_cast<const float4*>(pst + e);
     }
   }
   dstamp(p, 9);
@@ -633,20 +724,20 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   // partial index; all loads of a thread issued before the adds.
   {
     const int G = gridDim.x;
-    const int per = (ntot + G - 1) / G;
-    const int e0 = blockIdx.x * per, e1 = min(ntot, e0 + per);
+    const int per = (pstride + G - 1) / G;
+    const int e0 = blockIdx.x * per, e1 = min(pstride, e0 + per);
     for (int eb = e0; eb < e1; eb += 32) {
       const int e = eb + lane;
       float vals[24];
 #pragma unroll
       for (int t = 0; t < 24; ++t) {
         const int b = warp + 8 * t;
-        vals[t] = (e < e1 && b < G) ? p.partial[(size_t)b * ntot + e] : 0.f;
+        vals[t] = (e < e1 && b < G) ? p.partial[(size_t)b * pstride + e] : 0.f;
       }
       float s = 0.f;
 #pragma unroll
       for (int t = 0; t < 24; ++t) s += vals[t];
-      for (int b = warp + 8 * 24; b < G; b += 8) s += (e < e1) ? p.partial[(size_t)b * ntot + e] : 0.f;
+      for (int b = warp + 8 * 24; b < G; b += 8) s += (e < e1) ? p.partial[(size_t)b * pstride + e] : 0.f;
       red[warp * 32 + lane] = s;
       __syncthreads();
       if (warp == 0 && e < e1) {
@@ -667,18 +758,15 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   // the reduced raw tables are staged into shared memory with one burst of
   // independent 16-byte async copies, then the coefficients are formed from smem.
   {
-    for (int e = 4 * tid; e < ntot; e += 4 * UPD_THREADS) {
-      const int nb = min(4, ntot - e) * 4;
-      cp_async16(rs + e, p.raw + e, nb);
-    }
+    for (int e = 4 * tid; e < pstride; e += 4 * UPD_THREADS) cp_async16(rs + e, p.raw + e, 16);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
     dstamp(p, 19);
     const float* rA = rs;
-    const float* rC = rs + ntri;
-    const float* rB = rs + 2 * ntri;
-    const float* rN = rB + k;
+    const float* rB = rs + ntri;
+    const float* rC = rs + hA;
+    const float* rN = rC + ntri;
     if (tid < 64) {
       const int i = tid;
       float n = 0.f, is2 = 0.f, gb = 0.f;
