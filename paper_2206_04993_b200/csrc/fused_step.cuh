@@ -528,7 +528,7 @@ inline geig_status fused_cca_step(TcPlan& t, const void* X, const void* Y, int64
   p.upd.ga_done = (p.upd.dbg_mode & 16) ? 0 : 1;    // phase S forms G^A, G^B from z
   p.split = t.splitb;
   p.bwd_y_first = getenv("GEIG_BWD_X_FIRST") ? 0 : 1;
-  p.l2_keep = getenv("GEIG_NO_L2_KEEP") ? 0 : 1;
+  p.l2_keep = getenv("GEIG_L2_KEEP") ? 1 : 0;   // measured: evict-last on a whole view thrashes the state arrays (slower)
   p.dbg_nostore = getenv("GEIG_DBG_NOSTORE") ? 1 : 0;   // developer: drop GEMM epilogue stores (timing only)
   p.dbg_mode = getenv("GEIG_DBG_MODE") ? atoi(getenv("GEIG_DBG_MODE")) : 0;   // developer timing knobs (wrong results)
   const size_t stage_bytes = TC_BM * 128 + (size_t)t.BN * 128 * (t.splitb ? 2 : 1);

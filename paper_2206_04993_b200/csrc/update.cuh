@@ -408,7 +408,9 @@ update_kernel(UpdateArgs p) {
           an.z = xa.z + p.gamma * (ni * bv.z - xa.z);
           an.w = xa.w + p.gamma * (ni * bv.w - xa.w);
           const size_t o = (size_t)i * d + gx;
-          if (VEC && gx + 3 < c1) {
+          if (p.dbg_mode & 1024) {
+            if (vn.x == 12345.f && an.y == 54321.f) p.V[0] = 1.f;   // keep the math alive
+          } else if (VEC && gx + 3 < c1) {
             *reinterpret_cast<float4*>(p.V + o) = vn;
             *reinterpret_cast<float4*>(p.AUX + o) = an;
             if (p.Vbf) store_vbf4(p.Vbf, (int64_t)k * d, o, vn);
@@ -556,6 +558,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
 #pragma unroll
       for (int e = 0; e < 36; ++e) acc[e] = 0.f;
       const int q0 = sl * nq / 4, q1 = (p.dbg_mode & 128) ? q0 : (sl + 1) * nq / 4;
+#pragma unroll 1
       for (int q = q0; q < q1; ++q) {
         float4 va[8], pc[8];
 #pragma unroll
@@ -818,27 +821,12 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   dstamp(p, 13);
 
   // ---------------- phase 3b: grad, v'' and [Bv]' from the resident tiles ----------------
+  // Work item = (row-group pair, column quad): the triangular penalty sum
+  // sum_{j<i} L_ij [Bv]_j costs ~i per row, so row groups g (rows 4g..4g+3)
+  // and 15-g are paired for equal cost per item; both share the [Bv]_j loads.
   {
-    const int tq = tid & 15;           // column quads tq, tq+16, ...
-    const int tr = tid >> 4;           // rows 4tr..4tr+3
-    const int i0 = 4 * tr;
     const int nq = W / 4;
-    const int jmax = min(i0 + 3, k);   // L_ij = 0 for j >= i
-    for (int q = tq; q < nq; q += 16) {
-      float acc[4][4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
-      for (int j = 0; j < jmax; ++j) {
-        const float4 l = *reinterpret_cast<const float4*>(Lt + j * 64 + i0);
-        const float4 x = *reinterpret_cast<const float4*>(Ct + j * S + 4 * q);
-        const float lv[4] = {l.x, l.y, l.z, l.w}, xv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(lv[a], xv[b], acc[a][b]);
-      }
+    auto finish = [&](int i0, const float (&acc)[4][4], int q) {
       const int64_t gx = c0 + 4 * q;
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
@@ -860,7 +848,9 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
           an.z = xa.z + p.gamma * (ni * bv.z - xa.z);
           an.w = xa.w + p.gamma * (ni * bv.w - xa.w);
           const size_t o = (size_t)i * d + gx;
-          if (VEC && gx + 3 < c1) {
+          if (p.dbg_mode & 1024) {
+            if (vn.x == 12345.f && an.y == 54321.f) p.V[0] = 1.f;   // keep the math alive
+          } else if (VEC && gx + 3 < c1) {
             *reinterpret_cast<float4*>(p.V + o) = vn;
             *reinterpret_cast<float4*>(p.AUX + o) = an;
             if (p.Vbf) store_vbf4(p.Vbf, (int64_t)k * d, o, vn);
@@ -875,6 +865,43 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
           }
         }
       }
+    };
+    for (int item = tid; item < 8 * nq; item += UPD_THREADS) {
+      const int pr = item / nq, q = item - pr * nq;
+      const int iA = 4 * pr, iB = 4 * (15 - pr);
+      const int jA = min(iA + 3, k), jB = min(iB + 3, k);   // L_ij = 0 for j >= i
+      float accA[4][4], accB[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) accA[a][b] = accB[a][b] = 0.f;
+      int j = 0;
+#pragma unroll 4
+      for (; j < jA; ++j) {
+        const float4 x = *reinterpret_cast<const float4*>(Ct + j * S + 4 * q);
+        const float4 la = *reinterpret_cast<const float4*>(Lt + j * 64 + iA);
+        const float4 lb = *reinterpret_cast<const float4*>(Lt + j * 64 + iB);
+        const float xv[4] = {x.x, x.y, x.z, x.w}, lav[4] = {la.x, la.y, la.z, la.w}, lbv[4] = {lb.x, lb.y, lb.z, lb.w};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            accA[a][b] = fmaf(lav[a], xv[b], accA[a][b]);
+            accB[a][b] = fmaf(lbv[a], xv[b], accB[a][b]);
+          }
+      }
+#pragma unroll 4
+      for (; j < jB; ++j) {
+        const float4 x = *reinterpret_cast<const float4*>(Ct + j * S + 4 * q);
+        const float4 lb = *reinterpret_cast<const float4*>(Lt + j * 64 + iB);
+        const float xv[4] = {x.x, x.y, x.z, x.w}, lbv[4] = {lb.x, lb.y, lb.z, lb.w};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) accB[a][b] = fmaf(lbv[a], xv[b], accB[a][b]);
+      }
+      finish(iA, accA, q);
+      finish(iB, accB, q);
     }
   }
   stamp(p, 3);

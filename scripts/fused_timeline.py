@@ -39,3 +39,18 @@ for j, nm in names.items():
     col = ((t[:, j] - t0).double() / 1e3).tolist()
     ck = ((t[:, 32 + j] - t[:, 32]).double() / MHZ).tolist() if j != 15 else [0]
     print(f"  {j:2d} {nm:12s} {min(col):7.2f} {statistics.median(col):7.2f} {max(col):7.2f} | {statistics.median(ck):7.2f}")
+order = [0, 1, 2, 3, 23, 24, 25, 26, 4, 5, 17, 6, 7, 8, 27, 28, 9, 10, 11, 12, 19, 20, 13, 14]
+prev = None
+out = []
+for j in order:
+    col = t[:, 32 + j]
+    if (col == 0).all():
+        continue
+    med = statistics.median(((col - t[:, 32]).double() / MHZ).tolist())
+    if prev is not None:
+        out.append(f"{names.get(j, j)}:{med - prev:.2f}")
+    prev = med
+print("phase durations (clock64 us, medians):", " ".join(out), f"| total {prev:.2f}")
+dg = (t[:, 14] - t[:, 0]).double()
+dc = (t[:, 46] - t[:, 32]).double()
+print("effective SM clock over the kernel (clock64 / globaltimer): median %.0f MHz" % statistics.median((dc / dg * 1e3).tolist()))
