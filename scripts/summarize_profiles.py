@@ -13,7 +13,8 @@ def launch_list(path):
             continue
         v = float(r[vi].replace(",", ""))
         u = r[ui]
-        v = v / 1e3 if u == "nsecond" else (v * 1e3 if u == "msecond" else v)
+        u = u.strip().lower()
+        v = v / 1e3 if u in ("nsecond", "ns") else (v * 1e3 if u in ("msecond", "ms") else v)
         agg.setdefault(r[ki].split("(")[0].strip(), []).append(v)
     return agg
 
@@ -42,9 +43,12 @@ if __name__ == "__main__":
     fc = full_capture(sys.argv[3])
     lines = [f"# ncu summary — {tag}", "", "## Launch list (gpu__time_duration.sum, --clock-control none; cold-cache, serialised)", "",
              "| kernel | launches | mean us | share of listed time |", "|---|---|---|---|"]
-    tot = sum(sum(v) for v in ll.values())
+    ours = {k: v for k, v in ll.items() if "geig::" in k or "tc::" in k}
+    tot = sum(sum(v) for v in ours.values()) or 1.0
+    lines[-2] = "| kernel | launches | mean us | share of this repo's kernel time |"
     for k, v in ll.items():
-        lines.append(f"| `{k[:70]}` | {len(v)} | {sum(v)/len(v):.1f} | {sum(v)/tot:.3f} |")
+        share = f"{sum(v)/tot:.3f}" if k in ours else "(input synthesis, untimed)"
+        lines.append(f"| `{k[:70]}` | {len(v)} | {sum(v)/len(v):.1f} | {share} |")
     lines += ["", "## Full capture (--set full), per launch", ""]
     for d in fc:
         lines.append(f"### `{d['kernel'][:100]}`")
