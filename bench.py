@@ -62,7 +62,7 @@ class ClockSampler:
             h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
             smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
             bits = (0x8, 0x40, 0x20, 0x4)   # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
-            while not self._stop.is_set():
+            def sample():
                 sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
                 try:
                     rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
@@ -71,7 +71,15 @@ class ClockSampler:
                 util = pynvml.nvmlDeviceGetUtilizationRates(h).gpu
                 self.rows.append([str(sm), str(smax)] + ["Active" if rs & b else "Not Active" for b in bits]
                                  + [str(util)])
+
+            while not self._stop.is_set():
+                try:
+                    sample()
+                except Exception:
+                    pass
                 self._stop.wait(0.005)
+            if not self.rows:
+                sample()
             return
         except Exception:
             pass
@@ -262,16 +270,31 @@ def run_gpu(args, cfg, rank, world, local_rank):
             e2.record(stream)
             ev.append((e0, e1, e2))
 
+    # fused path: Alg. 2's loop over the K timed steps is ONE persistent launch
+    # (geig_run_cca); --per-step-launch times one geig_step_cca launch per step
+    multi = fused and not args.per_step_launch
+
+    def run_steps(i0, n):
+        geig.geig_run_cca(s.h, [Xs[(i0 + i) % P] for i in range(n)], [Ys[(i0 + i) % P] for i in range(n)], b,
+                          cfg.eta, cfg.gamma)
+
     # spin the clocks up from idle (untimed, ~0.5 s), then the W warm-up steps
     t_spin = time.perf_counter()
     i_spin = 0
     while time.perf_counter() - t_spin < args.spinup:
-        for _ in range(20):
-            step(i_spin, False)
-            i_spin += 1
+        if multi:
+            run_steps(i_spin, 20)
+            i_spin += 20
+        else:
+            for _ in range(20):
+                step(i_spin, False)
+                i_spin += 1
         torch.cuda.synchronize()
-    for i in range(args.warmup):
-        step(i, False)
+    if multi:
+        run_steps(0, args.warmup)
+    else:
+        for i in range(args.warmup):
+            step(i, False)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -283,16 +306,22 @@ def run_gpu(args, cfg, rank, world, local_rank):
         if world > 1:
             dist.barrier()
         t_start.record(stream)
-        for i in range(args.steps):
-            step(args.warmup + i, True)
+        if multi:
+            run_steps(args.warmup, args.steps)
+        else:
+            for i in range(args.steps):
+                step(args.warmup + i, True)
         t_end.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
     launches = s.launches() - l0
     elapsed_ms = t_start.elapsed_time(t_end)
-    prod_ms = statistics.mean(a.elapsed_time(b_) for a, b_, _ in ev)
-    upd_ms = statistics.mean(b_.elapsed_time(c) for _, b_, c in ev)
+    if multi:
+        prod_ms = upd_ms = elapsed_ms / args.steps       # one launch: the kernel time per step
+    else:
+        prod_ms = statistics.mean(a.elapsed_time(b_) for a, b_, _ in ev)
+        upd_ms = statistics.mean(b_.elapsed_time(c) for _, b_, c in ev)
     if world > 1:
         t = torch.tensor([elapsed_ms, prod_ms, upd_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -306,7 +335,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     kd = cfg.k * cfg.d
     if fused:
         alg_bytes = b * cfg.d * esz + 2 * kd * 4 + 2 * kd * 4 + kd * 2
-        kernel = "cca_step_kernel (fused: forward GEMM, reshuffle, backward GEMM, Gram, update)"
+        kernel = ("cca_step_kernel (fused: forward GEMM, reshuffle, backward GEMM, Gram, update; "
+                  + ("K steps in one persistent launch via geig_run_cca)" if multi else "one launch per step)"))
         k_ms = prod_ms
         ph = geig.geig_update_phase_ns(s.h)
         phases = {"forward_us": ph[3] / 1e3, "reshuffle_backward_us": ph[4] / 1e3, "gram_us": ph[0] / 1e3,
@@ -380,6 +410,8 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--spinup", type=float, default=0.5, help="seconds of untimed steps before warm-up")
+    ap.add_argument("--per-step-launch", action="store_true",
+                    help="fused path: one geig_step_cca launch per step instead of geig_run_cca")
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--math", default=None)
     ap.add_argument("--impl", default="b200")

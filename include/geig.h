@@ -148,6 +148,20 @@ geig_status geig_step_cca(geig_solver* s, const void* X, const void* Y,
 geig_status geig_step_dense(geig_solver* s, const void* A, const void* B,
                             double eta, double gamma);
 
+/* Alg. 2's loop over t ("for t = 1 : T"): nsteps
+ * consecutive CCA steps, step i on the minibatch (X[i], Y[i]) — host arrays
+ * of nsteps DEVICE pointers, each view b x d_view row-major in the solver's
+ * data dtype (batches may repeat).  Equivalent to nsteps calls of
+ * geig_step_cca (same kernels and arithmetic, bit-identical state); on the
+ * fused tensor-core path (bf16 / bf16x2, k <= 64) the steps run inside ONE
+ * persistent cooperative launch (grid barrier between steps), removing the
+ * per-step launch gap.  The pointer arrays are read during the call only.
+ * Errors: GEIG_ERR_ARG for NULL arrays or nsteps outside [0, 2^20]; the
+ * errors of geig_step_cca otherwise. */
+geig_status geig_run_cca(geig_solver* s, const void* const* X,
+                         const void* const* Y, int64_t b, int64_t nsteps,
+                         double eta, double gamma);
+
 /* End-to-end step from HOST buffers (pinned or pageable): copies X, Y host ->
  * device (stream-ordered), runs geig_step_cca and copies the k x k Gram table
  * GA (A-table of the step) back to `ga_host` (may be NULL), then synchronises.

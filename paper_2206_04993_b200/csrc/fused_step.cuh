@@ -30,9 +30,9 @@ namespace cg = cooperative_groups;
 constexpr int FS_THREADS = 256;
 
 struct FusedMaps {
-  CUtensorMap aF[2];   // forward A: X, Y (K-major, box {ATOM, 128})
+  CUtensorMap a[6];    // A operands of the batch: [0..1] forward X, Y (K-major, box {ATOM, 128});
+                       // [2..5] backward X[0:h], X[h:2h], Y[0:h], Y[h:2h] (MN-major, box {ATOM, ATOM})
   CUtensorMap bF[2];   // forward B: V_x, V_y (K-major, box {ATOM, BN})
-  CUtensorMap aB[4];   // backward A: X[0:h], X[h:2h], Y[0:h], Y[h:2h] (MN-major, box {ATOM, ATOM})
   CUtensorMap bB[4];   // backward B: Zb planes (K-major, box {ATOM, BN})
   CUtensorMap bFlo[2]; // bf16x2: low halves of V_x, V_y
   CUtensorMap bBlo[4]; // bf16x2: low halves of the Zb planes
@@ -41,6 +41,9 @@ struct FusedMaps {
 
 struct FusedParams {
   int rows, h, k, BN, stages, splitsF, mtF, mtB[2], split, bwd_y_first, dbg_nostore, dbg_mode, l2_keep;
+  int nsteps;                      // steps of Alg. 2 run by this launch (one batch each)
+  uint32_t bar_off;                // smem offset of the ring mbarriers (past the ring AND the update arena)
+  const CUtensorMap* xmaps;        // nsteps x 6 A-operand maps in global memory (nullptr: maps.a, one step)
   int kbF[2], kbB;                 // K blocks: forward per view, backward per half
   int64_t dv[2], d, ldz, hpad;
   float scale;
@@ -64,7 +67,8 @@ struct Item {
   bool keep_a;        // A operand (a view of the batch) is read again in phase B: keep it in L2
 };
 
-__device__ __forceinline__ void decode_forward(const FusedMaps& M, const FusedParams& p, int idx, Item& it) {
+__device__ __forceinline__ void decode_forward(const FusedMaps& M, const CUtensorMap* A, const FusedParams& p, int idx,
+                                               Item& it) {
   const int per_view = p.mtF * p.splitsF;
   const int v = idx / per_view, r = idx % per_view;
   const int mt = r / p.splitsF, sp = r % p.splitsF;
@@ -75,7 +79,7 @@ __device__ __forceinline__ void decode_forward(const FusedMaps& M, const FusedPa
   it.kb0[0] = (int)((int64_t)kb * sp / p.splitsF);
   it.kbn[0] = (int)((int64_t)kb * (sp + 1) / p.splitsF) - it.kb0[0];
   it.kb0[1] = it.kbn[1] = 0;
-  it.ma[0] = v == 0 ? &M.aF[0] : &M.aF[1];
+  it.ma[0] = &A[v];
   it.mb[0] = v == 0 ? &M.bF[0] : &M.bF[1];
   it.ma[1] = it.ma[0];
   it.mb[1] = it.mb[0];
@@ -87,7 +91,8 @@ __device__ __forceinline__ void decode_forward(const FusedMaps& M, const FusedPa
   it.scale = 1.f;
 }
 
-__device__ __forceinline__ void decode_backward(const FusedMaps& M, const FusedParams& p, int idx, Item& it) {
+__device__ __forceinline__ void decode_backward(const FusedMaps& M, const CUtensorMap* A, const FusedParams& p, int idx,
+                                                Item& it) {
   // view Y first: phase F streamed Y last, so part of it is still in L2
   const int first = p.bwd_y_first ? 1 : 0;
   const int v = idx < p.mtB[first] ? first : 1 - first;
@@ -97,8 +102,8 @@ __device__ __forceinline__ void decode_backward(const FusedMaps& M, const FusedP
   it.mbound = (int)(v == 0 ? p.dv[0] : p.dv[1]);
   it.kb0[0] = it.kb0[1] = 0;
   it.kbn[0] = it.kbn[1] = p.kbB;
-  it.ma[0] = v == 0 ? &M.aB[0] : &M.aB[2];
-  it.ma[1] = v == 0 ? &M.aB[1] : &M.aB[3];
+  it.ma[0] = &A[2 + 2 * v];
+  it.ma[1] = &A[3 + 2 * v];
   it.mb[0] = v == 0 ? &M.bB[0] : &M.bB[2];
   it.mb[1] = v == 0 ? &M.bB[1] : &M.bB[3];
   it.mblo[0] = v == 0 ? &M.bBlo[0] : &M.bBlo[2];
@@ -117,7 +122,8 @@ struct RingState {
 
 // One GEMM phase over this CTA's items (idx = blockIdx.x, +gridDim.x, ...).
 template <int EB, bool A_MN>
-__device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams& p, int nitems, uint8_t* ring,
+__device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap* A, const FusedParams& p, int nitems,
+                                           uint8_t* ring,
                                            uint64_t* full_bar, uint64_t* empty_bar, uint64_t* accf_bar,
                                            uint64_t* acce_bar, uint32_t tmem_base, RingState& rs) {
   constexpr int ATOM = 128 / EB;
@@ -135,7 +141,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
     // ---------------- TMA producer ----------------
     const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
     for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
-      if (A_MN) decode_backward(M, p, idx, it); else decode_forward(M, p, idx, it);
+      if (A_MN) decode_backward(M, A, p, idx, it); else decode_forward(M, A, p, idx, it);
       for (int s = 0; s < it.nseg; ++s) {
         for (int j = 0; j < it.kbn[s]; ++j, ++rs.it_prod) {
           const int st = rs.it_prod % S;
@@ -163,7 +169,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
   } else if (threadIdx.x == 32) {
     // ---------------- MMA issuer ----------------
     for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++rs.items) {
-      if (A_MN) decode_backward(M, p, idx, it); else decode_forward(M, p, idx, it);
+      if (A_MN) decode_backward(M, A, p, idx, it); else decode_forward(M, A, p, idx, it);
       if (rs.items > 0) mbar_wait(acce_bar, (rs.items - 1) & 1);   // epilogue drained the accumulator
       tc_fence_after();
       // bf16x2: the hi and lo tiles of the B operand sit back to back in smem
@@ -195,7 +201,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const FusedParams
     // ---------------- epilogue warps: TMEM -> registers -> global ----------------
     const int ew = warp - 4;
     for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++rs.items) {
-      if (A_MN) decode_backward(M, p, idx, it); else decode_forward(M, p, idx, it);
+      if (A_MN) decode_backward(M, A, p, idx, it); else decode_forward(M, A, p, idx, it);
       mbar_wait(accf_bar, rs.items & 1);
       __syncwarp();
       tc_fence_after();
@@ -240,7 +246,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t STAGE_BYTES = TC_BM * 128 + (uint32_t)p.BN * 128 * (p.split ? 2 : 1);
   uint8_t* ring = smem;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + p.stages * STAGE_BYTES);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + p.bar_off);
   uint64_t* empty_bar = full_bar + TC_MAX_STAGES;
   uint64_t* accf_bar = empty_bar + TC_MAX_STAGES;
   uint64_t* acce_bar = accf_bar + 1;
@@ -256,7 +262,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     mbar_init(accf_bar, 1);
     mbar_init(acce_bar, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int v = 0; v < 2; ++v) { tma_prefetch_desc(&maps.aF[v]); tma_prefetch_desc(&maps.bF[v]); }
+    for (int v = 0; v < 2; ++v) tma_prefetch_desc(&maps.bF[v]);
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -271,9 +277,17 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   dstamp(p.upd, 1);
   RingState rs;
 
+  // Alg. 2's loop over t: one batch per step, the state stays in HBM/L2, the
+  // TMEM allocation, mbarrier ring and its phase counters persist.
+  for (int t = 0; t < p.nsteps; ++t) {
+  const CUtensorMap* A = p.xmaps ? p.xmaps + 6 * t : maps.a;
+  if (t > 0) stamp(p.upd, 4);
+  if (threadIdx.x == 0)
+    for (int v = 0; v < 2; ++v) tma_prefetch_desc(&A[v]);
+
   // ---- phase F: forward split-K partials ----
   if (!(p.dbg_mode & 8))
-    gemm_phase<EB, false>(maps, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
+    gemm_phase<EB, false>(maps, A, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
   __syncthreads();
   dstamp(p.upd, 2);
   grid.sync();
@@ -429,9 +443,9 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
 
   // ---- phase B: backward products into AV, BV ----
   if (threadIdx.x == 0)
-    for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&maps.aB[v]); tma_prefetch_desc(&maps.bB[v]); }
+    for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&A[2 + v]); tma_prefetch_desc(&maps.bB[v]); }
   if (!(p.dbg_mode & 32))
-    gemm_phase<EB, true>(maps, p, p.mtB[0] + p.mtB[1], ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
+    gemm_phase<EB, true>(maps, A, p, p.mtB[0] + p.mtB[1], ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
   tc_fence_before();
   if (p.upd.dbg && threadIdx.x >= 128) {
     if (threadIdx.x == 128) {
@@ -458,12 +472,26 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   stamp(p.upd, 7);
   dstamp(p.upd, 7);
 
-  // ---- release TMEM, then phase U: Gram tables + fused update ----
+  // ---- phase U: Gram tables + fused update ----
+  if (!(p.dbg_mode & 64)) update_res_phases<true>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um);
+  if (t + 1 < p.nsteps) {
+    // next step: its forward TMA reads the new bf16 shadow of V (generic
+    // stores above) and refills the smem ring the update phase used
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    grid.sync();
+    tc_fence_after();
+  }
+  }  // steps
+
+  // ---- release TMEM ----
+  tc_fence_before();
+  __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(NCOLS));
   }
-  if (!(p.dbg_mode & 64)) update_res_phases<true>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um);
 }
 
 
@@ -474,29 +502,79 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
 // Whole CCA step in one cooperative launch (bf16 tensor cores, k <= 64).
 // `upd` carries the update arguments (state, AV/BV scratch, eta, gamma...);
 // its grid partition (gridDim = G, segw) is reused by the GEMM phases.
-inline geig_status fused_cca_step(TcPlan& t, const void* X, const void* Y, int64_t b, float scale,
-                                  const __nv_bfloat16* Vbf, float* AV, float* BV, UpdateArgs upd, int grid_ctas,
-                                  size_t upd_bytes, cudaStream_t st) {
+// The six A-operand maps of one batch (X, Y sample-major, b = 2h rows):
+// [0..1] forward K-major boxes, [2..5] backward MN-major boxes of the halves.
+inline bool make_batch_maps(CUtensorMap* a, const TcPlan& t, const void* X, const void* Y, int h) {
+  const int eb = 2, ATOM = 64;
+  const int64_t dv[2] = {t.dx, t.dy};
+  const void* Xv[2] = {X, Y};
+  for (int v = 0; v < 2; ++v) {
+    if (!make_map(&a[v], Xv[v], eb, dv[v], 2 * h, dv[v], ATOM, TC_BM)) return false;
+    for (int s = 0; s < 2; ++s) {
+      const char* xb = (const char*)Xv[v] + (int64_t)s * h * dv[v] * eb;
+      if (!make_map(&a[2 + 2 * v + s], xb, eb, dv[v], h, dv[v], ATOM, ATOM)) return false;
+    }
+  }
+  return true;
+}
+
+// Whole CCA step(s) in one cooperative launch (bf16 tensor cores, k <= 64):
+// nsteps consecutive steps of Alg. 2, step i on batch (X[i], Y[i]) (device
+// pointers, b rows each).  `upd` carries the update arguments (state, AV/BV
+// scratch, eta, gamma...); its grid partition (gridDim = G, segw) is reused
+// by the GEMM phases.
+inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* const* Y, int nsteps, int64_t b,
+                                  float scale, const __nv_bfloat16* Vbf, float* AV, float* BV, UpdateArgs upd,
+                                  int grid_ctas, size_t upd_bytes, cudaStream_t st) {
   if (!t.ready || t.math != GEIG_MATH_BF16) return tc_fail(GEIG_ERR_STATE, "fused step needs the bf16 plan");
+  if (nsteps < 1) return tc_fail(GEIG_ERR_ARG, "nsteps < 1");
   // (t.math is BF16 for both GEIG_MATH_BF16 and GEIG_MATH_BF16X2; t.splitb selects hi+lo operands)
   const int eb = 2, ATOM = 64;
   const int h = (int)(b / 2), rows = 2 * h, k = t.k;
   const int64_t dv[2] = {t.dx, t.dy};
-  const void* Xv[2] = {X, Y};
   FusedMaps maps;
   FusedParams p{};
+  if (!make_batch_maps(maps.a, t, X[0], Y[0], h)) return tc_fail(GEIG_ERR_CUDA, "tensor map encode (batch) failed");
+  p.nsteps = nsteps;
+  p.xmaps = nullptr;
+  if (nsteps > 1) {
+    // per-step A maps in global memory (distinct batches encoded once)
+    if (t.xm_cap < nsteps) {
+      if (t.xm_dev) cudaFree(t.xm_dev);
+      if (t.xm_host) cudaFreeHost(t.xm_host);
+      t.xm_dev = nullptr; t.xm_host = nullptr; t.xm_cap = 0;
+      if (cudaMalloc((void**)&t.xm_dev, (size_t)nsteps * 6 * sizeof(CUtensorMap)) != cudaSuccess ||
+          cudaMallocHost((void**)&t.xm_host, (size_t)nsteps * 6 * sizeof(CUtensorMap)) != cudaSuccess)
+        return tc_fail(GEIG_ERR_CUDA, "allocating per-step tensor maps failed");
+      t.xm_cap = nsteps;
+    }
+    if (!t.xm_ev && cudaEventCreateWithFlags(&t.xm_ev, cudaEventDisableTiming) != cudaSuccess)
+      return tc_fail(GEIG_ERR_CUDA, "cudaEventCreate failed");
+    cudaEventSynchronize(t.xm_ev);   // the previous call's copy out of the pinned staging buffer is done
+    for (int i = 0; i < nsteps; ++i) {
+      int j = 0;
+      while (j < i && !(X[j] == X[i] && Y[j] == Y[i])) ++j;
+      if (j < i) {
+        memcpy(&t.xm_host[6 * i], &t.xm_host[6 * j], 6 * sizeof(CUtensorMap));
+      } else if (!make_batch_maps(&t.xm_host[6 * i], t, X[i], Y[i], h)) {
+        return tc_fail(GEIG_ERR_CUDA, "tensor map encode (batch) failed");
+      }
+    }
+    if (cudaMemcpyAsync(t.xm_dev, t.xm_host, (size_t)nsteps * 6 * sizeof(CUtensorMap), cudaMemcpyHostToDevice, st) !=
+            cudaSuccess ||
+        cudaEventRecord(t.xm_ev, st) != cudaSuccess)
+      return tc_fail(GEIG_ERR_CUDA, "copying per-step tensor maps failed");
+    p.xmaps = t.xm_dev;
+  }
   for (int v = 0; v < 2; ++v) {
     const char* vb = (const char*)Vbf + (v == 0 ? 0 : t.dx * eb);
-    if (!make_map(&maps.aF[v], Xv[v], eb, dv[v], rows, dv[v], ATOM, TC_BM) ||
-        !make_map(&maps.bF[v], vb, eb, dv[v], k, t.d, ATOM, t.BN))
+    if (!make_map(&maps.bF[v], vb, eb, dv[v], k, t.d, ATOM, t.BN))
       return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused forward) failed");
     if (t.splitb && !make_map(&maps.bFlo[v], vb + (int64_t)k * t.d * eb, eb, dv[v], k, t.d, ATOM, t.BN))
       return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused forward lo) failed");
     for (int s = 0; s < 2; ++s) {
-      const char* xb = (const char*)Xv[v] + (int64_t)s * h * dv[v] * eb;
       const char* zb = (const char*)t.Zb + (int64_t)(v * 2 + s) * k * t.hpad * eb;
-      if (!make_map(&maps.aB[v * 2 + s], xb, eb, dv[v], h, dv[v], ATOM, ATOM) ||
-          !make_map(&maps.bB[v * 2 + s], zb, eb, h, k, t.hpad, ATOM, t.BN))
+      if (!make_map(&maps.bB[v * 2 + s], zb, eb, h, k, t.hpad, ATOM, t.BN))
         return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused backward) failed");
       if (t.splitb && !make_map(&maps.bBlo[v * 2 + s], zb + (int64_t)4 * k * t.hpad * eb, eb, h, k, t.hpad, ATOM, t.BN))
         return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused backward lo) failed");
@@ -533,7 +611,9 @@ inline geig_status fused_cca_step(TcPlan& t, const void* X, const void* Y, int64
   p.dbg_mode = getenv("GEIG_DBG_MODE") ? atoi(getenv("GEIG_DBG_MODE")) : 0;   // developer timing knobs (wrong results)
   const size_t stage_bytes = TC_BM * 128 + (size_t)t.BN * 128 * (t.splitb ? 2 : 1);
   p.stages = (int)std::min<size_t>(TC_MAX_STAGES, (200 * 1024) / stage_bytes);
-  const size_t smem = 1024 + std::max((size_t)p.stages * stage_bytes + (2 * TC_MAX_STAGES + 4) * 8, upd_bytes);
+  p.bar_off = (uint32_t)((std::max((size_t)p.stages * stage_bytes, upd_bytes) + 15) & ~(size_t)15);
+  const size_t smem = 1024 + p.bar_off + (2 * TC_MAX_STAGES + 4) * 8;
+  if (smem > 227 * 1024) return tc_fail(GEIG_ERR_UNSUPPORTED, "fused step: shared memory budget exceeded");
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(cca_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)

@@ -394,17 +394,22 @@ static bool fused_ok(const geig_solver* s, const void* X, const void* Y) {
   return (((uintptr_t)X | (uintptr_t)Y) % 16) == 0;
 }
 
+static UpdateArgs update_args(geig_solver* s, double eta, double gamma) {
+  UpdateArgs a{};
+  a.V = s->V; a.AUX = s->AUX; a.AV = s->AV; a.BV = s->BV;
+  a.Vbf = s->Vbf; a.partial = s->partial; a.raw = s->raw; a.gram = s->gram;
+  a.k = s->k; a.d = s->d; a.segw = s->upd_segw;
+  a.eta = (float)eta; a.gamma = (float)gamma; a.rho = s->rho; a.ts = s->ts;
+  return a;
+}
+
 extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* Y, int64_t b, double eta,
                                      double gamma) {
   if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
   if (s->problem == GEIG_CCA && b >= 2 && b <= s->max_rows && X && Y && fused_ok(s, X, Y)) {
     // whole step in one persistent cooperative launch (fused_step.cuh)
     CU(cudaSetDevice(s->device));
-    UpdateArgs a{};
-    a.V = s->V; a.AUX = s->AUX; a.AV = s->AV; a.BV = s->BV;
-    a.Vbf = s->Vbf; a.partial = s->partial; a.raw = s->raw; a.gram = s->gram;
-    a.k = s->k; a.d = s->d; a.segw = s->upd_segw;
-    a.eta = (float)eta; a.gamma = (float)gamma; a.rho = s->rho; a.ts = s->ts;
+    const UpdateArgs a = update_args(s, eta, gamma);
     geig_status st;
     // The dataflow schedule (dataflow_step.cuh) is correct but, measured on
     // B200, not yet faster than the phase-ordered kernel (its split-K fix-ups
@@ -413,7 +418,7 @@ extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* 
       st = tc::df_cca_step(s->tc, s->df, X, Y, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a, s->upd_smem,
                            s->stream);
     else
-      st = tc::fused_cca_step(s->tc, X, Y, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a, s->upd_grid,
+      st = tc::fused_cca_step(s->tc, &X, &Y, 1, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a, s->upd_grid,
                               s->upd_smem, s->stream);
     if (st) return fail(st, "%s", tc::last_error());
     s->launches++;
@@ -424,6 +429,30 @@ extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* 
   if (st) return st;
   s->fused_last = false;
   return geig_update(s, s->AV, s->BV, eta, gamma);
+}
+
+extern "C" geig_status geig_run_cca(geig_solver* s, const void* const* X, const void* const* Y, int64_t b,
+                                    int64_t nsteps, double eta, double gamma) {
+  if (!s || !X || !Y) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (nsteps < 0 || nsteps > (1 << 20)) return fail(GEIG_ERR_ARG, "nsteps = %lld out of range", (long long)nsteps);
+  if (nsteps == 0) return GEIG_OK;
+  bool fused = s->problem == GEIG_CCA && b >= 2 && b <= s->max_rows && !getenv("GEIG_DATAFLOW");
+  for (int64_t i = 0; fused && i < nsteps; ++i) fused = X[i] && Y[i] && fused_ok(s, X[i], Y[i]);
+  if (!fused) {
+    for (int64_t i = 0; i < nsteps; ++i) {
+      geig_status st = geig_step_cca(s, X[i], Y[i], b, eta, gamma);
+      if (st) return st;
+    }
+    return GEIG_OK;
+  }
+  // Alg. 2's loop over t in ONE persistent cooperative launch (fused_step.cuh)
+  CU(cudaSetDevice(s->device));
+  geig_status st = tc::fused_cca_step(s->tc, X, Y, (int)nsteps, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV,
+                                      update_args(s, eta, gamma), s->upd_grid, s->upd_smem, s->stream);
+  if (st) return fail(st, "%s", tc::last_error());
+  s->launches++;
+  s->fused_last = true;
+  return GEIG_OK;
 }
 
 extern "C" geig_status geig_step_dense(geig_solver* s, const void* A, const void* B, double eta,

@@ -440,6 +440,10 @@ struct TcPlan {
   int64_t dx = 0, dy = 0, d = 0, max_rows = 0, ldz = 0, hpad = 0;
   float* Zt = nullptr;     // TC_MAX_SPLITS x 2 x k x ldz fp32 (CCA forward split-K partials)
   void* Zb = nullptr;      // 2 x 2 x k x hpad (bf16 or fp32)
+  CUtensorMap* xm_dev = nullptr;    // multi-step fused launch: per-step A-operand maps (device)
+  CUtensorMap* xm_host = nullptr;   // pinned staging of the same
+  int xm_cap = 0;                   // steps of capacity
+  cudaEvent_t xm_ev = nullptr;      // last copy of the staging buffer
 };
 
 inline unsigned long long*& dbg_ptr() {
@@ -584,6 +588,10 @@ inline geig_status plan_create(TcPlan& t, int problem, int64_t dx, int64_t dy, i
 inline void plan_destroy(TcPlan& t) {
   if (t.Zt) cudaFree(t.Zt);
   if (t.Zb) cudaFree(t.Zb);
+  if (t.xm_dev) cudaFree(t.xm_dev);
+  if (t.xm_host) cudaFreeHost(t.xm_host);
+  if (t.xm_ev) cudaEventDestroy(t.xm_ev);
+  t.xm_dev = nullptr; t.xm_host = nullptr; t.xm_cap = 0; t.xm_ev = nullptr;
   t.Zt = nullptr; t.Zb = nullptr; t.ready = 0;
 }
 

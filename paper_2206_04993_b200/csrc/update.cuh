@@ -876,7 +876,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
 #pragma unroll
         for (int b = 0; b < 4; ++b) accA[a][b] = accB[a][b] = 0.f;
       int j = 0;
-#pragma unroll 4
+#pragma unroll 1
       for (; j < jA; ++j) {
         const float4 x = *reinterpret_cast<const float4*>(Ct + j * S + 4 * q);
         const float4 la = *reinterpret_cast<const float4*>(Lt + j * 64 + iA);
@@ -890,7 +890,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
             accB[a][b] = fmaf(lbv[a], xv[b], accB[a][b]);
           }
       }
-#pragma unroll 4
+#pragma unroll 1
       for (; j < jB; ++j) {
         const float4 x = *reinterpret_cast<const float4*>(Ct + j * S + 4 * q);
         const float4 lb = *reinterpret_cast<const float4*>(Lt + j * 64 + iB);

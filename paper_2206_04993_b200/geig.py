@@ -49,6 +49,7 @@ _SIGS = {
     "geig_update": [_vp, _vp, _vp, _f64, _f64],
     "geig_step_cca": [_vp, _vp, _vp, _i64, _f64, _f64],
     "geig_step_dense": [_vp, _vp, _vp, _f64, _f64],
+    "geig_run_cca": [_vp, _vp, _vp, _i64, _i64, _f64, _f64],
     "geig_step_cca_host": [_vp, _vp, _vp, _i64, _f64, _f64, _vp, ctypes.POINTER(_i64),
                            ctypes.POINTER(_i64)],
     "geig_get_gram": [_vp, _vp, _vp, _vp],
@@ -65,7 +66,7 @@ _lib.geig_version.restype = ctypes.c_char_p
 
 EXPORTED = ["geig_create", "geig_destroy", "geig_set_stream", "geig_sync", "geig_init_state",
             "geig_set_state", "geig_get", "geig_products_cca", "geig_products_dense", "geig_update",
-            "geig_step_cca", "geig_step_dense", "geig_step_cca_host", "geig_get_gram",
+            "geig_step_cca", "geig_step_dense", "geig_run_cca", "geig_step_cca_host", "geig_get_gram",
             "geig_launch_count", "geig_last_error", "geig_version", "geig_update_phase_ns"]
 
 
@@ -147,6 +148,17 @@ def geig_update(h, AV, BV, eta: float, gamma: float):
 
 def geig_step_cca(h, X, Y, b: int, eta: float, gamma: float):
     _check(_lib.geig_step_cca(h, _ptr(X), _ptr(Y), b, eta, gamma))
+
+
+def geig_run_cca(h, Xs, Ys, b: int, eta: float, gamma: float):
+    """nsteps = len(Xs) steps, step i on (Xs[i], Ys[i]) (device tensors)."""
+    if len(Xs) != len(Ys):
+        raise ValueError("Xs and Ys must have the same length")
+    n = len(Xs)
+    xa = (ctypes.c_void_p * max(n, 1))(*[_ptr(x).value for x in Xs])
+    ya = (ctypes.c_void_p * max(n, 1))(*[_ptr(y).value for y in Ys])
+    _check(_lib.geig_run_cca(h, ctypes.cast(xa, ctypes.c_void_p), ctypes.cast(ya, ctypes.c_void_p), b, n, eta,
+                             gamma))
 
 
 def geig_step_dense(h, A, B, eta: float, gamma: float):

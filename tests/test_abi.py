@@ -26,7 +26,8 @@ def _declared():
 def test_header_declares_the_boundary():
     names = _declared()
     for n in ["geig_create", "geig_destroy", "geig_products_cca", "geig_products_dense", "geig_update",
-              "geig_step_cca", "geig_step_dense", "geig_get", "geig_init_state", "geig_step_cca_host"]:
+              "geig_step_cca", "geig_step_dense", "geig_run_cca", "geig_get", "geig_init_state",
+              "geig_step_cca_host"]:
         assert n in names
 
 

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 import torch
 
-from tests.gpu_harness import check_cca_step, rel_err, random_state
+from tests.gpu_harness import check_cca_step, oracle_cca_step, rel_err, random_state
 
 pytestmark = pytest.mark.gpu
 
@@ -278,3 +278,57 @@ def test_bf16x2_fp32_level_parity(geig, cfg_idx, rows, k, dx, dy, use_step):
     step = errs.pop("step")
     _assert(errs, 1e-4)
     assert step < 1e-3, errs
+
+
+# --- Alg. 2's loop in one launch (geig_run_cca) --------------------------------
+
+@pytest.mark.parametrize("math,cfg_idx,rows,k,dx,dy", [("bf16x2", 3, 4096, None, None, None),
+                                                       ("bf16", 2, 1000, None, None, None),
+                                                       ("bf16x2", 2, 300, 24, 200, 136)])
+def test_run_cca_matches_single_steps_and_oracle(geig, math, cfg_idx, rows, k, dx, dy):
+    """geig_run_cca (T steps in one persistent launch, distinct and repeated
+    batches) leaves exactly the state of T geig_step_cca calls (same kernel
+    code, deterministic reductions: bit-identical), and that state matches T
+    oracle steps of Alg. 2."""
+    from synth import CONFIGS, cca_views
+    cfg = CONFIGS[cfg_idx]
+    k = k or cfg.k
+    dx, dy = dx or cfg.dx, dy or cfg.dy
+    T = 4
+    x, y = cca_views(cfg, 2 * rows, seed=11)
+    x, y = x[:, :dx].contiguous(), y[:, :dy].contiguous()
+    batches = [(x[:rows], y[:rows]), (x[rows:], y[rows:]), (x[:rows], y[:rows]), (x[rows:], y[rows:])]
+    V, aux = random_state(k, dx + dy, 3)
+    V32 = V.astype(np.float32).astype(np.float64)
+    aux32 = aux.astype(np.float32).astype(np.float64)
+    flag = 1 if x.dtype == torch.bfloat16 else 0
+    eta, gamma = cfg.eta, cfg.gamma
+    dev = "cuda:0"
+    Xd = [b_[0].to(dev).contiguous() for b_ in batches]
+    Yd = [b_[1].to(dev).contiguous() for b_ in batches]
+    states = []
+    for run in (True, False):
+        s = geig.Solver(geig.GEIG_CCA, dx, dy, k, math=math, data_dtype=flag, rho=cfg.rho, max_rows=rows)
+        try:
+            s.set_state(torch.tensor(V32, dtype=torch.float32, device=dev),
+                        torch.tensor(aux32, dtype=torch.float32, device=dev))
+            if run:
+                l0 = s.launches()
+                geig.geig_run_cca(s.h, Xd, Yd, rows, eta, gamma)
+                assert s.launches() - l0 == 1      # T steps, one persistent launch
+            else:
+                for t in range(T):
+                    geig.geig_step_cca(s.h, Xd[t], Yd[t], rows, eta, gamma)
+            Vg, Ag = s.state()
+            states.append((Vg.cpu().numpy(), Ag.cpu().numpy()))
+        finally:
+            s.close()
+    assert np.array_equal(states[0][0], states[1][0]) and np.array_equal(states[0][1], states[1][1])
+    # oracle: T steps of Alg. 2 in fp64 on the same batches
+    Vo, Ao = V32, aux32
+    for t in range(T):
+        _, _, Vo, Ao = oracle_cca_step(batches[t][0].double().numpy(), batches[t][1].double().numpy(), Vo, Ao,
+                                       eta, gamma, cfg.rho)
+    tol = 1e-2 if math == "bf16" else 1e-3
+    assert rel_err(states[0][0] - V32, Vo - V32) < tol
+    assert rel_err(states[0][1], Ao) < tol
