@@ -28,6 +28,7 @@ namespace geig { namespace tc {
 namespace cg = cooperative_groups;
 
 constexpr int FS_THREADS = 256;
+constexpr int TC_RUN_CHUNK = 4096;   // steps per persistent launch (per-step A maps: 3 MiB device + pinned)
 
 struct FusedMaps {
   CUtensorMap a[6];    // A operands of the batch: [0..1] forward X, Y (K-major, box {ATOM, 128});
@@ -251,6 +252,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   uint64_t* accf_bar = empty_bar + TC_MAX_STAGES;
   uint64_t* acce_bar = accf_bar + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce_bar + 1);
+  float* side_scratch = reinterpret_cast<float*>(acce_bar + 3);   // 64 floats for warps 2-3
   const int warp = threadIdx.x >> 5;
   constexpr uint32_t NCOLS = 256;   // >= 2 * BN (backward: A-half and B-half accumulators)
 
@@ -285,9 +287,12 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   if (threadIdx.x == 0)
     for (int v = 0; v < 2; ++v) tma_prefetch_desc(&A[v]);
 
-  // ---- phase F: forward split-K partials ----
-  if (!(p.dbg_mode & 8))
+  // ---- phase F: forward split-K partials; warps 2-3: G^C, ||v''||^2 partials ----
+  if (warp == 2 || warp == 3) {
+    if (p.upd.pre_reduced) gram_c_side(p.upd, threadIdx.x - 64);
+  } else if (!(p.dbg_mode & 8)) {
     gemm_phase<EB, false>(maps, A, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
+  }
   __syncthreads();
   dstamp(p.upd, 2);
   grid.sync();
@@ -444,8 +449,11 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   // ---- phase B: backward products into AV, BV ----
   if (threadIdx.x == 0)
     for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&A[2 + v]); tma_prefetch_desc(&maps.bB[v]); }
-  if (!(p.dbg_mode & 32))
+  if (warp == 2 || warp == 3) {    // warps 2-3: reduce the (now complete) Gram partial rows
+    if (p.upd.pre_reduced) reduce_side(p.upd, threadIdx.x - 64, side_scratch);
+  } else if (!(p.dbg_mode & 32)) {
     gemm_phase<EB, true>(maps, A, p, p.mtB[0] + p.mtB[1], ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
+  }
   tc_fence_before();
   if (p.upd.dbg && threadIdx.x >= 128) {
     if (threadIdx.x == 128) {
@@ -539,14 +547,12 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.xmaps = nullptr;
   if (nsteps > 1) {
     // per-step A maps in global memory (distinct batches encoded once)
-    if (t.xm_cap < nsteps) {
-      if (t.xm_dev) cudaFree(t.xm_dev);
-      if (t.xm_host) cudaFreeHost(t.xm_host);
-      t.xm_dev = nullptr; t.xm_host = nullptr; t.xm_cap = 0;
-      if (cudaMalloc((void**)&t.xm_dev, (size_t)nsteps * 6 * sizeof(CUtensorMap)) != cudaSuccess ||
-          cudaMallocHost((void**)&t.xm_host, (size_t)nsteps * 6 * sizeof(CUtensorMap)) != cudaSuccess)
+    if (nsteps > TC_RUN_CHUNK) return tc_fail(GEIG_ERR_ARG, "fused run: more than TC_RUN_CHUNK steps per launch");
+    if (!t.xm_dev) {   // fixed capacity, allocated once (never inside a timed loop of later calls)
+      if (cudaMalloc((void**)&t.xm_dev, (size_t)TC_RUN_CHUNK * 6 * sizeof(CUtensorMap)) != cudaSuccess ||
+          cudaMallocHost((void**)&t.xm_host, (size_t)TC_RUN_CHUNK * 6 * sizeof(CUtensorMap)) != cudaSuccess)
         return tc_fail(GEIG_ERR_CUDA, "allocating per-step tensor maps failed");
-      t.xm_cap = nsteps;
+      t.xm_cap = TC_RUN_CHUNK;
     }
     if (!t.xm_ev && cudaEventCreateWithFlags(&t.xm_ev, cudaEventDisableTiming) != cudaSuccess)
       return tc_fail(GEIG_ERR_CUDA, "cudaEventCreate failed");
@@ -604,6 +610,7 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.upd.dbg = dbg_ptr();
   p.upd.dbg_mode = getenv("GEIG_DBG_MODE") ? atoi(getenv("GEIG_DBG_MODE")) : 0;
   p.upd.ga_done = (p.upd.dbg_mode & 16) ? 0 : 1;    // phase S forms G^A, G^B from z
+  p.upd.pre_reduced = (p.upd.ga_done && !getenv("GEIG_NO_SIDE")) ? 1 : 0;   // G^C in F, reduction in B
   p.split = t.splitb;
   p.bwd_y_first = getenv("GEIG_BWD_X_FIRST") ? 0 : 1;
   p.l2_keep = getenv("GEIG_L2_KEEP") ? 1 : 0;   // measured: evict-last on a whole view thrashes the state arrays (slower)
@@ -612,7 +619,7 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   const size_t stage_bytes = TC_BM * 128 + (size_t)t.BN * 128 * (t.splitb ? 2 : 1);
   p.stages = (int)std::min<size_t>(TC_MAX_STAGES, (200 * 1024) / stage_bytes);
   p.bar_off = (uint32_t)((std::max((size_t)p.stages * stage_bytes, upd_bytes) + 15) & ~(size_t)15);
-  const size_t smem = 1024 + p.bar_off + (2 * TC_MAX_STAGES + 4) * 8;
+  const size_t smem = 1024 + p.bar_off + (2 * TC_MAX_STAGES + 4) * 8 + 64 * 4;
   if (smem > 227 * 1024) return tc_fail(GEIG_ERR_UNSUPPORTED, "fused step: shared memory budget exceeded");
   static bool attr = false;
   if (!attr) {

@@ -445,12 +445,16 @@ extern "C" geig_status geig_run_cca(geig_solver* s, const void* const* X, const 
     }
     return GEIG_OK;
   }
-  // Alg. 2's loop over t in ONE persistent cooperative launch (fused_step.cuh)
+  // Alg. 2's loop over t in persistent cooperative launches of up to
+  // TC_RUN_CHUNK steps each (fused_step.cuh)
   CU(cudaSetDevice(s->device));
-  geig_status st = tc::fused_cca_step(s->tc, X, Y, (int)nsteps, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV,
-                                      update_args(s, eta, gamma), s->upd_grid, s->upd_smem, s->stream);
-  if (st) return fail(st, "%s", tc::last_error());
-  s->launches++;
+  for (int64_t i0 = 0; i0 < nsteps; i0 += tc::TC_RUN_CHUNK) {
+    const int n = (int)std::min<int64_t>(tc::TC_RUN_CHUNK, nsteps - i0);
+    geig_status st = tc::fused_cca_step(s->tc, X + i0, Y + i0, n, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV,
+                                        update_args(s, eta, gamma), s->upd_grid, s->upd_smem, s->stream);
+    if (st) return fail(st, "%s", tc::last_error());
+    s->launches++;
+  }
   s->fused_last = true;
   return GEIG_OK;
 }

@@ -60,6 +60,7 @@ struct UpdateArgs {
   unsigned long long* dbg; // developer: 64 stamps per CTA (%globaltimer, then clock64) (fused step), nullable
   int dbg_mode;            // developer timing knobs (results wrong when set)
   int ga_done;             // fused step: phase S wrote tri(G^A), diag(G^B) of the partial rows
+  int pre_reduced;         // fused step: partial rows written and reduced into raw during F/S/B
 };
 
 // developer timeline stamp: slot `slot` of this CTA (thread 0 only)
@@ -453,6 +454,99 @@ __host__ __device__ constexpr int upd_raw_floats_res(int k) { return 2 * ((k * (
 
 __device__ __forceinline__ int tri_index(int i, int j) { return i * (i + 1) / 2 + j; }
 
+// ---------------------------------------------------------------------------
+// Fused step side work for the otherwise idle warps 2-3 (64 threads, no smem
+// beyond a 64-float scratch) of the GEMM phases:
+//   during phase F: this CTA's partial G^C_ij = <v''_i, [Bv]_j> (j <= i) and
+//     ||v''_i||^2 over its W columns, from global memory (the state is fixed
+//     for the whole step), into the second half of its Gram partial row;
+//   during phase B: this CTA's slice of the deterministic reduction of all
+//     Gram partial rows (complete after phase S) into the raw tables.
+// The update phase then starts at the coefficients (UpdateArgs::pre_reduced).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void gram_c_side(const UpdateArgs& p, int t) {
+  const int k = p.k;
+  const int64_t d = p.d;
+  const int W = (int)p.segw;
+  const int64_t c0 = (int64_t)blockIdx.x * W;
+  const int64_t c1 = min(d, c0 + W);
+  const int ntri = k * (k + 1) / 2, hA = (ntri + k + 3) & ~3;
+  float* out = p.partial + (size_t)blockIdx.x * (2 * hA) + hA;
+  const int nq = c1 > c0 ? (int)((c1 - c0) / 4) : 0;      // d % 4 == 0 on the fused path
+  const int I = t & 7, J = t >> 3;                          // rows i = I + 8a, j = J + 8b
+  auto ld = [&](const float* base, int r, int q) -> float4 {
+    return r < k ? *reinterpret_cast<const float4*>(base + (int64_t)r * d + c0 + 4 * q)
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  float acc[36];
+#pragma unroll
+  for (int e = 0; e < 36; ++e) acc[e] = 0.f;
+#pragma unroll 1
+  for (int q = 0; q < nq; ++q) {
+    float4 va[8], pc[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      va[a] = ld(p.V, I + 8 * a, q);
+      pc[a] = ld(p.AUX, J + 8 * a, q);
+    }
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b) {
+        float& c = acc[a * (a + 1) / 2 + b];
+        c = fmaf(va[a].x, pc[b].x, c);
+        c = fmaf(va[a].y, pc[b].y, c);
+        c = fmaf(va[a].z, pc[b].z, c);
+        c = fmaf(va[a].w, pc[b].w, c);
+      }
+  }
+  float nn = 0.f;
+  if (t < k)
+    for (int q = 0; q < nq; ++q) {
+      const float4 v = ld(p.V, t, q);
+      nn = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, nn))));
+    }
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b <= a; ++b) {
+      const int i = I + 8 * a, j = J + 8 * b;
+      if (i < k && j <= i) out[tri_index(i, j)] = acc[a * (a + 1) / 2 + b];
+    }
+  if (t < k) out[ntri + t] = nn;
+  for (int e = ntri + k + t; e < hA; e += 64) out[e] = 0.f;
+}
+
+// Warps 2-3 (named barrier 1, 64 threads): this CTA's slice [e0, e1) of the
+// reduction of all Gram partial rows into the raw tables (fixed order).
+__device__ __forceinline__ void reduce_side(const UpdateArgs& p, int t, float* scratch) {
+  const int k = p.k;
+  const int ntri = k * (k + 1) / 2, hA = (ntri + k + 3) & ~3, pstride = 2 * hA;
+  const int G = gridDim.x;
+  const int per = (pstride + G - 1) / G;
+  const int e0 = blockIdx.x * per, e1 = min(pstride, e0 + per);
+  const int lane = t & 31, half = t >> 5;
+  for (int eb = e0; eb < e1; eb += 32) {
+    const int e = eb + lane;
+    float s = 0.f;
+    if (e < e1) {
+      int b = half;
+      for (; b + 2 * 15 < G; b += 2 * 16) {      // 16 independent loads in flight
+        float v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = p.partial[(size_t)(b + 2 * u) * pstride + e];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) s += v[u];
+      }
+      for (; b < G; b += 2) s += p.partial[(size_t)b * pstride + e];
+    }
+    scratch[t] = s;
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    if (half == 0 && e < e1) p.raw[e] = s + scratch[t + 32];
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+  }
+}
+
 // fp32 k x d state arrays as TMA tensors (box = one CTA's W+4 columns x 64
 // rows, no swizzle; rows >= k and columns >= d are zero-filled by the TMA
 // unit).  Order: V'', AV, [Bv], BV — the smem tile order.
@@ -537,6 +631,8 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   }
   dstamp(p, 8);
 
+  if (p.pre_reduced) { stamp(p, 1); stamp(p, 2); }   // phases 1-2 ran as side work of the GEMM phases
+  if (!p.pre_reduced) {
   // ---------------- phase 1: Gram partials ----------------
   // Partial row layout (pstride = 2 hA floats):
   //   [tri(G^A) | diag(G^B) | pad][tri(G^C) | diag ||v''||^2 | pad].
@@ -756,6 +852,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   grid.sync();
   stamp(p, 2);
   dstamp(p, 12);
+  }  // !pre_reduced
 
   // ---------------- phase 3a: coefficients ----------------
   // the reduced raw tables are staged into shared memory with one burst of

@@ -150,13 +150,21 @@ def geig_step_cca(h, X, Y, b: int, eta: float, gamma: float):
     _check(_lib.geig_step_cca(h, _ptr(X), _ptr(Y), b, eta, gamma))
 
 
-def geig_run_cca(h, Xs, Ys, b: int, eta: float, gamma: float):
-    """nsteps = len(Xs) steps, step i on (Xs[i], Ys[i]) (device tensors)."""
+def cca_batches(Xs, Ys):
+    """Marshal the minibatch lists of geig_run_cca once (device tensors):
+    returns (n, X pointer array, Y pointer array)."""
     if len(Xs) != len(Ys):
         raise ValueError("Xs and Ys must have the same length")
     n = len(Xs)
     xa = (ctypes.c_void_p * max(n, 1))(*[_ptr(x).value for x in Xs])
     ya = (ctypes.c_void_p * max(n, 1))(*[_ptr(y).value for y in Ys])
+    return n, xa, ya
+
+
+def geig_run_cca(h, Xs, Ys, b: int, eta: float, gamma: float, batches=None):
+    """nsteps = len(Xs) steps, step i on (Xs[i], Ys[i]) (device tensors);
+    `batches` = a cca_batches(Xs, Ys) result to skip the marshalling."""
+    n, xa, ya = batches if batches is not None else cca_batches(Xs, Ys)
     _check(_lib.geig_run_cca(h, ctypes.cast(xa, ctypes.c_void_p), ctypes.cast(ya, ctypes.c_void_p), b, n, eta,
                              gamma))
 

@@ -80,26 +80,17 @@ void run(const void* X, int R, int C, unsigned long long* sink) {
 }
 
 int main() {
-  const int R = 8192, C = 8192;   // 128 MiB bf16 (X and Y of config 3 stacked), > L2
-  void* X;
-  cudaMalloc(&X, (size_t)R * C * 2);
-  cudaMemset(X, 1, (size_t)R * C * 2);
   unsigned long long* sink;
   cudaMalloc(&sink, 8);
-  // forward-phase pattern: 64 row strips x split 2 = 128 CTAs
-  run<128, 1, 6, 0, 2>(X, R, C, sink);
-  run<128, 1, 12, 0, 2>(X, R, C, sink);
-  run<128, 2, 6, 0, 2>(X, R, C, sink);
-  run<128, 4, 3, 0, 2>(X, R, C, sink);
-  run<128, 2, 3, 0, 2>(X, R, C, sink);
-  // 256 CTAs (2 waves / 2 per SM if smem allows)
-  run<128, 1, 6, 0, 4>(X, R, C, sink);
-  run<128, 2, 6, 0, 4>(X, R, C, sink);
-  run<64, 2, 6, 0, 2>(X, R, C, sink);
-  run<64, 4, 6, 0, 2>(X, R, C, sink);
-  // backward-like: CTA walks rows of a column strip (128 strips of 64 cols)
-  run<64, 2, 6, 1, 1>(X, R, C, sink);
-  run<128, 2, 6, 1, 1>(X, R, C, sink);
-  run<64, 1, 12, 1, 1>(X, R, C, sink);
+  for (int R : {8192, 4096, 2048}) {
+    const int C = 8192;
+    void* X;
+    cudaMalloc(&X, (size_t)R * C * 2);
+    cudaMemset(X, 1, (size_t)R * C * 2);
+    printf("R=%d (%d MiB): back-to-back reps (L2 reuse when the matrix fits)\n", R, R * C * 2 >> 20);
+    run<128, 2, 6, 0, 2>(X, R, C, sink);
+    run<64, 1, 12, 1, 1>(X, R, C, sink);
+    cudaFree(X);
+  }
   return 0;
 }
