@@ -289,7 +289,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
 
   // ---- phase F: forward split-K partials; warps 2-3: G^C, ||v''||^2 partials ----
   if (warp == 2 || warp == 3) {
-    if (p.upd.pre_reduced) gram_c_side(p.upd, threadIdx.x - 64);
+    gram_c_side(p.upd, threadIdx.x - 64);
   } else if (!(p.dbg_mode & 8)) {
     gemm_phase<EB, false>(maps, A, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
   }
@@ -311,7 +311,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   // (zx1 = X[0:h] v''_x, zy2 = Y[h:2h] v''_y, ...), i.e. k^2 h instead of
   // k^2 d multiply-adds.  The CTA's sums go to the first half of its Gram
   // partial row; the update phase adds G^C and ||v''||^2 and reduces.
-  if (!(p.dbg_mode & 16)) {
+  {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // ring smem: async-proxy writes before
     const int64_t vstride = (int64_t)p.k * p.ldz;
     const int64_t plane = (int64_t)p.k * p.hpad;
@@ -450,7 +450,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   if (threadIdx.x == 0)
     for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&A[2 + v]); tma_prefetch_desc(&maps.bB[v]); }
   if (warp == 2 || warp == 3) {    // warps 2-3: reduce the (now complete) Gram partial rows
-    if (p.upd.pre_reduced) reduce_side(p.upd, threadIdx.x - 64, side_scratch);
+    reduce_side(p.upd, threadIdx.x - 64, side_scratch);
   } else if (!(p.dbg_mode & 32)) {
     gemm_phase<EB, true>(maps, A, p, p.mtB[0] + p.mtB[1], ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
   }
@@ -481,7 +481,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   dstamp(p.upd, 7);
 
   // ---- phase U: Gram tables + fused update ----
-  if (!(p.dbg_mode & 64)) update_res_phases<true>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um);
+  if (!(p.dbg_mode & 64)) update_res_phases<true, 1>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um);
   if (t + 1 < p.nsteps) {
     // next step: its forward TMA reads the new bf16 shadow of V (generic
     // stores above) and refills the smem ring the update phase used
@@ -609,8 +609,8 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.upd = upd;
   p.upd.dbg = dbg_ptr();
   p.upd.dbg_mode = getenv("GEIG_DBG_MODE") ? atoi(getenv("GEIG_DBG_MODE")) : 0;
-  p.upd.ga_done = (p.upd.dbg_mode & 16) ? 0 : 1;    // phase S forms G^A, G^B from z
-  p.upd.pre_reduced = (p.upd.ga_done && !getenv("GEIG_NO_SIDE")) ? 1 : 0;   // G^C in F, reduction in B
+  p.upd.ga_done = 1;       // phase S forms G^A, G^B from z
+  p.upd.pre_reduced = 1;   // G^C, ||v''||^2 in F (warps 2-3), reduction in B (warps 2-3)
   p.split = t.splitb;
   p.bwd_y_first = getenv("GEIG_BWD_X_FIRST") ? 0 : 1;
   p.l2_keep = getenv("GEIG_L2_KEEP") ? 1 : 0;   // measured: evict-last on a whole view thrashes the state arrays (slower)

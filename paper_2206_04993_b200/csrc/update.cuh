@@ -409,9 +409,7 @@ update_kernel(UpdateArgs p) {
           an.z = xa.z + p.gamma * (ni * bv.z - xa.z);
           an.w = xa.w + p.gamma * (ni * bv.w - xa.w);
           const size_t o = (size_t)i * d + gx;
-          if (p.dbg_mode & 1024) {
-            if (vn.x == 12345.f && an.y == 54321.f) p.V[0] = 1.f;   // keep the math alive
-          } else if (VEC && gx + 3 < c1) {
+          if (VEC && gx + 3 < c1) {
             *reinterpret_cast<float4*>(p.V + o) = vn;
             *reinterpret_cast<float4*>(p.AUX + o) = an;
             if (p.Vbf) store_vbf4(p.Vbf, (int64_t)k * d, o, vn);
@@ -558,7 +556,7 @@ struct UpdMaps {
 // arena, so the fused step kernel (fused_step.cuh) can run it after its GEMM
 // phases inside the same cooperative launch.  `um` (param-space tensor maps)
 // selects TMA staging of the tiles; nullptr stages them with cp.async.
-template <bool VEC>
+template <bool VEC, int PRE = -1>   // PRE: -1 runtime p.pre_reduced, 0 / 1 compile-time (fused kernel: 1)
 __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* smem, cg::grid_group& grid,
                                                   const UpdMaps* um = nullptr) {
   const int tid = threadIdx.x;
@@ -631,8 +629,9 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   }
   dstamp(p, 8);
 
-  if (p.pre_reduced) { stamp(p, 1); stamp(p, 2); }   // phases 1-2 ran as side work of the GEMM phases
-  if (!p.pre_reduced) {
+  const bool pre = PRE < 0 ? p.pre_reduced != 0 : PRE != 0;
+  if (pre) { stamp(p, 1); stamp(p, 2); }   // phases 1-2 ran as side work of the GEMM phases
+  if constexpr (PRE != 1) if (!pre) {
   // ---------------- phase 1: Gram partials ----------------
   // Partial row layout (pstride = 2 hA floats):
   //   [tri(G^A) | diag(G^B) | pad][tri(G^C) | diag ||v''||^2 | pad].
@@ -945,9 +944,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
           an.z = xa.z + p.gamma * (ni * bv.z - xa.z);
           an.w = xa.w + p.gamma * (ni * bv.w - xa.w);
           const size_t o = (size_t)i * d + gx;
-          if (p.dbg_mode & 1024) {
-            if (vn.x == 12345.f && an.y == 54321.f) p.V[0] = 1.f;   // keep the math alive
-          } else if (VEC && gx + 3 < c1) {
+          if (VEC && gx + 3 < c1) {
             *reinterpret_cast<float4*>(p.V + o) = vn;
             *reinterpret_cast<float4*>(p.AUX + o) = an;
             if (p.Vbf) store_vbf4(p.Vbf, (int64_t)k * d, o, vn);
