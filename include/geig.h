@@ -67,10 +67,13 @@ typedef enum { GEIG_DENSE = 0, GEIG_CCA = 1 } geig_problem;
  *  GEIG_MATH_F32   : FFMA fp32 on CUDA cores (exactness-check variant)
  *  GEIG_MATH_BF16  : tcgen05 tensor cores, bf16 operands, fp32 accumulate
  *  GEIG_MATH_TF32  : tcgen05 tensor cores, tf32 operands, fp32 accumulate
- *  GEIG_MATH_3XTF32: tcgen05 tf32 with hi/lo split (fp32-accurate; not built)
- *  GEIG_MATH_BF16X2: tcgen05 bf16 with the V and Z operands split into
- *                    hi + lo bf16 halves (2 MMAs per K step): the bf16
- *                    data is exact, so the products are ~fp32-accurate
+ *                    (dense GEP only; geig_create returns
+ *                    GEIG_ERR_UNSUPPORTED for CCA)
+ *  GEIG_MATH_3XTF32: tcgen05 tf32 with hi/lo split (not built:
+ *                    GEIG_ERR_UNSUPPORTED)
+ *  GEIG_MATH_BF16X2: tcgen05 bf16 with the V and Z operands carried as
+ *                    hi + lo bf16 halves (one N = 2k MMA per K step): the
+ *                    bf16 data is exact, so the products are ~fp32-accurate
  * The Gram tables and the update are always fp32. */
 typedef enum {
   GEIG_MATH_F32 = 0,

@@ -327,7 +327,8 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     float* pst = Ps + 64 * 65;                               // [hA]
     const int ntri = k * (k + 1) / 2;
     const int hA = (ntri + k + 3) & ~3;
-    for (int e = tid; e < 4 * ZR * 64; e += FS_THREADS) zs[e] = 0.f;
+    if (k < 64)   // z of players n >= k stays zero (the loops below read all 64 columns)
+      for (int e = tid; e < 4 * ZR * 64; e += FS_THREADS) zs[e] = 0.f;
     const int ib = tid & 15, jb = tid >> 4;                  // P tile rows 4ib.., cols 4jb..
     float P[4][4];
 #pragma unroll
@@ -415,18 +416,14 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     {
       float* pr = pst;
       const float sc = p.scale;
+      // the z-Gram is symmetric: each thread writes the lower-triangle entries of its 4x4 tile
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) Ps[(4 * ib + a) * 65 + 4 * jb + c] = P[a][c];
-      __syncthreads();
-      for (int e = tid; e < ntri; e += FS_THREADS) {   // e = i(i+1)/2 + j, j <= i
-        int i = (int)((sqrtf(8.f * (float)e + 1.f) - 1.f) * 0.5f);
-        if ((i + 1) * (i + 2) / 2 <= e) ++i;
-        if (i * (i + 1) / 2 > e) --i;
-        const int j = e - i * (i + 1) / 2;
-        pr[e] = sc * Ps[i * 65 + j];
-      }
+        for (int c = 0; c < 4; ++c) {
+          const int i = 4 * ib + a, j = 4 * jb + c;
+          if (i < k && j <= i) pr[tri_index(i, j)] = sc * P[a][c];
+        }
       if (tid < k) pr[ntri + tid] = sc * gB;
       for (int e = ntri + k + tid; e < hA; e += FS_THREADS) pr[e] = 0.f;
       __syncthreads();

@@ -151,6 +151,10 @@ def test_errors_are_loud(geig):
     with pytest.raises(geig.GeigError):
         geig.geig_products_cca(s.h, x, x, 16, 1.0, AV, AV)      # b > max_rows
     s.close()
+    # unbuilt arithmetic variants are refused at creation, never silently wrong
+    for math in (geig.GEIG_MATH_TF32, geig.GEIG_MATH_3XTF32):
+        with pytest.raises(geig.GeigError, match="not built"):
+            geig.geig_create(geig.GEIG_CCA, 64, 64, 4, math, geig.GEIG_DATA_F32, 0.1, 64, 0)
 
 
 # --- tensor-core variants (tcgen05): bf16 1e-2, tf32 1e-2 ---------------------
