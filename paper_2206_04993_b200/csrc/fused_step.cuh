@@ -43,6 +43,7 @@ struct FusedMaps {
 struct FusedParams {
   int rows, h, k, BN, stages, splitsF, mtF, mtB[2], split, bwd_y_first, dbg_nostore, dbg_mode, l2_keep;
   int nsteps;                      // steps of Alg. 2 run by this launch (one batch each)
+  int products_only;               // 1: phases F, S, B only (AV, BV to global; multi-GPU: all-reduce, then geig_update)
   uint32_t bar_off;                // smem offset of the ring mbarriers (past the ring AND the update arena)
   const CUtensorMap* xmaps;        // nsteps x 6 A-operand maps in global memory (nullptr: maps.a, one step)
   int kbF[2], kbB;                 // K blocks: forward per view, backward per half
@@ -289,7 +290,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
 
   // ---- phase F: forward split-K partials; warps 2-3: G^C, ||v''||^2 partials ----
   if (warp == 2 || warp == 3) {
-    gram_c_side(p.upd, threadIdx.x - 64);
+    if (!p.products_only) gram_c_side(p.upd, threadIdx.x - 64);
   } else if (!(p.dbg_mode & 8)) {
     gemm_phase<EB, false>(maps, A, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
   }
@@ -413,7 +414,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
       dstamp(p.upd, 25);
     }
     // first half of this CTA's Gram partial row: [tri(G^A) | diag(G^B) | pad]
-    {
+    if (!p.products_only) {
       float* pr = pst;
       const float sc = p.scale;
       // the z-Gram is symmetric: each thread writes the lower-triangle entries of its 4x4 tile
@@ -447,7 +448,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   if (threadIdx.x == 0)
     for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&A[2 + v]); tma_prefetch_desc(&maps.bB[v]); }
   if (warp == 2 || warp == 3) {    // warps 2-3: reduce the (now complete) Gram partial rows
-    reduce_side(p.upd, threadIdx.x - 64, side_scratch);
+    if (!p.products_only) reduce_side(p.upd, threadIdx.x - 64, side_scratch);
   } else if (!(p.dbg_mode & 32)) {
     gemm_phase<EB, true>(maps, A, p, p.mtB[0] + p.mtB[1], ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
   }
@@ -478,7 +479,8 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   dstamp(p.upd, 7);
 
   // ---- phase U: Gram tables + fused update ----
-  if (!(p.dbg_mode & 64)) update_res_phases<true, 1>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um);
+  if (!p.products_only && !(p.dbg_mode & 64))
+    update_res_phases<true, 1>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um);
   if (t + 1 < p.nsteps) {
     // next step: its forward TMA reads the new bf16 shadow of V (generic
     // stores above) and refills the smem ring the update phase used
@@ -530,7 +532,7 @@ inline bool make_batch_maps(CUtensorMap* a, const TcPlan& t, const void* X, cons
 // by the GEMM phases.
 inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* const* Y, int nsteps, int64_t b,
                                   float scale, const __nv_bfloat16* Vbf, float* AV, float* BV, UpdateArgs upd,
-                                  int grid_ctas, size_t upd_bytes, cudaStream_t st) {
+                                  int grid_ctas, size_t upd_bytes, cudaStream_t st, bool products_only = false) {
   if (!t.ready || t.math != GEIG_MATH_BF16) return tc_fail(GEIG_ERR_STATE, "fused step needs the bf16 plan");
   if (nsteps < 1) return tc_fail(GEIG_ERR_ARG, "nsteps < 1");
   // (t.math is BF16 for both GEIG_MATH_BF16 and GEIG_MATH_BF16X2; t.splitb selects hi+lo operands)
@@ -541,6 +543,8 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   FusedParams p{};
   if (!make_batch_maps(maps.a, t, X[0], Y[0], h)) return tc_fail(GEIG_ERR_CUDA, "tensor map encode (batch) failed");
   p.nsteps = nsteps;
+  p.products_only = products_only ? 1 : 0;
+  if (products_only && nsteps != 1) return tc_fail(GEIG_ERR_ARG, "products-only launch runs one step");
   p.xmaps = nullptr;
   if (nsteps > 1) {
     // per-step A maps in global memory (distinct batches encoded once)

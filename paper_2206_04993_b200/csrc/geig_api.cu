@@ -321,6 +321,9 @@ static geig_status products_cca_simt(geig_solver* s, const T* X, const T* Y, int
   return GEIG_OK;
 }
 
+static bool fused_ok(const geig_solver* s, const void* X, const void* Y);
+static UpdateArgs update_args(geig_solver* s, double eta, double gamma);
+
 extern "C" geig_status geig_products_cca(geig_solver* s, const void* X, const void* Y, int64_t b,
                                          float scale, float* AV, float* BV) {
   if (!s || !X || !Y || !AV || !BV) return fail(GEIG_ERR_ARG, "NULL argument");
@@ -332,6 +335,15 @@ extern "C" geig_status geig_products_cca(geig_solver* s, const void* X, const vo
     if (s->dtype == GEIG_DATA_F32)
       return products_cca_simt(s, (const float*)X, (const float*)Y, b, scale, AV, BV);
     return products_cca_simt(s, (const __nv_bfloat16*)X, (const __nv_bfloat16*)Y, b, scale, AV, BV);
+  }
+  if (fused_ok(s, X, Y) && !getenv("GEIG_STAGED_PRODUCTS")) {
+    // phases F, S, B of the fused step kernel in one launch, AV / BV to the
+    // caller's buffers (e.g. before a cross-GPU all-reduce and geig_update)
+    geig_status st = tc::fused_cca_step(s->tc, &X, &Y, 1, b, scale, s->Vbf, AV, BV, update_args(s, 0.0, 0.0),
+                                        s->upd_grid, s->upd_smem, s->stream, /*products_only=*/true);
+    if (st) return fail(st, "%s", tc::last_error());
+    s->launches++;
+    return GEIG_OK;
   }
   int64_t nl = 0;
   geig_status st = tc::products_cca(s->tc, X, Y, b, scale, s->Vbf, s->V, AV, BV, s->stream, &nl);

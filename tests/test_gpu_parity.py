@@ -336,3 +336,13 @@ def test_run_cca_matches_single_steps_and_oracle(geig, math, cfg_idx, rows, k, d
     tol = 1e-2 if math == "bf16" else 1e-3
     assert rel_err(states[0][0] - V32, Vo - V32) < tol
     assert rel_err(states[0][1], Ao) < tol
+
+
+def test_staged_tensor_core_products_still_match(geig, monkeypatch):
+    """geig_products_cca uses phases F, S, B of the fused kernel; the staged
+    three-launch products (tc_gemm forward, zshuffle, tc_gemm backward — the
+    path for k > 64 or d % 4 != 0) stay covered here."""
+    monkeypatch.setenv("GEIG_STAGED_PRODUCTS", "1")
+    for math, tol in (("bf16", 1e-2), ("bf16x2", 1e-3)):
+        errs, _ = check_cca_step(geig, 3, 1024, k=64, dx=2048, dy=1024, math=math)
+        _assert(errs, tol)
