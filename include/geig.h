@@ -165,6 +165,34 @@ geig_status geig_run_cca(geig_solver* s, const void* const* X,
                          const void* const* Y, int64_t b, int64_t nsteps,
                          double eta, double gamma);
 
+/* Variants of the update, applied by every following step (geig_update,
+ * geig_step_cca, geig_run_cca, geig_step_dense); resident update only
+ * (k <= 64, otherwise GEIG_ERR_UNSUPPORTED).
+ *
+ * geig_set_smooth: Alg. 3, "Smooth Stochastic gamma-EigenGame"
+ * (PAPER.md:1597-1621): the clipped denominators of Alg. 2 l.8 are replaced
+ * by [<v,Bv>]_j = exp(log rho + (log nu - log rho) sigma(z_j)) (l.7), and
+ * z_i += gamma (<v_i,[Bv]_i> - [<v,Bv>]_i) [<v,Bv>]_i (log nu - log rho)
+ * sigma(z_i)(1 - sigma(z_i)) (l.14, l.21; ascent sign as in the box, DESIGN
+ * reading R6).  nu (upper bound of lambda_max(B)) must exceed rho > 0;
+ * nu <= 0 switches back to Alg. 2.  Resets z to 0 (l.4).  Errors:
+ * GEIG_ERR_ARG for rho >= nu or rho == 0.
+ *
+ * geig_smooth_state: copy the k values of z in (device z_in, may be NULL)
+ * and/or out (device z_out, may be NULL), stream-ordered.  GEIG_ERR_STATE
+ * when Alg. 3 is off.
+ *
+ * geig_set_adam: Adam(b1, b2, eps) ascent on v_i (Appendix H)
+ * with the Alg. 2 (or 3) direction as the gradient and eta of each step as
+ * the learning rate: m = b1 m + (1-b1) g, s = b2 s + (1-b2) g^2,
+ * v' = v + eta (m / (1-b1^t)) / (sqrt(s / (1-b2^t)) + eps), then the sphere
+ * retraction (l.17).  Zeroes the moments (k x d fp32 each, owned by the
+ * solver) and the step count t.  b1 < 0 switches back to plain ascent.
+ * Needs d % 4 == 0. */
+geig_status geig_set_smooth(geig_solver* s, double nu);
+geig_status geig_smooth_state(geig_solver* s, const float* z_in, float* z_out);
+geig_status geig_set_adam(geig_solver* s, double b1, double b2, double eps);
+
 /* End-to-end step from HOST buffers (pinned or pageable): copies X, Y host ->
  * device (stream-ordered), runs geig_step_cca and copies the k x k Gram table
  * GA (A-table of the step) back to `ga_host` (may be NULL), then synchronises.

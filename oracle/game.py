@@ -244,3 +244,24 @@ def adam_ascent(v, g, m, s, t, lr, b1=0.9, b2=0.999, eps=1e-8):
     mh = m / (1 - b1 ** t)
     sh = s / (1 - b2 ** t)
     return v + lr * mh / (np.sqrt(sh) + eps), m, s
+
+
+def step_alg2_adam(V, AUX, Mom, Sec, t, machines, lr, gamma, rho, b1=0.9, b2=0.999, eps=1e-8):
+    """One iteration of Alg. 2 with the ascent of line 16
+    replaced by Adam on v_i (Appendix H: "Adam(b1=0.9,
+    b2=0.999, eps=1e-8) was used for learning v_i"): the averaged direction of
+    lines 10-14 is Adam's gradient, then the sphere retraction of line 17 and
+    the aux update of line 19 as in step_alg2.  `t` is the 1-based step count
+    of the bias corrections; Mom, Sec are the k x d moments.  Returns
+    (V, AUX, Mom, Sec)."""
+    k = V.shape[0]
+    M = len(machines)
+    V_new, AUX_new = np.empty_like(V), np.empty_like(AUX)
+    Mom_new, Sec_new = np.empty_like(Mom), np.empty_like(Sec)
+    for i in range(k):
+        g = sum(direction_alg2(i, V, AUX, av, bv, rho) for av, bv in machines) / M
+        gbv = sum(aux_direction(i, AUX, bv) for _, bv in machines) / M
+        vp, Mom_new[i], Sec_new[i] = adam_ascent(V[i], g, Mom[i], Sec[i], t, lr, b1, b2, eps)
+        V_new[i] = vp / np.linalg.norm(vp)
+        AUX_new[i] = AUX[i] + gamma * gbv
+    return V_new, AUX_new, Mom_new, Sec_new

@@ -480,7 +480,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
 
   // ---- phase U: Gram tables + fused update ----
   if (!p.products_only && !(p.dbg_mode & 64))
-    update_res_phases<true, 1>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um);
+    update_res_phases<true, 1>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um, t);
   if (t + 1 < p.nsteps) {
     // next step: its forward TMA reads the new bf16 shadow of V (generic
     // stores above) and refills the smem ring the update phase used

@@ -63,6 +63,16 @@ struct geig_solver {
   int upd_grid = 1;
   bool upd_res = false;                               // resident (k <= 64) update kernel
   bool fused_last = false;                            // last step ran the fused cooperative kernel
+  // update variants (geig_set_smooth / geig_set_adam)
+  int smooth = 0;
+  float nu = 0.f;
+  float* zbuf = nullptr;                              // 2 x 64 (double-buffered z of Alg. 3)
+  int zpar = 0;
+  int adam = 0;
+  float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
+  float* am = nullptr;                                // k x d Adam moments
+  float* as = nullptr;
+  long long adam_t = 0;
   int64_t upd_segw = 32;
   size_t upd_smem = 0;
   int64_t launches = 0;
@@ -188,7 +198,8 @@ extern "C" geig_status geig_destroy(geig_solver* s) {
   cudaSetDevice(s->device);
   for (void* p : {(void*)s->arena,
                   (void*)s->gram, (void*)s->raw, (void*)s->partial,
-                  (void*)s->Wx, (void*)s->Wy, (void*)s->ts, (void*)s->Wxb, (void*)s->Wyb, s->hX, s->hY})
+                  (void*)s->Wx, (void*)s->Wy, (void*)s->ts, (void*)s->Wxb, (void*)s->Wyb, s->hX, s->hY,
+                  (void*)s->zbuf, (void*)s->am, (void*)s->as})
     if (p) cudaFree(p);
   tc::df_destroy(s->df);
   tc::plan_destroy(s->tc);
@@ -323,6 +334,7 @@ static geig_status products_cca_simt(geig_solver* s, const T* X, const T* Y, int
 
 static bool fused_ok(const geig_solver* s, const void* X, const void* Y);
 static UpdateArgs update_args(geig_solver* s, double eta, double gamma);
+static void advance_variant_state(geig_solver* s, int64_t n);
 
 extern "C" geig_status geig_products_cca(geig_solver* s, const void* X, const void* Y, int64_t b,
                                          float scale, float* AV, float* BV) {
@@ -389,11 +401,8 @@ extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float*
                                    double gamma) {
   if (!s || !AV || !BV) return fail(GEIG_ERR_ARG, "NULL argument");
   CU(cudaSetDevice(s->device));
-  UpdateArgs a{};
-  a.V = s->V; a.AUX = s->AUX; a.AV = AV; a.BV = BV;
-  a.Vbf = s->Vbf; a.partial = s->partial; a.raw = s->raw; a.gram = s->gram;
-  a.k = s->k; a.d = s->d; a.segw = s->upd_segw;
-  a.eta = (float)eta; a.gamma = (float)gamma; a.rho = s->rho; a.ts = s->ts;
+  UpdateArgs a = update_args(s, eta, gamma);
+  a.AV = AV; a.BV = BV;
   void* args[] = {&a};
   const bool vec = (s->d % 4 == 0) && (((uintptr_t)AV | (uintptr_t)BV) % 16 == 0);
   void* fn;
@@ -402,6 +411,7 @@ extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float*
   else fn = vec ? (void*)update_kernel<2, true> : (void*)update_kernel<2, false>;
   CU(cudaLaunchCooperativeKernel(fn, dim3(s->upd_grid), dim3(UPD_THREADS), args, s->upd_smem, s->stream));
   s->launches++;
+  advance_variant_state(s, 1);
   return GEIG_OK;
 }
 
@@ -417,7 +427,17 @@ static UpdateArgs update_args(geig_solver* s, double eta, double gamma) {
   a.Vbf = s->Vbf; a.partial = s->partial; a.raw = s->raw; a.gram = s->gram;
   a.k = s->k; a.d = s->d; a.segw = s->upd_segw;
   a.eta = (float)eta; a.gamma = (float)gamma; a.rho = s->rho; a.ts = s->ts;
+  a.smooth = s->smooth; a.zbuf = s->zbuf; a.zpar = s->zpar;
+  a.lnrho = logf(std::max(s->rho, 1e-30f)); a.lnnu = logf(std::max(s->nu, 1e-30f));
+  a.adam = s->adam; a.am = s->am; a.as = s->as; a.b1 = s->b1; a.b2 = s->b2; a.eps = s->eps;
+  a.adam_t0 = s->adam_t;
   return a;
+}
+
+// the variant state advances with every update launched (n steps)
+static void advance_variant_state(geig_solver* s, int64_t n) {
+  s->zpar = (int)((s->zpar + n) & 1);
+  s->adam_t += n;
 }
 
 extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* Y, int64_t b, double eta,
@@ -440,6 +460,7 @@ extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* 
     if (st) return fail(st, "%s", tc::last_error());
     s->launches++;
     s->fused_last = true;
+    advance_variant_state(s, 1);
     return GEIG_OK;
   }
   geig_status st = geig_products_cca(s, X, Y, b, 1.0f / (float)(b / 2), s->AV, s->BV);
@@ -471,6 +492,7 @@ extern "C" geig_status geig_run_cca(geig_solver* s, const void* const* X, const 
                                         update_args(s, eta, gamma), s->upd_grid, s->upd_smem, s->stream);
     if (st) return fail(st, "%s", tc::last_error());
     s->launches++;
+    advance_variant_state(s, n);
   }
   s->fused_last = true;
   return GEIG_OK;
@@ -506,6 +528,49 @@ extern "C" geig_status geig_step_cca_host(geig_solver* s, const void* X_host, co
   CU(cudaStreamSynchronize(s->stream));
   if (h2d) *h2d = (int64_t)(bx + by);
   if (d2h) *d2h = ga_host ? (int64_t)gb : 0;
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_set_smooth(geig_solver* s, double nu) {
+  if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  if (!(nu > 0.0)) { s->smooth = 0; return GEIG_OK; }
+  if (!(nu > (double)s->rho) || !(s->rho > 0.f))
+    return fail(GEIG_ERR_ARG, "Alg. 3 needs 0 < rho < nu (rho=%g, nu=%g)", (double)s->rho, nu);
+  if (!s->upd_res) return fail(GEIG_ERR_UNSUPPORTED, "Alg. 3 needs the resident update (k <= 64)");
+  CU(cudaSetDevice(s->device));
+  if (!s->zbuf) CU(cudaMalloc((void**)&s->zbuf, 2 * 64 * sizeof(float)));
+  CU(cudaMemsetAsync(s->zbuf, 0, 2 * 64 * sizeof(float), s->stream));   // Alg. 3 l.4: z_i = 0
+  s->zpar = 0;
+  s->nu = (float)nu;
+  s->smooth = 1;
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_smooth_state(geig_solver* s, const float* z_in, float* z_out) {
+  if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  if (!s->smooth) return fail(GEIG_ERR_STATE, "Alg. 3 is not enabled (geig_set_smooth)");
+  CU(cudaSetDevice(s->device));
+  float* cur = s->zbuf + (s->zpar & 1) * 64;
+  if (z_in) CU(cudaMemcpyAsync(cur, z_in, (size_t)s->k * sizeof(float), cudaMemcpyDeviceToDevice, s->stream));
+  if (z_out) CU(cudaMemcpyAsync(z_out, cur, (size_t)s->k * sizeof(float), cudaMemcpyDeviceToDevice, s->stream));
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_set_adam(geig_solver* s, double b1, double b2, double eps) {
+  if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  if (b1 < 0.0) { s->adam = 0; return GEIG_OK; }
+  if (!(b1 < 1.0) || !(b2 >= 0.0 && b2 < 1.0) || !(eps >= 0.0)) return fail(GEIG_ERR_ARG, "bad Adam parameters");
+  if (!s->upd_res || s->d % 4 != 0)
+    return fail(GEIG_ERR_UNSUPPORTED, "Adam needs the resident update (k <= 64) and d %% 4 == 0");
+  CU(cudaSetDevice(s->device));
+  const size_t kd = (size_t)s->k * s->d;
+  if (!s->am) CU(cudaMalloc((void**)&s->am, kd * sizeof(float)));
+  if (!s->as) CU(cudaMalloc((void**)&s->as, kd * sizeof(float)));
+  CU(cudaMemsetAsync(s->am, 0, kd * sizeof(float), s->stream));
+  CU(cudaMemsetAsync(s->as, 0, kd * sizeof(float), s->stream));
+  s->adam_t = 0;
+  s->b1 = (float)b1; s->b2 = (float)b2; s->eps = (float)eps;
+  s->adam = 1;
   return GEIG_OK;
 }
 

@@ -61,6 +61,20 @@ struct UpdateArgs {
   int dbg_mode;            // developer timing knobs (results wrong when set)
   int ga_done;             // fused step: phase S wrote tri(G^A), diag(G^B) of the partial rows
   int pre_reduced;         // fused step: partial rows written and reduced into raw during F/S/B
+  // Alg. 3 (smooth gamma-EigenGame): s_j^2 = exp(log rho +
+  // (log nu - log rho) sigmoid(z_j)); z double-buffered: step t of a launch
+  // reads zbuf[(zpar + t) & 1] and writes zbuf[(zpar + t + 1) & 1] (64 each)
+  int smooth;
+  float* zbuf;
+  int zpar;
+  float lnrho, lnnu;
+  // Adam ascent on v_i (Appendix H): moments am, as (k x d);
+  // step t of a launch uses bias corrections of the global count adam_t0 + t + 1
+  int adam;
+  float* am;
+  float* as;
+  float b1, b2, eps;
+  long long adam_t0;
 };
 
 // developer timeline stamp: slot `slot` of this CTA (thread 0 only)
@@ -558,7 +572,7 @@ struct UpdMaps {
 // selects TMA staging of the tiles; nullptr stages them with cp.async.
 template <bool VEC, int PRE = -1>   // PRE: -1 runtime p.pre_reduced, 0 / 1 compile-time (fused kernel: 1)
 __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* smem, cg::grid_group& grid,
-                                                  const UpdMaps* um = nullptr) {
+                                                  const UpdMaps* um = nullptr, int step = 0) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int k = p.k;
@@ -872,7 +886,21 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
       if (i < k) {
         n = rsqrtf(rN[i]);
         gb = n * n * rB[i];
-        is2 = 1.f / fmaxf(n * rC[tri_index(i, i)], p.rho);
+        const float gcii = n * rC[tri_index(i, i)];            // <v_i, [Bv]_i>
+        if (p.smooth) {
+          // Alg. 3 l.7: [<v,Bv>]_i = exp(log rho + (log nu - log rho) sigma(z_i))
+          const float* zr = p.zbuf + ((p.zpar + step) & 1) * 64;
+          const float z = zr[i];
+          const float sg = 1.f / (1.f + expf(-z));
+          const float br = expf(p.lnrho + (p.lnnu - p.lnrho) * sg);
+          is2 = 1.f / br;
+          if (blockIdx.x == 0) {   // l.14 / l.21: z_i += gamma (<v_i,[Bv]_i> - br) br (log nu - log rho) sigma (1 - sigma)
+            float* zw = p.zbuf + ((p.zpar + step + 1) & 1) * 64;
+            zw[i] = z + p.gamma * (gcii - br) * br * (p.lnnu - p.lnrho) * sg * (1.f - sg);
+          }
+        } else {
+          is2 = 1.f / fmaxf(gcii, p.rho);                      // Alg. 2 l.8
+        }
       }
       Ns[i] = n; IS2[i] = is2; D1s[i] = gb;
     }
@@ -935,10 +963,35 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
           const float ni = Ns[i];
           const float d1 = D1s[i] * ni, d2 = D2s[i] * ni;
           float4 vn, an;
-          vn.x = ni * vv.x + p.eta * (d1 * av.x - d2 * bv.x - acc[a][0]);
-          vn.y = ni * vv.y + p.eta * (d1 * av.y - d2 * bv.y - acc[a][1]);
-          vn.z = ni * vv.z + p.eta * (d1 * av.z - d2 * bv.z - acc[a][2]);
-          vn.w = ni * vv.w + p.eta * (d1 * av.w - d2 * bv.w - acc[a][3]);
+          if (p.adam) {
+            // Appendix H: Adam ascent on v_i with the Alg. 2 direction as the gradient
+            const size_t o0 = (size_t)i * d + gx;
+            float4 g;
+            g.x = d1 * av.x - d2 * bv.x - acc[a][0];
+            g.y = d1 * av.y - d2 * bv.y - acc[a][1];
+            g.z = d1 * av.z - d2 * bv.z - acc[a][2];
+            g.w = d1 * av.w - d2 * bv.w - acc[a][3];
+            float4 m4 = *reinterpret_cast<const float4*>(p.am + o0);
+            float4 s4 = *reinterpret_cast<const float4*>(p.as + o0);
+            const float tt = (float)(p.adam_t0 + step + 1);
+            const float c1 = 1.f / (1.f - powf(p.b1, tt)), c2 = 1.f / (1.f - powf(p.b2, tt));
+            auto upd = [&](float gv, float& mv, float& sv, float v) {
+              mv = p.b1 * mv + (1.f - p.b1) * gv;
+              sv = p.b2 * sv + (1.f - p.b2) * gv * gv;
+              return v + p.eta * (mv * c1) / (sqrtf(sv * c2) + p.eps);
+            };
+            vn.x = upd(g.x, m4.x, s4.x, ni * vv.x);
+            vn.y = upd(g.y, m4.y, s4.y, ni * vv.y);
+            vn.z = upd(g.z, m4.z, s4.z, ni * vv.z);
+            vn.w = upd(g.w, m4.w, s4.w, ni * vv.w);
+            *reinterpret_cast<float4*>(p.am + o0) = m4;
+            *reinterpret_cast<float4*>(p.as + o0) = s4;
+          } else {
+            vn.x = ni * vv.x + p.eta * (d1 * av.x - d2 * bv.x - acc[a][0]);
+            vn.y = ni * vv.y + p.eta * (d1 * av.y - d2 * bv.y - acc[a][1]);
+            vn.z = ni * vv.z + p.eta * (d1 * av.z - d2 * bv.z - acc[a][2]);
+            vn.w = ni * vv.w + p.eta * (d1 * av.w - d2 * bv.w - acc[a][3]);
+          }
           an.x = xa.x + p.gamma * (ni * bv.x - xa.x);
           an.y = xa.y + p.gamma * (ni * bv.y - xa.y);
           an.z = xa.z + p.gamma * (ni * bv.z - xa.z);

@@ -50,6 +50,9 @@ _SIGS = {
     "geig_step_cca": [_vp, _vp, _vp, _i64, _f64, _f64],
     "geig_step_dense": [_vp, _vp, _vp, _f64, _f64],
     "geig_run_cca": [_vp, _vp, _vp, _i64, _i64, _f64, _f64],
+    "geig_set_smooth": [_vp, _f64],
+    "geig_smooth_state": [_vp, _vp, _vp],
+    "geig_set_adam": [_vp, _f64, _f64, _f64],
     "geig_step_cca_host": [_vp, _vp, _vp, _i64, _f64, _f64, _vp, ctypes.POINTER(_i64),
                            ctypes.POINTER(_i64)],
     "geig_get_gram": [_vp, _vp, _vp, _vp],
@@ -67,6 +70,7 @@ _lib.geig_version.restype = ctypes.c_char_p
 EXPORTED = ["geig_create", "geig_destroy", "geig_set_stream", "geig_sync", "geig_init_state",
             "geig_set_state", "geig_get", "geig_products_cca", "geig_products_dense", "geig_update",
             "geig_step_cca", "geig_step_dense", "geig_run_cca", "geig_step_cca_host", "geig_get_gram",
+            "geig_set_smooth", "geig_smooth_state", "geig_set_adam",
             "geig_launch_count", "geig_last_error", "geig_version", "geig_update_phase_ns"]
 
 
@@ -148,6 +152,18 @@ def geig_update(h, AV, BV, eta: float, gamma: float):
 
 def geig_step_cca(h, X, Y, b: int, eta: float, gamma: float):
     _check(_lib.geig_step_cca(h, _ptr(X), _ptr(Y), b, eta, gamma))
+
+
+def geig_set_smooth(h, nu: float):
+    _check(_lib.geig_set_smooth(h, nu))
+
+
+def geig_smooth_state(h, z_in=None, z_out=None):
+    _check(_lib.geig_smooth_state(h, _ptr(z_in, torch.float32), _ptr(z_out, torch.float32)))
+
+
+def geig_set_adam(h, b1: float = 0.9, b2: float = 0.999, eps: float = 1e-8):
+    _check(_lib.geig_set_adam(h, b1, b2, eps))
 
 
 def cca_batches(Xs, Ys):

@@ -238,3 +238,34 @@ def test_adam_first_step():
     assert np.allclose(v1, 0.1 * np.sign(g), atol=1e-6)
     v2, m2, s2 = game.adam_ascent(v, np.zeros(3), np.zeros(3), np.zeros(3), 1, 0.1)
     assert np.allclose(v2, 0.0)
+
+
+def test_alg2_adam_reduces_to_sign_ascent():
+    """Pins of step_alg2_adam against closed forms: with b1 = b2 = eps = 0 (and,
+    for any b1, b2, at t = 1 from zero moments) Adam's step is lr * sign(g)
+    per coordinate, so the iteration equals normalize(v + lr sign(grad_i)) with
+    the Alg. 2 direction; the aux update is that of step_alg2."""
+    rng = np.random.default_rng(4)
+    k, d = 3, 7
+    A = rng.standard_normal((d, d)); A = A + A.T
+    Bh = rng.standard_normal((d, d)); B = Bh @ Bh.T + d * np.eye(d)
+    V, _ = game.init_state(rng.standard_normal((k, d)))
+    AUX = V @ B.T + 0.1 * rng.standard_normal((k, d))
+    machines = [(V @ A.T, V @ B.T)]
+    lr, gamma, rho = 0.05, 0.5, 0.1
+    Vs, As = game.step_alg2(V, AUX, machines, lr, gamma, rho)
+    want = np.empty_like(V)
+    for i in range(k):
+        g = game.direction_alg2(i, V, AUX, machines[0][0], machines[0][1], rho)
+        vp = V[i] + lr * np.sign(g)
+        want[i] = vp / np.linalg.norm(vp)
+    Z = np.zeros_like(V)
+    for b1, b2, eps, t in [(0.0, 0.0, 0.0, 5), (0.9, 0.999, 0.0, 1)]:
+        Va, Aa, Ma, Sa = game.step_alg2_adam(V, AUX, Z, Z, t, machines, lr, gamma, rho, b1, b2, eps)
+        np.testing.assert_allclose(Va, want, rtol=0, atol=1e-12)
+        np.testing.assert_allclose(Aa, As, rtol=0, atol=0)
+    # the moments are the exponential averages of the direction
+    Va, Aa, Ma, Sa = game.step_alg2_adam(V, AUX, Z, Z, 1, machines, lr, gamma, rho, 0.9, 0.999, 1e-8)
+    g0 = game.direction_alg2(0, V, AUX, machines[0][0], machines[0][1], rho)
+    np.testing.assert_allclose(Ma[0], 0.1 * g0, rtol=1e-12)
+    np.testing.assert_allclose(Sa[0], 0.001 * g0 * g0, rtol=1e-12)
