@@ -239,6 +239,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
                     rho=cfg.rho, max_rows=b, device=local_rank, stream=stream.cuda_stream)
     G = torch.tensor(gaussian_init(cfg.k, cfg.d, 0), dtype=torch.float32, device=dev)
     s.init_state(G)
+    variant = "alg2"
+    if args.smooth_nu is not None:                     # Alg. 3
+        geig.geig_set_smooth(s.h, args.smooth_nu)
+        variant = f"alg3(nu={args.smooth_nu:g})"
+    if args.adam:                                      # Appendix H optimizer
+        geig.geig_set_adam(s.h, 0.9, 0.999, 1e-8)
+        variant += "+adam"
     AV = torch.empty(cfg.k, cfg.d, device=dev)
     BV = torch.empty_like(AV)
     scale = cca_scale(b, world)
@@ -398,7 +405,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "bf16" if math in ("bf16", "bf16x2") else ("f32" if math == "f32" else math),
                 "data": "synthetic",
-                "config": dict(_workload(cfg, math), parallelism=f"dp{world}", global_batch=world * b,
+                "config": dict(_workload(cfg, math), parallelism=f"dp{world}", global_batch=world * b, update=variant,
                                l2_policy=f"ring of {P} distinct batches ({P * batch_bytes / 2**20:.0f} MiB) "
                                          "> 126 MB L2, a new batch every step"),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -413,6 +420,9 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--spinup", type=float, default=0.5, help="seconds of untimed steps before warm-up")
+    ap.add_argument("--smooth-nu", type=float, default=None,
+                    help="Alg. 3 (smooth gamma-EigenGame) with this nu upper bound of lambda_max(B)")
+    ap.add_argument("--adam", action="store_true", help="Adam ascent on v_i (Appendix H)")
     ap.add_argument("--per-step-launch", action="store_true",
                     help="fused path: one geig_step_cca launch per step instead of geig_run_cca")
     ap.add_argument("--config", type=int, default=3)
