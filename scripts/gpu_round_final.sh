@@ -11,7 +11,9 @@ CMD="python bench.py --steps 5 --warmup 3 --spinup 0 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain_small.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench.csv $CMD > gpurun_out/ncu_list_bench.log 2>&1
 echo "list exit $?"
-$CMD > gpurun_out/plain_small2.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cca_step_kernel" -s 5 -c 1 -o gpurun_out/prof_final $CMD > gpurun_out/ncu_full_final.log 2>&1
+# full capture of ONE single-step launch (per-step DRAM traffic for the roofline)
+CMD2="python scripts/one_step.py 3 bf16x2 4"
+$CMD2 > gpurun_out/plain_small2.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cca_step_kernel" -s 3 -c 1 -o gpurun_out/prof_final $CMD2 > gpurun_out/ncu_full_final.log 2>&1
 echo "full exit $?"
 tail -c 400 gpurun_out/bench_default.json
