@@ -42,6 +42,9 @@ struct FusedMaps {
 
 struct FusedParams {
   int rows, h, k, BN, stages, splitsF, mtF, mtB[2], split, bwd_y_first, dbg_nostore, dbg_mode, l2_keep;
+  int tmF, tmB;                    // 128-row M tiles per work item (forward: sample rows; backward: feature
+                                   // columns): tm tiles share one B-operand tile per K step, so the ring
+                                   // holds tm x more batch bytes in flight per byte of V / Z re-read
   int nsteps;                      // steps of Alg. 2 run by this launch (one batch each)
   int products_only;               // 1: phases F, S, B only (AV, BV to global; multi-GPU: all-reduce, then geig_update)
   uint32_t bar_off;                // smem offset of the ring mbarriers (past the ring AND the update arena)
@@ -59,6 +62,7 @@ struct FusedParams {
 
 struct Item {
   int nseg, m0, mbound;
+  int mt;             // M tiles of this item (<= tm of the phase; fewer at the ragged end)
   int kb0[2], kbn[2];
   const CUtensorMap* ma[2];
   const CUtensorMap* mb[2];
@@ -75,8 +79,9 @@ __device__ __forceinline__ void decode_forward(const FusedMaps& M, const CUtenso
   const int v = idx / per_view, r = idx % per_view;
   const int mt = r / p.splitsF, sp = r % p.splitsF;
   it.nseg = 1;
-  it.m0 = mt * TC_BM;
+  it.m0 = mt * p.tmF * TC_BM;
   it.mbound = p.rows;
+  it.mt = min(p.tmF, (p.rows - it.m0 + TC_BM - 1) / TC_BM);
   const int kb = v == 0 ? p.kbF[0] : p.kbF[1];
   it.kb0[0] = (int)((int64_t)kb * sp / p.splitsF);
   it.kbn[0] = (int)((int64_t)kb * (sp + 1) / p.splitsF) - it.kb0[0];
@@ -95,25 +100,28 @@ __device__ __forceinline__ void decode_forward(const FusedMaps& M, const CUtenso
 
 __device__ __forceinline__ void decode_backward(const FusedMaps& M, const CUtensorMap* A, const FusedParams& p, int idx,
                                                 Item& it) {
-  // view Y first: phase F streamed Y last, so part of it is still in L2
+  // view Y first: phase F streamed Y last, so part of it is still in L2.
+  // Item = (feature tile of tmB x 128 columns, half): half 0 (rows [0,h))
+  // accumulates AV, half 1 (rows [h,2h)) BV (reading R1).
   const int first = p.bwd_y_first ? 1 : 0;
-  const int v = idx < p.mtB[first] ? first : 1 - first;
-  const int mt = v == first ? idx : idx - p.mtB[first];
-  it.nseg = 2;
-  it.m0 = mt * TC_BM;
+  const int nfirst = 2 * p.mtB[first];
+  const int v = idx < nfirst ? first : 1 - first;
+  const int r = v == first ? idx : idx - nfirst;
+  const int mt = r >> 1, seg = r & 1;
+  it.nseg = 1;
+  it.m0 = mt * p.tmB * TC_BM;
   it.mbound = (int)(v == 0 ? p.dv[0] : p.dv[1]);
+  it.mt = min(p.tmB, (it.mbound - it.m0 + TC_BM - 1) / TC_BM);
   it.kb0[0] = it.kb0[1] = 0;
-  it.kbn[0] = it.kbn[1] = p.kbB;
-  it.ma[0] = &A[2 + 2 * v];
-  it.ma[1] = &A[3 + 2 * v];
-  it.mb[0] = v == 0 ? &M.bB[0] : &M.bB[2];
-  it.mb[1] = v == 0 ? &M.bB[1] : &M.bB[3];
-  it.mblo[0] = v == 0 ? &M.bBlo[0] : &M.bBlo[2];
-  it.mblo[1] = v == 0 ? &M.bBlo[1] : &M.bBlo[3];
+  it.kbn[0] = p.kbB;
+  it.kbn[1] = 0;
+  it.ma[0] = it.ma[1] = &A[2 + 2 * v + seg];
+  it.mb[0] = it.mb[1] = &M.bB[2 * v + seg];       // Zb planes: y1, x2 (view x); x1, y2 (view y)
+  it.mblo[0] = it.mblo[1] = &M.bBlo[2 * v + seg];
   const int64_t off = v == 0 ? 0 : p.dv[0];
   it.keep_a = false;
-  it.out[0] = p.AV + off;
-  it.out[1] = p.BV + off;
+  it.out[0] = (seg == 0 ? p.AV : p.BV) + off;
+  it.out[1] = nullptr;
   it.ldo = p.d;
   it.scale = p.scale;
 }
@@ -127,11 +135,13 @@ template <int EB, bool A_MN>
 __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap* A, const FusedParams& p, int nitems,
                                            uint8_t* ring,
                                            uint64_t* full_bar, uint64_t* empty_bar, uint64_t* accf_bar,
-                                           uint64_t* acce_bar, uint32_t tmem_base, RingState& rs) {
+                                           uint64_t* acce_bar, uint32_t tmem_base, RingState& rs, float* epi) {
   constexpr int ATOM = 128 / EB;
   constexpr int BK = ATOM;
   constexpr int UK = 32 / EB;
-  constexpr uint32_t A_BYTES = TC_BM * 128;
+  constexpr uint32_t A_TILE = TC_BM * 128;         // one 128-row M tile of A for one K block (16 KB)
+  const int tm = A_MN ? p.tmB : p.tmF;
+  const uint32_t A_BYTES = (uint32_t)tm * A_TILE;   // stage: tm A tiles, then the (shared) B tile(s)
   const uint32_t B_BYTES = (uint32_t)p.BN * 128;
   const bool split = p.split != 0;
   const uint32_t STAGE_BYTES = A_BYTES + B_BYTES * (split ? 2 : 1);
@@ -151,15 +161,20 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
           uint8_t* sa = ring + st * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
           const bool nob = (p.dbg_mode & 2) != 0;
-          mbar_expect_tx(&full_bar[st], nob ? A_BYTES : STAGE_BYTES);
+          const uint32_t abytes = (uint32_t)it.mt * A_TILE;
+          mbar_expect_tx(&full_bar[st], abytes + (nob ? 0u : STAGE_BYTES - A_BYTES));
           const int k0 = (it.kb0[s] + j) * BK;
           const uint64_t pa = it.keep_a ? pol_keep : pol_stream;
-          if (A_MN) {
+          for (int mtile = 0; mtile < it.mt; ++mtile) {
+            const int mm = it.m0 + mtile * TC_BM;
+            uint8_t* sat = sa + mtile * A_TILE;
+            if (A_MN) {
 #pragma unroll
-            for (int q = 0; q < TC_BM / ATOM; ++q)
-              tma_load_2d_hint(sa + q * (BK * 128), it.ma[s], &full_bar[st], it.m0 + q * ATOM, k0, pa);
-          } else {
-            tma_load_2d_hint(sa, it.ma[s], &full_bar[st], k0, it.m0, pa);
+              for (int q = 0; q < TC_BM / ATOM; ++q)
+                tma_load_2d_hint(sat + q * (BK * 128), it.ma[s], &full_bar[st], mm + q * ATOM, k0, pa);
+            } else {
+              tma_load_2d_hint(sat, it.ma[s], &full_bar[st], k0, mm, pa);
+            }
           }
           if (!nob) {   // V / Z tiles: small, re-read by every CTA
             tma_load_2d_hint(sb, it.mb[s], &full_bar[st], k0, 0, pol_keep);
@@ -179,20 +194,26 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
       // accumulator holds A.B_hi^T in columns [0, BN) and A.B_lo^T in [BN, 2BN)
       // (summed by the epilogue): half the MMA issues and A-operand smem reads
       // of two N = BN MMAs.
+      // tm M tiles per K step share the B tile; accumulator of M tile mtile
+      // (segment s) at TMEM columns (s * mt + mtile) * acols
+      const uint32_t acols = (uint32_t)(p.BN * (split ? 2 : 1));
       for (int s = 0; s < it.nseg; ++s) {
-        const uint32_t d_tmem = tmem_base + (uint32_t)(s * p.BN * (split ? 2 : 1));
         for (int j = 0; j < it.kbn[s]; ++j, ++rs.it_mma) {
           const int st = rs.it_mma % S;
           mbar_wait(&full_bar[st], (rs.it_mma / S) & 1);
           tc_fence_after();
-          const uint32_t sa = smem_u32(ring + st * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+          const uint32_t sa0 = smem_u32(ring + st * STAGE_BYTES);
+          const uint32_t sb = sa0 + A_BYTES;
+          for (int mtile = 0; mtile < it.mt; ++mtile) {
+            const uint32_t d_tmem = tmem_base + (uint32_t)(s * it.mt + mtile) * acols;
+            const uint32_t sa = sa0 + (uint32_t)mtile * A_TILE;
 #pragma unroll
-          for (int kk = 0; kk < BK / UK; ++kk) {
-            if (p.dbg_mode & 1) break;
-            const uint64_t ad = A_MN ? make_sdesc(sa + kk * UK * 128, BK * 128, 1024) : make_sdesc(sa + kk * 32, 16, 1024);
-            const uint64_t bd = make_sdesc(sb + kk * 32, 16, 1024);
-            umma<EB>(d_tmem, ad, bd, idesc, (j > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < BK / UK; ++kk) {
+              if (p.dbg_mode & 1) break;
+              const uint64_t ad = A_MN ? make_sdesc(sa + kk * UK * 128, BK * 128, 1024) : make_sdesc(sa + kk * 32, 16, 1024);
+              const uint64_t bd = make_sdesc(sb + kk * 32, 16, 1024);
+              umma<EB>(d_tmem, ad, bd, idesc, (j > 0 || kk > 0) ? 1u : 0u);
+            }
           }
           umma_commit(&empty_bar[st]);
         }
@@ -200,30 +221,55 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
       umma_commit(accf_bar);
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue warps: TMEM -> registers -> global ----------------
+    // ---------------- epilogue warps: TMEM -> registers -> smem -> global ----------------
+    // Each warp drains its 32 TMEM lanes (32 consecutive m) 16 columns (n) at
+    // a time, transposes the 32 x 16 block through its 2 KB of smem and
+    // writes it as float4 rows (one instruction: 4 rows x 128 B): a quarter
+    // of the store instructions of lane-per-m scalar stores, no per-element
+    // bounds branches on full tiles.
     const int ew = warp - 4;
+    float* ws = epi + ew * (16 * 32);              // [16 n][32 m]
     for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++rs.items) {
       if (A_MN) decode_backward(M, A, p, idx, it); else decode_forward(M, A, p, idx, it);
       mbar_wait(accf_bar, rs.items & 1);
       __syncwarp();
       tc_fence_after();
-      const int m = it.m0 + ew * 32 + lane;
-      const bool mok = m < it.mbound;
+      if (threadIdx.x == 128) tstamp(p.upd, A_MN ? 11 : 9);
       const int acols = p.BN * (p.split ? 2 : 1);
-      for (int s = 0; s < it.nseg; ++s) {
-        float* out = it.out[s] + m;
+      for (int s = 0; s < it.nseg * it.mt; ++s) {
+        const int seg = s / it.mt, mtile = s - seg * it.mt;
+        const int mw = it.m0 + mtile * TC_BM + ew * 32;           // this warp's first m
+        float* __restrict__ outw = it.out[seg] + mw;
         const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(s * acols);
+        const int q = lane & 7, rr = lane >> 3;                    // float4 column q, row offset rr
+        const bool full_m = mw + 32 <= it.mbound;
+        const bool q_ok = mw + 4 * q + 3 < it.mbound;
         for (int c0 = 0; c0 < p.BN; c0 += 16) {
           uint32_t r[16], rl[16];
           tmem_ld16(tb + (uint32_t)c0, r);
           if (p.split) tmem_ld16(tb + (uint32_t)(p.BN + c0), rl);
-          if (mok && !p.dbg_nostore) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const float v = p.split ? __uint_as_float(r[j]) + __uint_as_float(rl[j]) : __uint_as_float(r[j]);
-              if (c0 + j < p.k) out[(int64_t)(c0 + j) * it.ldo] = it.scale * v;
+          for (int j = 0; j < 16; ++j)
+            ws[j * 32 + lane] = it.scale * (p.split ? __uint_as_float(r[j]) + __uint_as_float(rl[j]) : __uint_as_float(r[j]));
+          __syncwarp();
+          if (!p.dbg_nostore) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const int jn = 4 * g + rr, n = c0 + jn;
+              if (n < p.k) {
+                const float4 v = *reinterpret_cast<const float4*>(ws + jn * 32 + 4 * q);
+                float* o = outw + (int64_t)n * it.ldo + 4 * q;
+                if (full_m || q_ok) {
+                  __stcg(reinterpret_cast<float4*>(o), v);
+                } else {
+                  const float vv[4] = {v.x, v.y, v.z, v.w};
+                  for (int e = 0; e < 4; ++e)
+                    if (mw + 4 * q + e < it.mbound) o[e] = vv[e];
+                }
+              }
             }
           }
+          __syncwarp();
         }
       }
       tc_fence_before();
@@ -254,8 +300,9 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   uint64_t* acce_bar = accf_bar + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce_bar + 1);
   float* side_scratch = reinterpret_cast<float*>(acce_bar + 3);   // 64 floats for warps 2-3
+  float* epi_stage = reinterpret_cast<float*>(smem + p.bar_off + 512);   // 4 x 2 KB epilogue transpose tiles
   const int warp = threadIdx.x >> 5;
-  constexpr uint32_t NCOLS = 256;   // >= 2 * BN (backward: A-half and B-half accumulators)
+  constexpr uint32_t NCOLS = 256;   // >= tm * BN * (split ? 2 : 1): one accumulator per M tile of an item
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -291,8 +338,12 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   // ---- phase F: forward split-K partials; warps 2-3: G^C, ||v''||^2 partials ----
   if (warp == 2 || warp == 3) {
     if (!p.products_only) gram_c_side(p.upd, threadIdx.x - 64);
+    if (threadIdx.x == 64) tstamp(p.upd, 31);
   } else if (!(p.dbg_mode & 8)) {
-    gemm_phase<EB, false>(maps, A, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
+    gemm_phase<EB, false>(maps, A, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs,
+                          epi_stage);
+    if (threadIdx.x == 32) tstamp(p.upd, 29);
+    if (threadIdx.x == 128) tstamp(p.upd, 30);
   }
   __syncthreads();
   dstamp(p.upd, 2);
@@ -450,7 +501,8 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   if (warp == 2 || warp == 3) {    // warps 2-3: reduce the (now complete) Gram partial rows
     if (!p.products_only) reduce_side(p.upd, threadIdx.x - 64, side_scratch);
   } else if (!(p.dbg_mode & 32)) {
-    gemm_phase<EB, true>(maps, A, p, p.mtB[0] + p.mtB[1], ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs);
+    gemm_phase<EB, true>(maps, A, p, 2 * (p.mtB[0] + p.mtB[1]), ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs,
+                         epi_stage);
   }
   tc_fence_before();
   if (p.upd.dbg && threadIdx.x >= 128) {
@@ -588,7 +640,18 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
     }
     p.dv[v] = dv[v];
     p.kbF[v] = (int)((dv[v] + ATOM - 1) / ATOM);
-    p.mtB[v] = (int)((dv[v] + TC_BM - 1) / TC_BM);
+  }
+  // M tiles per work item: 2 where the grid stays busy (the B-operand tile of
+  // each K step then serves 256 rows / columns), else 1
+  {
+    const int fixed = getenv("GEIG_TM") ? std::max(1, std::min(2, atoi(getenv("GEIG_TM")))) : 0;
+    int nB2 = 0;
+    for (int v = 0; v < 2; ++v) nB2 += 2 * (int)((dv[v] + 2 * TC_BM - 1) / (2 * TC_BM));
+    p.tmB = fixed ? fixed : (2 * nB2 >= grid_ctas ? 2 : 1);
+    p.tmF = fixed ? fixed : (rows >= 8 * TC_BM ? 2 : 1);
+    if (getenv("GEIG_TMF")) p.tmF = std::max(1, std::min(2, atoi(getenv("GEIG_TMF"))));   // developer A/B knobs
+    if (getenv("GEIG_TMB")) p.tmB = std::max(1, std::min(2, atoi(getenv("GEIG_TMB"))));
+    for (int v = 0; v < 2; ++v) p.mtB[v] = (int)((dv[v] + p.tmB * TC_BM - 1) / (p.tmB * TC_BM));
   }
   {
     const float* src[4] = {upd.V, AV, upd.AUX, BV};
@@ -598,7 +661,7 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   }
   p.rows = rows; p.h = h; p.k = k; p.BN = t.BN; p.d = t.d; p.ldz = t.ldz; p.hpad = t.hpad;
   p.scale = scale;
-  p.mtF = (rows + TC_BM - 1) / TC_BM;
+  p.mtF = (rows + p.tmF * TC_BM - 1) / (p.tmF * TC_BM);
   p.splitsF = std::min(TC_MAX_SPLITS, choose_splits_deep(2 * p.mtF, std::min(p.kbF[0], p.kbF[1]), grid_ctas));
   p.kbB = (h + ATOM - 1) / ATOM;
   p.idescF = make_idesc(eb, false, t.BN * (t.splitb ? 2 : 1), TC_BM);
@@ -617,10 +680,13 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.l2_keep = getenv("GEIG_L2_KEEP") ? 1 : 0;   // measured: evict-last on a whole view thrashes the state arrays (slower)
   p.dbg_nostore = getenv("GEIG_DBG_NOSTORE") ? 1 : 0;   // developer: drop GEMM epilogue stores (timing only)
   p.dbg_mode = getenv("GEIG_DBG_MODE") ? atoi(getenv("GEIG_DBG_MODE")) : 0;   // developer timing knobs (wrong results)
-  const size_t stage_bytes = TC_BM * 128 + (size_t)t.BN * 128 * (t.splitb ? 2 : 1);
+  const size_t stage_bytes = (size_t)std::max(p.tmF, p.tmB) * TC_BM * 128 + (size_t)t.BN * 128 * (t.splitb ? 2 : 1);
+  if ((size_t)std::max(p.tmF, p.tmB) * t.BN * (t.splitb ? 2 : 1) > 256)
+    return tc_fail(GEIG_ERR_UNSUPPORTED, "fused step: accumulators exceed the TMEM allocation");
   p.stages = (int)std::min<size_t>(TC_MAX_STAGES, (200 * 1024) / stage_bytes);
   p.bar_off = (uint32_t)((std::max((size_t)p.stages * stage_bytes, upd_bytes) + 15) & ~(size_t)15);
-  const size_t smem = 1024 + p.bar_off + (2 * TC_MAX_STAGES + 4) * 8 + 64 * 4;
+  static_assert((2 * TC_MAX_STAGES + 4) * 8 + 64 * 4 <= 512, "barrier + scratch area");
+  const size_t smem = 1024 + p.bar_off + 512 + 4 * 16 * 32 * 4;
   if (smem > 227 * 1024) return tc_fail(GEIG_ERR_UNSUPPORTED, "fused step: shared memory budget exceeded");
   static bool attr = false;
   if (!attr) {

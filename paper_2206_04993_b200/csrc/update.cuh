@@ -87,6 +87,16 @@ __device__ __forceinline__ void dstamp(const UpdateArgs& p, int slot) {
   }
 }
 
+// developer timeline stamp by the calling thread (role threads of the fused kernel)
+__device__ __forceinline__ void tstamp(const UpdateArgs& p, int slot) {
+  if (p.dbg) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) :: "memory");
+    p.dbg[(size_t)blockIdx.x * 64 + slot] = t;
+    p.dbg[(size_t)blockIdx.x * 64 + 32 + slot] = clock64();
+  }
+}
+
 // bf16 "x2" shadow of v: hi = bf16(v), lo = bf16(v - hi); the products may
 // use hi alone (bf16) or hi + lo (bf16x2, ~fp32-accurate operand).
 __device__ __forceinline__ void store_vbf4(__nv_bfloat16* hi, int64_t lo_off, size_t o, float4 v) {
