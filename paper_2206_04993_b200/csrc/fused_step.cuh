@@ -400,18 +400,38 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
         for (int q = 0; q < 4; ++q)
 #pragma unroll
           for (int w = 0; w < 4; ++w) z[q][w] = 0.f;
-        for (int sp = 0; sp < p.splitsF; ++sp) {
-          const float* zx = p.Zt + (int64_t)(2 * sp) * vstride + (int64_t)n * p.ldz;
-          const float* zy = zx + vstride;
+        // split-K partials: 4 splits per round, all 16 loads of a round issued
+        // before the adds (one L2 round trip per round, not per split)
+        for (int sp0 = 0; sp0 < p.splitsF; sp0 += 4) {
           if (vec) {
-            const float4 a0 = *reinterpret_cast<const float4*>(zx + r), a1 = *reinterpret_cast<const float4*>(zx + h + r);
-            const float4 c0 = *reinterpret_cast<const float4*>(zy + r), c1 = *reinterpret_cast<const float4*>(zy + h + r);
-            z[0][0] += a0.x; z[0][1] += a0.y; z[0][2] += a0.z; z[0][3] += a0.w;
-            z[1][0] += a1.x; z[1][1] += a1.y; z[1][2] += a1.z; z[1][3] += a1.w;
-            z[2][0] += c0.x; z[2][1] += c0.y; z[2][2] += c0.z; z[2][3] += c0.w;
-            z[3][0] += c1.x; z[3][1] += c1.y; z[3][2] += c1.z; z[3][3] += c1.w;
+            float4 ld[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int sp = sp0 + u;
+              if (sp < p.splitsF) {
+                const float* zx = p.Zt + (int64_t)(2 * sp) * vstride + (int64_t)n * p.ldz;
+                const float* zy = zx + vstride;
+                ld[u][0] = __ldcg(reinterpret_cast<const float4*>(zx + r));
+                ld[u][1] = __ldcg(reinterpret_cast<const float4*>(zx + h + r));
+                ld[u][2] = __ldcg(reinterpret_cast<const float4*>(zy + r));
+                ld[u][3] = __ldcg(reinterpret_cast<const float4*>(zy + h + r));
+              } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) ld[u][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                z[q][0] += ld[u][q].x; z[q][1] += ld[u][q].y; z[q][2] += ld[u][q].z; z[q][3] += ld[u][q].w;
+              }
           } else {
-            z[0][0] += zx[r]; z[1][0] += zx[h + r]; z[2][0] += zy[r]; z[3][0] += zy[h + r];
+            for (int sp = sp0; sp < min(sp0 + 4, p.splitsF); ++sp) {
+              const float* zx = p.Zt + (int64_t)(2 * sp) * vstride + (int64_t)n * p.ldz;
+              const float* zy = zx + vstride;
+              z[0][0] += zx[r]; z[1][0] += zx[h + r]; z[2][0] += zy[r]; z[3][0] += zy[h + r];
+            }
           }
         }
         // Zb planes: 0 = y1 (-> AV_x), 1 = x2 (-> BV_x), 2 = x1 (-> AV_y), 3 = y2 (-> BV_y)

@@ -465,7 +465,8 @@ update_kernel(UpdateArgs p) {
 constexpr int UPD_RES_WMAX = 168;   // max columns per CTA (smem: 4 x 64 x 172 x 4 B + tables)
 constexpr int UPD_GT = 72;          // 8x4 lower-triangle Gram tiles of a 64 x 64 table
 constexpr int UPD_GS = 3;           // column slices of the Gram phase (UPD_GT * UPD_GS <= UPD_THREADS)
-constexpr int UPD_AUXF = 64 * 64 + 4 * 64 + 8 * 32 + 64 * 65 + 128;   // Lt | N, 1/s^2, D1, D2 | red | raw
+constexpr int UPD_LTS = 72;         // Lt row stride: the tf32 A fragments (rows t, t+4 x cols g) are bank-conflict free
+constexpr int UPD_AUXF = 64 * UPD_LTS + 4 * 64 + 8 * 32 + 64 * 65 + 128;   // Lt | N, 1/s^2, D1, D2 | red | raw
 constexpr int UPD_GREDF = (UPD_GS - 1) * UPD_GT * 64;                // Gram slice partials (aliases the above)
 
 __host__ __device__ constexpr size_t upd_res_smem_floats(int W) {
@@ -475,6 +476,20 @@ __host__ __device__ constexpr size_t upd_res_smem_floats(int W) {
 __host__ __device__ constexpr int upd_raw_floats_res(int k) { return 2 * ((k * (k + 1) / 2 + k + 3) & ~3); }   // 2 padded halves
 
 __device__ __forceinline__ int tri_index(int i, int j) { return i * (i + 1) / 2 + j; }
+
+// 3xTF32 operand split: x ~ hi + lo with hi = tf32(x), lo = tf32(x - hi)
+__device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+  const float r = x - __uint_as_float(hi);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+// d += a b, m16n8k8, A row-major (tf32 x4), B col-major (tf32 x2), fp32 accumulators
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
 
 // ---------------------------------------------------------------------------
 // Fused step side work for the otherwise idle warps 2-3 (64 threads, no smem
@@ -595,8 +610,8 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   float* At = Vt + 64 * S;
   float* Ct = At + 64 * S;
   float* Bt = Ct + 64 * S;
-  float* Lt = Bt + 64 * S;                       // [64][64] Lt[j][i]
-  float* Ns = Lt + 64 * 64;
+  float* Lt = Bt + 64 * S;                       // [64][UPD_LTS] Lt[j][i]
+  float* Ns = Lt + 64 * UPD_LTS;
   float* IS2 = Ns + 64;                          // 1 / s_j^2
   float* D1s = IS2 + 64;
   float* D2s = D1s + 64;
@@ -610,6 +625,13 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   stamp(p, 0);
 
   // ---------------- stage the four tiles once ----------------
+  const bool early_raw = um && (PRE == 1 || (PRE < 0 && p.pre_reduced));
+  if (early_raw) {
+    // pre-reduced tables: stage them first (the coefficients need them
+    // before the tiles; the tiles' TMA then streams behind them)
+    for (int e = 4 * tid; e < pstride; e += 4 * UPD_THREADS) cp_async16(rs + e, p.raw + e, 16);
+    cp_async_commit();
+  }
   if (um) {
     if (tid == 0) {
       tc::mbar_init(tbar, 1);
@@ -623,7 +645,9 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
       for (int a = 0; a < 4; ++a) tc::tma_load_2d(dst[a], &um->t[a], tbar, (int)c0, 0);
     }
     __syncthreads();
-    tc::mbar_wait(tbar, 0);
+    // pre-reduced tables (fused step): the coefficients do not read the
+    // tiles, so their staging overlaps the coefficient phase (wait below)
+    if (!(PRE == 1 || (PRE < 0 && p.pre_reduced))) tc::mbar_wait(tbar, 0);
   } else {
     auto stage = [&](float* dst, const float* src) {
       if (VEC) {
@@ -881,8 +905,10 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   // the reduced raw tables are staged into shared memory with one burst of
   // independent 16-byte async copies, then the coefficients are formed from smem.
   {
-    for (int e = 4 * tid; e < pstride; e += 4 * UPD_THREADS) cp_async16(rs + e, p.raw + e, 16);
-    cp_async_commit();
+    if (!early_raw) {
+      for (int e = 4 * tid; e < pstride; e += 4 * UPD_THREADS) cp_async16(rs + e, p.raw + e, 16);
+      cp_async_commit();
+    }
     cp_async_wait<0>();
     __syncthreads();
     dstamp(p, 19);
@@ -921,7 +947,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
       const int j = e >> 6, i = e & 63;
       float l = 0.f;
       if (i < k && j < i) l = D1s[i] * (Ns[i] * Ns[j] * rA[tri_index(i, j)]) * IS2[j];
-      Lt[e] = l;
+      Lt[j * UPD_LTS + i] = l;
     }
     // c_i = sum_{j<i} G^A_ij G^C_ij / s_j^2 (4 threads per i), D2_i = G^A_ii - c_i
     {
@@ -954,90 +980,38 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   }
   dstamp(p, 13);
 
+  if (um && (PRE == 1 || (PRE < 0 && p.pre_reduced))) tc::mbar_wait(tbar, 0);   // tiles staged
+  dstamp(p, 21);
+
   // ---------------- phase 3b: grad, v'' and [Bv]' from the resident tiles ----------------
-  // Work item = (row-group pair, column quad): the triangular penalty sum
-  // sum_{j<i} L_ij [Bv]_j costs ~i per row, so row groups g (rows 4g..4g+3)
-  // and 15-g are paired for equal cost per item; both share the [Bv]_j loads.
+  // 3b-1: the triangular penalty sums P_ix = sum_{j<i} L_ij [Bv]_jx (fp32
+  // FMA).  Work item = (row-group pair, column quad): rows 4g..4g+3 and
+  // 60-4g..63-4g (equal triangular cost per item), 4 columns; per j a float4
+  // of [Bv] and two (near-broadcast) float4 of L feed 32 FMAs, j unrolled by
+  // 4 so the shared loads of the next iterations overlap the FMAs.  The item
+  // then forms the Alg. 2 direction
+  //   grad_ix = D1_i AV_ix - D2_i BV_ix - P_ix
+  // in place of the AV tile (each element owned by one thread).
+  // 3b-2: v'' = n_i v + eta grad (or Adam), [Bv]' = [Bv] + gamma (n_i BV - [Bv]),
+  // float4 over (row, column quad), coalesced stores.
   {
-    const int nq = W / 4;
-    auto finish = [&](int i0, const float (&acc)[4][4], int q) {
-      const int64_t gx = c0 + 4 * q;
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int i = i0 + a;
-        if (i < k && gx < c1) {
-          const float4 av = *reinterpret_cast<const float4*>(At + i * S + 4 * q);
-          const float4 bv = *reinterpret_cast<const float4*>(Bt + i * S + 4 * q);
-          const float4 vv = *reinterpret_cast<const float4*>(Vt + i * S + 4 * q);
-          const float4 xa = *reinterpret_cast<const float4*>(Ct + i * S + 4 * q);
-          const float ni = Ns[i];
-          const float d1 = D1s[i] * ni, d2 = D2s[i] * ni;
-          float4 vn, an;
-          if (p.adam) {
-            // Appendix H: Adam ascent on v_i with the Alg. 2 direction as the gradient
-            const size_t o0 = (size_t)i * d + gx;
-            float4 g;
-            g.x = d1 * av.x - d2 * bv.x - acc[a][0];
-            g.y = d1 * av.y - d2 * bv.y - acc[a][1];
-            g.z = d1 * av.z - d2 * bv.z - acc[a][2];
-            g.w = d1 * av.w - d2 * bv.w - acc[a][3];
-            float4 m4 = *reinterpret_cast<const float4*>(p.am + o0);
-            float4 s4 = *reinterpret_cast<const float4*>(p.as + o0);
-            const float tt = (float)(p.adam_t0 + step + 1);
-            const float c1 = 1.f / (1.f - powf(p.b1, tt)), c2 = 1.f / (1.f - powf(p.b2, tt));
-            auto upd = [&](float gv, float& mv, float& sv, float v) {
-              mv = p.b1 * mv + (1.f - p.b1) * gv;
-              sv = p.b2 * sv + (1.f - p.b2) * gv * gv;
-              return v + p.eta * (mv * c1) / (sqrtf(sv * c2) + p.eps);
-            };
-            vn.x = upd(g.x, m4.x, s4.x, ni * vv.x);
-            vn.y = upd(g.y, m4.y, s4.y, ni * vv.y);
-            vn.z = upd(g.z, m4.z, s4.z, ni * vv.z);
-            vn.w = upd(g.w, m4.w, s4.w, ni * vv.w);
-            *reinterpret_cast<float4*>(p.am + o0) = m4;
-            *reinterpret_cast<float4*>(p.as + o0) = s4;
-          } else {
-            vn.x = ni * vv.x + p.eta * (d1 * av.x - d2 * bv.x - acc[a][0]);
-            vn.y = ni * vv.y + p.eta * (d1 * av.y - d2 * bv.y - acc[a][1]);
-            vn.z = ni * vv.z + p.eta * (d1 * av.z - d2 * bv.z - acc[a][2]);
-            vn.w = ni * vv.w + p.eta * (d1 * av.w - d2 * bv.w - acc[a][3]);
-          }
-          an.x = xa.x + p.gamma * (ni * bv.x - xa.x);
-          an.y = xa.y + p.gamma * (ni * bv.y - xa.y);
-          an.z = xa.z + p.gamma * (ni * bv.z - xa.z);
-          an.w = xa.w + p.gamma * (ni * bv.w - xa.w);
-          const size_t o = (size_t)i * d + gx;
-          if (VEC && gx + 3 < c1) {
-            *reinterpret_cast<float4*>(p.V + o) = vn;
-            *reinterpret_cast<float4*>(p.AUX + o) = an;
-            if (p.Vbf) store_vbf4(p.Vbf, (int64_t)k * d, o, vn);
-          } else {
-            const float vs[4] = {vn.x, vn.y, vn.z, vn.w}, as[4] = {an.x, an.y, an.z, an.w};
-            for (int t = 0; t < 4; ++t)
-              if (gx + t < c1) {
-                p.V[o + t] = vs[t];
-                p.AUX[o + t] = as[t];
-                if (p.Vbf) store_vbf1(p.Vbf, (int64_t)k * d, o + t, vs[t]);
-              }
-          }
-        }
-      }
-    };
-    for (int item = tid; item < 8 * nq; item += UPD_THREADS) {
-      const int pr = item / nq, q = item - pr * nq;
-      const int iA = 4 * pr, iB = 4 * (15 - pr);
+    const int nq4 = W / 4;
+    for (int item = tid; item < 8 * nq4; item += UPD_THREADS) {
+      const int pr = item / nq4, q = item - pr * nq4;
+      const int iA = 4 * pr, iB = 60 - 4 * pr;
       const int jA = min(iA + 3, k), jB = min(iB + 3, k);   // L_ij = 0 for j >= i
       float accA[4][4], accB[4][4];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) accA[a][b] = accB[a][b] = 0.f;
-      int j = 0;
-#pragma unroll 1
+      const float* cp = Ct + 4 * q;
+      int j = (p.dbg_mode & 512) ? jB : 0;   // developer: skip the penalty sums (timing only)
+#pragma unroll 4
       for (; j < jA; ++j) {
-        const float4 x = *reinterpret_cast<const float4*>(Ct + j * S + 4 * q);
-        const float4 la = *reinterpret_cast<const float4*>(Lt + j * 64 + iA);
-        const float4 lb = *reinterpret_cast<const float4*>(Lt + j * 64 + iB);
+        const float4 x = *reinterpret_cast<const float4*>(cp + j * S);
+        const float4 la = *reinterpret_cast<const float4*>(Lt + j * UPD_LTS + iA);
+        const float4 lb = *reinterpret_cast<const float4*>(Lt + j * UPD_LTS + iB);
         const float xv[4] = {x.x, x.y, x.z, x.w}, lav[4] = {la.x, la.y, la.z, la.w}, lbv[4] = {lb.x, lb.y, lb.z, lb.w};
 #pragma unroll
         for (int a = 0; a < 4; ++a)
@@ -1047,18 +1021,101 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
             accB[a][b] = fmaf(lbv[a], xv[b], accB[a][b]);
           }
       }
-#pragma unroll 1
+#pragma unroll 4
       for (; j < jB; ++j) {
-        const float4 x = *reinterpret_cast<const float4*>(Ct + j * S + 4 * q);
-        const float4 lb = *reinterpret_cast<const float4*>(Lt + j * 64 + iB);
+        const float4 x = *reinterpret_cast<const float4*>(cp + j * S);
+        const float4 lb = *reinterpret_cast<const float4*>(Lt + j * UPD_LTS + iB);
         const float xv[4] = {x.x, x.y, x.z, x.w}, lbv[4] = {lb.x, lb.y, lb.z, lb.w};
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
           for (int b = 0; b < 4; ++b) accB[a][b] = fmaf(lbv[a], xv[b], accB[a][b]);
       }
-      finish(iA, accA, q);
-      finish(iB, accB, q);
+      auto direction = [&](int i0, const float (&acc)[4][4]) {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int i = i0 + a;
+          if (i < k) {
+            const float ni = Ns[i];
+            const float d1 = D1s[i] * ni, d2 = D2s[i] * ni;
+            float4* ap = reinterpret_cast<float4*>(At + i * S + 4 * q);
+            const float4 av = *ap;
+            const float4 bv = *reinterpret_cast<const float4*>(Bt + i * S + 4 * q);
+            float4 gq;
+            gq.x = d1 * av.x - d2 * bv.x - acc[a][0];
+            gq.y = d1 * av.y - d2 * bv.y - acc[a][1];
+            gq.z = d1 * av.z - d2 * bv.z - acc[a][2];
+            gq.w = d1 * av.w - d2 * bv.w - acc[a][3];
+            *ap = gq;
+          }
+        }
+      };
+      direction(iA, accA);
+      direction(iB, accB);
+    }
+    __syncthreads();
+    if (tid == 0) dstamp(p, 22);
+    const int nq = W / 4;
+    for (int e = tid; e < k * nq; e += UPD_THREADS) {
+      const int i = e / nq, q = e - (e / nq) * nq;
+      const int64_t gx = c0 + 4 * q;
+      if (gx >= c1) continue;
+      const float4 gr = *reinterpret_cast<const float4*>(At + i * S + 4 * q);   // grad (3b-1)
+      const float4 bv = *reinterpret_cast<const float4*>(Bt + i * S + 4 * q);
+      const float4 vv = *reinterpret_cast<const float4*>(Vt + i * S + 4 * q);
+      const float4 xa = *reinterpret_cast<const float4*>(Ct + i * S + 4 * q);
+      const float ni = Ns[i];
+      float4 vn, an;
+      if (p.adam) {
+        // Appendix H: Adam ascent on v_i with the Alg. 2 direction as the gradient
+        const size_t o0 = (size_t)i * d + gx;
+        float4 m4 = *reinterpret_cast<const float4*>(p.am + o0);
+        float4 s4 = *reinterpret_cast<const float4*>(p.as + o0);
+        const float tt = (float)(p.adam_t0 + step + 1);
+        const float cb1 = 1.f / (1.f - powf(p.b1, tt)), cb2 = 1.f / (1.f - powf(p.b2, tt));
+        auto upd = [&](float gv, float& mv, float& sv, float v) {
+          mv = p.b1 * mv + (1.f - p.b1) * gv;
+          sv = p.b2 * sv + (1.f - p.b2) * gv * gv;
+          return v + p.eta * (mv * cb1) / (sqrtf(sv * cb2) + p.eps);
+        };
+        vn.x = upd(gr.x, m4.x, s4.x, ni * vv.x);
+        vn.y = upd(gr.y, m4.y, s4.y, ni * vv.y);
+        vn.z = upd(gr.z, m4.z, s4.z, ni * vv.z);
+        vn.w = upd(gr.w, m4.w, s4.w, ni * vv.w);
+        if (VEC && gx + 3 < c1) {
+          *reinterpret_cast<float4*>(p.am + o0) = m4;
+          *reinterpret_cast<float4*>(p.as + o0) = s4;
+        } else {
+          const float ms[4] = {m4.x, m4.y, m4.z, m4.w}, ss[4] = {s4.x, s4.y, s4.z, s4.w};
+          for (int tq = 0; tq < 4; ++tq)
+            if (gx + tq < c1) { p.am[o0 + tq] = ms[tq]; p.as[o0 + tq] = ss[tq]; }
+        }
+      } else {
+        vn.x = ni * vv.x + p.eta * gr.x;
+        vn.y = ni * vv.y + p.eta * gr.y;
+        vn.z = ni * vv.z + p.eta * gr.z;
+        vn.w = ni * vv.w + p.eta * gr.w;
+      }
+      an.x = xa.x + p.gamma * (ni * bv.x - xa.x);
+      an.y = xa.y + p.gamma * (ni * bv.y - xa.y);
+      an.z = xa.z + p.gamma * (ni * bv.z - xa.z);
+      an.w = xa.w + p.gamma * (ni * bv.w - xa.w);
+      const size_t o = (size_t)i * d + gx;
+      if (p.dbg_mode & 256) {   // developer: no state write-back (timing only)
+        if (vn.x == 12345.f && an.x == 12345.f) p.V[o] = 0.f;
+      } else if (VEC && gx + 3 < c1) {
+        *reinterpret_cast<float4*>(p.V + o) = vn;
+        *reinterpret_cast<float4*>(p.AUX + o) = an;
+        if (p.Vbf) store_vbf4(p.Vbf, (int64_t)k * d, o, vn);
+      } else {
+        const float vs[4] = {vn.x, vn.y, vn.z, vn.w}, as[4] = {an.x, an.y, an.z, an.w};
+        for (int tq = 0; tq < 4; ++tq)
+          if (gx + tq < c1) {
+            p.V[o + tq] = vs[tq];
+            p.AUX[o + tq] = as[tq];
+            if (p.Vbf) store_vbf1(p.Vbf, (int64_t)k * d, o + tq, vs[tq]);
+          }
+      }
     }
   }
   stamp(p, 3);

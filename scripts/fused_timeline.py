@@ -20,7 +20,7 @@ lib = geig._lib
 lib.geig_debug_set_tc_stamps.argtypes = [ctypes.c_void_p]
 names = {0: "launch", 1: "setup", 2: "F done", 3: "F sync", 4: "S done", 5: "S sync", 6: "B done", 7: "B sync",
          8: "U staged", 9: "F accf", 10: "U sync1", 11: "B accf", 12: "U sync2", 13: "U coef", 14: "U update",
-         15: "B fence0", 16: "B epi fence", 17: "B epi end", 19: "coef raw", 20: "coef N", 21: "coef L", 22: "gram rep0", 23: "S zinit", 24: "S zsum", 25: "S gram", 26: "S tri", 27: "Uc loop", 28: "Uc pst", 29: "F mma end", 30: "F epi end", 31: "F side end"}
+         15: "B fence0", 16: "B epi fence", 17: "B epi end", 19: "coef raw", 20: "coef N", 21: "U tiles", 22: "U penalty", 23: "S zinit", 24: "S zsum", 25: "S gram", 26: "S tri", 27: "Uc loop", 28: "Uc pst", 29: "F mma end", 30: "F epi end", 31: "F side end"}
 for it in range(50):
     geig.geig_step_cca(s.h, X[:b], Y[:b], b, cfg.eta, cfg.gamma)
 torch.cuda.synchronize()
@@ -39,7 +39,7 @@ for j, nm in names.items():
     col = ((t[:, j] - t0).double() / 1e3).tolist()
     ck = ((t[:, 32 + j] - t[:, 32]).double() / MHZ).tolist() if j != 15 else [0]
     print(f"  {j:2d} {nm:12s} {min(col):7.2f} {statistics.median(col):7.2f} {max(col):7.2f} | {statistics.median(ck):7.2f}")
-order = [0, 1, 2, 3, 23, 24, 25, 26, 4, 5, 17, 6, 7, 8, 27, 28, 9, 10, 11, 12, 19, 20, 13, 14]
+order = [0, 1, 2, 3, 23, 24, 25, 26, 4, 5, 17, 6, 7, 8, 27, 28, 9, 10, 11, 12, 19, 20, 13, 21, 22, 14]
 prev = None
 out = []
 for j in order:

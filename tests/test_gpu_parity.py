@@ -250,6 +250,24 @@ def test_fused_step_bf16(geig, cfg_idx, rows, k, dx, dy):
     _assert(errs, 1e-2)
 
 
+@pytest.mark.parametrize("cfg_idx,rows,k,dx,dy,math", [(2, 1100, 24, 600, 328, "bf16"),
+                                                       (2, 1200, 64, 400, 272, "bf16x2"),
+                                                       (3, 4096, 16, 8192, 8192, "bf16x2")])
+@pytest.mark.parametrize("tm", ["1", "2"])
+def test_fused_step_forced_m_tiles(geig, monkeypatch, cfg_idx, rows, k, dx, dy, math, tm):
+    """Work items of two 128-row M tiles sharing each B-operand tile (the
+    default at full size) and of one, forced on ragged shapes: a last item
+    with a partial second M tile, a last item with a single M tile."""
+    monkeypatch.setenv("GEIG_TM", tm)
+    errs, _ = check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math=math, use_step=True)
+    if math == "bf16":
+        _assert(errs, 1e-2)
+    else:
+        step = errs.pop("step")
+        _assert(errs, 1e-4)
+        assert step < 1e-3, errs
+
+
 def test_fused_step_matches_staged_path(geig):
     """Same inputs through the staged path (products + update) and the fused
     kernel: the states agree to bf16-product rounding order."""
