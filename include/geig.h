@@ -67,8 +67,8 @@ typedef enum { GEIG_DENSE = 0, GEIG_CCA = 1 } geig_problem;
  *  GEIG_MATH_F32   : FFMA fp32 on CUDA cores (exactness-check variant)
  *  GEIG_MATH_BF16  : tcgen05 tensor cores, bf16 operands, fp32 accumulate
  *  GEIG_MATH_TF32  : tcgen05 tensor cores, tf32 operands, fp32 accumulate
- *                    (dense GEP only; geig_create returns
- *                    GEIG_ERR_UNSUPPORTED for CCA)
+ *                    (fp32 data; the CCA backward reads X^T as an MN-major
+ *                    tf32 operand in the 128-byte / 32-byte-chunk swizzle)
  *  GEIG_MATH_3XTF32: tcgen05 tf32 with hi/lo split (not built:
  *                    GEIG_ERR_UNSUPPORTED)
  *  GEIG_MATH_BF16X2: tcgen05 bf16 with the V and Z operands carried as

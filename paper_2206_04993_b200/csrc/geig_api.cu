@@ -101,10 +101,6 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
   if ((math == GEIG_MATH_TF32 || math == GEIG_MATH_3XTF32) && data_dtype != GEIG_DATA_F32)
     return fail(GEIG_ERR_ARG, "tf32 math requires fp32 data");
   if (math == GEIG_MATH_3XTF32) return fail(GEIG_ERR_UNSUPPORTED, "GEIG_MATH_3XTF32 is not built");
-  if (problem == GEIG_CCA && math == GEIG_MATH_TF32)
-    return fail(GEIG_ERR_UNSUPPORTED,
-                "tf32 CCA is not built: the backward product reads X^T as an MN-major tf32 tcgen05 operand, "
-                "which this build does not support; use GEIG_MATH_F32 (fp32 data) or GEIG_MATH_BF16X2 (bf16 data)");
   if (!(rho >= 0.0)) return fail(GEIG_ERR_ARG, "rho must be >= 0");
   if (problem == GEIG_CCA && max_rows < 2) return fail(GEIG_ERR_ARG, "max_rows must be >= 2");
   if (k > dx + dy) return fail(GEIG_ERR_ARG, "k > d");

@@ -123,13 +123,16 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 }
 
 // Shared-memory matrix descriptor, SWIZZLE_128B, sm_100 version bits = 1.
-__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// layout: 2 = SWIZZLE_128B; 1 = SWIZZLE_128B_BASE32B (128-byte rows swizzled in
+// 32-byte chunks, 4-row atoms): the MN-major layout of 32-bit (tf32) operands,
+// written by TMA with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)layout << 61;
   return d;
 }
 
@@ -271,7 +274,10 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
           for (int kk = 0; kk < BK / UK; ++kk) {
             uint64_t ad, bd;
             if constexpr (A_MN) {
-              ad = make_sdesc(sa + kk * UK * 128, BK * 128, 1024);
+              // MN-major A: 16-bit types in 128B-swizzle atoms of 8 rows (SBO 1024 B);
+              // tf32 in 128B / 32B-chunk atoms of 4 rows (SBO 512 B)
+              ad = EB == 2 ? make_sdesc(sa + kk * UK * 128, BK * 128, 1024)
+                           : make_sdesc(sa + kk * UK * 128, BK * 128, 512, 1);
             } else {
               ad = make_sdesc(sa + kk * 32, 16, 1024);
             }
@@ -475,7 +481,7 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D row-major tensor [outer][inner] with row stride `stride_el` elements.
 inline bool make_map(CUtensorMap* m, const void* base, int eb, int64_t inner, int64_t outer, int64_t stride_el,
-                     int box_inner, int box_outer, bool swizzle = true) {
+                     int box_inner, int box_outer, bool swizzle = true, bool atom32 = false) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
@@ -484,7 +490,9 @@ inline bool make_map(CUtensorMap* m, const void* base, int eb, int64_t inner, in
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(m, eb == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                   const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  swizzle ? (atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B)
+                          : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -676,7 +684,7 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
       for (int s = 0; s < 2; ++s) {
         const char* xb = (const char*)Xv[v] + (int64_t)s * h * dv[v] * eb;
         const char* zb = (const char*)t.Zb + (int64_t)(v * 2 + s) * plane * eb;
-        if (!make_map(&maps.a[v * 2 + s], xb, eb, dv[v], h, dv[v], ATOM, ATOM) ||
+        if (!make_map(&maps.a[v * 2 + s], xb, eb, dv[v], h, dv[v], ATOM, ATOM, true, eb == 4) ||
             !make_map(&maps.b[v * 2 + s], zb, eb, h, k, t.hpad, ATOM, t.BN))
           return tc_fail(GEIG_ERR_CUDA, "tensor map encode (backward) failed");
         if (t.splitb && !make_map(&maps.blo[v * 2 + s], zb + 4 * plane * eb, eb, h, k, t.hpad, ATOM, t.BN))

@@ -78,6 +78,14 @@ def test_converges_smooth_alg3_bf16x2(geig):
     assert ang.mean() < 1e-3 and se < 1e-6
 
 
+def test_converges_tf32_cca_variant(geig):
+    """fp32 data on the tf32 tensor cores (measured: 2.3e-4 rad mean angle,
+    subspace error 4e-8): meets the 1e-3 rad bar."""
+    ang, se = _run_cca(geig, "tf32", torch.float32)
+    print("tf32 tcgen05 CCA variant: angles", ang, "mean", ang.mean(), "subspace error", se)
+    assert ang.mean() < 1e-3 and se < 1e-6
+
+
 def test_converges_tf32_dense_config0(geig):
     from oracle import linalg, metrics
     from synth import CONFIGS, dense_gep_small, gaussian_init

@@ -152,9 +152,10 @@ def test_errors_are_loud(geig):
         geig.geig_products_cca(s.h, x, x, 16, 1.0, AV, AV)      # b > max_rows
     s.close()
     # unbuilt arithmetic variants are refused at creation, never silently wrong
-    for math in (geig.GEIG_MATH_TF32, geig.GEIG_MATH_3XTF32):
-        with pytest.raises(geig.GeigError, match="not built"):
-            geig.geig_create(geig.GEIG_CCA, 64, 64, 4, math, geig.GEIG_DATA_F32, 0.1, 64, 0)
+    with pytest.raises(geig.GeigError, match="not built"):
+        geig.geig_create(geig.GEIG_CCA, 64, 64, 4, geig.GEIG_MATH_3XTF32, geig.GEIG_DATA_F32, 0.1, 64, 0)
+    with pytest.raises(geig.GeigError, match="fp32 data"):
+        geig.geig_create(geig.GEIG_CCA, 64, 64, 4, geig.GEIG_MATH_TF32, geig.GEIG_DATA_BF16, 0.1, 64, 0)
 
 
 # --- tensor-core variants (tcgen05): bf16 1e-2, tf32 1e-2 ---------------------
@@ -208,6 +209,22 @@ def _dense_step_check(geig, a, b, k, math, rho, eta, gamma, seed=0, tol=1e-2):
         s.close()
     _assert(errs, tol)
     return errs
+
+
+@pytest.mark.parametrize("cfg_idx,rows,k,dx,dy", [(1, 256, None, None, None), (2, 300, 24, 200, 136),
+                                                  (2, 1024, 16, 784, 784), (3, 2048, 64, 1024, 512),
+                                                  (2, 130, 5, 64, 8)])
+def test_cca_tf32_tcgen05(geig, monkeypatch, cfg_idx, rows, k, dx, dy):
+    """fp32 data on the tf32 tensor cores (staged path): forward K-major, the
+    backward's X^T an MN-major tf32 operand (TMA 128B/32B-chunk swizzle,
+    descriptor layout SWIZZLE_128B_BASE32B).  tf32 keeps 10 mantissa bits:
+    the 1e-2 tensor-core bar; measured ~7e-4."""
+    import tests.gpu_harness as gh
+    cv = gh.cca_views
+    monkeypatch.setattr(gh, "cca_views", lambda *a, **kw: tuple(t.float() for t in cv(*a, **kw)))
+    errs, _ = gh.check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math="tf32")
+    _assert(errs, 1e-2)
+    assert errs["av"] < 3e-3 and errs["bv"] < 3e-3, errs
 
 
 def test_dense_config0_tf32_tcgen05(geig):
