@@ -69,8 +69,11 @@ typedef enum { GEIG_DENSE = 0, GEIG_CCA = 1 } geig_problem;
  *  GEIG_MATH_TF32  : tcgen05 tensor cores, tf32 operands, fp32 accumulate
  *                    (fp32 data; the CCA backward reads X^T as an MN-major
  *                    tf32 operand in the 128-byte / 32-byte-chunk swizzle)
- *  GEIG_MATH_3XTF32: tcgen05 tf32 with hi/lo split (not built:
- *                    GEIG_ERR_UNSUPPORTED)
+ *  GEIG_MATH_3XTF32: tcgen05 tf32 with hi/lo split (fp32 data): the
+ *                    streamed A tile is split in shared memory into
+ *                    tf32_rna(a) + (a - hi), B arrives as hi / lo planes,
+ *                    A_hi B_hi + A_hi B_lo + A_lo B_hi per K step
+ *                    (~fp32-accurate tensor-core products)
  *  GEIG_MATH_BF16X2: tcgen05 bf16 with the V and Z operands carried as
  *                    hi + lo bf16 halves (one N = 2k MMA per K step): the
  *                    bf16 data is exact, so the products are ~fp32-accurate

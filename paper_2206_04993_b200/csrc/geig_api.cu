@@ -100,7 +100,6 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
     return fail(GEIG_ERR_ARG, "GEIG_MATH_BF16/BF16X2 require bf16 data");
   if ((math == GEIG_MATH_TF32 || math == GEIG_MATH_3XTF32) && data_dtype != GEIG_DATA_F32)
     return fail(GEIG_ERR_ARG, "tf32 math requires fp32 data");
-  if (math == GEIG_MATH_3XTF32) return fail(GEIG_ERR_UNSUPPORTED, "GEIG_MATH_3XTF32 is not built");
   if (!(rho >= 0.0)) return fail(GEIG_ERR_ARG, "rho must be >= 0");
   if (problem == GEIG_CCA && max_rows < 2) return fail(GEIG_ERR_ARG, "max_rows must be >= 2");
   if (k > dx + dy) return fail(GEIG_ERR_ARG, "k > d");

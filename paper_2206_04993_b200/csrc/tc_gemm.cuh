@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <string>
+#include <type_traits>
 #include <cstdlib>
 #include "../../include/geig.h"
 
@@ -123,6 +124,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 }
 
 // Shared-memory matrix descriptor, SWIZZLE_128B, sm_100 version bits = 1.
+// tf32 with round-to-nearest (ties away), low 13 mantissa bits zero
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 // layout: 2 = SWIZZLE_128B; 1 = SWIZZLE_128B_BASE32B (128-byte rows swizzled in
 // 32-byte chunks, 4-row atoms): the MN-major layout of 32-bit (tf32) operands,
 // written by TMA with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.
@@ -167,9 +175,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-template <int EB, bool A_MN, int TC_STAGES, bool SPLIT>
+// 3xTF32 (X3, EB = 4, with SPLIT): the A tile is split in shared memory by
+// warps 2-3 into hi = tf32_rna(a) (in place) and lo = a - hi (next to it);
+// the B operand arrives as hi / lo planes; each K step issues
+// A_hi B_hi + A_hi B_lo + A_lo B_hi (the a_lo b_lo term is below fp32 ulp).
+template <int EB, bool A_MN, int TC_STAGES, bool SPLIT, bool X3 = false>
 __global__ void __launch_bounds__(TC_THREADS)
 tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
+  static_assert(!X3 || (EB == 4 && SPLIT), "3xTF32 needs tf32 operands with B hi/lo planes");
   constexpr int ATOM = 128 / EB;           // elements per 128B row
   constexpr int BK = ATOM;                 // K per stage
   constexpr int UK = 32 / EB;              // K per MMA (16 bf16 / 8 tf32)
@@ -181,7 +194,8 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   if (m0 >= Mg) return;
   const int BN = p.BN;
   const uint32_t B_BYTES = (uint32_t)BN * 128;
-  const uint32_t STAGE_BYTES = A_BYTES + B_BYTES * (SPLIT ? 2 : 1);
+  constexpr uint32_t A_TOT = A_BYTES * (X3 ? 2 : 1);   // X3: A hi, A lo
+  const uint32_t STAGE_BYTES = A_TOT + B_BYTES * (SPLIT ? 2 : 1);
 
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned view of the dynamic smem that stays in the shared
@@ -191,7 +205,8 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + TC_STAGES * STAGE_BYTES);
   uint64_t* empty_bar = full_bar + TC_STAGES;
   uint64_t* accum_bar = empty_bar + TC_STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_bar + 1);
+  uint64_t* conv_bar = accum_bar + 1;                    // X3: A split done (2 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(conv_bar + TC_STAGES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t cta_id = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
@@ -215,6 +230,7 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
     for (int s = 0; s < TC_STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
+      if (X3) mbar_init(&conv_bar[s], 2);
     }
     mbar_init(accum_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -245,8 +261,8 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
           const int st = it % TC_STAGES;
           if (it >= TC_STAGES) mbar_wait(&empty_bar[st], ((it / TC_STAGES) + 1) & 1);
           uint8_t* sa = smem + st * STAGE_BYTES;
-          uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(&full_bar[st], STAGE_BYTES);
+          uint8_t* sb = sa + A_TOT;
+          mbar_expect_tx(&full_bar[st], STAGE_BYTES - (A_TOT - A_BYTES));   // X3: A lo is written by warps 2-3
           const int k0 = (kb_beg[s] + j) * BK;
           if constexpr (A_MN) {
 #pragma unroll
@@ -265,11 +281,11 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
         const uint32_t d_tmem = tmem_base + (uint32_t)(s * BN);
         for (int j = 0; j < kb_cnt[s]; ++j, ++it) {
           const int st = it % TC_STAGES;
-          mbar_wait(&full_bar[st], (it / TC_STAGES) & 1);
+          mbar_wait(X3 ? &conv_bar[st] : &full_bar[st], (it / TC_STAGES) & 1);
           if (p.dbg && it == 0) p.dbg[cta_id * 4 + 1] = gtimer();
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + st * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+          const uint32_t sb = sa + A_TOT;
 #pragma unroll
           for (int kk = 0; kk < BK / UK; ++kk) {
             uint64_t ad, bd;
@@ -284,11 +300,35 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
             bd = make_sdesc(sb + kk * 32, 16, 1024);
             umma<EB>(d_tmem, ad, bd, p.idesc, (j > 0 || kk > 0) ? 1u : 0u);
             if constexpr (SPLIT) umma<EB>(d_tmem, ad, make_sdesc(sb + B_BYTES + kk * 32, 16, 1024), p.idesc, 1u);
+            if constexpr (X3) umma<EB>(d_tmem, ad + (uint64_t)(A_BYTES >> 4), bd, p.idesc, 1u);   // A lo x B hi
           }
           umma_commit(&empty_bar[st]);
         }
       }
       umma_commit(accum_bar);
+    } else if (X3 && warp >= 2) {
+      // ---------------- A-tile split (warps 2-3) ----------------
+      const int ct = threadIdx.x - 64;
+      int it = 0;
+      for (int s = 0; s < p.nseg; ++s) {
+        for (int j = 0; j < kb_cnt[s]; ++j, ++it) {
+          const int st = it % TC_STAGES;
+          mbar_wait(&full_bar[st], (it / TC_STAGES) & 1);
+          float4* a = reinterpret_cast<float4*>(smem + st * STAGE_BYTES);
+          float4* al = a + A_BYTES / 16;
+#pragma unroll 4
+          for (int e = ct; e < (int)(A_BYTES / 16); e += 64) {
+            float4 x = a[e], hi, lo;
+            hi.x = tf32_rna(x.x); hi.y = tf32_rna(x.y); hi.z = tf32_rna(x.z); hi.w = tf32_rna(x.w);
+            lo.x = x.x - hi.x; lo.y = x.y - hi.y; lo.z = x.z - hi.z; lo.w = x.w - hi.w;
+            a[e] = hi;
+            al[e] = lo;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tcgen05.mma reads
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv_bar[st]);
+        }
+      }
     }
     // ---------------- epilogue (all 4 warps) ----------------
     // TMEM -> registers -> smem tile[n][m] (the idle pipeline buffers) ->
@@ -369,7 +409,11 @@ __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* dst, float 
 }
 
 template <typename T>
-__device__ __forceinline__ void store4_lo(T* dst, float a, float b, float c, float d) {}
+__device__ __forceinline__ void store4_lo(T* dst, float a, float b, float c, float d);
+template <>
+__device__ __forceinline__ void store4_lo<float>(float* dst, float a, float b, float c, float d) {   // 3xTF32
+  store4<float>(dst, a - tf32_rna(a), b - tf32_rna(b), c - tf32_rna(c), d - tf32_rna(d));
+}
 template <>
 __device__ __forceinline__ void store4_lo<__nv_bfloat16>(__nv_bfloat16* dst, float a, float b, float c, float d) {
   const float ha = __bfloat162float(__float2bfloat16_rn(a)), hb = __bfloat162float(__float2bfloat16_rn(b));
@@ -402,10 +446,12 @@ __global__ void zshuffle_kernel(const float* __restrict__ Zp, T* __restrict__ Zb
         y1.x += d.x; y1.y += d.y; y1.z += d.z; y1.w += d.w;
       }
       const int64_t o = (int64_t)n * hpad + r;
-      store4<T>(Zb + 0 * plane + o, y0.x, y0.y, y0.z, y0.w);   // view x, half 0
-      store4<T>(Zb + 1 * plane + o, x1.x, x1.y, x1.z, x1.w);   // view x, half 1
-      store4<T>(Zb + 2 * plane + o, x0.x, x0.y, x0.z, x0.w);   // view y, half 0
-      store4<T>(Zb + 3 * plane + o, y1.x, y1.y, y1.z, y1.w);   // view y, half 1
+      const bool x3 = std::is_same<T, float>::value && lo;     // 3xTF32: hi planes hold tf32_rna(z)
+      auto hv = [&](float v) { return x3 ? tf32_rna(v) : v; };
+      store4<T>(Zb + 0 * plane + o, hv(y0.x), hv(y0.y), hv(y0.z), hv(y0.w));   // view x, half 0
+      store4<T>(Zb + 1 * plane + o, hv(x1.x), hv(x1.y), hv(x1.z), hv(x1.w));   // view x, half 1
+      store4<T>(Zb + 2 * plane + o, hv(x0.x), hv(x0.y), hv(x0.z), hv(x0.w));   // view y, half 0
+      store4<T>(Zb + 3 * plane + o, hv(y1.x), hv(y1.y), hv(y1.z), hv(y1.w));   // view y, half 1
       if (lo) {                                                 // bf16x2 low halves
         store4_lo<T>(Zb + 4 * plane + o, y0.x, y0.y, y0.z, y0.w);
         store4_lo<T>(Zb + 5 * plane + o, x1.x, x1.y, x1.z, x1.w);
@@ -425,13 +471,12 @@ __global__ void zshuffle_kernel(const float* __restrict__ Zp, T* __restrict__ Zb
       x0 += zx[r]; x1 += zx[h + r]; y0 += zy[r]; y1 += zy[h + r];
     }
     const int64_t o = (int64_t)n * hpad + r;
-    Zb[0 * plane + o] = (T)y0;
-    Zb[1 * plane + o] = (T)x1;
-    Zb[2 * plane + o] = (T)x0;
-    Zb[3 * plane + o] = (T)y1;
-    if (lo) {
-      const float v4[4] = {y0, x1, x0, y1};
-      for (int q = 0; q < 4; ++q) Zb[(4 + q) * plane + o] = (T)(v4[q] - (float)(T)v4[q]);
+    const float v4[4] = {y0, x1, x0, y1};
+    const bool x3 = std::is_same<T, float>::value && lo;     // 3xTF32: hi = tf32_rna(z), lo = z - hi
+    for (int q = 0; q < 4; ++q) {
+      const float hi = x3 ? tf32_rna(v4[q]) : (float)(T)v4[q];
+      Zb[q * plane + o] = x3 ? (T)hi : (T)v4[q];
+      if (lo) Zb[(4 + q) * plane + o] = (T)(v4[q] - hi);
     }
   }
 }
@@ -450,6 +495,8 @@ struct TcPlan {
   CUtensorMap* xm_host = nullptr;   // pinned staging of the same
   int xm_cap = 0;                   // steps of capacity
   cudaEvent_t xm_ev = nullptr;      // last copy of the staging buffer
+  int x3 = 0;                       // 3xTF32 products (tf32 plan with hi/lo operands)
+  float* Vx3 = nullptr;             // 3xTF32: [hi plane | lo plane] of V (2 x k x d fp32)
 };
 
 inline unsigned long long*& dbg_ptr() {
@@ -503,18 +550,18 @@ inline uint32_t make_idesc(int eb, bool a_mn, int N, int M) {
          ((uint32_t)(M >> 4) << 24);
 }
 
-inline size_t smem_bytes(int BN, int stages, bool split = false) {
-  return 1024 + (size_t)stages * (TC_BM * 128 + (size_t)BN * 128 * (split ? 2 : 1)) + 256;
+inline size_t smem_bytes(int BN, int stages, bool split = false, bool x3 = false) {
+  return 1024 + (size_t)stages * (TC_BM * 128 * (x3 ? 2 : 1) + (size_t)BN * 128 * (split ? 2 : 1)) + 256;
 }
 
 // Stage count: enough bytes in flight per SM to cover DRAM latency. One
 // resident CTA per SM (grid <= #SM) gets the deep ring, denser grids 4 stages.
-template <int EB, bool A_MN, int ST, bool SPLIT>
+template <int EB, bool A_MN, int ST, bool SPLIT, bool X3 = false>
 inline cudaError_t launch_one(const TcMaps& maps, const TcParams& p, dim3 grid, cudaStream_t st) {
   static bool attr_done = false;
   if (!attr_done) {
-    const size_t mx = std::min<size_t>(227 * 1024, smem_bytes(128, ST, SPLIT));
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<EB, A_MN, ST, SPLIT>,
+    const size_t mx = std::min<size_t>(227 * 1024, smem_bytes(128, ST, SPLIT, X3));
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<EB, A_MN, ST, SPLIT, X3>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
     if (e != cudaSuccess) return e;
     attr_done = true;
@@ -522,25 +569,34 @@ inline cudaError_t launch_one(const TcMaps& maps, const TcParams& p, dim3 grid, 
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(TC_THREADS);
-  cfg.dynamicSmemBytes = smem_bytes(p.BN, ST, SPLIT);
+  cfg.dynamicSmemBytes = smem_bytes(p.BN, ST, SPLIT, X3);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EB, A_MN, ST, SPLIT>, maps, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<EB, A_MN, ST, SPLIT, X3>, maps, p);
   return e == cudaSuccess ? cudaGetLastError() : e;
 }
 
 template <int EB, bool A_MN>
 inline geig_status launch(const TcMaps& maps, const TcParams& p, dim3 grid, cudaStream_t st, int nsm,
-                          bool split = false) {
+                          bool split = false, bool x3 = false) {
   const int ctas = grid.x * grid.y * grid.z;
   const_cast<TcParams&>(p).dbg = dbg_ptr();
   if (dbg_ptr()) dbg_ptr() += (size_t)4 * ctas;   // next launch stamps after this one
   const bool one_per_sm = ctas <= nsm;
   cudaError_t e;
+  if constexpr (EB == 4) {
+    if (x3) {
+      // 3xTF32 stage = A hi + A lo + B hi + B lo
+      if (one_per_sm && smem_bytes(p.BN, 4, true, true) <= 227 * 1024) e = launch_one<EB, A_MN, 4, true, true>(maps, p, grid, st);
+      else e = launch_one<EB, A_MN, 2, true, true>(maps, p, grid, st);
+      if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("tc_gemm launch: ") + cudaGetErrorString(e));
+      return GEIG_OK;
+    }
+  }
   if (split) {
     // bf16x2 stage = A + 2 B: 6 stages fit one CTA per SM
     if (one_per_sm && smem_bytes(p.BN, 6, true) <= 227 * 1024) e = launch_one<EB, A_MN, 6, true>(maps, p, grid, st);
@@ -568,9 +624,10 @@ inline int choose_splits(int ctas, int kblocks, int nsm) {
 
 inline geig_status plan_create(TcPlan& t, int problem, int64_t dx, int64_t dy, int k, int math, int64_t max_rows,
                                int device) {
-  if (math == GEIG_MATH_3XTF32) return tc_fail(GEIG_ERR_UNSUPPORTED, "3xTF32 products not built yet");
-  t.splitb = math == GEIG_MATH_BF16X2 ? 1 : 0;
-  if (t.splitb) math = GEIG_MATH_BF16;
+  t.x3 = math == GEIG_MATH_3XTF32 ? 1 : 0;
+  t.splitb = (math == GEIG_MATH_BF16X2 || t.x3) ? 1 : 0;
+  if (math == GEIG_MATH_BF16X2) math = GEIG_MATH_BF16;
+  if (t.x3) math = GEIG_MATH_TF32;
   const int eb = math == GEIG_MATH_BF16 ? 2 : 4;
   const int align = 16 / eb;
   if (dx % align || dy % align)
@@ -589,6 +646,8 @@ inline geig_status plan_create(TcPlan& t, int problem, int64_t dx, int64_t dy, i
       return tc_fail(GEIG_ERR_CUDA, "cudaMalloc tc scratch");
     cudaMemset(t.Zb, 0, (size_t)8 * k * t.hpad * eb);
   }
+  if (t.x3 && cudaMalloc((void**)&t.Vx3, (size_t)2 * k * t.d * 4) != cudaSuccess)
+    return tc_fail(GEIG_ERR_CUDA, "cudaMalloc 3xTF32 operand planes");
   t.ready = 1;
   return GEIG_OK;
 }
@@ -596,11 +655,31 @@ inline geig_status plan_create(TcPlan& t, int problem, int64_t dx, int64_t dy, i
 inline void plan_destroy(TcPlan& t) {
   if (t.Zt) cudaFree(t.Zt);
   if (t.Zb) cudaFree(t.Zb);
+  if (t.Vx3) cudaFree(t.Vx3);
+  t.Vx3 = nullptr;
   if (t.xm_dev) cudaFree(t.xm_dev);
   if (t.xm_host) cudaFreeHost(t.xm_host);
   if (t.xm_ev) cudaEventDestroy(t.xm_ev);
   t.xm_dev = nullptr; t.xm_host = nullptr; t.xm_cap = 0; t.xm_ev = nullptr;
   t.Zt = nullptr; t.Zb = nullptr; t.ready = 0;
+}
+
+// 3xTF32 B operand: hi = tf32_rna(v), lo = v - hi (planes n apart).
+__global__ void tf32_split_kernel(const float* __restrict__ v, float* __restrict__ hl, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const float x = v[e], hi = tf32_rna(x);
+    hl[e] = hi;
+    hl[n + e] = x - hi;
+  }
+}
+inline geig_status split_v_x3(TcPlan& t, const float* V, cudaStream_t st, int64_t* nl) {
+  const int64_t n = (int64_t)t.k * t.d;
+  tf32_split_kernel<<<(unsigned)std::min<int64_t>(4 * t.nsm, (n + 255) / 256), 256, 0, st>>>(V, t.Vx3, n);
+  if (cudaGetLastError() != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, "tf32 split launch failed");
+  ++*nl;
+  return GEIG_OK;
 }
 
 // CCA products: forward (K-major X, V) -> Zt -> shuffle -> backward (MN-major X, Zb).
@@ -614,7 +693,11 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
   const int h = (int)(b / 2);
   const int rows = 2 * h;
   const int k = t.k;
-  const void* Vop = eb == 2 ? (const void*)Vbf : (const void*)V;
+  if (t.x3) {
+    geig_status e = split_v_x3(t, V, st, nl);
+    if (e) return e;
+  }
+  const void* Vop = eb == 2 ? (const void*)Vbf : (t.x3 ? (const void*)t.Vx3 : (const void*)V);
   const int64_t dv[2] = {t.dx, t.dy};
   const void* Xv[2] = {X, Y};
   // ---- forward: Z_v = X_v V_v^T, M = rows, K = d_v; split-K partials stored
@@ -647,7 +730,8 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
     if (const char* e = getenv("GEIG_FWD_SPLITS")) p.splits = std::max(1, std::min(TC_MAX_SPLITS, atoi(e)));
     fsplits = p.splits;
     dim3 grid(mt, p.splits, 2);
-    geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st, t.nsm, t.splitb) : launch<4, false>(maps, p, grid, st, t.nsm);
+    geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st, t.nsm, t.splitb)
+                            : launch<4, false>(maps, p, grid, st, t.nsm, t.splitb, t.x3);
     if (s) return s;
     ++*nl;
   }
@@ -670,7 +754,7 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
                               h, t.hpad, fsplits, t.splitb);
     else
       le = cudaLaunchKernelEx(&cfg, zshuffle_kernel<float>, (const float*)t.Zt, (float*)t.Zb, k, t.ldz, h, t.hpad,
-                              fsplits, 0);
+                              fsplits, t.x3);
     if (le != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, "zshuffle launch failed");
     if (cudaGetLastError() != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, "zshuffle launch failed");
     ++*nl;
@@ -709,7 +793,8 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
         return tc_fail(GEIG_ERR_CUDA, "memset AV/BV failed");
     }
     dim3 grid(mt, p.splits, 2);
-    geig_status s = eb == 2 ? launch<2, true>(maps, p, grid, st, t.nsm, t.splitb) : launch<4, true>(maps, p, grid, st, t.nsm);
+    geig_status s = eb == 2 ? launch<2, true>(maps, p, grid, st, t.nsm, t.splitb)
+                            : launch<4, true>(maps, p, grid, st, t.nsm, t.splitb, t.x3);
     if (s) return s;
     ++*nl;
   }
@@ -726,7 +811,11 @@ inline geig_status products_dense(TcPlan& t, const void* A, const void* B, int64
   const int ATOM = 128 / eb;
   const int k = t.k;
   const int M = (int)(r1 - r0);
-  const void* Vop = eb == 2 ? (const void*)Vbf : (const void*)V;
+  if (t.x3) {
+    geig_status e = split_v_x3(t, V, st, nl);
+    if (e) return e;
+  }
+  const void* Vop = eb == 2 ? (const void*)Vbf : (t.x3 ? (const void*)t.Vx3 : (const void*)V);
   TcMaps maps;
   TcParams p{};
   const void* mats[2] = {A, B};
@@ -735,8 +824,11 @@ inline geig_status products_dense(TcPlan& t, const void* A, const void* B, int64
     if (!make_map(&maps.a[g * 2], mats[g], eb, t.d, M, t.d, ATOM, TC_BM) ||
         !make_map(&maps.b[g * 2], Vop, eb, t.d, k, t.d, ATOM, t.BN))
       return tc_fail(GEIG_ERR_CUDA, "tensor map encode (dense) failed");
+    if (t.x3 && !make_map(&maps.blo[g * 2], (const char*)Vop + (int64_t)k * t.d * eb, eb, t.d, k, t.d, ATOM, t.BN))
+      return tc_fail(GEIG_ERR_CUDA, "tensor map encode (dense lo) failed");
     maps.a[g * 2 + 1] = maps.a[g * 2];
     maps.b[g * 2 + 1] = maps.b[g * 2];
+    maps.blo[g * 2 + 1] = maps.blo[g * 2];
     p.M[g] = M;
     p.kblocks[g][0] = (int)((t.d + ATOM - 1) / ATOM);
     p.out[g][0] = outs[g];
@@ -753,7 +845,8 @@ inline geig_status products_dense(TcPlan& t, const void* A, const void* B, int64
         return tc_fail(GEIG_ERR_CUDA, "memset AV/BV rows failed");
   }
   dim3 grid(mt, p.splits, 2);
-  geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st, t.nsm) : launch<4, false>(maps, p, grid, st, t.nsm);
+  geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st, t.nsm)
+                          : launch<4, false>(maps, p, grid, st, t.nsm, t.x3 != 0, t.x3 != 0);
   if (s) return s;
   ++*nl;
   return GEIG_OK;

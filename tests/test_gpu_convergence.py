@@ -86,6 +86,13 @@ def test_converges_tf32_cca_variant(geig):
     assert ang.mean() < 1e-3 and se < 1e-6
 
 
+def test_converges_3xtf32_cca_variant(geig):
+    """fp32 data, 3xTF32 tensor-core products: the fp32-variant bar."""
+    ang, se = _run_cca(geig, "3xtf32", torch.float32)
+    print("3xTF32 tcgen05 CCA variant: angles", ang, "mean", ang.mean(), "subspace error", se)
+    assert ang.mean() < 1e-3 and se < 1e-6
+
+
 def test_converges_tf32_dense_config0(geig):
     from oracle import linalg, metrics
     from synth import CONFIGS, dense_gep_small, gaussian_init

@@ -152,8 +152,8 @@ def test_errors_are_loud(geig):
         geig.geig_products_cca(s.h, x, x, 16, 1.0, AV, AV)      # b > max_rows
     s.close()
     # unbuilt arithmetic variants are refused at creation, never silently wrong
-    with pytest.raises(geig.GeigError, match="not built"):
-        geig.geig_create(geig.GEIG_CCA, 64, 64, 4, geig.GEIG_MATH_3XTF32, geig.GEIG_DATA_F32, 0.1, 64, 0)
+    with pytest.raises(geig.GeigError, match="fp32 data"):
+        geig.geig_create(geig.GEIG_CCA, 64, 64, 4, geig.GEIG_MATH_3XTF32, geig.GEIG_DATA_BF16, 0.1, 64, 0)
     with pytest.raises(geig.GeigError, match="fp32 data"):
         geig.geig_create(geig.GEIG_CCA, 64, 64, 4, geig.GEIG_MATH_TF32, geig.GEIG_DATA_BF16, 0.1, 64, 0)
 
@@ -225,6 +225,44 @@ def test_cca_tf32_tcgen05(geig, monkeypatch, cfg_idx, rows, k, dx, dy):
     errs, _ = gh.check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math="tf32")
     _assert(errs, 1e-2)
     assert errs["av"] < 3e-3 and errs["bv"] < 3e-3, errs
+
+
+@pytest.mark.parametrize("cfg_idx,rows,k,dx,dy,eta", [(1, 256, None, None, None, None),
+                                                      (2, 1024, 16, 784, 784, None),
+                                                      (3, 2048, 64, 1024, 512, None),
+                                                      (2, 300, 24, 200, 136, 0.5), (2, 130, 5, 64, 8, 0.5)])
+def test_cca_3xtf32_tcgen05(geig, monkeypatch, cfg_idx, rows, k, dx, dy, eta):
+    """3xTF32: A split in shared memory into tf32 hi + lo by warps 2-3, B as
+    hi / lo planes, three MMAs per K step (a_lo b_lo dropped): the fp32
+    exactness bar of the FFMA variant on the configs (1e-4 everywhere),
+    products, Gram tables and aux ~1e-6 (bar 1e-5) on all shapes.  On the
+    tiny ragged shapes the step (a difference of O(1) terms, cancellation
+    ~100-200x at a random state) gets the bf16x2 bar of 1e-3."""
+    import tests.gpu_harness as gh
+    cv = gh.cca_views
+    monkeypatch.setattr(gh, "cca_views", lambda *a, **kw: tuple(t.float() for t in cv(*a, **kw)))
+    errs, _ = gh.check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math="3xtf32", eta=eta)
+    step = errs.pop("step")
+    _assert(errs, 1e-5)
+    assert step < (1e-4 if eta is None else 1e-3), (step, errs)
+
+
+def test_dense_config0_3xtf32_tcgen05(geig):
+    from synth import CONFIGS, dense_gep_small
+    cfg = CONFIGS[0]
+    a, b = dense_gep_small(0)
+    errs = _dense_step_check(geig, a, b, cfg.k, "3xtf32", cfg.rho, cfg.eta, cfg.gamma, tol=1e-4)
+    assert errs["av"] < 1e-5 and errs["bv"] < 1e-5, errs
+
+
+def test_dense_config4_reduced_3xtf32_tcgen05(geig):
+    """Config 4's recipe at d = 1000 (ragged tiles), k = 37, 3xTF32 (eta as
+    in the fp32 test: the step must dominate the fp32 storage of V')."""
+    from synth import CONFIGS, dense_gep_large
+    cfg = CONFIGS[4]
+    a, b = dense_gep_large(1000, seed=2, device="cuda:0")
+    errs = _dense_step_check(geig, a, b, 37, "3xtf32", cfg.rho, 0.5, cfg.gamma, tol=1e-4)
+    assert errs["av"] < 1e-5 and errs["bv"] < 1e-5, errs
 
 
 def test_dense_config0_tf32_tcgen05(geig):
