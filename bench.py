@@ -211,7 +211,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     from paper_2206_04993_b200 import geig
-    from paper_2206_04993_b200.parallel import cca_scale
+    from paper_2206_04993_b200.parallel import allreduce_products, cca_scale, product_buffers
     from synth import cca_views, dense_gep_large, gaussian_init
 
     dev = torch.device(f"cuda:{local_rank}")
@@ -246,8 +246,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if args.adam:                                      # Appendix H optimizer
         geig.geig_set_adam(s.h, 0.9, 0.999, 1e-8)
         variant += "+adam"
-    AV = torch.empty(cfg.k, cfg.d, device=dev)
-    BV = torch.empty_like(AV)
+    AV, BV = product_buffers(cfg.k, cfg.d, device=dev)   # one buffer: in-place all-reduce
     scale = cca_scale(b, world)
 
     ev = []
@@ -268,10 +267,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
             if timed:
                 e1.record(stream)
             if world > 1:
-                flat = torch.stack([AV, BV])
-                dist.all_reduce(flat)
-                AV.copy_(flat[0])
-                BV.copy_(flat[1])
+                allreduce_products(AV, BV)
             geig.geig_update(s.h, AV, BV, cfg.eta, cfg.gamma)
         if timed:
             e2.record(stream)

@@ -17,6 +17,32 @@ import torch
 import torch.distributed as dist
 
 
+def product_buffers(k: int, d: int, **kw) -> tuple[torch.Tensor, torch.Tensor]:
+    """AV, BV as the two halves of ONE contiguous [2, k, d] buffer, so the
+    Appendix-F all-reduce runs in place on both (no stack / copy-back)."""
+    buf = torch.empty(2, k, d, **kw)
+    return buf[0], buf[1]
+
+
+def allreduce_products(AV: torch.Tensor, BV: torch.Tensor, group=None):
+    """SUM all-reduce of the partial products of every rank: in place when AV
+    and BV are the adjacent halves of one buffer (product_buffers), else one
+    fused all-reduce of a stacked copy."""
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return
+    n = AV.numel()
+    adjacent = (AV.is_contiguous() and BV.is_contiguous() and AV.dtype == BV.dtype and BV.numel() == n
+                and BV.data_ptr() == AV.data_ptr() + n * AV.element_size())
+    if adjacent:
+        flat = AV.as_strided((2 * n,), (1,))
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    else:
+        flat = torch.stack([AV, BV])
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+        AV.copy_(flat[0])
+        BV.copy_(flat[1])
+
+
 def shard_rows(n_rows: int, world: int, rank: int) -> tuple[int, int]:
     """Contiguous row range [r0, r1) of `rank`; sizes differ by at most one."""
     base, rem = divmod(n_rows, world)
@@ -35,12 +61,7 @@ class ShardedStep:
 
     def __call__(self, AV: torch.Tensor, BV: torch.Tensor):
         self.products(AV, BV)
-        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
-            # one fused all-reduce of the two k x d products
-            flat = torch.stack([AV, BV])
-            dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
-            AV.copy_(flat[0])
-            BV.copy_(flat[1])
+        allreduce_products(AV, BV, self.group)   # one fused all-reduce of the two k x d products
         self.update(AV, BV)
 
 
@@ -53,8 +74,5 @@ def cca_scale(b_local: int, world: int) -> float:
 def dense_allgather_rows(AV: torch.Tensor, BV: torch.Tensor, d: int, world: int, group=None):
     """Dense row sharding: rank r wrote columns [r0, r1) of AV, BV (zeros
     elsewhere); a SUM all-reduce assembles the full products."""
-    if dist.is_initialized() and world > 1:
-        flat = torch.stack([AV, BV])
-        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
-        AV.copy_(flat[0])
-        BV.copy_(flat[1])
+    if world > 1:
+        allreduce_products(AV, BV, group)

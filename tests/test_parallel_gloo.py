@@ -11,7 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2206_04993_b200.parallel import ShardedStep, cca_scale, dense_allgather_rows, shard_rows
+from paper_2206_04993_b200.parallel import ShardedStep, cca_scale, dense_allgather_rows, product_buffers, shard_rows
 
 
 def _free_port():
@@ -46,8 +46,15 @@ def _worker(rank, world, port, x, y, V, aux, out_q):
                                                       0.1, 0.5, 1e-3)
 
         step = ShardedStep(products, update)
-        AV = torch.zeros(V.shape, dtype=torch.float64)
-        BV = torch.zeros_like(AV)
+        # rank 0: AV, BV halves of one buffer (in-place all-reduce); rank 1:
+        # separate tensors (stacked all-reduce) -- both paths must agree
+        if rank == 0:
+            AV, BV = product_buffers(V.shape[0], V.shape[1], dtype=torch.float64)
+            AV.zero_()
+            BV.zero_()
+        else:
+            AV = torch.zeros(V.shape, dtype=torch.float64)
+            BV = torch.zeros_like(AV)
         step(AV, BV)
         out_q.put((rank, AV.numpy().copy(), state["V"], state["aux"]))
         # dense row sharding: each rank writes its columns, all-reduce assembles
