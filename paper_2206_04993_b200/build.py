@@ -29,7 +29,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
     cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v", "-o", OUT + ".tmp", os.path.join(CSRC, "geig_api.cu")]
+           "-Xptxas", "-v", *os.environ.get("GEIG_NVCC_EXTRA", "").split(), "-o", OUT + ".tmp",
+           os.path.join(CSRC, "geig_api.cu")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -465,6 +465,10 @@ update_kernel(UpdateArgs p) {
 constexpr int UPD_RES_WMAX = 168;   // max columns per CTA (smem: 4 x 64 x 172 x 4 B + tables)
 constexpr int UPD_GT = 72;          // 8x4 lower-triangle Gram tiles of a 64 x 64 table
 constexpr int UPD_GS = 3;           // column slices of the Gram phase (UPD_GT * UPD_GS <= UPD_THREADS)
+#ifndef GEIG_PEN_UNROLL
+#define GEIG_PEN_UNROLL 4
+#endif
+constexpr int kPenUnroll = GEIG_PEN_UNROLL;   // penalty-sum j unroll (developer A/B: -DGEIG_PEN_UNROLL=n)
 constexpr int UPD_LTS = 72;         // Lt row stride: the tf32 A fragments (rows t, t+4 x cols g) are bank-conflict free
 constexpr int UPD_AUXF = 64 * UPD_LTS + 4 * 64 + 8 * 32 + 64 * 65 + 128;   // Lt | N, 1/s^2, D1, D2 | red | raw
 constexpr int UPD_GREDF = (UPD_GS - 1) * UPD_GT * 64;                // Gram slice partials (aliases the above)
@@ -1007,7 +1011,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
         for (int b = 0; b < 4; ++b) accA[a][b] = accB[a][b] = 0.f;
       const float* cp = Ct + 4 * q;
       int j = (p.dbg_mode & 512) ? jB : 0;   // developer: skip the penalty sums (timing only)
-#pragma unroll 4
+#pragma unroll kPenUnroll
       for (; j < jA; ++j) {
         const float4 x = *reinterpret_cast<const float4*>(cp + j * S);
         const float4 la = *reinterpret_cast<const float4*>(Lt + j * UPD_LTS + iA);
@@ -1021,7 +1025,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
             accB[a][b] = fmaf(lbv[a], xv[b], accB[a][b]);
           }
       }
-#pragma unroll 4
+#pragma unroll kPenUnroll
       for (; j < jB; ++j) {
         const float4 x = *reinterpret_cast<const float4*>(cp + j * S);
         const float4 lb = *reinterpret_cast<const float4*>(Lt + j * UPD_LTS + iB);
