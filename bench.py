@@ -214,7 +214,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
     from paper_2206_04993_b200.parallel import allreduce_products, cca_scale, product_buffers
     from synth import cca_views, dense_gep_large, gaussian_init
 
-    dev = torch.device(f"cuda:{local_rank}")
+    # (GEIG_BENCH_SHARE_GPU: functional check of the multi-rank path with
+    # every rank on the available GPUs; never a measurement)
+    ndev = torch.cuda.device_count()
+    dev = torch.device(f"cuda:{local_rank % ndev if os.environ.get('GEIG_BENCH_SHARE_GPU') else local_rank}")
     torch.cuda.set_device(dev)
     stream = torch.cuda.current_stream(dev)
     peaks, peaks_src = _peaks()
@@ -236,7 +239,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     Ys = [Y[i * b:(i + 1) * b] for i in range(P)]
     s = geig.Solver(geig.GEIG_CCA, cfg.dx, cfg.dy, cfg.k, math=math,
                     data_dtype=geig.GEIG_DATA_BF16 if data_bf16 else geig.GEIG_DATA_F32,
-                    rho=cfg.rho, max_rows=b, device=local_rank, stream=stream.cuda_stream)
+                    rho=cfg.rho, max_rows=b, device=dev.index, stream=stream.cuda_stream)
     G = torch.tensor(gaussian_init(cfg.k, cfg.d, 0), dtype=torch.float32, device=dev)
     s.init_state(G)
     variant = "alg2"
@@ -307,7 +310,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     timed_args = run_args(args.warmup, args.steps) if multi else None
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(dev.index) as clk:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -349,7 +352,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
                   "reduce_us": ph[1] / 1e3, "coef_update_us": ph[2] / 1e3, "source": "%globaltimer, CTA 0, last step"}
     else:
         alg_bytes = b * cfg.d * esz + kd * (2 if math in ("bf16", "bf16x2") else 4) + 2 * kd * 4
-        kernel = "products stage (tc_gemm forward + zshuffle + tc_gemm backward)"
+        kernel = ("cca_step_kernel products-only launch (phases F, S, B; multi-GPU: then all-reduce + update)"
+                  if math in ("bf16", "bf16x2") and cfg.k <= 64 and not args.staged
+                  else "products stage (tc_gemm forward + zshuffle + tc_gemm backward)")
         k_ms = prod_ms
         phases = {"products_ms": prod_ms, "update_ms": upd_ms}
     achieved = alg_bytes / (k_ms / 1e3) / 1e9
@@ -375,12 +380,32 @@ def run_gpu(args, cfg, rank, world, local_rank):
         hy = Ys[0].cpu().pin_memory()
         ga = torch.empty(cfg.k, cfg.k).pin_memory()
         n_e2e = max(3, min(args.steps, 20))
-        geig.geig_step_cca_host(s.h, hx, hy, b, cfg.eta, cfg.gamma, ga)
+        if world == 1:
+            def e2e_step():
+                return geig.geig_step_cca_host(s.h, hx, hy, b, cfg.eta, cfg.gamma, ga)
+        else:
+            # the Appendix-F step of every rank from its pinned host shard:
+            # H2D copy, products, in-place all-reduce, update, D2H of the Gram
+            # table (the same result the single-GPU host call reads back)
+            xd, yd = torch.empty_like(Xs[0]), torch.empty_like(Ys[0])
+            gd = torch.empty(3, cfg.k, cfg.k, device=dev)
+
+            def e2e_step():
+                xd.copy_(hx, non_blocking=True)
+                yd.copy_(hy, non_blocking=True)
+                geig.geig_products_cca(s.h, xd, yd, b, scale, AV, BV)
+                allreduce_products(AV, BV)
+                geig.geig_update(s.h, AV, BV, cfg.eta, cfg.gamma)
+                geig.geig_get_gram(s.h, gd[0], gd[1], gd[2])
+                ga.copy_(gd[0])
+                return hx.numel() * hx.element_size() + hy.numel() * hy.element_size(), ga.numel() * 4
+        e2e_step()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(n_e2e):
-            h2d, d2h = geig.geig_step_cca_host(s.h, hx, hy, b, cfg.eta, cfg.gamma, ga)
+            h2d, d2h = e2e_step()
+        torch.cuda.synchronize()
         el = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([el], device=dev)
@@ -444,8 +469,9 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local_rank % torch.cuda.device_count() if os.environ.get("GEIG_BENCH_SHARE_GPU")
+                              else local_rank)
+        dist.init_process_group(os.environ.get("GEIG_BENCH_BACKEND", "nccl"))
     run_gpu(args, cfg, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
