@@ -249,12 +249,21 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if args.adam:                                      # Appendix H optimizer
         geig.geig_set_adam(s.h, 0.9, 0.999, 1e-8)
         variant += "+adam"
-    AV, BV = product_buffers(cfg.k, cfg.d, device=dev)   # one buffer: in-place all-reduce
     scale = cca_scale(b, world)
+    # multi-GPU step: the fused kernel's products + Gram-table partials in one
+    # launch, ONE in-place all-reduce of [AV | BV | tables], then the update
+    # from the aggregated tables (geig_products_cca_tables / geig_update_tables)
+    tables = (world > 1 or args.split_step) and math in ("bf16", "bf16x2") and cfg.k <= 64 and not args.staged \
+        and not args.no_tables
+    if tables:
+        AV, BV, T = product_buffers(cfg.k, cfg.d, geig.geig_table_floats(s.h), device=dev)
+    else:
+        AV, BV = product_buffers(cfg.k, cfg.d, device=dev)   # one buffer: in-place all-reduce
+        T = None
 
     ev = []
 
-    fused = world == 1 and math in ("bf16", "bf16x2") and cfg.k <= 64 and not args.staged
+    fused = world == 1 and math in ("bf16", "bf16x2") and cfg.k <= 64 and not args.staged and not args.split_step
 
     def step(i, timed):
         if timed:
@@ -265,6 +274,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
             geig.geig_step_cca(s.h, Xs[i % P], Ys[i % P], b, cfg.eta, cfg.gamma)
             if timed:
                 e1.record(stream)
+        elif tables:
+            geig.geig_products_cca_tables(s.h, Xs[i % P], Ys[i % P], b, scale, AV, BV, T)
+            if timed:
+                e1.record(stream)
+            if world > 1:
+                allreduce_products(AV, BV, T=T)
+            geig.geig_update_tables(s.h, AV, BV, T, cfg.eta, cfg.gamma)
         else:
             geig.geig_products_cca(s.h, Xs[i % P], Ys[i % P], b, scale, AV, BV)
             if timed:
@@ -393,9 +409,14 @@ def run_gpu(args, cfg, rank, world, local_rank):
             def e2e_step():
                 xd.copy_(hx, non_blocking=True)
                 yd.copy_(hy, non_blocking=True)
-                geig.geig_products_cca(s.h, xd, yd, b, scale, AV, BV)
-                allreduce_products(AV, BV)
-                geig.geig_update(s.h, AV, BV, cfg.eta, cfg.gamma)
+                if tables:
+                    geig.geig_products_cca_tables(s.h, xd, yd, b, scale, AV, BV, T)
+                    allreduce_products(AV, BV, T=T)
+                    geig.geig_update_tables(s.h, AV, BV, T, cfg.eta, cfg.gamma)
+                else:
+                    geig.geig_products_cca(s.h, xd, yd, b, scale, AV, BV)
+                    allreduce_products(AV, BV)
+                    geig.geig_update(s.h, AV, BV, cfg.eta, cfg.gamma)
                 geig.geig_get_gram(s.h, gd[0], gd[1], gd[2])
                 ga.copy_(gd[0])
                 return hx.numel() * hx.element_size() + hy.numel() * hy.element_size(), ga.numel() * 4
@@ -427,6 +448,10 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 "dtype": "bf16" if math in ("bf16", "bf16x2") else ("f32" if math == "f32" else math),
                 "data": "synthetic",
                 "config": dict(_workload(cfg, math), parallelism=f"dp{world}", global_batch=world * b, update=variant,
+                               step=("fused single launch (geig_run_cca)" if multi else
+                                     "fused single launch per step" if fused else
+                                     "products+tables launch, all-reduce, update_tables" if tables else
+                                     "products launch, all-reduce, update"),
                                l2_policy=f"ring of {P} distinct batches ({P * batch_bytes / 2**20:.0f} MiB) "
                                          "> 126 MB L2, a new batch every step"),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -453,6 +478,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--staged", action="store_true", help="products + update as separate launches")
+    ap.add_argument("--split-step", action="store_true",
+                    help="N=1: the multi-GPU step structure (products launch, then update launch)")
+    ap.add_argument("--no-tables", action="store_true",
+                    help="multi-GPU / split step: update re-forms the Gram tables (geig_update) instead of "
+                         "aggregating them with the products")
     args = ap.parse_args()
     from synth import CONFIGS
     cfg = CONFIGS[args.config]

@@ -145,6 +145,27 @@ geig_status geig_products_dense(geig_solver* s, const void* A, const void* B,
 geig_status geig_update(geig_solver* s, const float* AV, const float* BV,
                         double eta, double gamma);
 
+/* Multi-GPU form of the step (Appendix F) with the Gram
+ * tables aggregated beside the products.  geig_products_cca_tables writes,
+ * in ONE launch of the fused kernel's phases F, S, B, this rank's scaled
+ * partial products AV, BV (like geig_products_cca) and into T the partial
+ * sums of the tables that depend on the rank's rows — tri(G^A) and diag(G^B)
+ * formed from the forward products (Alg. 2 lines 8-11; reading R3') — while
+ * G^C and ||v''||^2, which depend only on the replicated state, stay in the
+ * solver.  The caller sums AV, BV and T over the ranks (one all-reduce when
+ * the three are adjacent in one buffer) and calls geig_update_tables, which
+ * runs the update from the summed products and tables without re-forming
+ * the Gram tables.  T: geig_table_floats(s) device floats.  Needs the fused
+ * path (bf16 / bf16x2 math, k <= 64, d % 4 == 0): GEIG_ERR_UNSUPPORTED
+ * otherwise (use geig_products_cca + geig_update).  The state must not change
+ * between the two calls. */
+int64_t geig_table_floats(const geig_solver* s);
+geig_status geig_products_cca_tables(geig_solver* s, const void* X, const void* Y,
+                                     int64_t b, float scale, float* AV, float* BV,
+                                     float* T);
+geig_status geig_update_tables(geig_solver* s, const float* AV, const float* BV,
+                               const float* T, double eta, double gamma);
+
 /* One full step = products + update on the solver's scratch.  On the bf16
  * tensor-core path with k <= 64 the whole step is ONE persistent cooperative
  * kernel (forward GEMM, split-K reduction, backward GEMM, Gram tables and

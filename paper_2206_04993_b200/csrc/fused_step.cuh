@@ -47,6 +47,8 @@ struct FusedParams {
                                    // holds tm x more batch bytes in flight per byte of V / Z re-read
   int nsteps;                      // steps of Alg. 2 run by this launch (one batch each)
   int products_only;               // 1: phases F, S, B only (AV, BV to global; multi-GPU: all-reduce, then geig_update)
+  int tables;                      // products-only launch that also forms the Gram tables (G^A, G^B of the
+                                   // local rows into upd.raw_a, G^C of the state into upd.raw)
   uint32_t bar_off;                // smem offset of the ring mbarriers (past the ring AND the update arena)
   const CUtensorMap* xmaps;        // nsteps x 6 A-operand maps in global memory (nullptr: maps.a, one step)
   int kbF[2], kbB;                 // K blocks: forward per view, backward per half
@@ -337,7 +339,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
 
   // ---- phase F: forward split-K partials; warps 2-3: G^C, ||v''||^2 partials ----
   if (warp == 2 || warp == 3) {
-    if (!p.products_only) gram_c_side(p.upd, threadIdx.x - 64);
+    if (!p.products_only || p.tables) gram_c_side(p.upd, threadIdx.x - 64);
     if (threadIdx.x == 64) tstamp(p.upd, 31);
   } else if (!(p.dbg_mode & 8)) {
     gemm_phase<EB, false>(maps, A, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs,
@@ -485,7 +487,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
       dstamp(p.upd, 25);
     }
     // first half of this CTA's Gram partial row: [tri(G^A) | diag(G^B) | pad]
-    if (!p.products_only) {
+    if (!p.products_only || p.tables) {
       float* pr = pst;
       const float sc = p.scale;
       // the z-Gram is symmetric: each thread writes the lower-triangle entries of its 4x4 tile
@@ -519,7 +521,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   if (threadIdx.x == 0)
     for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&A[2 + v]); tma_prefetch_desc(&maps.bB[v]); }
   if (warp == 2 || warp == 3) {    // warps 2-3: reduce the (now complete) Gram partial rows
-    if (!p.products_only) reduce_side(p.upd, threadIdx.x - 64, side_scratch);
+    if (!p.products_only || p.tables) reduce_side(p.upd, threadIdx.x - 64, side_scratch);
   } else if (!(p.dbg_mode & 32)) {
     gemm_phase<EB, true>(maps, A, p, 2 * (p.mtB[0] + p.mtB[1]), ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs,
                          epi_stage);
@@ -604,7 +606,8 @@ inline bool make_batch_maps(CUtensorMap* a, const TcPlan& t, const void* X, cons
 // by the GEMM phases.
 inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* const* Y, int nsteps, int64_t b,
                                   float scale, const __nv_bfloat16* Vbf, float* AV, float* BV, UpdateArgs upd,
-                                  int grid_ctas, size_t upd_bytes, cudaStream_t st, bool products_only = false) {
+                                  int grid_ctas, size_t upd_bytes, cudaStream_t st, bool products_only = false,
+                                  bool tables = false) {
   if (!t.ready || t.math != GEIG_MATH_BF16) return tc_fail(GEIG_ERR_STATE, "fused step needs the bf16 plan");
   if (nsteps < 1) return tc_fail(GEIG_ERR_ARG, "nsteps < 1");
   // (t.math is BF16 for both GEIG_MATH_BF16 and GEIG_MATH_BF16X2; t.splitb selects hi+lo operands)
@@ -616,6 +619,7 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   if (!make_batch_maps(maps.a, t, X[0], Y[0], h)) return tc_fail(GEIG_ERR_CUDA, "tensor map encode (batch) failed");
   p.nsteps = nsteps;
   p.products_only = products_only ? 1 : 0;
+  p.tables = (products_only && tables) ? 1 : 0;
   if (products_only && nsteps != 1) return tc_fail(GEIG_ERR_ARG, "products-only launch runs one step");
   p.xmaps = nullptr;
   if (nsteps > 1) {

@@ -359,6 +359,49 @@ extern "C" geig_status geig_products_cca(geig_solver* s, const void* X, const vo
   return GEIG_OK;
 }
 
+extern "C" int64_t geig_table_floats(const geig_solver* s) {
+  if (!s) return 0;
+  const int64_t ntri = (int64_t)s->k * (s->k + 1) / 2;
+  return (ntri + s->k + 3) & ~(int64_t)3;
+}
+
+extern "C" geig_status geig_products_cca_tables(geig_solver* s, const void* X, const void* Y, int64_t b,
+                                                float scale, float* AV, float* BV, float* T) {
+  if (!s || !X || !Y || !AV || !BV || !T) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (s->problem != GEIG_CCA) return fail(GEIG_ERR_STATE, "solver is not a CCA solver");
+  if (b < 2 || b > s->max_rows) return fail(GEIG_ERR_ARG, "b=%lld outside [2, max_rows=%lld]",
+                                            (long long)b, (long long)s->max_rows);
+  if (!fused_ok(s, X, Y))
+    return fail(GEIG_ERR_UNSUPPORTED, "products with tables need the fused path (bf16 math, k <= 64, d %% 4 == 0)");
+  CU(cudaSetDevice(s->device));
+  UpdateArgs a = update_args(s, 0.0, 0.0);
+  a.raw_a = T;
+  geig_status st = tc::fused_cca_step(s->tc, &X, &Y, 1, b, scale, s->Vbf, AV, BV, a, s->upd_grid, s->upd_smem,
+                                      s->stream, /*products_only=*/true, /*tables=*/true);
+  if (st) return fail(st, "%s", tc::last_error());
+  s->launches++;
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_update_tables(geig_solver* s, const float* AV, const float* BV, const float* T,
+                                          double eta, double gamma) {
+  if (!s || !AV || !BV || !T) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (!s->upd_res || s->d % 4 != 0) return fail(GEIG_ERR_UNSUPPORTED, "update from tables needs k <= 64, d %% 4 == 0");
+  CU(cudaSetDevice(s->device));
+  UpdateArgs a = update_args(s, eta, gamma);
+  a.AV = AV; a.BV = BV;
+  a.raw_a = const_cast<float*>(T);
+  a.pre_reduced = 1;
+  void* args[] = {&a};
+  const bool vec = ((uintptr_t)AV | (uintptr_t)BV) % 16 == 0;
+  void* fn = vec ? (void*)update_res_kernel<true> : (void*)update_res_kernel<false>;
+  CU(cudaLaunchCooperativeKernel(fn, dim3(s->upd_grid), dim3(UPD_THREADS), args, s->upd_smem, s->stream));
+  s->launches++;
+  s->fused_last = false;
+  advance_variant_state(s, 1);
+  return GEIG_OK;
+}
+
 extern "C" geig_status geig_products_dense(geig_solver* s, const void* A, const void* B, int64_t r0,
                                            int64_t r1, float* AV, float* BV) {
   if (!s || !A || !B || !AV || !BV) return fail(GEIG_ERR_ARG, "NULL argument");

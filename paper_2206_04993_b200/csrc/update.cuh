@@ -51,6 +51,8 @@ struct UpdateArgs {
   __nv_bfloat16* Vbf;    // 2 x k x d bf16 shadow of the new V: hi plane, then lo = bf16(v - hi) (nullable)
   float* partial;        // gridDim x (2*KP*KP + 2*KP) scratch
   float* raw;            // 2*KP*KP + 2*KP reduced un-normalised tables
+  float* raw_a;          // nullable: the first half of the resident raw row (tri(G^A) | diag G^B)
+                         // lives here instead of raw (multi-GPU: summed over ranks with AV, BV)
   float* gram;           // 3 x k x k out: normalised GA, GB, GC of the step
   int k;
   int64_t d;
@@ -583,7 +585,10 @@ __device__ __forceinline__ void reduce_side(const UpdateArgs& p, int t, float* s
     }
     scratch[t] = s;
     asm volatile("bar.sync 1, 64;" ::: "memory");
-    if (half == 0 && e < e1) p.raw[e] = s + scratch[t + 32];
+    if (half == 0 && e < e1) {
+      if (p.raw_a && e < hA) p.raw_a[e] = s + scratch[t + 32];
+      else p.raw[e] = s + scratch[t + 32];
+    }
     asm volatile("bar.sync 1, 64;" ::: "memory");
   }
 }
@@ -633,7 +638,8 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   if (early_raw) {
     // pre-reduced tables: stage them first (the coefficients need them
     // before the tiles; the tiles' TMA then streams behind them)
-    for (int e = 4 * tid; e < pstride; e += 4 * UPD_THREADS) cp_async16(rs + e, p.raw + e, 16);
+    for (int e = 4 * tid; e < pstride; e += 4 * UPD_THREADS)
+      cp_async16(rs + e, (p.raw_a && e < hA) ? p.raw_a + e : p.raw + e, 16);
     cp_async_commit();
   }
   if (um) {
@@ -910,7 +916,8 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   // independent 16-byte async copies, then the coefficients are formed from smem.
   {
     if (!early_raw) {
-      for (int e = 4 * tid; e < pstride; e += 4 * UPD_THREADS) cp_async16(rs + e, p.raw + e, 16);
+      for (int e = 4 * tid; e < pstride; e += 4 * UPD_THREADS)
+        cp_async16(rs + e, (p.raw_a && e < hA) ? p.raw_a + e : p.raw + e, 16);
       cp_async_commit();
     }
     cp_async_wait<0>();

@@ -47,6 +47,8 @@ _SIGS = {
     "geig_products_cca": [_vp, _vp, _vp, _i64, _f32, _vp, _vp],
     "geig_products_dense": [_vp, _vp, _vp, _i64, _i64, _vp, _vp],
     "geig_update": [_vp, _vp, _vp, _f64, _f64],
+    "geig_products_cca_tables": [_vp, _vp, _vp, _i64, _f32, _vp, _vp, _vp],
+    "geig_update_tables": [_vp, _vp, _vp, _vp, _f64, _f64],
     "geig_step_cca": [_vp, _vp, _vp, _i64, _f64, _f64],
     "geig_step_dense": [_vp, _vp, _vp, _f64, _f64],
     "geig_run_cca": [_vp, _vp, _vp, _i64, _i64, _f64, _f64],
@@ -62,6 +64,8 @@ for _name, _args in _SIGS.items():
     _fn = getattr(_lib, _name)
     _fn.argtypes = _args
     _fn.restype = ctypes.c_int
+_lib.geig_table_floats.argtypes = [_vp]
+_lib.geig_table_floats.restype = _i64
 _lib.geig_launch_count.argtypes = [_vp]
 _lib.geig_launch_count.restype = _i64
 _lib.geig_last_error.restype = ctypes.c_char_p
@@ -71,7 +75,8 @@ EXPORTED = ["geig_create", "geig_destroy", "geig_set_stream", "geig_sync", "geig
             "geig_set_state", "geig_get", "geig_products_cca", "geig_products_dense", "geig_update",
             "geig_step_cca", "geig_step_dense", "geig_run_cca", "geig_step_cca_host", "geig_get_gram",
             "geig_set_smooth", "geig_smooth_state", "geig_set_adam",
-            "geig_launch_count", "geig_last_error", "geig_version", "geig_update_phase_ns"]
+            "geig_launch_count", "geig_last_error", "geig_version", "geig_update_phase_ns",
+            "geig_table_floats", "geig_products_cca_tables", "geig_update_tables"]
 
 
 def _check(st: int):
@@ -148,6 +153,20 @@ def geig_products_dense(h, A, B, r0: int, r1: int, AV, BV):
 
 def geig_update(h, AV, BV, eta: float, gamma: float):
     _check(_lib.geig_update(h, _ptr(AV, torch.float32), _ptr(BV, torch.float32), eta, gamma))
+
+
+def geig_table_floats(h) -> int:
+    return int(_lib.geig_table_floats(h))
+
+
+def geig_products_cca_tables(h, X, Y, b: int, scale: float, AV, BV, T):
+    _check(_lib.geig_products_cca_tables(h, _ptr(X), _ptr(Y), b, scale, _ptr(AV, torch.float32),
+                                         _ptr(BV, torch.float32), _ptr(T, torch.float32)))
+
+
+def geig_update_tables(h, AV, BV, T, eta: float, gamma: float):
+    _check(_lib.geig_update_tables(h, _ptr(AV, torch.float32), _ptr(BV, torch.float32), _ptr(T, torch.float32),
+                                   eta, gamma))
 
 
 def geig_step_cca(h, X, Y, b: int, eta: float, gamma: float):

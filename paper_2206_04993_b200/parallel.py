@@ -17,25 +17,40 @@ import torch
 import torch.distributed as dist
 
 
-def product_buffers(k: int, d: int, **kw) -> tuple[torch.Tensor, torch.Tensor]:
-    """AV, BV as the two halves of ONE contiguous [2, k, d] buffer, so the
-    Appendix-F all-reduce runs in place on both (no stack / copy-back)."""
-    buf = torch.empty(2, k, d, **kw)
-    return buf[0], buf[1]
+def product_buffers(k: int, d: int, n_tables: int = 0, **kw):
+    """AV, BV as the two halves of ONE contiguous buffer, so the Appendix-F
+    all-reduce runs in place on both (no stack / copy-back); with n_tables > 0
+    a third view T of n_tables floats follows them in the same buffer (the
+    Gram-table partials of geig_products_cca_tables) and is returned too."""
+    kd = k * d
+    buf = torch.empty(2 * kd + n_tables, **kw)
+    AV, BV = buf[:kd].view(k, d), buf[kd:2 * kd].view(k, d)
+    if n_tables:
+        return AV, BV, buf[2 * kd:]
+    return AV, BV
 
 
-def allreduce_products(AV: torch.Tensor, BV: torch.Tensor, group=None):
-    """SUM all-reduce of the partial products of every rank: in place when AV
-    and BV are the adjacent halves of one buffer (product_buffers), else one
-    fused all-reduce of a stacked copy."""
+def allreduce_products(AV: torch.Tensor, BV: torch.Tensor, group=None, T: torch.Tensor | None = None):
+    """SUM all-reduce of the partial products (and table partials T) of every
+    rank: in place when AV, BV (, T) are adjacent in one buffer
+    (product_buffers), else one fused all-reduce of a stacked copy."""
     if not (dist.is_initialized() and dist.get_world_size(group) > 1):
         return
     n = AV.numel()
+    es = AV.element_size()
     adjacent = (AV.is_contiguous() and BV.is_contiguous() and AV.dtype == BV.dtype and BV.numel() == n
-                and BV.data_ptr() == AV.data_ptr() + n * AV.element_size())
+                and BV.data_ptr() == AV.data_ptr() + n * es)
+    if T is not None:
+        adjacent = adjacent and T.is_contiguous() and T.dtype == AV.dtype and T.data_ptr() == AV.data_ptr() + 2 * n * es
     if adjacent:
-        flat = AV.as_strided((2 * n,), (1,))
+        flat = AV.as_strided((2 * n + (T.numel() if T is not None else 0),), (1,))
         dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    elif T is not None:
+        flat = torch.cat([AV.reshape(-1), BV.reshape(-1), T.reshape(-1)])
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+        AV.copy_(flat[:n].view_as(AV))
+        BV.copy_(flat[n:2 * n].view_as(BV))
+        T.copy_(flat[2 * n:])
     else:
         flat = torch.stack([AV, BV])
         dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)

@@ -1,0 +1,5 @@
+bash scripts/gpu_mr.sh 2>&1 | head -3
+for r in 1 2; do
+for f in "" "--split-step" "--split-step --no-tables"; do
+  python bench.py --steps 1000 --warmup 20 --no-cpu-baseline --no-e2e $f | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$f', round(d['ms_per_step']*1e3,2), 'us', d['config']['step'], d['roofline']['phases'] if 'products_ms' in d['roofline']['phases'] else '')"
+done; done

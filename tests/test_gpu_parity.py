@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 import torch
 
-from tests.gpu_harness import check_cca_step, oracle_cca_step, rel_err, random_state
+from tests.gpu_harness import check_cca_step, gram_ref, oracle_cca_step, rel_err, random_state
 
 pytestmark = pytest.mark.gpu
 
@@ -419,3 +419,87 @@ def test_staged_tensor_core_products_still_match(geig, monkeypatch):
     for math, tol in (("bf16", 1e-2), ("bf16x2", 1e-3)):
         errs, _ = check_cca_step(geig, 3, 1024, k=64, dx=2048, dy=1024, math=math)
         _assert(errs, tol)
+
+
+# --- multi-GPU form: products + Gram tables aggregated across ranks -------------
+
+@pytest.mark.parametrize("math,tol_p,tol_s", [("bf16x2", 1e-4, 1e-3), ("bf16", 1e-2, 1e-2)])
+def test_products_tables_two_shards_match_appendix_f(geig, math, tol_p, tol_s):
+    """Appendix F on one GPU: two row shards through
+    geig_products_cca_tables (scale 1/(M h)), their products AND table partials
+    summed (the all-reduce), then geig_update_tables — vs the oracle's
+    aggregated-products step.  The tables (G^A, G^B of each shard's rows) must
+    aggregate like the products."""
+    from oracle import estimators, game
+    from synth import CONFIGS, cca_views
+    from paper_2206_04993_b200.parallel import product_buffers
+    cfg = CONFIGS[2]
+    k, dx, dy, rows, M = 16, 784, 784, 512, 2
+    x, y = cca_views(cfg, M * rows, seed=3)
+    d = dx + dy
+    V, aux = random_state(k, d, 5)
+    V = V.astype(np.float32).astype(np.float64)
+    aux = aux.astype(np.float32).astype(np.float64)
+    dev = "cuda:0"
+    s = geig.Solver(geig.GEIG_CCA, dx, dy, k, math=math, data_dtype=geig.GEIG_DATA_BF16, rho=cfg.rho, max_rows=rows)
+    try:
+        s.set_state(torch.tensor(V, dtype=torch.float32, device=dev), torch.tensor(aux, dtype=torch.float32, device=dev))
+        nt = geig.geig_table_floats(s.h)
+        AV, BV, T = product_buffers(k, d, nt, device=dev)
+        AV1, BV1, T1 = product_buffers(k, d, nt, device=dev)
+        xd, yd = x.to(dev), y.to(dev)
+        scale = 1.0 / (M * (rows // 2))
+        geig.geig_products_cca_tables(s.h, xd[:rows].contiguous(), yd[:rows].contiguous(), rows, scale, AV, BV, T)
+        geig.geig_products_cca_tables(s.h, xd[rows:].contiguous(), yd[rows:].contiguous(), rows, scale, AV1, BV1, T1)
+        AV += AV1
+        BV += BV1
+        T += T1
+        geig.geig_update_tables(s.h, AV, BV, T, cfg.eta, cfg.gamma)
+        V2g, aux2g = s.state()
+        ga, gb, gc = s.gram()
+    finally:
+        s.close()
+    x64, y64 = x.double().numpy(), y.double().numpy()
+    machines = [estimators.cca_products(x64[:rows], y64[:rows], V), estimators.cca_products(x64[rows:], y64[rows:], V)]
+    V2, aux2 = game.step_alg2_appendix_f(V, aux, machines, cfg.eta, cfg.gamma, cfg.rho)
+    av = sum(m[0] for m in machines) / M
+    bv = sum(m[1] for m in machines) / M
+    ga_r, gb_r, gc_r = gram_ref(V, aux, av, bv)
+    errs = dict(av=rel_err(AV.double().cpu().numpy(), av), bv=rel_err(BV.double().cpu().numpy(), bv),
+                ga=rel_err(ga.double().cpu().numpy(), ga_r), gb=rel_err(gb.double().cpu().numpy(), gb_r),
+                gc=rel_err(gc.double().cpu().numpy(), gc_r), aux=rel_err(aux2g.double().cpu().numpy(), aux2))
+    step = rel_err(V2g.double().cpu().numpy() - V, V2 - V)
+    _assert(dict(errs, sphere=0.0), tol_p)
+    assert step < tol_s, (step, errs)
+
+
+def test_products_tables_single_shard_equals_fused_step(geig):
+    """One rank: geig_products_cca_tables + geig_update_tables reproduce the
+    fused single-launch step (same products, same tables, same update)."""
+    from synth import CONFIGS, cca_views
+    from paper_2206_04993_b200.parallel import product_buffers
+    cfg = CONFIGS[3]
+    rows = 4096
+    x, y = cca_views(cfg, rows, seed=7)
+    V, aux = random_state(cfg.k, cfg.d, 2)
+    dev = "cuda:0"
+    out = []
+    for mode in ("fused", "tables"):
+        s = geig.Solver(geig.GEIG_CCA, cfg.dx, cfg.dy, cfg.k, math="bf16x2", data_dtype=geig.GEIG_DATA_BF16,
+                        rho=cfg.rho, max_rows=rows)
+        try:
+            s.set_state(torch.tensor(V, dtype=torch.float32, device=dev),
+                        torch.tensor(aux, dtype=torch.float32, device=dev))
+            xd, yd = x.to(dev), y.to(dev)
+            if mode == "fused":
+                geig.geig_step_cca(s.h, xd, yd, rows, cfg.eta, cfg.gamma)
+            else:
+                AV, BV, T = product_buffers(cfg.k, cfg.d, geig.geig_table_floats(s.h), device=dev)
+                geig.geig_products_cca_tables(s.h, xd, yd, rows, 1.0 / (rows // 2), AV, BV, T)
+                geig.geig_update_tables(s.h, AV, BV, T, cfg.eta, cfg.gamma)
+            out.append([t.double().cpu().numpy() for t in s.state()])
+        finally:
+            s.close()
+    (Vf, af), (Vt, at) = out
+    assert rel_err(Vt - V, Vf - V) < 1e-5
+    assert rel_err(at, af) < 1e-6
