@@ -47,6 +47,7 @@ struct FusedParams {
                                    // holds tm x more batch bytes in flight per byte of V / Z re-read
   int nsteps;                      // steps of Alg. 2 run by this launch (one batch each)
   int products_only;               // 1: phases F, S, B only (AV, BV to global; multi-GPU: all-reduce, then geig_update)
+  int update_only;                 // phase U only (multi-GPU: from the all-reduced products and tables)
   int tables;                      // products-only launch that also forms the Gram tables (G^A, G^B of the
                                    // local rows into upd.raw_a, G^C of the state into upd.raw)
   uint32_t bar_off;                // smem offset of the ring mbarriers (past the ring AND the update arena)
@@ -334,6 +335,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   for (int t = 0; t < p.nsteps; ++t) {
   const CUtensorMap* A = p.xmaps ? p.xmaps + 6 * t : maps.a;
   if (t > 0) stamp(p.upd, 4);
+  if (!p.update_only) {   // (update-only launch: phase U alone, from given products and tables)
   if (threadIdx.x == 0)
     for (int v = 0; v < 2; ++v) tma_prefetch_desc(&A[v]);
 
@@ -551,6 +553,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   grid.sync();
   stamp(p.upd, 7);
   dstamp(p.upd, 7);
+  }  // !update_only
 
   // ---- phase U: Gram tables + fused update ----
   if (!p.products_only && !(p.dbg_mode & 64))
@@ -607,7 +610,7 @@ inline bool make_batch_maps(CUtensorMap* a, const TcPlan& t, const void* X, cons
 inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* const* Y, int nsteps, int64_t b,
                                   float scale, const __nv_bfloat16* Vbf, float* AV, float* BV, UpdateArgs upd,
                                   int grid_ctas, size_t upd_bytes, cudaStream_t st, bool products_only = false,
-                                  bool tables = false) {
+                                  bool tables = false, bool update_only = false) {
   if (!t.ready || t.math != GEIG_MATH_BF16) return tc_fail(GEIG_ERR_STATE, "fused step needs the bf16 plan");
   if (nsteps < 1) return tc_fail(GEIG_ERR_ARG, "nsteps < 1");
   // (t.math is BF16 for both GEIG_MATH_BF16 and GEIG_MATH_BF16X2; t.splitb selects hi+lo operands)
@@ -616,10 +619,13 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   const int64_t dv[2] = {t.dx, t.dy};
   FusedMaps maps;
   FusedParams p{};
-  if (!make_batch_maps(maps.a, t, X[0], Y[0], h)) return tc_fail(GEIG_ERR_CUDA, "tensor map encode (batch) failed");
+  if (update_only && (products_only || nsteps != 1)) return tc_fail(GEIG_ERR_ARG, "update-only launch: one step");
+  if (!update_only && !make_batch_maps(maps.a, t, X[0], Y[0], h))
+    return tc_fail(GEIG_ERR_CUDA, "tensor map encode (batch) failed");
   p.nsteps = nsteps;
   p.products_only = products_only ? 1 : 0;
   p.tables = (products_only && tables) ? 1 : 0;
+  p.update_only = update_only ? 1 : 0;
   if (products_only && nsteps != 1) return tc_fail(GEIG_ERR_ARG, "products-only launch runs one step");
   p.xmaps = nullptr;
   if (nsteps > 1) {
@@ -655,7 +661,7 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
       return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused forward) failed");
     if (t.splitb && !make_map(&maps.bFlo[v], vb + (int64_t)k * t.d * eb, eb, dv[v], k, t.d, ATOM, t.BN))
       return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused forward lo) failed");
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < 2 && !update_only; ++s) {
       const char* zb = (const char*)t.Zb + (int64_t)(v * 2 + s) * k * t.hpad * eb;
       if (!make_map(&maps.bB[v * 2 + s], zb, eb, h, k, t.hpad, ATOM, t.BN))
         return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused backward) failed");

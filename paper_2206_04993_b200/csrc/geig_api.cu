@@ -392,6 +392,19 @@ extern "C" geig_status geig_update_tables(geig_solver* s, const float* AV, const
   a.AV = AV; a.BV = BV;
   a.raw_a = const_cast<float*>(T);
   a.pre_reduced = 1;
+  if ((s->math == GEIG_MATH_BF16 || s->math == GEIG_MATH_BF16X2) && !getenv("GEIG_NO_FUSED") &&
+      ((uintptr_t)AV | (uintptr_t)BV) % 16 == 0) {
+    // phase U of the fused kernel alone (TMA-staged tiles, early table staging)
+    const void* none[1] = {nullptr};
+    geig_status st = tc::fused_cca_step(s->tc, none, none, 1, 0, 1.f, s->Vbf, const_cast<float*>(AV),
+                                        const_cast<float*>(BV), a, s->upd_grid, s->upd_smem, s->stream,
+                                        /*products_only=*/false, /*tables=*/false, /*update_only=*/true);
+    if (st) return fail(st, "%s", tc::last_error());
+    s->launches++;
+    s->fused_last = false;
+    advance_variant_state(s, 1);
+    return GEIG_OK;
+  }
   void* args[] = {&a};
   const bool vec = ((uintptr_t)AV | (uintptr_t)BV) % 16 == 0;
   void* fn = vec ? (void*)update_res_kernel<true> : (void*)update_res_kernel<false>;
