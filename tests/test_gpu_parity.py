@@ -423,8 +423,11 @@ def test_staged_tensor_core_products_still_match(geig, monkeypatch):
 
 # --- multi-GPU form: products + Gram tables aggregated across ranks -------------
 
-@pytest.mark.parametrize("math,tol_p,tol_s", [("bf16x2", 1e-4, 1e-3), ("bf16", 1e-2, 1e-2)])
-def test_products_tables_two_shards_match_appendix_f(geig, math, tol_p, tol_s):
+@pytest.mark.parametrize("math,tol_p,tol_s,k,dx,dy,rows", [("bf16x2", 1e-4, 1e-3, 16, 784, 784, 512),
+                                                           ("bf16", 1e-2, 1e-2, 16, 784, 784, 512),
+                                                           ("bf16x2", 1e-4, 1e-3, 24, 200, 136, 301),
+                                                           ("bf16x2", 1e-4, 1e-3, 5, 64, 8, 130)])
+def test_products_tables_two_shards_match_appendix_f(geig, math, tol_p, tol_s, k, dx, dy, rows):
     """Appendix F on one GPU: two row shards through
     geig_products_cca_tables (scale 1/(M h)), their products AND table partials
     summed (the all-reduce), then geig_update_tables — vs the oracle's
@@ -434,8 +437,9 @@ def test_products_tables_two_shards_match_appendix_f(geig, math, tol_p, tol_s):
     from synth import CONFIGS, cca_views
     from paper_2206_04993_b200.parallel import product_buffers
     cfg = CONFIGS[2]
-    k, dx, dy, rows, M = 16, 784, 784, 512, 2
+    M = 2
     x, y = cca_views(cfg, M * rows, seed=3)
+    x, y = x[:, :dx].contiguous(), y[:, :dy].contiguous()
     d = dx + dy
     V, aux = random_state(k, d, 5)
     V = V.astype(np.float32).astype(np.float64)
