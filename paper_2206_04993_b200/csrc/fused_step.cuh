@@ -285,7 +285,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
   __syncwarp();
 }
 
-template <int EB>
+template <int EB, bool ADAM>
 __global__ void __launch_bounds__(FS_THREADS, 1)
 cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   cg::grid_group grid = cg::this_grid();
@@ -557,7 +557,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
 
   // ---- phase U: Gram tables + fused update ----
   if (!p.products_only && !(p.dbg_mode & 64))
-    update_res_phases<true, 1>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um, t);
+    update_res_phases<true, 1, ADAM>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um, t);
   if (t + 1 < p.nsteps) {
     // next step: its forward TMA reads the new bf16 shadow of V (generic
     // stores above) and refills the smem ring the update phase used
@@ -720,12 +720,16 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   if (smem > 227 * 1024) return tc_fail(GEIG_ERR_UNSUPPORTED, "fused step: shared memory budget exceeded");
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(cca_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+    if (cudaFuncSetAttribute(cca_step_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(cca_step_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+            cudaSuccess)
       return tc_fail(GEIG_ERR_CUDA, "cudaFuncSetAttribute(cca_step_kernel) failed");
     attr = true;
   }
   void* args[] = {(void*)&maps, (void*)&p};
-  cudaError_t e = cudaLaunchCooperativeKernel((void*)cca_step_kernel<2>, dim3(grid_ctas), dim3(FS_THREADS), args, smem, st);
+  void* kfn = p.upd.adam ? (void*)cca_step_kernel<2, true> : (void*)cca_step_kernel<2, false>;
+  cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(grid_ctas), dim3(FS_THREADS), args, smem, st);
   if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("cca_step_kernel launch: ") + cudaGetErrorString(e));
   return GEIG_OK;
 }

@@ -604,7 +604,11 @@ struct UpdMaps {
 // arena, so the fused step kernel (fused_step.cuh) can run it after its GEMM
 // phases inside the same cooperative launch.  `um` (param-space tensor maps)
 // selects TMA staging of the tiles; nullptr stages them with cp.async.
-template <bool VEC, int PRE = -1>   // PRE: -1 runtime p.pre_reduced, 0 / 1 compile-time (fused kernel: 1)
+// PRE: -1 runtime p.pre_reduced, 0 / 1 compile-time (fused kernel: 1).
+// ADAM: the Appendix-H branch of the write-back is compiled in (runtime
+// p.adam); the fused kernel's plain instance leaves it out (its untaken
+// per-element branch measured ~1 us of the update phase).
+template <bool VEC, int PRE = -1, bool ADAM = true>
 __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* smem, cg::grid_group& grid,
                                                   const UpdMaps* um = nullptr, int step = 0) {
   const int tid = threadIdx.x;
@@ -1077,7 +1081,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
       const float4 xa = *reinterpret_cast<const float4*>(Ct + i * S + 4 * q);
       const float ni = Ns[i];
       float4 vn, an;
-      if (p.adam) {
+      if (ADAM && p.adam) {
         // Appendix H: Adam ascent on v_i with the Alg. 2 direction as the gradient
         const size_t o0 = (size_t)i * d + gx;
         float4 m4 = *reinterpret_cast<const float4*>(p.am + o0);
