@@ -163,7 +163,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
           if (rs.it_prod >= S) mbar_wait(&empty_bar[st], ((rs.it_prod / S) + 1) & 1);
           uint8_t* sa = ring + st * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          const bool nob = (p.dbg_mode & 2) != 0;
+          const bool nob = (kDevKnobs && (p.dbg_mode & 2) != 0);
           const uint32_t abytes = (uint32_t)it.mt * A_TILE;
           mbar_expect_tx(&full_bar[st], abytes + (nob ? 0u : STAGE_BYTES - A_BYTES));
           const int k0 = (it.kb0[s] + j) * BK;
@@ -212,7 +212,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
             const uint32_t sa = sa0 + (uint32_t)mtile * A_TILE;
 #pragma unroll
             for (int kk = 0; kk < BK / UK; ++kk) {
-              if (p.dbg_mode & 1) break;
+              if (kDevKnobs && (p.dbg_mode & 1)) break;
               const uint64_t ad = A_MN ? make_sdesc(sa + kk * UK * 128, BK * 128, 1024) : make_sdesc(sa + kk * 32, 16, 1024);
               const uint64_t bd = make_sdesc(sb + kk * 32, 16, 1024);
               umma<EB>(d_tmem, ad, bd, idesc, (j > 0 || kk > 0) ? 1u : 0u);
@@ -255,7 +255,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
           for (int j = 0; j < 16; ++j)
             ws[j * 32 + lane] = it.scale * (p.split ? __uint_as_float(r[j]) + __uint_as_float(rl[j]) : __uint_as_float(r[j]));
           __syncwarp();
-          if (!p.dbg_nostore) {
+          if (!(kDevKnobs && p.dbg_nostore)) {
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
               const int jn = 4 * g + rr, n = c0 + jn;
@@ -343,7 +343,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   if (warp == 2 || warp == 3) {
     if (!p.products_only || p.tables) gram_c_side(p.upd, threadIdx.x - 64);
     if (threadIdx.x == 64) tstamp(p.upd, 31);
-  } else if (!(p.dbg_mode & 8)) {
+  } else if (!(kDevKnobs && (p.dbg_mode & 8))) {
     gemm_phase<EB, false>(maps, A, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs,
                           epi_stage);
     if (threadIdx.x == 32) tstamp(p.upd, 29);
@@ -524,7 +524,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&A[2 + v]); tma_prefetch_desc(&maps.bB[v]); }
   if (warp == 2 || warp == 3) {    // warps 2-3: reduce the (now complete) Gram partial rows
     if (!p.products_only || p.tables) reduce_side(p.upd, threadIdx.x - 64, side_scratch);
-  } else if (!(p.dbg_mode & 32)) {
+  } else if (!(kDevKnobs && (p.dbg_mode & 32))) {
     gemm_phase<EB, true>(maps, A, p, 2 * (p.mtB[0] + p.mtB[1]), ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs,
                          epi_stage);
   }
@@ -556,7 +556,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   }  // !update_only
 
   // ---- phase U: Gram tables + fused update ----
-  if (!p.products_only && !(p.dbg_mode & 64))
+  if (!p.products_only && !(kDevKnobs && (p.dbg_mode & 64)))
     update_res_phases<true, 1, ADAM>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um, t);
   if (t + 1 < p.nsteps) {
     // next step: its forward TMA reads the new bf16 shadow of V (generic

@@ -471,7 +471,13 @@ constexpr int UPD_GS = 3;           // column slices of the Gram phase (UPD_GT *
 #define GEIG_PEN_UNROLL 4
 #endif
 constexpr int kPenUnroll = GEIG_PEN_UNROLL;   // penalty-sum j unroll (developer A/B: -DGEIG_PEN_UNROLL=n)
-constexpr int UPD_LTS = 72;         // Lt row stride: the tf32 A fragments (rows t, t+4 x cols g) are bank-conflict free
+#ifndef GEIG_DEV_KNOBS
+#define GEIG_DEV_KNOBS 0
+#endif
+// developer timing knobs (GEIG_DBG_MODE / GEIG_DBG_NOSTORE: skip work, wrong
+// results) are compiled in only with -DGEIG_DEV_KNOBS=1 (GEIG_NVCC_EXTRA)
+constexpr bool kDevKnobs = GEIG_DEV_KNOBS;
+constexpr int UPD_LTS = 72;         // Lt row stride (padded)
 constexpr int UPD_AUXF = 64 * UPD_LTS + 4 * 64 + 8 * 32 + 64 * 65 + 128;   // Lt | N, 1/s^2, D1, D2 | red | raw
 constexpr int UPD_GREDF = (UPD_GS - 1) * UPD_GT * 64;                // Gram slice partials (aliases the above)
 
@@ -714,7 +720,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
       float acc[36];
 #pragma unroll
       for (int e = 0; e < 36; ++e) acc[e] = 0.f;
-      const int q0 = sl * nq / 4, q1 = (p.dbg_mode & 128) ? q0 : (sl + 1) * nq / 4;
+      const int q0 = sl * nq / 4, q1 = (kDevKnobs && (p.dbg_mode & 128)) ? q0 : (sl + 1) * nq / 4;
 #pragma unroll 1
       for (int q = q0; q < q1; ++q) {
         float4 va[8], pc[8];
@@ -1021,7 +1027,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
 #pragma unroll
         for (int b = 0; b < 4; ++b) accA[a][b] = accB[a][b] = 0.f;
       const float* cp = Ct + 4 * q;
-      int j = (p.dbg_mode & 512) ? jB : 0;   // developer: skip the penalty sums (timing only)
+      int j = (kDevKnobs && (p.dbg_mode & 512)) ? jB : 0;   // developer: skip the penalty sums (timing only)
 #pragma unroll kPenUnroll
       for (; j < jA; ++j) {
         const float4 x = *reinterpret_cast<const float4*>(cp + j * S);
@@ -1116,7 +1122,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
       an.z = xa.z + p.gamma * (ni * bv.z - xa.z);
       an.w = xa.w + p.gamma * (ni * bv.w - xa.w);
       const size_t o = (size_t)i * d + gx;
-      if (p.dbg_mode & 256) {   // developer: no state write-back (timing only)
+      if (kDevKnobs && (p.dbg_mode & 256)) {   // developer: no state write-back (timing only)
         if (vn.x == 12345.f && an.x == 12345.f) p.V[o] = 0.f;
       } else if (VEC && gx + 3 < c1) {
         *reinterpret_cast<float4*>(p.V + o) = vn;
