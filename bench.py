@@ -185,7 +185,8 @@ def run_reference(args, cfg, rank, world):
         return
     # warmup steps (untimed), then K timed steps, each a full oracle step
     oracle_sample(cfg, 0.0, max_steps=max(1, args.warmup))
-    v, n, rows, el = oracle_sample(cfg, 1e9, max_steps=args.steps)
+    # K full oracle steps, bounded to ~150 s of host time (the line reports the steps run)
+    v, n, rows, el = oracle_sample(cfg, 150.0, max_steps=args.steps)
     unit = "samples/s" if cfg.problem == "cca" else "steps/s"
     cores = _blas_threads()
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": unit, "n_gpus": world,
