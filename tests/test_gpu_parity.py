@@ -477,9 +477,11 @@ def test_products_tables_two_shards_match_appendix_f(geig, math, tol_p, tol_s, k
     assert step < tol_s, (step, errs)
 
 
-def test_products_tables_single_shard_equals_fused_step(geig):
+@pytest.mark.parametrize("variant", ["alg2", "alg3", "adam"])
+def test_products_tables_single_shard_equals_fused_step(geig, variant):
     """One rank: geig_products_cca_tables + geig_update_tables reproduce the
-    fused single-launch step (same products, same tables, same update)."""
+    fused single-launch step (same products, same tables, same update), for
+    Alg. 2, Alg. 3 (smooth denominators) and Adam ascent, over 3 steps."""
     from synth import CONFIGS, cca_views
     from paper_2206_04993_b200.parallel import product_buffers
     cfg = CONFIGS[3]
@@ -494,13 +496,18 @@ def test_products_tables_single_shard_equals_fused_step(geig):
         try:
             s.set_state(torch.tensor(V, dtype=torch.float32, device=dev),
                         torch.tensor(aux, dtype=torch.float32, device=dev))
+            if variant == "alg3":
+                geig.geig_set_smooth(s.h, 10.0)
+            if variant == "adam":
+                geig.geig_set_adam(s.h, 0.9, 0.999, 1e-8)
             xd, yd = x.to(dev), y.to(dev)
-            if mode == "fused":
-                geig.geig_step_cca(s.h, xd, yd, rows, cfg.eta, cfg.gamma)
-            else:
-                AV, BV, T = product_buffers(cfg.k, cfg.d, geig.geig_table_floats(s.h), device=dev)
-                geig.geig_products_cca_tables(s.h, xd, yd, rows, 1.0 / (rows // 2), AV, BV, T)
-                geig.geig_update_tables(s.h, AV, BV, T, cfg.eta, cfg.gamma)
+            for _ in range(3):
+                if mode == "fused":
+                    geig.geig_step_cca(s.h, xd, yd, rows, cfg.eta, cfg.gamma)
+                else:
+                    AV, BV, T = product_buffers(cfg.k, cfg.d, geig.geig_table_floats(s.h), device=dev)
+                    geig.geig_products_cca_tables(s.h, xd, yd, rows, 1.0 / (rows // 2), AV, BV, T)
+                    geig.geig_update_tables(s.h, AV, BV, T, cfg.eta, cfg.gamma)
             out.append([t.double().cpu().numpy() for t in s.state()])
         finally:
             s.close()
