@@ -355,6 +355,9 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   stamp(p.upd, 5);
   dstamp(p.upd, 3);
 
+  if (threadIdx.x == 0)   // the backward's descriptors, ahead of phase B
+    for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&A[2 + v]); tma_prefetch_desc(&maps.bB[v]); }
+
   // ---- phase S: sum partials, route halves, cast to bf16; Gram tables G^A, G^B ----
   // CTA c owns a contiguous range of sample rows of each half.  For every
   // row it sums the split-K partials of z = X_v v''^T (both views, both
@@ -554,6 +557,9 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   stamp(p.upd, 7);
   dstamp(p.upd, 7);
   }  // !update_only
+
+  if (t + 1 < p.nsteps && p.xmaps && threadIdx.x == 0)   // the next step's batch descriptors, ahead of its phase F
+    for (int v = 0; v < 2; ++v) tma_prefetch_desc(p.xmaps + 6 * (t + 1) + v);
 
   // ---- phase U: Gram tables + fused update ----
   if (!p.products_only && !(kDevKnobs && (p.dbg_mode & 64)))
