@@ -28,6 +28,7 @@ namespace geig { namespace tc {
 namespace cg = cooperative_groups;
 
 constexpr int FS_THREADS = 256;
+constexpr int GEIG_COEF_FLOATS = 64 * UPD_LTS + 4 * 64;   // Lt | N | 1/s^2 | D1 | D2 (coef_early)
 constexpr int TC_RUN_CHUNK = 4096;   // steps per persistent launch (per-step A maps: 3 MiB device + pinned)
 
 struct FusedMaps {
@@ -42,6 +43,13 @@ struct FusedMaps {
 
 struct FusedParams {
   int rows, h, k, BN, stages, splitsF, mtF, mtB[2], split, bwd_y_first, dbg_nostore, dbg_mode, l2_keep;
+  // Early coefficients: every CTA counts its finished slice of the Gram
+  // reduction on rcnt (monotonic across launches: step e = rc_epoch + t needs
+  // G (e + 1)); warps 2-3 wait for all slices during phase B and form the
+  // update's coefficients there (coef_early) instead of at the start of U
+  int* rcnt;
+  long long rc_epoch;
+  int early_coef;
   int tmF, tmB;                    // 128-row M tiles per work item (forward: sample rows; backward: feature
                                    // columns): tm tiles share one B-operand tile per K step, so the ring
                                    // holds tm x more batch bytes in flight per byte of V / Z re-read
@@ -304,6 +312,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce_bar + 1);
   float* side_scratch = reinterpret_cast<float*>(acce_bar + 3);   // 64 floats for warps 2-3
   float* epi_stage = reinterpret_cast<float*>(smem + p.bar_off + 512);   // 4 x 2 KB epilogue transpose tiles
+  float* coef_smem = epi_stage + 4 * 16 * 32;                              // early coefficients (GEIG_COEF_FLOATS)
   const int warp = threadIdx.x >> 5;
   constexpr uint32_t NCOLS = 256;   // >= tm * BN * (split ? 2 : 1): one accumulator per M tile of an item
 
@@ -526,7 +535,32 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   if (threadIdx.x == 0)
     for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&A[2 + v]); tma_prefetch_desc(&maps.bB[v]); }
   if (warp == 2 || warp == 3) {    // warps 2-3: reduce the (now complete) Gram partial rows
-    if (!p.products_only || p.tables) reduce_side(p.upd, threadIdx.x - 64, side_scratch);
+    if (!p.products_only || p.tables) {
+      reduce_side(p.upd, threadIdx.x - 64, side_scratch);
+      if (threadIdx.x == 64) tstamp(p.upd, 27);
+      if (p.rcnt) {
+        asm volatile("bar.sync 1, 64;" ::: "memory");
+        if (threadIdx.x == 64) {
+          __threadfence();
+          atomicAdd(p.rcnt, 1);
+        }
+        if (p.early_coef) {
+          if (threadIdx.x == 64) {
+            const int target = (int)((p.rc_epoch + t + 1) * (long long)gridDim.x);
+            int v;
+            long long polls = 0;
+            do {
+              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p.rcnt) : "memory");
+              if (++polls > (1ll << 22)) __trap();   // a lost count must fail loudly (seconds), never hang
+            } while (v - target < 0);
+          }
+          asm volatile("bar.sync 1, 64;" ::: "memory");
+          if (threadIdx.x == 64) tstamp(p.upd, 12);
+          coef_early(p.upd, coef_smem, t, threadIdx.x - 64);
+          if (threadIdx.x == 64) tstamp(p.upd, 10);
+        }
+      }
+    }
   } else if (!(kDevKnobs && (p.dbg_mode & 32))) {
     gemm_phase<EB, true>(maps, A, p, 2 * (p.mtB[0] + p.mtB[1]), ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs,
                          epi_stage);
@@ -563,7 +597,8 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
 
   // ---- phase U: Gram tables + fused update ----
   if (!p.products_only && !(kDevKnobs && (p.dbg_mode & 64)))
-    update_res_phases<true, 1, ADAM>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um, t);
+    update_res_phases<true, 1, ADAM>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um, t,
+                                     p.early_coef ? coef_smem : nullptr);
   if (t + 1 < p.nsteps) {
     // next step: its forward TMA reads the new bf16 shadow of V (generic
     // stores above) and refills the smem ring the update phase used
@@ -616,7 +651,7 @@ inline bool make_batch_maps(CUtensorMap* a, const TcPlan& t, const void* X, cons
 inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* const* Y, int nsteps, int64_t b,
                                   float scale, const __nv_bfloat16* Vbf, float* AV, float* BV, UpdateArgs upd,
                                   int grid_ctas, size_t upd_bytes, cudaStream_t st, bool products_only = false,
-                                  bool tables = false, bool update_only = false) {
+                                  bool tables = false, bool update_only = false, long long* rc_epoch = nullptr) {
   if (!t.ready || t.math != GEIG_MATH_BF16) return tc_fail(GEIG_ERR_STATE, "fused step needs the bf16 plan");
   if (nsteps < 1) return tc_fail(GEIG_ERR_ARG, "nsteps < 1");
   // (t.math is BF16 for both GEIG_MATH_BF16 and GEIG_MATH_BF16X2; t.splitb selects hi+lo operands)
@@ -632,6 +667,24 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.products_only = products_only ? 1 : 0;
   p.tables = (products_only && tables) ? 1 : 0;
   p.update_only = update_only ? 1 : 0;
+  // Gram-reduction counter: every launch that runs the reduction (full steps,
+  // products + tables) counts it; the full steps also use it for the early
+  // coefficients.  The solver's epoch advances only with a launch that was
+  // enqueued (below), so targets always match the counts.
+  p.rcnt = nullptr;
+  p.rc_epoch = 0;
+  p.early_coef = 0;
+  const bool runs_reduce = !update_only && (!products_only || tables);
+  if (rc_epoch && runs_reduce && !getenv("GEIG_NO_EARLY_COEF")) {
+    if (!t.dep) {
+      if (cudaMalloc((void**)&t.dep, 64 * sizeof(int)) != cudaSuccess ||
+          cudaMemsetAsync(t.dep, 0, 64 * sizeof(int), st) != cudaSuccess)
+        return tc_fail(GEIG_ERR_CUDA, "allocating the Gram-reduction counter failed");
+    }
+    p.rcnt = t.dep;
+    p.rc_epoch = *rc_epoch;
+    p.early_coef = products_only ? 0 : 1;
+  }
   if (products_only && nsteps != 1) return tc_fail(GEIG_ERR_ARG, "products-only launch runs one step");
   p.xmaps = nullptr;
   if (nsteps > 1) {
@@ -722,8 +775,12 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.stages = (int)std::min<size_t>(TC_MAX_STAGES, (200 * 1024) / stage_bytes);
   p.bar_off = (uint32_t)((std::max((size_t)p.stages * stage_bytes, upd_bytes) + 15) & ~(size_t)15);
   static_assert((2 * TC_MAX_STAGES + 4) * 8 + 64 * 4 <= 512, "barrier + scratch area");
-  const size_t smem = 1024 + p.bar_off + 512 + 4 * 16 * 32 * 4;
+  size_t smem = 1024 + p.bar_off + 512 + 4 * 16 * 32 * 4;
   if (smem > 227 * 1024) return tc_fail(GEIG_ERR_UNSUPPORTED, "fused step: shared memory budget exceeded");
+  if (p.early_coef) {   // the coefficient region follows the epilogue tiles when it fits
+    if (smem + (size_t)GEIG_COEF_FLOATS * 4 <= 227 * 1024) smem += (size_t)GEIG_COEF_FLOATS * 4;
+    else p.early_coef = 0;
+  }
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(cca_step_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
@@ -737,6 +794,7 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   void* kfn = p.upd.adam ? (void*)cca_step_kernel<2, true> : (void*)cca_step_kernel<2, false>;
   cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(grid_ctas), dim3(FS_THREADS), args, smem, st);
   if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("cca_step_kernel launch: ") + cudaGetErrorString(e));
+  if (p.rcnt) *rc_epoch += nsteps;
   return GEIG_OK;
 }
 

@@ -495,6 +495,7 @@ struct TcPlan {
   CUtensorMap* xm_host = nullptr;   // pinned staging of the same
   int xm_cap = 0;                   // steps of capacity
   cudaEvent_t xm_ev = nullptr;      // last copy of the staging buffer
+  int* dep = nullptr;               // fused step: Gram-reduction counter (monotonic, zeroed once)
   int x3 = 0;                       // 3xTF32 products (tf32 plan with hi/lo operands)
   float* Vx3 = nullptr;             // 3xTF32: [hi plane | lo plane] of V (2 x k x d fp32)
 };
@@ -660,6 +661,8 @@ inline void plan_destroy(TcPlan& t) {
   if (t.xm_dev) cudaFree(t.xm_dev);
   if (t.xm_host) cudaFreeHost(t.xm_host);
   if (t.xm_ev) cudaEventDestroy(t.xm_ev);
+  if (t.dep) cudaFree(t.dep);
+  t.dep = nullptr;
   t.xm_dev = nullptr; t.xm_host = nullptr; t.xm_cap = 0; t.xm_ev = nullptr;
   t.Zt = nullptr; t.Zb = nullptr; t.ready = 0;
 }

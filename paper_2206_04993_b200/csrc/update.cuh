@@ -610,13 +610,95 @@ struct UpdMaps {
 // arena, so the fused step kernel (fused_step.cuh) can run it after its GEMM
 // phases inside the same cooperative launch.  `um` (param-space tensor maps)
 // selects TMA staging of the tiles; nullptr stages them with cp.async.
+// Coefficients of the update (Alg. 2 lines 8-11, the phase-3a algebra
+// below) formed by warps 2-3 of the fused kernel during the backward phase,
+// as soon as every CTA's slice of the Gram reduction is in p.raw (64 threads,
+// named barrier 1; thread i owns player i).  `cf` (shared memory outside the
+// GEMM ring): Lt [64][UPD_LTS] (Lt[j][i] = L_ij) | N | 1/s^2 | D1 | D2.  The
+// raw rows are read from global memory (L2): row i of tri(G^A) and tri(G^C)
+// is contiguous.  Also writes this CTA's slice of the normalised tables
+// (geig_get_gram) and, in CTA 0, the Alg. 3 z ascent.
+__device__ __forceinline__ void coef_early(const UpdateArgs& p, float* cf, int step, int t) {
+  const int k = p.k;
+  const int ntri = k * (k + 1) / 2, hA = (ntri + k + 3) & ~3;
+  const float* rA = p.raw_a ? p.raw_a : p.raw;                 // [tri(G^A) | diag(G^B)]
+  const float* rB = rA + ntri;
+  const float* rC = p.raw + hA;                                 // [tri(G^C) | diag ||v''||^2]
+  const float* rN = rC + ntri;
+  float* Lt = cf;
+  float* Ns = Lt + 64 * UPD_LTS;
+  float* IS2 = Ns + 64;
+  float* D1s = IS2 + 64;
+  float* D2s = D1s + 64;
+  const int i = t;
+  {
+    float n = 0.f, is2 = 0.f, gb = 0.f;
+    if (i < k) {
+      n = rsqrtf(__ldcg(rN + i));
+      gb = n * n * __ldcg(rB + i);
+      const float gcii = n * __ldcg(rC + tri_index(i, i));      // <v_i, [Bv]_i>
+      if (p.smooth) {
+        // Alg. 3 l.7: [<v,Bv>]_i = exp(log rho + (log nu - log rho) sigma(z_i))
+        const float* zr = p.zbuf + ((p.zpar + step) & 1) * 64;
+        const float z = zr[i];
+        const float sg = 1.f / (1.f + expf(-z));
+        const float br = expf(p.lnrho + (p.lnnu - p.lnrho) * sg);
+        is2 = 1.f / br;
+        if (blockIdx.x == 0) {   // l.14 / l.21: z_i += gamma (<v_i,[Bv]_i> - br) br (log nu - log rho) sigma (1 - sigma)
+          float* zw = p.zbuf + ((p.zpar + step + 1) & 1) * 64;
+          zw[i] = z + p.gamma * (gcii - br) * br * (p.lnnu - p.lnrho) * sg * (1.f - sg);
+        }
+      } else {
+        is2 = 1.f / fmaxf(gcii, p.rho);                        // Alg. 2 l.8
+      }
+    }
+    Ns[i] = n; IS2[i] = is2; D1s[i] = gb;
+  }
+  asm volatile("bar.sync 1, 64;" ::: "memory");
+  // row i: L_ij = G^B_ii G^A_ij / s_j^2 (j < i) into Lt[j][i]; c_i = sum_{j<i} G^A_ij G^C_ij / s_j^2
+  {
+    const float ni = Ns[i], d1 = D1s[i];
+    const int base = i * (i + 1) / 2;
+    float c = 0.f;
+#pragma unroll 8
+    for (int j = 0; j < 64; ++j) {
+      float l = 0.f;
+      if (i < k && j < i) {
+        const float aij = ni * Ns[j] * __ldcg(rA + base + j);
+        l = d1 * aij * IS2[j];
+        c = fmaf(aij, ni * __ldcg(rC + base + j) * IS2[j], c);
+      }
+      Lt[j * UPD_LTS + i] = l;
+    }
+    D2s[i] = i < k ? ni * ni * __ldcg(rA + base + i) - c : 0.f;
+  }
+  // the step's normalised tables (geig_get_gram), written by all CTAs in slices
+  {
+    const int G = gridDim.x, kk = k * k;
+    const int per = (kk + G - 1) / G;
+    const int e1 = min(kk, (int)(blockIdx.x + 1) * per);
+    for (int e = blockIdx.x * per + t; e < e1; e += 64) {
+      const int ii = e / k, j = e - (e / k) * k;
+      const bool low = j <= ii;
+      const int tij = tri_index(ii, low ? j : 0);
+      p.gram[e] = low ? Ns[ii] * Ns[j] * __ldcg(rA + tij) : 0.f;
+      p.gram[(size_t)kk + e] = (ii == j) ? D1s[ii] : 0.f;
+      p.gram[2 * (size_t)kk + e] = low ? Ns[ii] * __ldcg(rC + tij) : 0.f;
+    }
+  }
+  asm volatile("bar.sync 1, 64;" ::: "memory");
+}
+
 // PRE: -1 runtime p.pre_reduced, 0 / 1 compile-time (fused kernel: 1).
 // ADAM: the Appendix-H branch of the write-back is compiled in (runtime
 // p.adam); the fused kernel's plain instance leaves it out (its untaken
 // per-element branch measured ~1 us of the update phase).
 template <bool VEC, int PRE = -1, bool ADAM = true>
 __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* smem, cg::grid_group& grid,
-                                                  const UpdMaps* um = nullptr, int step = 0) {
+                                                  const UpdMaps* um = nullptr, int step = 0,
+                                                  float* coef = nullptr) {
+  // coef: coefficients already formed (coef_early, fused kernel) — no table
+  // staging, phase 3a skipped
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int k = p.k;
@@ -629,7 +711,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   float* At = Vt + 64 * S;
   float* Ct = At + 64 * S;
   float* Bt = Ct + 64 * S;
-  float* Lt = Bt + 64 * S;                       // [64][UPD_LTS] Lt[j][i]
+  float* Lt = coef ? coef : Bt + 64 * S;         // [64][UPD_LTS] Lt[j][i]
   float* Ns = Lt + 64 * UPD_LTS;
   float* IS2 = Ns + 64;                          // 1 / s_j^2
   float* D1s = IS2 + 64;
@@ -637,14 +719,14 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   float* red = D2s + 64;                         // [8][32]
   float* rs = red + 8 * 32;                      // staged raw tables
   float* gred = Lt;                              // phase 1 only: Gram slice partials
-  uint64_t* tbar = reinterpret_cast<uint64_t*>(Lt + (UPD_AUXF > UPD_GREDF ? UPD_AUXF : UPD_GREDF));
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(Bt + 64 * S + (UPD_AUXF > UPD_GREDF ? UPD_AUXF : UPD_GREDF));
   const int ntri = k * (k + 1) / 2;
   const int hA = (ntri + k + 3) & ~3;            // half row: [tri | diag | pad]
   const int pstride = 2 * hA;                    // per-CTA partial row (16-byte multiple)
   stamp(p, 0);
 
   // ---------------- stage the four tiles once ----------------
-  const bool early_raw = um && (PRE == 1 || (PRE < 0 && p.pre_reduced));
+  const bool early_raw = um && !coef && (PRE == 1 || (PRE < 0 && p.pre_reduced));
   if (early_raw) {
     // pre-reduced tables: stage them first (the coefficients need them
     // before the tiles; the tiles' TMA then streams behind them)
@@ -921,6 +1003,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   dstamp(p, 12);
   }  // !pre_reduced
 
+  if (!coef) {
   // ---------------- phase 3a: coefficients ----------------
   // the reduced raw tables are staged into shared memory with one burst of
   // independent 16-byte async copies, then the coefficients are formed from smem.
@@ -999,6 +1082,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
     }
     __syncthreads();
   }
+  }  // !coef
   dstamp(p, 13);
 
   if (um && (PRE == 1 || (PRE < 0 && p.pre_reduced))) tc::mbar_wait(tbar, 0);   // tiles staged

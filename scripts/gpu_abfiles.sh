@@ -3,6 +3,6 @@ rm -rf /tmp/csrc_new; cp -r paper_2206_04993_b200/csrc /tmp/csrc_new
 for r in 1 2; do
   cp /tmp/csrc_new/* paper_2206_04993_b200/csrc/; python -c "from paper_2206_04993_b200 import build; build.build(force=True)"
   echo new; python scripts/ab.py 2 "A=1" | tail -1
-  cp gpurun_in/*.cuh paper_2206_04993_b200/csrc/; python -c "from paper_2206_04993_b200 import build; build.build(force=True)"
+  cp gpurun_in/* paper_2206_04993_b200/csrc/; python -c "from paper_2206_04993_b200 import build; build.build(force=True)"
   echo old; python scripts/ab.py 2 "A=1" | tail -1
 done
