@@ -226,6 +226,12 @@ static void set_l2_window(geig_solver* s) {
 
 extern "C" geig_status geig_set_stream(geig_solver* s, void* stream) {
   if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  // the fused launches of one solver count the Gram reduction on a shared
+  // counter in launch order: drain the old stream before switching
+  if ((cudaStream_t)stream != s->stream) {
+    CU(cudaSetDevice(s->device));
+    CU(cudaStreamSynchronize(s->stream));
+  }
   s->stream = (cudaStream_t)stream;
   if (s->stream) set_l2_window(s);
   return GEIG_OK;
