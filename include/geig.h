@@ -102,7 +102,9 @@ geig_status geig_create(geig_solver** out, int problem, int64_t dx, int64_t dy,
 /* Destroy the solver and free everything it owns (NULL is a no-op). */
 geig_status geig_destroy(geig_solver* s);
 
-/* Stream (a cudaStream_t passed as void*; NULL = legacy default stream). */
+/* Stream (a cudaStream_t passed as void*; NULL = legacy default stream).
+ * Switching to a different stream first waits for the work already enqueued
+ * on the old one (the solver's fused launches must run in call order). */
 geig_status geig_set_stream(geig_solver* s, void* stream);
 
 /* Block the host until all work enqueued by this solver has finished. */
