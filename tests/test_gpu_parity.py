@@ -514,3 +514,49 @@ def test_products_tables_single_shard_equals_fused_step(geig, variant):
     (Vf, af), (Vt, at) = out
     assert rel_err(Vt - V, Vf - V) < 1e-5
     assert rel_err(at, af) < 1e-6
+
+
+def test_mixed_call_sequence_keeps_the_launch_counters_consistent(geig):
+    """The fused launches of a solver count the Gram reduction on a
+    monotonic counter (early coefficients in phase B).  An arbitrary mix of
+    single steps, multi-step launches, the multi-GPU tables path, standalone
+    updates, state resets and stream switches must neither hang nor drift:
+    two solvers driven by the same sequence end bit-identical, and the
+    fused single step still matches the oracle afterwards."""
+    from synth import CONFIGS, cca_views
+    from paper_2206_04993_b200.parallel import product_buffers
+    cfg = CONFIGS[2]
+    k, dx, dy, rows = 16, 784, 784, 512
+    x, y = cca_views(cfg, 4 * rows, seed=9)
+    dev = "cuda:0"
+    xs = [x[i * rows:(i + 1) * rows].to(dev).contiguous() for i in range(4)]
+    ys = [y[i * rows:(i + 1) * rows].to(dev).contiguous() for i in range(4)]
+    V, aux = random_state(k, dx + dy, 4)
+    outs = []
+    for rep in range(2):
+        s = geig.Solver(geig.GEIG_CCA, dx, dy, k, math="bf16x2", data_dtype=geig.GEIG_DATA_BF16, rho=cfg.rho,
+                        max_rows=rows)
+        try:
+            Vd = torch.tensor(V, dtype=torch.float32, device=dev)
+            Ad = torch.tensor(aux, dtype=torch.float32, device=dev)
+            s.set_state(Vd, Ad)
+            geig.geig_step_cca(s.h, xs[0], ys[0], rows, cfg.eta, cfg.gamma)
+            geig.geig_run_cca(s.h, xs[:3], ys[:3], rows, cfg.eta, cfg.gamma)
+            AV, BV, T = product_buffers(k, dx + dy, geig.geig_table_floats(s.h), device=dev)
+            geig.geig_products_cca_tables(s.h, xs[1], ys[1], rows, 1.0 / (rows // 2), AV, BV, T)
+            geig.geig_update_tables(s.h, AV, BV, T, cfg.eta, cfg.gamma)
+            geig.geig_products_cca(s.h, xs[2], ys[2], rows, 1.0 / (rows // 2), AV, BV)
+            geig.geig_update(s.h, AV, BV, cfg.eta, cfg.gamma)
+            side = torch.cuda.Stream()
+            geig.geig_set_stream(s.h, side.cuda_stream)
+            geig.geig_run_cca(s.h, xs[1:4], ys[1:4], rows, cfg.eta, cfg.gamma)
+            geig.geig_set_stream(s.h, torch.cuda.current_stream().cuda_stream)
+            geig.geig_step_cca(s.h, xs[3], ys[3], rows, cfg.eta, cfg.gamma)
+            outs.append([t.double().cpu().numpy() for t in s.state()])
+        finally:
+            s.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    errs, _ = check_cca_step(geig, 2, rows, k=k, dx=dx, dy=dy, math="bf16x2", use_step=True)
+    step = errs.pop("step")
+    _assert(errs, 1e-4)
+    assert step < 1e-3
