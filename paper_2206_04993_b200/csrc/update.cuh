@@ -467,10 +467,6 @@ update_kernel(UpdateArgs p) {
 constexpr int UPD_RES_WMAX = 168;   // max columns per CTA (smem: 4 x 64 x 172 x 4 B + tables)
 constexpr int UPD_GT = 72;          // 8x4 lower-triangle Gram tiles of a 64 x 64 table
 constexpr int UPD_GS = 3;           // column slices of the Gram phase (UPD_GT * UPD_GS <= UPD_THREADS)
-#ifndef GEIG_PEN_UNROLL
-#define GEIG_PEN_UNROLL 4
-#endif
-constexpr int kPenUnroll = GEIG_PEN_UNROLL;   // penalty-sum j unroll (developer A/B: -DGEIG_PEN_UNROLL=n)
 #ifndef GEIG_DEV_KNOBS
 #define GEIG_DEV_KNOBS 0
 #endif
@@ -1104,37 +1100,57 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
     for (int item = tid; item < 8 * nq4; item += UPD_THREADS) {
       const int pr = item / nq4, q = item - pr * nq4;
       const int iA = 4 * pr, iB = 60 - 4 * pr;
-      const int jA = min(iA + 3, k), jB = min(iB + 3, k);   // L_ij = 0 for j >= i
+      // j bounds rounded up to multiples of 4 (L_ij = 0 for j >= i, the rows
+      // of Ct past k are zero): 4 j per iteration with no remainder branches,
+      // so the 12 shared loads of an iteration issue ahead of its 128 FMAs
+      const int kr = (k + 3) & ~3;
+      const int jA = min(iA + 4, kr), jB = min(iB + 4, kr);
       float accA[4][4], accB[4][4];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) accA[a][b] = accB[a][b] = 0.f;
       const float* cp = Ct + 4 * q;
-      int j = (kDevKnobs && (p.dbg_mode & 512)) ? jB : 0;   // developer: skip the penalty sums (timing only)
-#pragma unroll kPenUnroll
-      for (; j < jA; ++j) {
-        const float4 x = *reinterpret_cast<const float4*>(cp + j * S);
-        const float4 la = *reinterpret_cast<const float4*>(Lt + j * UPD_LTS + iA);
-        const float4 lb = *reinterpret_cast<const float4*>(Lt + j * UPD_LTS + iB);
-        const float xv[4] = {x.x, x.y, x.z, x.w}, lav[4] = {la.x, la.y, la.z, la.w}, lbv[4] = {lb.x, lb.y, lb.z, lb.w};
+      int j0 = (kDevKnobs && (p.dbg_mode & 512)) ? jB : 0;   // developer: skip the penalty sums (timing only)
+#pragma unroll 1
+      for (; j0 < jA; j0 += 4) {
+        float4 x[4], la[4], lb[4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int u = 0; u < 4; ++u) {
+          x[u] = *reinterpret_cast<const float4*>(cp + (j0 + u) * S);
+          la[u] = *reinterpret_cast<const float4*>(Lt + (j0 + u) * UPD_LTS + iA);
+          lb[u] = *reinterpret_cast<const float4*>(Lt + (j0 + u) * UPD_LTS + iB);
+        }
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            accA[a][b] = fmaf(lav[a], xv[b], accA[a][b]);
-            accB[a][b] = fmaf(lbv[a], xv[b], accB[a][b]);
-          }
+        for (int u = 0; u < 4; ++u) {
+          const float xv[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+          const float lav[4] = {la[u].x, la[u].y, la[u].z, la[u].w}, lbv[4] = {lb[u].x, lb[u].y, lb[u].z, lb[u].w};
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              accA[a][b] = fmaf(lav[a], xv[b], accA[a][b]);
+              accB[a][b] = fmaf(lbv[a], xv[b], accB[a][b]);
+            }
+        }
       }
-#pragma unroll kPenUnroll
-      for (; j < jB; ++j) {
-        const float4 x = *reinterpret_cast<const float4*>(cp + j * S);
-        const float4 lb = *reinterpret_cast<const float4*>(Lt + j * UPD_LTS + iB);
-        const float xv[4] = {x.x, x.y, x.z, x.w}, lbv[4] = {lb.x, lb.y, lb.z, lb.w};
+#pragma unroll 1
+      for (; j0 < jB; j0 += 4) {
+        float4 x[4], lb[4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int u = 0; u < 4; ++u) {
+          x[u] = *reinterpret_cast<const float4*>(cp + (j0 + u) * S);
+          lb[u] = *reinterpret_cast<const float4*>(Lt + (j0 + u) * UPD_LTS + iB);
+        }
 #pragma unroll
-          for (int b = 0; b < 4; ++b) accB[a][b] = fmaf(lbv[a], xv[b], accB[a][b]);
+        for (int u = 0; u < 4; ++u) {
+          const float xv[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+          const float lbv[4] = {lb[u].x, lb[u].y, lb[u].z, lb[u].w};
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) accB[a][b] = fmaf(lbv[a], xv[b], accB[a][b]);
+        }
       }
       auto direction = [&](int i0, const float (&acc)[4][4]) {
 #pragma unroll
