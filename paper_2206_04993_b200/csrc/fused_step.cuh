@@ -41,14 +41,29 @@ struct FusedMaps {
   UpdMaps um;          // phase U: fp32 state tiles (V'', AV, [Bv], BV)
 };
 
+// wait until *c >= target (acquire); a lost count traps (seconds) instead of hanging
+__device__ __forceinline__ void spin_geq_trap(const int* c, int target) {
+  int v;
+  long long polls = 0;
+  do {
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+    if (++polls > (1ll << 22)) __trap();
+  } while (v - target < 0);
+}
+
 struct FusedParams {
   int rows, h, k, BN, stages, splitsF, mtF, mtB[2], split, bwd_y_first, dbg_nostore, dbg_mode, l2_keep;
-  // Early coefficients: every CTA counts its finished slice of the Gram
-  // reduction on rcnt (monotonic across launches: step e = rc_epoch + t needs
-  // G (e + 1)); warps 2-3 wait for all slices during phase B and form the
-  // update's coefficients there (coef_early) instead of at the start of U
+  // Dependency counters (zero at launch start; CTA 0 zeroes them again after
+  // the last step's B barrier, when nothing reads them any more):
+  //  rcnt: CTAs whose slice of the Gram reduction is done — step t needs
+  //        G (t + 1); warps 2-3 wait for it during phase B and form the
+  //        update's coefficients there (coef_early);
+  //  fcnt[r]: forward items done on 128-row tile r — step t needs
+  //        fper (t + 1) (2 views x splitsF items cover a tile); phase S of a
+  //        CTA waits for the tiles of its rows instead of a grid barrier.
   int* rcnt;
-  long long rc_epoch;
+  int* fcnt;
+  int fper;
   int early_coef;
   int tmF, tmB;                    // 128-row M tiles per work item (forward: sample rows; backward: feature
                                    // columns): tm tiles share one B-operand tile per K step, so the ring
@@ -285,6 +300,14 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
       }
       tc_fence_before();
       mbar_arrive(acce_bar);
+      if (!A_MN && p.fcnt) {
+        // this item's split-K partials are stored: count them on its row tiles (release)
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (threadIdx.x == 128) {
+          __threadfence();
+          for (int mtile = 0; mtile < it.mt; ++mtile) atomicAdd(p.fcnt + it.m0 / TC_BM + mtile, 1);
+        }
+      }
     }
   }
   // Reconverge warps 0/1 (lane 0 ran a role, lanes 1-31 did not) before any
@@ -360,7 +383,25 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   }
   __syncthreads();
   dstamp(p.upd, 2);
-  grid.sync();
+  if (p.fcnt) {
+    // phase S of this CTA reads the split-K partials of its own rows only:
+    // wait for the forward items of those 128-row tiles (both halves)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int U = (((p.h & 3) == 0) && ((p.ldz & 3) == 0) && ((p.hpad & 3) == 0)) ? 4 : 1;   // as phase S
+      const int nu = p.h / U;
+      const int ua = (int)((int64_t)nu * blockIdx.x / gridDim.x), ub = (int)((int64_t)nu * (blockIdx.x + 1) / gridDim.x);
+      const int target = (t + 1) * p.fper;
+      if (ub > ua)
+        for (int half = 0; half < 2; ++half) {
+          const int r0 = half * p.h + ua * U, r1 = half * p.h + ub * U - 1;
+          for (int tile = r0 / TC_BM; tile <= r1 / TC_BM; ++tile) spin_geq_trap(p.fcnt + tile, target);
+        }
+    }
+    __syncthreads();
+  } else {
+    grid.sync();
+  }
   stamp(p.upd, 5);
   dstamp(p.upd, 3);
 
@@ -545,15 +586,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
           atomicAdd(p.rcnt, 1);
         }
         if (p.early_coef) {
-          if (threadIdx.x == 64) {
-            const int target = (int)((p.rc_epoch + t + 1) * (long long)gridDim.x);
-            int v;
-            long long polls = 0;
-            do {
-              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p.rcnt) : "memory");
-              if (++polls > (1ll << 22)) __trap();   // a lost count must fail loudly (seconds), never hang
-            } while (v - target < 0);
-          }
+          if (threadIdx.x == 64) spin_geq_trap(p.rcnt, (t + 1) * (int)gridDim.x);
           asm volatile("bar.sync 1, 64;" ::: "memory");
           if (threadIdx.x == 64) tstamp(p.upd, 12);
           coef_early(p.upd, coef_smem, t, threadIdx.x - 64);
@@ -590,6 +623,12 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   grid.sync();
   stamp(p.upd, 7);
   dstamp(p.upd, 7);
+  if (t + 1 == p.nsteps && blockIdx.x == 0 && threadIdx.x == 0) {
+    // every CTA is past its last counter read: back to zero for the next launch
+    if (p.rcnt) *p.rcnt = 0;
+    if (p.fcnt)
+      for (int r = 0; r < (p.rows + TC_BM - 1) / TC_BM; ++r) p.fcnt[r] = 0;
+  }
   }  // !update_only
 
   if (t + 1 < p.nsteps && p.xmaps && threadIdx.x == 0)   // the next step's batch descriptors, ahead of its phase F
@@ -651,7 +690,7 @@ inline bool make_batch_maps(CUtensorMap* a, const TcPlan& t, const void* X, cons
 inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* const* Y, int nsteps, int64_t b,
                                   float scale, const __nv_bfloat16* Vbf, float* AV, float* BV, UpdateArgs upd,
                                   int grid_ctas, size_t upd_bytes, cudaStream_t st, bool products_only = false,
-                                  bool tables = false, bool update_only = false, long long* rc_epoch = nullptr) {
+                                  bool tables = false, bool update_only = false) {
   if (!t.ready || t.math != GEIG_MATH_BF16) return tc_fail(GEIG_ERR_STATE, "fused step needs the bf16 plan");
   if (nsteps < 1) return tc_fail(GEIG_ERR_ARG, "nsteps < 1");
   // (t.math is BF16 for both GEIG_MATH_BF16 and GEIG_MATH_BF16X2; t.splitb selects hi+lo operands)
@@ -671,19 +710,23 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   // products + tables) counts it; the full steps also use it for the early
   // coefficients.  The solver's epoch advances only with a launch that was
   // enqueued (below), so targets always match the counts.
-  p.rcnt = nullptr;
-  p.rc_epoch = 0;
+  p.rcnt = p.fcnt = nullptr;
+  p.fper = 0;
   p.early_coef = 0;
-  const bool runs_reduce = !update_only && (!products_only || tables);
-  if (rc_epoch && runs_reduce && !getenv("GEIG_NO_EARLY_COEF")) {
-    if (!t.dep) {
-      if (cudaMalloc((void**)&t.dep, 64 * sizeof(int)) != cudaSuccess ||
-          cudaMemsetAsync(t.dep, 0, 64 * sizeof(int), st) != cudaSuccess)
-        return tc_fail(GEIG_ERR_CUDA, "allocating the Gram-reduction counter failed");
+  if (!update_only) {
+    const int ntiles = (int)((t.max_rows + TC_BM - 1) / TC_BM);
+    if (!t.dep) {   // [rcnt | pad | fcnt per 128-row tile], zero between launches
+      const size_t words = 32 + (size_t)ntiles;
+      if (cudaMalloc((void**)&t.dep, words * sizeof(int)) != cudaSuccess ||
+          cudaMemsetAsync(t.dep, 0, words * sizeof(int), st) != cudaSuccess)
+        return tc_fail(GEIG_ERR_CUDA, "allocating the dependency counters failed");
     }
-    p.rcnt = t.dep;
-    p.rc_epoch = *rc_epoch;
-    p.early_coef = products_only ? 0 : 1;
+    const bool runs_reduce = !products_only || tables;
+    if (runs_reduce && !getenv("GEIG_NO_EARLY_COEF")) {
+      p.rcnt = t.dep;
+      p.early_coef = products_only ? 0 : 1;
+    }
+    if (!getenv("GEIG_F_BARRIER")) p.fcnt = t.dep + 32;   // GEIG_F_BARRIER: developer A/B (grid barrier after F)
   }
   if (products_only && nsteps != 1) return tc_fail(GEIG_ERR_ARG, "products-only launch runs one step");
   p.xmaps = nullptr;
@@ -752,6 +795,7 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.scale = scale;
   p.mtF = (rows + p.tmF * TC_BM - 1) / (p.tmF * TC_BM);
   p.splitsF = std::min(TC_MAX_SPLITS, choose_splits_deep(2 * p.mtF, std::min(p.kbF[0], p.kbF[1]), grid_ctas));
+  p.fper = 2 * p.splitsF;   // forward items covering each 128-row tile per step
   p.kbB = (h + ATOM - 1) / ATOM;
   p.idescF = make_idesc(eb, false, t.BN * (t.splitb ? 2 : 1), TC_BM);
   p.idescB = make_idesc(eb, true, t.BN * (t.splitb ? 2 : 1), TC_BM);
@@ -794,7 +838,7 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   void* kfn = p.upd.adam ? (void*)cca_step_kernel<2, true> : (void*)cca_step_kernel<2, false>;
   cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(grid_ctas), dim3(FS_THREADS), args, smem, st);
   if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("cca_step_kernel launch: ") + cudaGetErrorString(e));
-  if (p.rcnt) *rc_epoch += nsteps;
+
   return GEIG_OK;
 }
 

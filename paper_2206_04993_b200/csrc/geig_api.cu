@@ -63,7 +63,6 @@ struct geig_solver {
   int upd_grid = 1;
   bool upd_res = false;                               // resident (k <= 64) update kernel
   bool fused_last = false;                            // last step ran the fused cooperative kernel
-  long long rc_epoch = 0;                             // fused launches' Gram-reduction steps counted so far
   // update variants (geig_set_smooth / geig_set_adam)
   int smooth = 0;
   float nu = 0.f;
@@ -384,7 +383,7 @@ extern "C" geig_status geig_products_cca_tables(geig_solver* s, const void* X, c
   UpdateArgs a = update_args(s, 0.0, 0.0);
   a.raw_a = T;
   geig_status st = tc::fused_cca_step(s->tc, &X, &Y, 1, b, scale, s->Vbf, AV, BV, a, s->upd_grid, s->upd_smem,
-                                      s->stream, /*products_only=*/true, /*tables=*/true, false, &s->rc_epoch);
+                                      s->stream, /*products_only=*/true, /*tables=*/true);
   if (st) return fail(st, "%s", tc::last_error());
   s->launches++;
   return GEIG_OK;
@@ -514,7 +513,7 @@ extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* 
                            s->stream);
     else
       st = tc::fused_cca_step(s->tc, &X, &Y, 1, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a, s->upd_grid,
-                              s->upd_smem, s->stream, false, false, false, &s->rc_epoch);
+                              s->upd_smem, s->stream);
     if (st) return fail(st, "%s", tc::last_error());
     s->launches++;
     s->fused_last = true;
@@ -547,8 +546,7 @@ extern "C" geig_status geig_run_cca(geig_solver* s, const void* const* X, const 
   for (int64_t i0 = 0; i0 < nsteps; i0 += tc::TC_RUN_CHUNK) {
     const int n = (int)std::min<int64_t>(tc::TC_RUN_CHUNK, nsteps - i0);
     geig_status st = tc::fused_cca_step(s->tc, X + i0, Y + i0, n, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV,
-                                        update_args(s, eta, gamma), s->upd_grid, s->upd_smem, s->stream, false,
-                                        false, false, &s->rc_epoch);
+                                        update_args(s, eta, gamma), s->upd_grid, s->upd_smem, s->stream);
     if (st) return fail(st, "%s", tc::last_error());
     s->launches++;
     advance_variant_state(s, n);
