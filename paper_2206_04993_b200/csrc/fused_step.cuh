@@ -61,8 +61,13 @@ struct FusedParams {
   //  fcnt[r]: forward items done on 128-row tile r — step t needs
   //        fper (t + 1) (2 views x splitsF items cover a tile); phase S of a
   //        CTA waits for the tiles of its rows instead of a grid barrier.
+  //  bcnt[v * btiles + c]: backward items done on 128-column tile c of view
+  //        v — step t needs 2 (t + 1) (the A-half and B-half items); the
+  //        update phase of a CTA waits for the tiles of its columns
   int* rcnt;
   int* fcnt;
+  int* bcnt;
+  int btiles;
   int fper;
   int early_coef;
   int tmF, tmB;                    // 128-row M tiles per work item (forward: sample rows; backward: feature
@@ -88,6 +93,7 @@ struct FusedParams {
 
 struct Item {
   int nseg, m0, mbound;
+  int view;           // backward item: view of the feature columns
   int mt;             // M tiles of this item (<= tm of the phase; fewer at the ragged end)
   int kb0[2], kbn[2];
   const CUtensorMap* ma[2];
@@ -135,6 +141,7 @@ __device__ __forceinline__ void decode_backward(const FusedMaps& M, const CUtens
   const int r = v == first ? idx : idx - nfirst;
   const int mt = r >> 1, seg = r & 1;
   it.nseg = 1;
+  it.view = v;
   it.m0 = mt * p.tmB * TC_BM;
   it.mbound = (int)(v == 0 ? p.dv[0] : p.dv[1]);
   it.mt = min(p.tmB, (it.mbound - it.m0 + TC_BM - 1) / TC_BM);
@@ -306,6 +313,16 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
         if (threadIdx.x == 128) {
           __threadfence();
           for (int mtile = 0; mtile < it.mt; ++mtile) atomicAdd(p.fcnt + it.m0 / TC_BM + mtile, 1);
+        }
+      }
+      if (A_MN && p.bcnt) {
+        // this item's AV / BV columns are final: count them on its column tiles
+        // (release; the update phases stage them through TMA, the async proxy)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (threadIdx.x == 128) {
+          __threadfence();
+          for (int mtile = 0; mtile < it.mt; ++mtile) atomicAdd(p.bcnt + it.view * p.btiles + it.m0 / TC_BM + mtile, 1);
         }
       }
     }
@@ -620,15 +637,28 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     p.upd.dbg[(size_t)blockIdx.x * 64 + 18] = *(volatile unsigned long long*)&p.upd.dbg[(size_t)blockIdx.x * 64 + 17];
     __threadfence(); dstamp(p.upd, 15);
   }
-  grid.sync();
+  if (p.bcnt && !p.products_only) {
+    // the update phase of this CTA needs the Gram reduction of every CTA and
+    // the backward items of its own columns [c W, (c + 1) W) only
+    if (threadIdx.x == 0) {
+      if (p.rcnt) spin_geq_trap(p.rcnt, (t + 1) * (int)gridDim.x);
+      const int64_t W = p.upd.segw;
+      const int64_t c0 = (int64_t)blockIdx.x * W, c1 = min(p.d, c0 + W);
+      for (int v = 0; v < 2; ++v) {
+        const int64_t lo = v == 0 ? 0 : p.dv[0], hi = v == 0 ? p.dv[0] : p.d;
+        const int64_t a = max(c0, lo), b = min(c1, hi);
+        if (a < b)
+          for (int tile = (int)((a - lo) / TC_BM); tile <= (int)((b - 1 - lo) / TC_BM); ++tile)
+            spin_geq_trap(p.bcnt + v * p.btiles + tile, 2 * (t + 1));
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncthreads();
+  } else {
+    grid.sync();
+  }
   stamp(p.upd, 7);
   dstamp(p.upd, 7);
-  if (t + 1 == p.nsteps && blockIdx.x == 0 && threadIdx.x == 0) {
-    // every CTA is past its last counter read: back to zero for the next launch
-    if (p.rcnt) *p.rcnt = 0;
-    if (p.fcnt)
-      for (int r = 0; r < (p.rows + TC_BM - 1) / TC_BM; ++r) p.fcnt[r] = 0;
-  }
   }  // !update_only
 
   if (t + 1 < p.nsteps && p.xmaps && threadIdx.x == 0)   // the next step's batch descriptors, ahead of its phase F
@@ -648,6 +678,18 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     tc_fence_after();
   }
   }  // steps
+
+  if (p.rcnt || p.fcnt || p.bcnt) {
+    // every CTA is past its last counter read: back to zero for the next launch
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (p.rcnt) *p.rcnt = 0;
+      if (p.fcnt)
+        for (int r = 0; r < (p.rows + TC_BM - 1) / TC_BM; ++r) p.fcnt[r] = 0;
+      if (p.bcnt)
+        for (int r = 0; r < 2 * p.btiles; ++r) p.bcnt[r] = 0;
+    }
+  }
 
   // ---- release TMEM ----
   tc_fence_before();
@@ -710,13 +752,15 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   // products + tables) counts it; the full steps also use it for the early
   // coefficients.  The solver's epoch advances only with a launch that was
   // enqueued (below), so targets always match the counts.
-  p.rcnt = p.fcnt = nullptr;
+  p.rcnt = p.fcnt = p.bcnt = nullptr;
+  p.btiles = 0;
   p.fper = 0;
   p.early_coef = 0;
   if (!update_only) {
     const int ntiles = (int)((t.max_rows + TC_BM - 1) / TC_BM);
-    if (!t.dep) {   // [rcnt | pad | fcnt per 128-row tile], zero between launches
-      const size_t words = 32 + (size_t)ntiles;
+    const int btiles = (int)((std::max(t.dx, t.dy) + TC_BM - 1) / TC_BM);
+    if (!t.dep) {   // [rcnt | pad | fcnt per 128-row tile | bcnt per view x 128-column tile], zero between launches
+      const size_t words = 32 + (size_t)ntiles + 2 * (size_t)btiles;
       if (cudaMalloc((void**)&t.dep, words * sizeof(int)) != cudaSuccess ||
           cudaMemsetAsync(t.dep, 0, words * sizeof(int), st) != cudaSuccess)
         return tc_fail(GEIG_ERR_CUDA, "allocating the dependency counters failed");
@@ -727,6 +771,8 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
       p.early_coef = products_only ? 0 : 1;
     }
     if (!getenv("GEIG_F_BARRIER")) p.fcnt = t.dep + 32;   // GEIG_F_BARRIER: developer A/B (grid barrier after F)
+    p.btiles = btiles;
+    if (!products_only && !getenv("GEIG_BU_BARRIER")) p.bcnt = t.dep + 32 + ntiles;   // (grid barrier after B)
   }
   if (products_only && nsteps != 1) return tc_fail(GEIG_ERR_ARG, "products-only launch runs one step");
   p.xmaps = nullptr;
