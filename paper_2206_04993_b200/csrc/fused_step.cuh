@@ -9,7 +9,10 @@
 //            TMA straight from the sample-major views, 2 TMEM accumulators)
 //   phase U  Gram tables, coefficients, fused update (update_res_phases)
 //                                                                  [rows a2-a4]
-// separated by grid barriers.  One CTA per SM (256 threads): warp 0 lane 0
+// ordered by a grid barrier S -> B and between steps, and by per-tile
+// dependency counters F -> S (a CTA's phase S waits for the forward items of
+// its row tiles) and B -> U (its update waits for the Gram reduction and the
+// backward items of its columns).  One CTA per SM (256 threads): warp 0 lane 0
 // issues TMA, warp 1 lane 0 issues tcgen05.mma, warp 2 owns TMEM, warps 4-7
 // drain the accumulators (tcgen05.ld -> registers -> coalesced stores); the
 // smem ring and its mbarrier phases persist across the work items of F and B,
