@@ -560,3 +560,35 @@ def test_mixed_call_sequence_keeps_the_launch_counters_consistent(geig):
     step = errs.pop("step")
     _assert(errs, 1e-4)
     assert step < 1e-3
+
+
+def _fuzz_cases(n=12, seed=2024):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for _ in range(n):
+        k = int(rng.integers(1, 65))
+        dx = int(rng.integers(1, 99)) * 8
+        dy = int(rng.integers(1, 99)) * 8
+        rows = int(rng.integers(2, 2600))
+        math = "bf16x2" if rng.random() < 0.7 else "bf16"
+        cases.append((k, dx, dy, rows, math))
+    return cases
+
+
+@pytest.mark.parametrize("k,dx,dy,rows,math", _fuzz_cases())
+def test_fused_step_random_shapes(geig, k, dx, dy, rows, math):
+    """Seeded random shapes through the fused single-launch step (k <= 64,
+    d % 8 == 0, any b >= 2: ragged M tiles, odd b, k not a multiple of 16,
+    split-K over few K blocks, the per-tile dependency counters) vs the
+    fp64 oracle."""
+    from synth import CONFIGS
+    cfg = CONFIGS[2]
+    if dx > cfg.dx or dy > cfg.dy:   # config 2's generator draws 784-column views
+        pytest.skip("views wider than the recipe")
+    errs, _ = check_cca_step(geig, 2, rows, k=k, dx=dx, dy=dy, math=math, use_step=True, eta=0.5)
+    if math == "bf16":
+        _assert(errs, 1e-2)
+    else:
+        step = errs.pop("step")
+        _assert(errs, 1e-4)
+        assert step < 1e-3, errs
