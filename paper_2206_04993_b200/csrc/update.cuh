@@ -366,9 +366,11 @@ update_kernel(UpdateArgs p) {
       c = warp_sum(c);
       if (lane == 0) D2s[i] = i < k ? ni * ni * rA[i * KP + i] - c : 0.f;
     }
-    if (blockIdx.x == 0) {
-      // diagnostics: normalised tables of the iteration-start state
-      for (int e = tid; e < k * k; e += UPD_THREADS) {
+    {
+      // diagnostics: normalised tables of the iteration-start state (slices over the CTAs)
+      const int kk = k * k, per = (kk + (int)gridDim.x - 1) / (int)gridDim.x;
+      const int e1 = min(kk, (int)(blockIdx.x + 1) * per);
+      for (int e = blockIdx.x * per + tid; e < e1; e += UPD_THREADS) {
         const int i = e / k, j = e % k;
         const bool low = j <= i;
         p.gram[e] = low ? rsqrtf(rN[i]) * rsqrtf(rN[j]) * rA[i * KP + j] : 0.f;
@@ -403,15 +405,25 @@ update_kernel(UpdateArgs p) {
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
       if (i0 < KP) {
-        const int jmax = min(i0 + 3, k);         // L_ij = 0 for j >= i
-        for (int j = 0; j < jmax; ++j) {
-          const float4 l = *reinterpret_cast<const float4*>(Lt + j * KP + i0);
-          const float4 x = *reinterpret_cast<const float4*>(Ct + j * UPD_S + 4 * tx);
-          const float lv[4] = {l.x, l.y, l.z, l.w}, xv[4] = {x.x, x.y, x.z, x.w};
+        // j bound rounded up to a multiple of 4 (L_ij = 0 for j >= i, rows of
+        // the staged tiles past k are zero): 4 j per branch-free iteration
+        const int jmax = min(i0 + 4, (k + 3) & ~3);
+#pragma unroll 1
+        for (int j0 = 0; j0 < jmax; j0 += 4) {
+          float4 l[4], x[4];
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
+          for (int u = 0; u < 4; ++u) {
+            l[u] = *reinterpret_cast<const float4*>(Lt + (j0 + u) * KP + i0);
+            x[u] = *reinterpret_cast<const float4*>(Ct + (j0 + u) * UPD_S + 4 * tx);
+          }
 #pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(lv[a], xv[b], acc[a][b]);
+          for (int u = 0; u < 4; ++u) {
+            const float lv[4] = {l[u].x, l[u].y, l[u].z, l[u].w}, xv[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(lv[a], xv[b], acc[a][b]);
+          }
         }
       }
       const int64_t gx = c0 + (int64_t)sc * UPD_XC + 4 * tx;
