@@ -73,6 +73,7 @@ struct FusedParams {
   int btiles;
   int fper;
   int early_coef;
+  int splitB;                      // backward: z as hi + lo bf16 (bf16x2), else hi only
   int tmF, tmB;                    // 128-row M tiles per work item (forward: sample rows; backward: feature
                                    // columns): tm tiles share one B-operand tile per K step, so the ring
                                    // holds tm x more batch bytes in flight per byte of V / Z re-read
@@ -179,7 +180,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
   const int tm = A_MN ? p.tmB : p.tmF;
   const uint32_t A_BYTES = (uint32_t)tm * A_TILE;   // stage: tm A tiles, then the (shared) B tile(s)
   const uint32_t B_BYTES = (uint32_t)p.BN * 128;
-  const bool split = p.split != 0;
+  const bool split = (A_MN ? p.splitB : p.split) != 0;   // hi + lo B operands of this phase
   const uint32_t STAGE_BYTES = A_BYTES + B_BYTES * (split ? 2 : 1);
   const int S = p.stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -271,7 +272,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
       __syncwarp();
       tc_fence_after();
       if (threadIdx.x == 128) tstamp(p.upd, A_MN ? 11 : 9);
-      const int acols = p.BN * (p.split ? 2 : 1);
+      const int acols = p.BN * (split ? 2 : 1);
       for (int s = 0; s < it.nseg * it.mt; ++s) {
         const int seg = s / it.mt, mtile = s - seg * it.mt;
         const int mw = it.m0 + mtile * TC_BM + ew * 32;           // this warp's first m
@@ -283,10 +284,10 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
         for (int c0 = 0; c0 < p.BN; c0 += 16) {
           uint32_t r[16], rl[16];
           tmem_ld16(tb + (uint32_t)c0, r);
-          if (p.split) tmem_ld16(tb + (uint32_t)(p.BN + c0), rl);
+          if (split) tmem_ld16(tb + (uint32_t)(p.BN + c0), rl);
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            ws[j * 32 + lane] = it.scale * (p.split ? __uint_as_float(r[j]) + __uint_as_float(rl[j]) : __uint_as_float(r[j]));
+            ws[j * 32 + lane] = it.scale * (split ? __uint_as_float(r[j]) + __uint_as_float(rl[j]) : __uint_as_float(r[j]));
           __syncwarp();
           if (!(kDevKnobs && p.dbg_nostore)) {
 #pragma unroll
@@ -346,7 +347,6 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   // address space (integer pointer round-trips would turn every later smem
   // access into a generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const uint32_t STAGE_BYTES = TC_BM * 128 + (uint32_t)p.BN * 128 * (p.split ? 2 : 1);
   uint8_t* ring = smem;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + p.bar_off);
   uint64_t* empty_bar = full_bar + TC_MAX_STAGES;
@@ -518,7 +518,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
           store4<__nv_bfloat16>(p.Zb + 1 * plane + o, z[1][0], z[1][1], z[1][2], z[1][3]);
           store4<__nv_bfloat16>(p.Zb + 2 * plane + o, z[0][0], z[0][1], z[0][2], z[0][3]);
           store4<__nv_bfloat16>(p.Zb + 3 * plane + o, z[3][0], z[3][1], z[3][2], z[3][3]);
-          if (p.split) {
+          if (p.splitB) {
             store4_lo<__nv_bfloat16>(p.Zb + 4 * plane + o, z[2][0], z[2][1], z[2][2], z[2][3]);
             store4_lo<__nv_bfloat16>(p.Zb + 5 * plane + o, z[1][0], z[1][1], z[1][2], z[1][3]);
             store4_lo<__nv_bfloat16>(p.Zb + 6 * plane + o, z[0][0], z[0][1], z[0][2], z[0][3]);
@@ -529,7 +529,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
           for (int q = 0; q < 4; ++q) {
             const __nv_bfloat16 hv = __float2bfloat16_rn(zv[q]);
             p.Zb[q * plane + o] = hv;
-            if (p.split) p.Zb[(4 + q) * plane + o] = __float2bfloat16_rn(zv[q] - __bfloat162float(hv));
+            if (p.splitB) p.Zb[(4 + q) * plane + o] = __float2bfloat16_rn(zv[q] - __bfloat162float(hv));
           }
         }
 #pragma unroll
@@ -858,6 +858,9 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.upd.ga_done = 1;       // phase S forms G^A, G^B from z
   p.upd.pre_reduced = 1;   // G^C, ||v''||^2 in F (warps 2-3), reduction in B (warps 2-3)
   p.split = t.splitb;
+  // backward B operand (z) as hi + lo too: GEIG_NO_ZLO drops the lo half (developer A/B)
+  p.splitB = (t.splitb && !getenv("GEIG_NO_ZLO")) ? 1 : 0;
+  p.idescB = make_idesc(eb, true, t.BN * (p.splitB ? 2 : 1), TC_BM);
   p.bwd_y_first = getenv("GEIG_BWD_X_FIRST") ? 0 : 1;
   p.l2_keep = getenv("GEIG_L2_KEEP") ? 1 : 0;   // measured: evict-last on a whole view thrashes the state arrays (slower)
   p.dbg_nostore = getenv("GEIG_DBG_NOSTORE") ? 1 : 0;   // developer: drop GEMM epilogue stores (timing only)
