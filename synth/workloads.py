@@ -61,7 +61,7 @@ CONFIGS = {
                       rho=1e-3, eta=0.1, gamma=1.0, latent=32, view_kind="image",
                       recipe="clip(sigmoid(zW+0.3 noise),0,1), latent 32"),
     3: WorkloadConfig(3, "cca_activation_d8192_k64", "cca", 8192, 8192, 64, 4096, 10_000_000, "bf16",
-                      rho=1e-2, eta=0.02, gamma=0.5, latent=256, view_kind="activation",
+                      rho=1e-2, eta=1e-4, gamma=0.5, latent=256, view_kind="activation",
                       recipe="ReLU(zW + t_3 noise), latent 256"),
     4: WorkloadConfig(4, "dense_d16384_k128", "dense", 16384, 0, 128, 0, 0, "f32",
                       rho=5e-4, eta=0.05, gamma=1.0,

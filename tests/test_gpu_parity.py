@@ -77,8 +77,10 @@ def test_cca_config2_bf16_data_fp32_math(geig):
 
 def test_cca_config3_full_size_fp32_math(geig):
     """Config 3 at full size (dx=dy=8192, b=4096, k=64, bf16 data): one step
-    through the FFMA exactness path vs the fp64 oracle."""
-    errs, _ = check_cca_step(geig, 3, 4096)
+    through the FFMA exactness path vs the fp64 oracle.  eta = 0.02 (not the
+    config's 1e-4): at 1e-4 the step (~0.1 of |V|) is resolved only to
+    ~1.4e-4 by the fp32 storage of V' itself."""
+    errs, _ = check_cca_step(geig, 3, 4096, eta=0.02)
     _assert(errs, 1e-4)
 
 
@@ -229,7 +231,7 @@ def test_cca_tf32_tcgen05(geig, monkeypatch, cfg_idx, rows, k, dx, dy):
 
 @pytest.mark.parametrize("cfg_idx,rows,k,dx,dy,eta", [(1, 256, None, None, None, None),
                                                       (2, 1024, 16, 784, 784, None),
-                                                      (3, 2048, 64, 1024, 512, None),
+                                                      (3, 2048, 64, 1024, 512, 0.02),
                                                       (2, 300, 24, 200, 136, 0.5), (2, 130, 5, 64, 8, 0.5)])
 def test_cca_3xtf32_tcgen05(geig, monkeypatch, cfg_idx, rows, k, dx, dy, eta):
     """3xTF32: A split in shared memory into tf32 hi + lo by warps 2-3, B as
@@ -244,7 +246,7 @@ def test_cca_3xtf32_tcgen05(geig, monkeypatch, cfg_idx, rows, k, dx, dy, eta):
     errs, _ = gh.check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math="3xtf32", eta=eta)
     step = errs.pop("step")
     _assert(errs, 1e-5)
-    assert step < (1e-4 if eta is None else 1e-3), (step, errs)
+    assert step < (1e-3 if rows < 500 else 1e-4), (step, errs)   # tiny ragged shapes: the bf16x2 step bar
 
 
 def test_dense_config0_3xtf32_tcgen05(geig):
