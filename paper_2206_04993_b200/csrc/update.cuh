@@ -497,20 +497,6 @@ __host__ __device__ constexpr int upd_raw_floats_res(int k) { return 2 * ((k * (
 
 __device__ __forceinline__ int tri_index(int i, int j) { return i * (i + 1) / 2 + j; }
 
-// 3xTF32 operand split: x ~ hi + lo with hi = tf32(x), lo = tf32(x - hi)
-__device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
-  const float r = x - __uint_as_float(hi);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
-}
-// d += a b, m16n8k8, A row-major (tf32 x4), B col-major (tf32 x2), fp32 accumulators
-__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
-}
-
 // ---------------------------------------------------------------------------
 // Fused step side work for the otherwise idle warps 2-3 (64 threads, no smem
 // beyond a 64-float scratch) of the GEMM phases:

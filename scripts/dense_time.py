@@ -31,3 +31,12 @@ for math in sys.argv[1:] or ["tf32", "3xtf32"]:
     print(f"{math}: products {tp*1e3:.1f} us ({byts / (tp*1e-3) / 1e12:.2f} TB/s of A,B), update {tu*1e3:.1f} us, "
           f"tensor {4 * cfg.k * cfg.d * cfg.d / (tp*1e-3) / 1e12:.1f} TFLOP/s")
     s.close()
+# phase split of the last update (CTA 0 %globaltimer): gram, reduce, coef+update
+s = geig.Solver(geig.GEIG_DENSE, cfg.d, 0, cfg.k, math="tf32", rho=cfg.rho)
+s.init_state(torch.tensor(gaussian_init(cfg.k, cfg.d, 0), dtype=torch.float32, device=dev))
+AV = torch.empty(cfg.k, cfg.d, device=dev); BV = torch.empty_like(AV)
+geig.geig_products_dense(s.h, a, b, 0, cfg.d, AV, BV)
+for _ in range(3):
+    geig.geig_update(s.h, AV, BV, cfg.eta, cfg.gamma)
+torch.cuda.synchronize()
+print("update phases (us):", [x / 1e3 for x in geig.geig_update_phase_ns(s.h)[:3]])
