@@ -203,6 +203,27 @@ def run_reference(args, cfg, rank, world):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def _box_copy_gbs(dev, n=1 << 28, reps=5):
+    """Best-of-`reps` bf16 device copy of n elements (read + write bytes) on
+    this box, CUDA events; None if it cannot allocate."""
+    import torch
+    try:
+        a = torch.empty(n, dtype=torch.bfloat16, device=dev).fill_(1.0)
+        b = torch.empty_like(a)
+        best = float("inf")
+        for _ in range(reps + 1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            b.copy_(a)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return 2 * n * 2 / (best / 1e3) / 1e9
+    except Exception:
+        return None
+
+
 def run_gpu(args, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -384,7 +405,12 @@ def run_gpu(args, cfg, rank, world, local_rank):
             traffic = tr["dram_bytes_per_launch"]
     except Exception:
         pass
+    # this box's own copy bandwidth (same method as MEASURED_PEAKS.json, after
+    # the timed region): HBM bandwidth differs between boxes of the pool by
+    # ~15%, so the line carries the denominator it was measured against too
+    box_copy = _box_copy_gbs(dev)
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "box_copy_gbs": box_copy, "frac_of_box_copy": (achieved / box_copy) if box_copy else None,
             "frac": achieved / hbm_peak, "traffic": traffic, "algorithmic_bytes": alg_bytes,
             "kernel": kernel, "peak_source": peaks_src, "ms_per_launch": k_ms, "phases": phases,
             "flops_per_step": 4.0 * cfg.k * cfg.d * b,
