@@ -74,8 +74,6 @@ struct FusedParams {
   int fper;
   int early_coef;
   int splitB;                      // backward: z as hi + lo bf16 (bf16x2), else hi only
-  int one_acc;                     // bf16x2: A.B_hi and A.B_lo accumulate into ONE accumulator (two N = BN
-                                   // MMAs per K step); 0: one N = 2 BN MMA, halves summed by the epilogue
   int tmF, tmB;                    // 128-row M tiles per work item (forward: sample rows; backward: feature
                                    // columns): tm tiles share one B-operand tile per K step, so the ring
                                    // holds tm x more batch bytes in flight per byte of V / Z re-read
@@ -228,16 +226,14 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
       if (A_MN) decode_backward(M, A, p, idx, it); else decode_forward(M, A, p, idx, it);
       if (rs.items > 0) mbar_wait(acce_bar, (rs.items - 1) & 1);   // epilogue drained the accumulator
       tc_fence_after();
-      // bf16x2: each K step issues A.B_hi^T and A.B_lo^T as two N = BN MMAs
-      // into ONE accumulator (same tensor time as one N = 2 BN MMA, half the
-      // TMEM the epilogue drains: the TMEM read of the accumulators is a
-      // measurable part of the epilogue at 64 B/clk).  one_acc = 0 (developer
-      // A/B): the hi and lo tiles, back to back in smem, form one N = 2 BN
-      // operand whose accumulator halves the epilogue adds.
+      // bf16x2: the hi and lo tiles of the B operand sit back to back in smem
+      // and form ONE N = 2 BN operand, so each K step is a single MMA whose
+      // accumulator holds A.B_hi^T in columns [0, BN) and A.B_lo^T in [BN, 2BN)
+      // (summed by the epilogue): half the MMA issues and A-operand smem reads
+      // of two N = BN MMAs.
       // tm M tiles per K step share the B tile; accumulator of M tile mtile
       // (segment s) at TMEM columns (s * mt + mtile) * acols
-      const bool two = split && !p.one_acc;   // hi / lo in separate accumulator halves
-      const uint32_t acols = (uint32_t)(p.BN * (two ? 2 : 1));
+      const uint32_t acols = (uint32_t)(p.BN * (split ? 2 : 1));
       for (int s = 0; s < it.nseg; ++s) {
         for (int j = 0; j < it.kbn[s]; ++j, ++rs.it_mma) {
           const int st = rs.it_mma % S;
@@ -254,8 +250,6 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
               const uint64_t ad = A_MN ? make_sdesc(sa + kk * UK * 128, BK * 128, 1024) : make_sdesc(sa + kk * 32, 16, 1024);
               const uint64_t bd = make_sdesc(sb + kk * 32, 16, 1024);
               umma<EB>(d_tmem, ad, bd, idesc, (j > 0 || kk > 0) ? 1u : 0u);
-              if (split && p.one_acc)   // + A.B_lo into the same accumulator
-                umma<EB>(d_tmem, ad, make_sdesc(sb + B_BYTES + kk * 32, 16, 1024), idesc, 1u);
             }
           }
           umma_commit(&empty_bar[st]);
@@ -278,8 +272,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
       __syncwarp();
       tc_fence_after();
       if (threadIdx.x == 128) tstamp(p.upd, A_MN ? 11 : 9);
-      const bool two = split && !p.one_acc;
-      const int acols = p.BN * (two ? 2 : 1);
+      const int acols = p.BN * (split ? 2 : 1);
       for (int s = 0; s < it.nseg * it.mt; ++s) {
         const int seg = s / it.mt, mtile = s - seg * it.mt;
         const int mw = it.m0 + mtile * TC_BM + ew * 32;           // this warp's first m
@@ -291,10 +284,10 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
         for (int c0 = 0; c0 < p.BN; c0 += 16) {
           uint32_t r[16], rl[16];
           tmem_ld16(tb + (uint32_t)c0, r);
-          if (two) tmem_ld16(tb + (uint32_t)(p.BN + c0), rl);
+          if (split) tmem_ld16(tb + (uint32_t)(p.BN + c0), rl);
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            ws[j * 32 + lane] = it.scale * (two ? __uint_as_float(r[j]) + __uint_as_float(rl[j]) : __uint_as_float(r[j]));
+            ws[j * 32 + lane] = it.scale * (split ? __uint_as_float(r[j]) + __uint_as_float(rl[j]) : __uint_as_float(r[j]));
           __syncwarp();
           if (!(kDevKnobs && p.dbg_nostore)) {
 #pragma unroll
@@ -853,8 +846,8 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.splitsF = std::min(TC_MAX_SPLITS, choose_splits_deep(2 * p.mtF, std::min(p.kbF[0], p.kbF[1]), grid_ctas));
   p.fper = 2 * p.splitsF;   // forward items covering each 128-row tile per step
   p.kbB = (h + ATOM - 1) / ATOM;
-  p.one_acc = getenv("GEIG_HILO_2ACC") ? 0 : 1;   // developer A/B: hi / lo in two accumulator halves
-  p.idescF = make_idesc(eb, false, t.BN * ((t.splitb && !p.one_acc) ? 2 : 1), TC_BM);
+  p.idescF = make_idesc(eb, false, t.BN * (t.splitb ? 2 : 1), TC_BM);
+  p.idescB = make_idesc(eb, true, t.BN * (t.splitb ? 2 : 1), TC_BM);
   p.Zt = t.Zt;
   p.Zb = (__nv_bfloat16*)t.Zb;
   p.AV = AV;
@@ -867,13 +860,13 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.split = t.splitb;
   // backward B operand (z) as hi + lo too: GEIG_NO_ZLO drops the lo half (developer A/B)
   p.splitB = (t.splitb && !getenv("GEIG_NO_ZLO")) ? 1 : 0;
-  p.idescB = make_idesc(eb, true, t.BN * ((p.splitB && !p.one_acc) ? 2 : 1), TC_BM);
+  p.idescB = make_idesc(eb, true, t.BN * (p.splitB ? 2 : 1), TC_BM);
   p.bwd_y_first = getenv("GEIG_BWD_X_FIRST") ? 0 : 1;
   p.l2_keep = getenv("GEIG_L2_KEEP") ? 1 : 0;   // measured: evict-last on a whole view thrashes the state arrays (slower)
   p.dbg_nostore = getenv("GEIG_DBG_NOSTORE") ? 1 : 0;   // developer: drop GEMM epilogue stores (timing only)
   p.dbg_mode = getenv("GEIG_DBG_MODE") ? atoi(getenv("GEIG_DBG_MODE")) : 0;   // developer timing knobs (wrong results)
   const size_t stage_bytes = (size_t)std::max(p.tmF, p.tmB) * TC_BM * 128 + (size_t)t.BN * 128 * (t.splitb ? 2 : 1);
-  if ((size_t)std::max(p.tmF, p.tmB) * t.BN * ((t.splitb && !p.one_acc) ? 2 : 1) > 256)
+  if ((size_t)std::max(p.tmF, p.tmB) * t.BN * (t.splitb ? 2 : 1) > 256)
     return tc_fail(GEIG_ERR_UNSUPPORTED, "fused step: accumulators exceed the TMEM allocation");
   p.stages = (int)std::min<size_t>(TC_MAX_STAGES, (200 * 1024) / stage_bytes);
   p.bar_off = (uint32_t)((std::max((size_t)p.stages * stage_bytes, upd_bytes) + 15) & ~(size_t)15);
