@@ -384,8 +384,17 @@ update_kernel(UpdateArgs p) {
   // ---------------- phase 3b: grad, v'' and [Bv]' for this CTA's columns ----------------
   {
     const int tx = tid & 7;            // columns 4tx..4tx+3 of the sub-chunk
-    const int tr = tid >> 3;           // rows 4tr..4tr+3
-    const int i0 = 4 * tr;
+    // Penalty sums sum_{j<i} L_ij [Bv]_j: row i needs i terms, so a fixed
+    // row-group-per-thread mapping leaves the last rows' threads with twice
+    // the average work.  NB == 2 (k > 64): thread pair (h = 0, 1; lanes l,
+    // l ^ 8) owns row groups g1 = q and g2 = 31 - q (4 rows each), splits
+    // their j range by alternating 4-blocks (h takes j0 = 4h, 4h + 8, ...)
+    // and exchanges the partial sums by one shuffle, so every thread does
+    // (g1 + g2 + 2) / 2 = 16.5 4-blocks; thread h writes back group g1 (h = 0)
+    // or g2 (h = 1).  NB == 1: one row group per thread (tr = tid >> 3).
+    const int hh = (tid >> 3) & 1;
+    const int q = tid >> 4;
+    const int i0 = NB == 2 ? 4 * (hh ? 31 - q : q) : 4 * (tid >> 3);
     if (nsub > 0) stage_tiles<KP, VEC>(buf0, src, k, d, c0, c1);
     cp_async_commit();
     for (int sc = 0; sc < nsub; ++sc) {
@@ -404,7 +413,61 @@ update_kernel(UpdateArgs p) {
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
-      if (i0 < KP) {
+      if constexpr (NB == 2) {
+        // j bounds rounded up to multiples of 4 (L_ij = 0 for j >= i, rows
+        // of the staged tiles past k are zero)
+        const int kr = (k + 3) & ~3;
+        const int r1 = 4 * q, r2 = 4 * (31 - q);
+        const int jm1 = min(r1 + 4, kr), jm2 = min(r2 + 4, kr);
+        float a1[4][4], a2[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) a1[a][b] = a2[a][b] = 0.f;
+        int j0 = 4 * hh;
+#pragma unroll 1
+        for (; j0 < jm1; j0 += 8) {      // both groups
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float4 l1 = *reinterpret_cast<const float4*>(Lt + (j0 + u) * KP + r1);
+            const float4 l2 = *reinterpret_cast<const float4*>(Lt + (j0 + u) * KP + r2);
+            const float4 x = *reinterpret_cast<const float4*>(Ct + (j0 + u) * UPD_S + 4 * tx);
+            const float lv1[4] = {l1.x, l1.y, l1.z, l1.w}, lv2[4] = {l2.x, l2.y, l2.z, l2.w};
+            const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                a1[a][b] = fmaf(lv1[a], xv[b], a1[a][b]);
+                a2[a][b] = fmaf(lv2[a], xv[b], a2[a][b]);
+              }
+          }
+        }
+#pragma unroll 1
+        for (; j0 < jm2; j0 += 8) {      // group g2 only
+          float4 l[4], x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            l[u] = *reinterpret_cast<const float4*>(Lt + (j0 + u) * KP + r2);
+            x[u] = *reinterpret_cast<const float4*>(Ct + (j0 + u) * UPD_S + 4 * tx);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float lv[4] = {l[u].x, l[u].y, l[u].z, l[u].w}, xv[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) a2[a][b] = fmaf(lv[a], xv[b], a2[a][b]);
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const float other = __shfl_xor_sync(0xffffffffu, hh ? a1[a][b] : a2[a][b], 8);
+            acc[a][b] = (hh ? a2[a][b] : a1[a][b]) + other;
+          }
+      } else if (i0 < KP) {
         // j bound rounded up to a multiple of 4 (L_ij = 0 for j >= i, rows of
         // the staged tiles past k are zero): 4 j per branch-free iteration
         const int jmax = min(i0 + 4, (k + 3) & ~3);

@@ -142,6 +142,19 @@ def test_init_state_matches_alg2_lines_2_3(geig):
         s.close()
 
 
+@pytest.mark.parametrize("d,k", [(333, 65), (1030, 97), (517, 128)])
+def test_dense_streamed_update_k_over_64_fp32(geig, d, k):
+    """The streamed update (k > 64, `update_kernel<2>`): the penalty sums
+    sum_{j<i} L_ij [Bv]_j split over thread pairs (row groups q and 31 - q,
+    alternating 4-blocks of j, shuffle-combined) — k not a multiple of 4
+    (rows past k), k = 128, d not a multiple of the 32-column sub-chunk;
+    fp32 FFMA products, so the step is held to the fp32 bar (PAPER.md:1017-1025,
+    Alg. 2 l.12-19)."""
+    from synth import dense_gep_small
+    a, b = dense_gep_small(seed=3, d=d)
+    _dense_step_check(geig, a, b, k, "f32", 0.1, 0.05, 0.5, seed=1, tol=1e-4)
+
+
 def test_errors_are_loud(geig):
     with pytest.raises(geig.GeigError):
         geig.geig_create(geig.GEIG_CCA, 0, 4, 2, 0, 0, 0.1, 8, 0)
