@@ -256,6 +256,14 @@ update_kernel(UpdateArgs p) {
     cp_async_wait<0>();
     float* out = p.partial + (size_t)blockIdx.x * PSTRIDE;
     {
+      // the micro-tiles go through the idle tile buffers (row stride KP + 4:
+      // the 16 ti lanes of a store hit distinct banks) and leave as coalesced
+      // float4 rows of the lower 64-blocks — the direct lane-per-row stores
+      // were uncoalesced (ncu: lg_throttle, 8% of the stall samples)
+      constexpr int KPS = KP + 4;
+      static_assert(2 * KP * KPS <= 8 * TILE, "Gram partials exceed the idle tile buffers");
+      float* sA = smem;
+      float* sC = smem + KP * KPS;
       int pr = 0;
 #pragma unroll
       for (int bi = 0; bi < NB; ++bi)
@@ -266,9 +274,20 @@ update_kernel(UpdateArgs p) {
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
               const int i = bi * 64 + ti + 16 * a, j = bj * 64 + tj + 16 * b;
-              out[i * KP + j] = accA[pr][a][b];
-              out[KP * KP + i * KP + j] = accC[pr][a][b];
+              sA[i * KPS + j] = accA[pr][a][b];
+              sC[i * KPS + j] = accC[pr][a][b];
             }
+      __syncthreads();
+      // row i of 64-block bi: columns [0, 64 (bi + 1)) (the blocks bj <= bi)
+      for (int e = tid; e < KP * KP / 4; e += UPD_THREADS) {
+        const int i = e / (KP / 4), c4 = e - i * (KP / 4);
+        if (4 * c4 < 64 * (i / 64 + 1)) {
+          const float4 va = *reinterpret_cast<const float4*>(sA + i * KPS + 4 * c4);
+          const float4 vc = *reinterpret_cast<const float4*>(sC + i * KPS + 4 * c4);
+          __stcg(reinterpret_cast<float4*>(out + i * KP + 4 * c4), va);
+          __stcg(reinterpret_cast<float4*>(out + KP * KP + i * KP + 4 * c4), vc);
+        }
+      }
     }
 #pragma unroll
     for (int q = 0; q < KP / 8; ++q) {
@@ -336,16 +355,33 @@ update_kernel(UpdateArgs p) {
   float* D1s = S2 + KP;                          // G^B_ii
   float* D2s = D1s + KP;                         // G^A_ii - c_i
   {
+    // The lower triangles of the raw G^A, G^C tables (written by phase 2 of
+    // all CTAs, L2-resident) are staged into the idle tile buffers first:
+    // every thread issues its float4 loads back to back, instead of the
+    // coefficient loop below waiting one L2 round trip per (row, 32 j)
+    // step (ncu: 11% of the kernel's stall samples on those loads).
     const float* rA = p.raw;
     const float* rC = p.raw + KP * KP;
     const float* rB = p.raw + 2 * KP * KP;
     const float* rN = rB + KP;
+    float* sA = smem;                            // [KP][KP] (lower triangle, rows < k), in buf0/buf1
+    float* sC = smem + KP * KP;
+    static_assert(2 * KP * KP <= 8 * TILE, "raw tables exceed the idle tile buffers");
+#pragma unroll 4
+    for (int e = tid; e < KP * KP / 4; e += UPD_THREADS) {
+      const int r = e / (KP / 4), c4 = e - r * (KP / 4);
+      if (r < k && 4 * c4 <= r) {
+        *reinterpret_cast<float4*>(sA + 4 * e) = __ldcg(reinterpret_cast<const float4*>(rA) + e);
+        *reinterpret_cast<float4*>(sC + 4 * e) = __ldcg(reinterpret_cast<const float4*>(rC) + e);
+      }
+    }
+    __syncthreads();
     for (int i = tid; i < KP; i += UPD_THREADS) {
       float n = 0.f, s2 = 1.f, gb = 0.f;
       if (i < k) {
         n = rsqrtf(rN[i]);
         gb = n * n * rB[i];
-        s2 = fmaxf(n * rC[i * KP + i], p.rho);
+        s2 = fmaxf(n * sC[i * KP + i], p.rho);
       }
       Ns[i] = n; S2[i] = s2; D1s[i] = gb;
     }
@@ -356,15 +392,15 @@ update_kernel(UpdateArgs p) {
       for (int j = lane; j < KP; j += 32) {
         float l = 0.f;
         if (i < k && j < i) {
-          const float ga = ni * Ns[j] * rA[i * KP + j];
-          const float gc = ni * rC[i * KP + j];
+          const float ga = ni * Ns[j] * sA[i * KP + j];
+          const float gc = ni * sC[i * KP + j];
           l = D1s[i] * ga / S2[j];
           c = fmaf(ga, gc / S2[j], c);
         }
         Lt[j * KP + i] = l;
       }
       c = warp_sum(c);
-      if (lane == 0) D2s[i] = i < k ? ni * ni * rA[i * KP + i] - c : 0.f;
+      if (lane == 0) D2s[i] = i < k ? ni * ni * sA[i * KP + i] - c : 0.f;
     }
     {
       // diagnostics: normalised tables of the iteration-start state (slices over the CTAs)

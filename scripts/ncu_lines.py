@@ -3,7 +3,7 @@ fused step kernel by CUDA source line using the cubin's line table.
 usage: python scripts/ncu_lines.py <report.ncu-rep> <file.cuh> <line_lo> <line_hi>"""
 import csv, io, re, subprocess, sys, tempfile, os
 rep, fname, lo, hi = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
-kern = "_ZN4geig2tc15cca_step_kernelILi2EEEvNS0_9FusedMapsENS0_11FusedParamsE"
+kern = os.environ.get("KERN", "_ZN4geig2tc15cca_step_kernelILi2EEEvNS0_9FusedMapsENS0_11FusedParamsE")
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 h = rows[1]; data = rows[2:]
