@@ -839,7 +839,26 @@ inline geig_status products_dense(TcPlan& t, const void* A, const void* B, int64
   p.N = k; p.BN = t.BN; p.nseg = 1; p.ldo = t.d; p.scale = 1.f;
   p.idesc = make_idesc(eb, false, t.BN, TC_BM);
   const int mt = (M + TC_BM - 1) / TC_BM;
-  p.splits = (2 * mt * 3 >= t.nsm * 2) ? 1 : choose_splits(2 * mt, p.kblocks[0][0], t.nsm);
+  if (2 * mt * 3 >= t.nsm * 2) {
+    // many M tiles (one CTA per SM, non-persistent grid).  3xTF32 is bound
+    // by the SMs (the in-smem A split), so K is split when that fills the
+    // last wave: config 4 (2 x 128 tiles on 148 SMs) runs 2 waves at 86%
+    // occupancy unsplit and 7 waves at 99% with 4 splits (atomic epilogue
+    // into the zeroed AV / BV rows): 1169 -> 1069 us.  tf32 / bf16 stream
+    // A and B at the HBM rate with the 108-CTA second wave already, and
+    // the split (atomics, more waves) measured slower: 403 -> 424 us.
+    auto eff = [&](int s) {
+      const long items = 2L * mt * s, waves = (items + t.nsm - 1) / t.nsm;
+      return (double)items / (double)(waves * t.nsm);
+    };
+    int best = 1;
+    for (int s = 2; t.x3 && s <= 8 && s <= p.kblocks[0][0]; ++s)
+      if (eff(s) > eff(best) + 0.05) best = s;
+    p.splits = best;
+    if (const char* e = getenv("GEIG_DENSE_SPLITS")) p.splits = std::max(1, atoi(e));   // developer A/B
+  } else {
+    p.splits = choose_splits(2 * mt, p.kblocks[0][0], t.nsm);
+  }
   p.atomic = p.splits > 1;
   p.split_stride = 0;
   if (p.atomic) {

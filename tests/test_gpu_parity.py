@@ -305,6 +305,17 @@ def test_dense_config4_full_size_tf32_tcgen05(geig):
     _dense_step_check(geig, a, b, cfg.k, "tf32", cfg.rho, cfg.eta, cfg.gamma)
 
 
+def test_dense_config4_full_size_3xtf32_split_k(geig):
+    """Config 4 at full size on 3xTF32: the products launch splits K in 4
+    (2 x 128 M tiles on 148 SMs fill 7 waves instead of 2, atomic epilogue
+    into the zeroed AV / BV rows) — held to 1e-3 (3xTF32 products are
+    ~5e-7 relative; the bar leaves room for fp32 storage of the step)."""
+    from synth import CONFIGS, dense_gep_large
+    cfg = CONFIGS[4]
+    a, b = dense_gep_large(cfg.d, seed=1, device="cuda:0")
+    _dense_step_check(geig, a, b, cfg.k, "3xtf32", cfg.rho, cfg.eta, cfg.gamma, tol=1e-3)
+
+
 # --- the fused single-launch step (geig_step_cca on the bf16 path) -------------
 
 @pytest.mark.parametrize("cfg_idx,rows,k,dx,dy", [(3, 4096, None, None, None), (2, 1024, None, None, None),
