@@ -31,10 +31,31 @@ def test_config0_converges_to_exact_solution():
     assert np.all(metrics.per_vector_angles(V1, Vt) < 1e-3)
 
 
+def _direction_minibatch_parent(i, V, AUX, AV, BV, rho):
+    """NEGATIVE CONTROL (not the paper's rule): Alg. 2's direction with the
+    parents' minibatch products B_t v_j in place of the auxiliary variable
+    [Bv]_j in [By]_j — the biased estimator that PAPER.md:991 introduces the
+    auxiliary variable to avoid ("This effectively replaces B y_j with a
+    non-random variable, avoiding the bias dilemma")."""
+    vi = V[i]
+    avi, bvi = AV[i], BV[i]
+    out = (vi @ bvi) * avi - (vi @ avi) * bvi
+    for j in range(i):
+        den = game.clip_denominator(V[j], AUX[j], rho)
+        a_yj, byj = AV[j] / den, BV[j] / den
+        out = out - (vi @ a_yj) * ((vi @ bvi) * byj - (vi @ byj) * bvi)
+    return out
+
+
 def test_stochastic_update_unbiased_monte_carlo():
-    """Appendix C: freeze a state with exact aux [Bv]_j = B v_j; the mean of
-    the stochastic direction over independent minibatches equals the
-    full-batch direction (4.5 standard errors componentwise)."""
+    """Appendix C and PAPER.md:989-991: freeze a state with a
+    non-random aux [Bv]_j = B v_j; the mean of Alg. 2's stochastic direction
+    over independent minibatches equals the full-batch direction (within 4.5
+    standard errors componentwise).  Positive control of the test's power:
+    the same draws through the estimator that uses the minibatch B_t v_j in
+    place of [Bv]_j (the bias the auxiliary variable exists to avoid) must
+    sit more than 8 standard errors away.  Minibatches of 4 rows (h = 2: A_t
+    and B_t from independent pairs of rows) make that bias large."""
     cfg = CONFIGS[1]
     x, y = cca_views(cfg, 4096, seed=1)
     x, y = x.double().numpy()[:, :6], y.double().numpy()[:, :6]
@@ -44,14 +65,19 @@ def test_stochastic_update_unbiased_monte_carlo():
     aux = (b @ V.T).T
     av, bv = estimators.dense_products(a, b, V)
     full = np.array([game.direction_alg2(i, V, aux, av, bv, 1e-3) for i in range(3)])
-    draws = []
-    for _ in range(4000):
-        idx = rng.choice(4096, size=16, replace=False)
+    paper, biased = [], []
+    for _ in range(40000):
+        idx = rng.choice(4096, size=4, replace=False)
         sav, sbv = estimators.cca_products(x[idx], y[idx], V)
-        draws.append([game.direction_alg2(i, V, aux, sav, sbv, 1e-3) for i in range(3)])
-    draws = np.array(draws)
-    se = draws.std(0) / np.sqrt(len(draws))
-    assert np.all(np.abs(draws.mean(0) - full) <= 4.5 * se + 1e-12)
+        paper.append([game.direction_alg2(i, V, aux, sav, sbv, 1e-3) for i in range(3)])
+        biased.append([_direction_minibatch_parent(i, V, aux, sav, sbv, 1e-3) for i in range(3)])
+    z = {}
+    for name, d in (("paper", np.array(paper)), ("biased", np.array(biased))):
+        se = d.std(0) / np.sqrt(len(d))
+        z[name] = np.abs(d.mean(0) - full) / (se + 1e-300)
+    assert np.all(z["paper"] <= 4.5), z["paper"].max()
+    # player 0 has no parents (both forms agree); the bias shows on the children
+    assert z["biased"][1:].max() > 8.0, z["biased"].max()
 
 
 def test_stochastic_cca_converges_small():

@@ -269,3 +269,146 @@ def test_alg2_adam_reduces_to_sign_ascent():
     g0 = game.direction_alg2(0, V, AUX, machines[0][0], machines[0][1], rho)
     np.testing.assert_allclose(Ma[0], 0.1 * g0, rtol=1e-12)
     np.testing.assert_allclose(Sa[0], 0.001 * g0 * g0, rtol=1e-12)
+
+
+# --- round-2 pins: the auxiliary variable, the rho floor, Alg. 3's z-gradient ---
+
+def _golden_hand_cases():
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "alg2_hand_directions.txt")
+    rows = []
+    for line in open(path):
+        if line.strip() and not line.startswith("#"):
+            f = line.split()
+            rows.append((f[0], np.array(f[1:4], float), np.array(f[4:7], float), np.array(f[7:10], float)))
+    return rows
+
+
+@pytest.mark.parametrize("case", _golden_hand_cases(), ids=lambda c: c[0])
+def test_alg2_direction_hand_worked_example(case):
+    """tests/golden/alg2_hand_directions.txt: Alg. 2 lines 8-12 worked by hand
+    (k = 2, d = 3) with [Bv]_0 != B_t v_0 — unclipped, clipped by rho and
+    with <v_0,[Bv]_0> negative (PAPER.md:991 'may not be positive ...
+    clip the result to be greater than or equal to rho')."""
+    name, aux0, g0, g1 = case
+    V = np.array([[1.0, 0, 0], [0, 1.0, 0]])
+    AV = np.array([[2.0, 1, 0], [1, 3, 1]])
+    BV = np.array([[1.0, 0, 0], [0, 2, 1]])
+    AUX = np.array([aux0, [1.0, 1, 1]])
+    np.testing.assert_allclose(game.direction_alg2(0, V, AUX, AV, BV, 0.5), g0, rtol=0, atol=1e-14)
+    np.testing.assert_allclose(game.direction_alg2(1, V, AUX, AV, BV, 0.5), g1, rtol=0, atol=1e-13)
+    V2, A2 = game.step_alg2(V, AUX, [(AV, BV)], 0.1, 0.25, 0.5)
+    np.testing.assert_allclose(A2, AUX + 0.25 * (BV - AUX), rtol=0, atol=1e-15)
+    for i, g in enumerate((g0, g1)):
+        vp = V[i] + 0.1 * g
+        np.testing.assert_allclose(V2[i], vp / np.sqrt(vp @ vp), rtol=0, atol=1e-15)
+
+
+def test_alg2_aux_scale_invariance():
+    """PAPER.md:989-991 and Alg. 2 lines 8-9: the parents enter only through
+    y_j = v_j / sqrt(<v_j,[Bv]_j>) and [By]_j = [Bv]_j / sqrt(<v_j,[Bv]_j>), so
+    with exact A, B and aux = c * B v_j (any c with c <v_j,Bv_j> >= rho) the
+    penalty is unchanged: c cancels between (v_i^T A y_j) ~ c^-1/2 and
+    [By]_j ~ c^1/2, and Alg. 2's direction equals Alg. 1's (exact
+    y_j = v_j / ||v_j||_B).  A direction that took [By]_j from anything but
+    the auxiliary variable scales with c and fails."""
+    a, b = dense_gep_small(4, 9)
+    rng = np.random.default_rng(11)
+    V, _ = game.init_state(rng.standard_normal((4, 9)))
+    av, bv = estimators.dense_products(a, b, V)
+    for c in (0.3, 1.0, 2.5, 7.0):
+        aux = c * bv
+        assert np.all(c * np.sum(V * bv, 1) > 0.01)
+        for i in range(4):
+            np.testing.assert_allclose(game.direction_alg2(i, V, aux, av, bv, 0.01),
+                                       game.direction_alg1(i, V, a, b), rtol=1e-10, atol=1e-10)
+
+
+def test_alg2_penalty_scales_with_the_clipped_denominator():
+    """Alg. 2 line 8 (the red max(., rho)): with one parent j,
+    grad_i = rewards_i - P_ij / max(<v_j,[Bv]_j>, rho) where P_ij does not
+    depend on rho — both the A y_j and the [By]_j factor carry one
+    1/sqrt(max(.)).  rewards_i is player i's direction without parents.  So
+    (rewards - grad) * max(<v_j,[Bv]_j>, rho) must be the same vector for rho
+    below the inner product (no clip), above it, and for a NEGATIVE inner
+    product; and for rho below the inner product the direction must not
+    depend on rho at all."""
+    rng = np.random.default_rng(12)
+    d = 7
+    V, _ = game.init_state(rng.standard_normal((2, d)))
+    AV, BV = rng.standard_normal((2, d)), rng.standard_normal((2, d))
+    for ip in (0.8, 0.05, -0.6):
+        aux0 = rng.standard_normal(d)
+        aux0 += (ip - V[0] @ aux0) * V[0]          # <v_0, [Bv]_0> = ip exactly
+        AUX = np.stack([aux0, rng.standard_normal(d)])
+        rewards = game.direction_alg2(0, V[::-1].copy(), AUX[::-1].copy(), AV[::-1].copy(), BV[::-1].copy(), 1.0)
+        P = []
+        for rho in (0.01, 0.3, 1.7):
+            g = game.direction_alg2(1, V, AUX, AV, BV, rho)
+            P.append((rewards - g) * max(ip, rho))
+        for p in P[1:]:
+            np.testing.assert_allclose(p, P[0], rtol=1e-12, atol=1e-12)
+        if ip > 0.3:
+            np.testing.assert_allclose(game.direction_alg2(1, V, AUX, AV, BV, 0.01),
+                                       game.direction_alg2(1, V, AUX, AV, BV, 0.3), rtol=1e-13, atol=1e-13)
+
+
+def test_alg3_z_direction_is_the_negative_gradient_of_the_bracket_fit():
+    """Appendix E: grad_z = -(<v_j,Bv_j> - [<v,Bv>]_j)
+    [<v,Bv>]_j (log nu - log rho) sigma(z_j)(1 - sigma(z_j)) is the derivative
+    of the fit loss 1/2 (<v_j,Bv_j> - [<v,Bv>]_j(z_j))^2 with
+    [<v,Bv>]_j(z) = exp(log rho + (log nu - log rho) sigma(z)); the algorithm
+    box drops the minus and ascends (line 21), i.e.
+    z_direction = -dL/dz (reading R6).  Checked by central differences of
+    the bracket itself at several z and targets, which pins the whole chain
+    factor br (log nu - log rho) sigma (1 - sigma)."""
+    rho, nu = 0.05, 20.0
+    for z in (-3.0, -0.4, 0.0, 0.9, 2.5):
+        for target in (0.01, 0.7, 4.0, 30.0):
+            v = np.array([[1.0, 0.0]])
+            aux = np.array([[target, 0.3]])
+            loss = lambda zz: 0.5 * (target - game.smooth_bracket(zz, rho, nu)) ** 2
+            h = 1e-5
+            fd = -(loss(z + h) - loss(z - h)) / (2 * h)
+            got = game.z_direction(0, v, aux, [z], rho, nu)
+            assert abs(got - fd) <= 1e-7 * max(1.0, abs(fd)), (z, target, got, fd)
+
+
+def test_alg3_bracket_limits_and_monotone():
+    """Alg. 3 line 7: the bracket runs from rho (z -> -inf) to nu (z -> +inf),
+    increasing in z, log-linear in sigma(z)."""
+    rho, nu = 0.05, 20.0
+    zs = np.linspace(-30, 30, 121)
+    br = np.array([game.smooth_bracket(z, rho, nu) for z in zs])
+    assert np.all(np.diff(br) > 0)
+    assert abs(br[0] - rho) < 1e-10 and abs(br[-1] - nu) < 1e-9
+    s = 1 / (1 + np.exp(-0.8))
+    assert np.isclose(np.log(game.smooth_bracket(0.8, rho, nu)), np.log(rho) + (np.log(nu) - np.log(rho)) * s,
+                      rtol=1e-14)
+
+
+def test_alg3_direction_equals_alg2_where_the_bracket_matches():
+    """Alg. 3 lines 7-12 differ from Alg. 2 lines 8-12
+    only in the denominator: with z_j set so that the bracket
+    [<v,Bv>]_j = exp(log rho + (log nu - log rho) sigma(z_j)) equals
+    <v_j,[Bv]_j> (> rho, so Alg. 2 does not clip), the two directions agree
+    for ANY auxiliary variables — and with rho > <v_j,[Bv]_j> and z -> -inf
+    the bracket is rho, Alg. 2's clipped value."""
+    rng = np.random.default_rng(13)
+    k, d = 4, 8
+    V, _ = game.init_state(rng.standard_normal((k, d)))
+    AV, BV = rng.standard_normal((k, d)), rng.standard_normal((k, d))
+    AUX = V * rng.uniform(0.5, 3.0, (k, 1)) + 0.2 * rng.standard_normal((k, d))
+    ip = np.sum(V * AUX, 1)
+    assert np.all(ip > 0.06)
+    rho, nu = 0.05, 50.0
+    s = (np.log(ip) - np.log(rho)) / (np.log(nu) - np.log(rho))
+    Z = np.log(s / (1 - s))
+    for i in range(k):
+        np.testing.assert_allclose(game.direction_alg3(i, V, AUX, Z, AV, BV, rho, nu),
+                                   game.direction_alg2(i, V, AUX, AV, BV, rho), rtol=1e-10, atol=1e-10)
+    rho_hi = 1.05 * ip.max()
+    Zlo = np.full(k, -60.0)
+    for i in range(k):
+        np.testing.assert_allclose(game.direction_alg3(i, V, AUX, Zlo, AV, BV, rho_hi, 10 * rho_hi),
+                                   game.direction_alg2(i, V, AUX, AV, BV, rho_hi), rtol=1e-10, atol=1e-10)
