@@ -28,6 +28,13 @@
  *   A_t v = (1/h) [X1^T (Y1 v_y) ; Y1^T (X1 v_x)]
  *   B_t v = (1/h) [X2^T (X2 v_x) ; Y2^T (Y2 v_y)]      (PAPER.md:831 CCA)
  *
+ * L2: the solver's state arena is marked persisting in L2 through an access-
+ * policy window attached to the library's own cooperative launches (no
+ * stream attribute is changed).  Side effect: geig_create raises the
+ * device's persisting-L2 set-aside (cudaLimitPersistingL2CacheSize) to at
+ * most the arena size and never lowers it; geig_destroy resets the device's
+ * persisting lines (cudaCtxResetPersistingL2Cache).
+ *
  * Ownership: the solver owns V, AUX and its scratch (allocated in
  * geig_create, freed in geig_destroy).  Every pointer argument is owned by the
  * caller and only read (or written, for outputs) during the call / the
@@ -235,6 +242,21 @@ geig_status geig_step_cca_host(geig_solver* s, const void* X_host,
  * "k x k inner-product tables" of the north star, from the iteration-start
  * state. */
 geig_status geig_get_gram(geig_solver* s, float* GA, float* GB, float* GC);
+
+/* Schedule options of a solver (they change which kernels run and how work
+ * is tiled, never the arithmetic of Alg. 2; results differ at most by
+ * floating-point summation order).  No environment variable is read by the
+ * library.
+ *  GEIG_OPT_FUSED_M_TILES   : 128-row M tiles per work item of the fused
+ *                             step's GEMM phases (0 = auto: 2 where the grid
+ *                             stays busy, else 1; 1; 2)
+ *  GEIG_OPT_STAGED_PRODUCTS : 1 = geig_products_cca runs the three-launch
+ *                             staged tcgen05 products (forward GEMM, z
+ *                             reshuffle, backward GEMM) instead of phases
+ *                             F, S, B of the fused kernel; 0 = fused (default)
+ * Errors: GEIG_ERR_ARG for an unknown option or a value out of range. */
+typedef enum { GEIG_OPT_FUSED_M_TILES = 1, GEIG_OPT_STAGED_PRODUCTS = 2 } geig_option;
+geig_status geig_set_option(geig_solver* s, int option, int64_t value);
 
 /* Phase durations (ns, %globaltimer of CTA 0) of the last update:
  * out[0] Gram partials, out[1] grid reduction, out[2] coefficients + fused

@@ -3,8 +3,41 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <atomic>
+#include <cstdlib>
+
+#ifndef GEIG_DEV_KNOBS
+#define GEIG_DEV_KNOBS 0
+#endif
 
 namespace geig {
+
+// Developer A/B and timing knobs read from the environment exist only in a
+// build with -DGEIG_DEV_KNOBS=1 (GEIG_NVCC_EXTRA); the default library reads
+// no environment variable, so nothing outside the ABI changes its schedule
+// or its numerics.
+inline const char* dev_knob(const char* name) {
+#if GEIG_DEV_KNOBS
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// function attributes are per device context, so a solver created on a
+// second device sets them again.  Thread-safe (setting twice is harmless).
+inline cudaError_t set_smem_attr_once(std::atomic<uint64_t>& done, const void* fn, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 __device__ __forceinline__ float to_f32(float x) { return x; }
 __device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }

@@ -713,6 +713,29 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
 // its grid partition (gridDim = G, segw) is reused by the GEMM phases.
 // The six A-operand maps of one batch (X, Y sample-major, b = 2h rows):
 // [0..1] forward K-major boxes, [2..5] backward MN-major boxes of the halves.
+// Cooperative launch with the solver's persisting-L2 window attached to THIS
+// launch only (no stream attribute is changed, so the caller's later kernels
+// on the same stream do not inherit it).
+inline cudaError_t launch_coop(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st,
+                               const cudaAccessPolicyWindow& win) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  attr[n].id = cudaLaunchAttributeCooperative;
+  attr[n++].val.cooperative = 1;
+  if (win.num_bytes > 0) {
+    attr[n].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[n++].val.accessPolicyWindow = win;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 inline bool make_batch_maps(CUtensorMap* a, const TcPlan& t, const void* X, const void* Y, int h) {
   const int eb = 2, ATOM = 64;
   const int64_t dv[2] = {t.dx, t.dy};
@@ -769,13 +792,13 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
         return tc_fail(GEIG_ERR_CUDA, "allocating the dependency counters failed");
     }
     const bool runs_reduce = !products_only || tables;
-    if (runs_reduce && !getenv("GEIG_NO_EARLY_COEF")) {
+    if (runs_reduce && !dev_knob("GEIG_NO_EARLY_COEF")) {
       p.rcnt = t.dep;
       p.early_coef = products_only ? 0 : 1;
     }
-    if (!getenv("GEIG_F_BARRIER")) p.fcnt = t.dep + 32;   // GEIG_F_BARRIER: developer A/B (grid barrier after F)
+    if (!dev_knob("GEIG_F_BARRIER")) p.fcnt = t.dep + 32;   // GEIG_F_BARRIER: developer A/B (grid barrier after F)
     p.btiles = btiles;
-    if (!products_only && !getenv("GEIG_BU_BARRIER")) p.bcnt = t.dep + 32 + ntiles;   // (grid barrier after B)
+    if (!products_only && !dev_knob("GEIG_BU_BARRIER")) p.bcnt = t.dep + 32 + ntiles;   // (grid barrier after B)
   }
   if (products_only && nsteps != 1) return tc_fail(GEIG_ERR_ARG, "products-only launch runs one step");
   p.xmaps = nullptr;
@@ -825,13 +848,13 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   // M tiles per work item: 2 where the grid stays busy (the B-operand tile of
   // each K step then serves 256 rows / columns), else 1
   {
-    const int fixed = getenv("GEIG_TM") ? std::max(1, std::min(2, atoi(getenv("GEIG_TM")))) : 0;
+    const int fixed = t.opt_m_tiles;   // geig_set_option(GEIG_OPT_FUSED_M_TILES), 0 = auto
     int nB2 = 0;
     for (int v = 0; v < 2; ++v) nB2 += 2 * (int)((dv[v] + 2 * TC_BM - 1) / (2 * TC_BM));
     p.tmB = fixed ? fixed : (2 * nB2 >= grid_ctas ? 2 : 1);
     p.tmF = fixed ? fixed : (rows >= 8 * TC_BM ? 2 : 1);
-    if (getenv("GEIG_TMF")) p.tmF = std::max(1, std::min(2, atoi(getenv("GEIG_TMF"))));   // developer A/B knobs
-    if (getenv("GEIG_TMB")) p.tmB = std::max(1, std::min(2, atoi(getenv("GEIG_TMB"))));
+    if (dev_knob("GEIG_TMF")) p.tmF = std::max(1, std::min(2, atoi(dev_knob("GEIG_TMF"))));   // developer A/B knobs
+    if (dev_knob("GEIG_TMB")) p.tmB = std::max(1, std::min(2, atoi(dev_knob("GEIG_TMB"))));
     for (int v = 0; v < 2; ++v) p.mtB[v] = (int)((dv[v] + p.tmB * TC_BM - 1) / (p.tmB * TC_BM));
   }
   {
@@ -854,17 +877,16 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.BV = BV;
   p.upd = upd;
   p.upd.dbg = dbg_ptr();
-  p.upd.dbg_mode = getenv("GEIG_DBG_MODE") ? atoi(getenv("GEIG_DBG_MODE")) : 0;
+  p.upd.dbg_mode = dev_knob("GEIG_DBG_MODE") ? atoi(dev_knob("GEIG_DBG_MODE")) : 0;
   p.upd.ga_done = 1;       // phase S forms G^A, G^B from z
   p.upd.pre_reduced = 1;   // G^C, ||v''||^2 in F (warps 2-3), reduction in B (warps 2-3)
   p.split = t.splitb;
-  // backward B operand (z) as hi + lo too: GEIG_NO_ZLO drops the lo half (developer A/B)
-  p.splitB = (t.splitb && !getenv("GEIG_NO_ZLO")) ? 1 : 0;
+  p.splitB = t.splitb;   // bf16x2: the backward B operand (z) as hi + lo too
   p.idescB = make_idesc(eb, true, t.BN * (p.splitB ? 2 : 1), TC_BM);
-  p.bwd_y_first = getenv("GEIG_BWD_X_FIRST") ? 0 : 1;
-  p.l2_keep = getenv("GEIG_L2_KEEP") ? 1 : 0;   // measured: evict-last on a whole view thrashes the state arrays (slower)
-  p.dbg_nostore = getenv("GEIG_DBG_NOSTORE") ? 1 : 0;   // developer: drop GEMM epilogue stores (timing only)
-  p.dbg_mode = getenv("GEIG_DBG_MODE") ? atoi(getenv("GEIG_DBG_MODE")) : 0;   // developer timing knobs (wrong results)
+  p.bwd_y_first = dev_knob("GEIG_BWD_X_FIRST") ? 0 : 1;
+  p.l2_keep = dev_knob("GEIG_L2_KEEP") ? 1 : 0;   // measured: evict-last on a whole view thrashes the state arrays (slower)
+  p.dbg_nostore = dev_knob("GEIG_DBG_NOSTORE") ? 1 : 0;   // developer: drop GEMM epilogue stores (timing only)
+  p.dbg_mode = dev_knob("GEIG_DBG_MODE") ? atoi(dev_knob("GEIG_DBG_MODE")) : 0;   // developer timing knobs (wrong results)
   const size_t stage_bytes = (size_t)std::max(p.tmF, p.tmB) * TC_BM * 128 + (size_t)t.BN * 128 * (t.splitb ? 2 : 1);
   if ((size_t)std::max(p.tmF, p.tmB) * t.BN * (t.splitb ? 2 : 1) > 256)
     return tc_fail(GEIG_ERR_UNSUPPORTED, "fused step: accumulators exceed the TMEM allocation");
@@ -877,18 +899,13 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
     if (smem + (size_t)GEIG_COEF_FLOATS * 4 <= 227 * 1024) smem += (size_t)GEIG_COEF_FLOATS * 4;
     else p.early_coef = 0;
   }
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(cca_step_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(cca_step_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
-            cudaSuccess)
-      return tc_fail(GEIG_ERR_CUDA, "cudaFuncSetAttribute(cca_step_kernel) failed");
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr_plain{0}, attr_adam{0};
+  if (set_smem_attr_once(attr_plain, (const void*)cca_step_kernel<2, false>, 227 * 1024) != cudaSuccess ||
+      set_smem_attr_once(attr_adam, (const void*)cca_step_kernel<2, true>, 227 * 1024) != cudaSuccess)
+    return tc_fail(GEIG_ERR_CUDA, "cudaFuncSetAttribute(cca_step_kernel) failed");
   void* args[] = {(void*)&maps, (void*)&p};
   void* kfn = p.upd.adam ? (void*)cca_step_kernel<2, true> : (void*)cca_step_kernel<2, false>;
-  cudaError_t e = cudaLaunchCooperativeKernel(kfn, dim3(grid_ctas), dim3(FS_THREADS), args, smem, st);
+  cudaError_t e = launch_coop(kfn, dim3(grid_ctas), dim3(FS_THREADS), args, smem, st, t.l2win);
   if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("cca_step_kernel launch: ") + cudaGetErrorString(e));
 
   return GEIG_OK;

@@ -16,7 +16,6 @@
 #include "update.cuh"
 #include "tc_gemm.cuh"
 #include "fused_step.cuh"
-#include "dataflow_step.cuh"
 
 using namespace geig;
 
@@ -77,12 +76,14 @@ struct geig_solver {
   size_t upd_smem = 0;
   int64_t launches = 0;
   tc::TcPlan tc;                                      // tcgen05 plans (tensor maps, scratch)
-  tc::DfPlan df;                                      // dataflow-step schedule + counters
+  int opt_staged = 0;                                 // geig_set_option(GEIG_OPT_STAGED_PRODUCTS)
 };
 
 extern "C" const char* geig_last_error(void) { return g_err.c_str(); }
 extern "C" const char* geig_version(void) { return "geig 0.1 (sm_100a)"; }
 extern "C" int64_t geig_launch_count(const geig_solver* s) { return s ? s->launches : 0; }
+
+static void set_l2_window(geig_solver* s);
 
 extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, int64_t dy,
                                    int32_t k, int math, int data_dtype, double rho,
@@ -183,6 +184,7 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
     geig_status st = tc::plan_create(s->tc, problem, dx, dy, k, math, max_rows, device);
     if (st != GEIG_OK) return cleanup(fail(st, "%s", tc::last_error()));
   }
+  set_l2_window(s);
   if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(fail(GEIG_ERR_CUDA, "create sync"));
   *out = s;
   return GEIG_OK;
@@ -191,35 +193,41 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
 extern "C" geig_status geig_destroy(geig_solver* s) {
   if (!s) return GEIG_OK;
   cudaSetDevice(s->device);
+  if (s->tc.l2win.num_bytes > 0) cudaCtxResetPersistingL2Cache();   // no persisting lines outlive the arena
   for (void* p : {(void*)s->arena,
                   (void*)s->gram, (void*)s->raw, (void*)s->partial,
                   (void*)s->Wx, (void*)s->Wy, (void*)s->ts, (void*)s->Wxb, (void*)s->Wyb, s->hX, s->hY,
                   (void*)s->zbuf, (void*)s->am, (void*)s->as})
     if (p) cudaFree(p);
-  tc::df_destroy(s->df);
   tc::plan_destroy(s->tc);
   delete s;
   return GEIG_OK;
 }
 
-// Pin the state arena in L2 (persisting access policy on the solver's stream)
-// so the update phases find V, [Bv], AV, BV in L2 after the products have
-// streamed the minibatch (> L2) through it.  Best effort: ignored on failure.
+// Persisting-L2 window over the state arena (V, [Bv], AV, BV, bf16 shadow)
+// so the update phases find the state in L2 after the products have streamed
+// the minibatch (> L2) through it.  The window is attached to the library's
+// own cooperative launches only (a launch attribute; no stream attribute is
+// changed).  Side effect (documented in geig.h): the device's persisting-L2
+// set-aside is raised to the arena size (never lowered); geig_destroy resets
+// the persisting lines.  Best effort: skipped when the device has no
+// set-aside.
 static void set_l2_window(geig_solver* s) {
-  if (getenv("GEIG_NO_L2_PERSIST")) return;
+  if (dev_knob("GEIG_NO_L2_PERSIST")) return;
   int max_persist = 0, max_window = 0;
   cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, s->device);
   cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, s->device);
   if (max_persist <= 0 || max_window <= 0) return;
   const size_t want = std::min<size_t>(s->arena_bytes, (size_t)max_persist);
-  cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-  cudaStreamAttrValue v = {};
-  v.accessPolicyWindow.base_ptr = s->arena;
-  v.accessPolicyWindow.num_bytes = std::min<size_t>(s->arena_bytes, (size_t)max_window);
-  v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)want / (float)v.accessPolicyWindow.num_bytes);
-  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-  cudaStreamSetAttribute(s->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+  size_t cur = 0;
+  cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+  if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+  cudaAccessPolicyWindow& w = s->tc.l2win;
+  w.base_ptr = s->arena;
+  w.num_bytes = std::min<size_t>(s->arena_bytes, (size_t)max_window);
+  w.hitRatio = std::min(1.0f, (float)want / (float)w.num_bytes);
+  w.hitProp = cudaAccessPropertyPersisting;
+  w.missProp = cudaAccessPropertyStreaming;
   cudaGetLastError();   // best effort
 }
 
@@ -232,7 +240,6 @@ extern "C" geig_status geig_set_stream(geig_solver* s, void* stream) {
     CU(cudaStreamSynchronize(s->stream));
   }
   s->stream = (cudaStream_t)stream;
-  if (s->stream) set_l2_window(s);
   return GEIG_OK;
 }
 
@@ -349,7 +356,7 @@ extern "C" geig_status geig_products_cca(geig_solver* s, const void* X, const vo
       return products_cca_simt(s, (const float*)X, (const float*)Y, b, scale, AV, BV);
     return products_cca_simt(s, (const __nv_bfloat16*)X, (const __nv_bfloat16*)Y, b, scale, AV, BV);
   }
-  if (fused_ok(s, X, Y) && !getenv("GEIG_STAGED_PRODUCTS")) {
+  if (fused_ok(s, X, Y) && !s->opt_staged) {
     // phases F, S, B of the fused step kernel in one launch, AV / BV to the
     // caller's buffers (e.g. before a cross-GPU all-reduce and geig_update)
     geig_status st = tc::fused_cca_step(s->tc, &X, &Y, 1, b, scale, s->Vbf, AV, BV, update_args(s, 0.0, 0.0),
@@ -398,7 +405,7 @@ extern "C" geig_status geig_update_tables(geig_solver* s, const float* AV, const
   a.AV = AV; a.BV = BV;
   a.raw_a = const_cast<float*>(T);
   a.pre_reduced = 1;
-  if ((s->math == GEIG_MATH_BF16 || s->math == GEIG_MATH_BF16X2) && !getenv("GEIG_NO_FUSED") &&
+  if ((s->math == GEIG_MATH_BF16 || s->math == GEIG_MATH_BF16X2) && !dev_knob("GEIG_NO_FUSED") &&
       ((uintptr_t)AV | (uintptr_t)BV) % 16 == 0) {
     // phase U of the fused kernel alone (TMA-staged tiles, early table staging)
     const void* none[1] = {nullptr};
@@ -414,7 +421,7 @@ extern "C" geig_status geig_update_tables(geig_solver* s, const float* AV, const
   void* args[] = {&a};
   const bool vec = ((uintptr_t)AV | (uintptr_t)BV) % 16 == 0;
   void* fn = vec ? (void*)update_res_kernel<true> : (void*)update_res_kernel<false>;
-  CU(cudaLaunchCooperativeKernel(fn, dim3(s->upd_grid), dim3(UPD_THREADS), args, s->upd_smem, s->stream));
+  CU(tc::launch_coop(fn, dim3(s->upd_grid), dim3(UPD_THREADS), args, s->upd_smem, s->stream, s->tc.l2win));
   s->launches++;
   s->fused_last = false;
   advance_variant_state(s, 1);
@@ -466,7 +473,7 @@ extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float*
   if (s->upd_res) fn = vec ? (void*)update_res_kernel<true> : (void*)update_res_kernel<false>;
   else if (s->k <= 64) fn = vec ? (void*)update_kernel<1, true> : (void*)update_kernel<1, false>;
   else fn = vec ? (void*)update_kernel<2, true> : (void*)update_kernel<2, false>;
-  CU(cudaLaunchCooperativeKernel(fn, dim3(s->upd_grid), dim3(UPD_THREADS), args, s->upd_smem, s->stream));
+  CU(tc::launch_coop(fn, dim3(s->upd_grid), dim3(UPD_THREADS), args, s->upd_smem, s->stream, s->tc.l2win));
   s->launches++;
   advance_variant_state(s, 1);
   return GEIG_OK;
@@ -474,7 +481,7 @@ extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float*
 
 static bool fused_ok(const geig_solver* s, const void* X, const void* Y) {
   if ((s->math != GEIG_MATH_BF16 && s->math != GEIG_MATH_BF16X2) || !s->upd_res || s->d % 4 != 0) return false;
-  if (getenv("GEIG_NO_FUSED")) return false;
+  if (dev_knob("GEIG_NO_FUSED")) return false;
   return (((uintptr_t)X | (uintptr_t)Y) % 16) == 0;
 }
 
@@ -504,16 +511,8 @@ extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* 
     // whole step in one persistent cooperative launch (fused_step.cuh)
     CU(cudaSetDevice(s->device));
     const UpdateArgs a = update_args(s, eta, gamma);
-    geig_status st;
-    // The dataflow schedule (dataflow_step.cuh) is correct but, measured on
-    // B200, not yet faster than the phase-ordered kernel (its split-K fix-ups
-    // sit on the critical path under full-DRAM load); opt-in via GEIG_DATAFLOW=1.
-    if (getenv("GEIG_DATAFLOW") && !s->tc.splitb && tc::df_prepare(s->df, s->tc, b, s->upd_grid))
-      st = tc::df_cca_step(s->tc, s->df, X, Y, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a, s->upd_smem,
-                           s->stream);
-    else
-      st = tc::fused_cca_step(s->tc, &X, &Y, 1, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a, s->upd_grid,
-                              s->upd_smem, s->stream);
+    geig_status st = tc::fused_cca_step(s->tc, &X, &Y, 1, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a,
+                                        s->upd_grid, s->upd_smem, s->stream);
     if (st) return fail(st, "%s", tc::last_error());
     s->launches++;
     s->fused_last = true;
@@ -531,7 +530,7 @@ extern "C" geig_status geig_run_cca(geig_solver* s, const void* const* X, const 
   if (!s || !X || !Y) return fail(GEIG_ERR_ARG, "NULL argument");
   if (nsteps < 0 || nsteps > (1 << 20)) return fail(GEIG_ERR_ARG, "nsteps = %lld out of range", (long long)nsteps);
   if (nsteps == 0) return GEIG_OK;
-  bool fused = s->problem == GEIG_CCA && b >= 2 && b <= s->max_rows && !getenv("GEIG_DATAFLOW");
+  bool fused = s->problem == GEIG_CCA && b >= 2 && b <= s->max_rows;
   for (int64_t i = 0; fused && i < nsteps; ++i) fused = X[i] && Y[i] && fused_ok(s, X[i], Y[i]);
   if (!fused) {
     for (int64_t i = 0; i < nsteps; ++i) {
@@ -629,6 +628,22 @@ extern "C" geig_status geig_set_adam(geig_solver* s, double b1, double b2, doubl
   s->b1 = (float)b1; s->b2 = (float)b2; s->eps = (float)eps;
   s->adam = 1;
   return GEIG_OK;
+}
+
+extern "C" geig_status geig_set_option(geig_solver* s, int option, int64_t value) {
+  if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  switch (option) {
+    case GEIG_OPT_FUSED_M_TILES:
+      if (value < 0 || value > 2) return fail(GEIG_ERR_ARG, "GEIG_OPT_FUSED_M_TILES must be 0, 1 or 2");
+      s->tc.opt_m_tiles = (int)value;
+      return GEIG_OK;
+    case GEIG_OPT_STAGED_PRODUCTS:
+      if (value != 0 && value != 1) return fail(GEIG_ERR_ARG, "GEIG_OPT_STAGED_PRODUCTS must be 0 or 1");
+      s->opt_staged = (int)value;
+      return GEIG_OK;
+    default:
+      return fail(GEIG_ERR_ARG, "unknown option %d", option);
+  }
 }
 
 extern "C" geig_status geig_update_phase_ns(geig_solver* s, int64_t* out) {

@@ -25,6 +25,7 @@
 #include <type_traits>
 #include <cstdlib>
 #include "../../include/geig.h"
+#include "common.cuh"
 
 namespace geig { namespace tc {
 
@@ -497,6 +498,8 @@ struct TcPlan {
   cudaEvent_t xm_ev = nullptr;      // last copy of the staging buffer
   int* dep = nullptr;               // fused step: Gram-reduction counter (monotonic, zeroed once)
   int x3 = 0;                       // 3xTF32 products (tf32 plan with hi/lo operands)
+  int opt_m_tiles = 0;              // geig_set_option(GEIG_OPT_FUSED_M_TILES): 0 = auto, 1 or 2
+  cudaAccessPolicyWindow l2win{};   // persisting-L2 window over the solver's state arena (num_bytes 0: none)
   float* Vx3 = nullptr;             // 3xTF32: [hi plane | lo plane] of V (2 x k x d fp32)
 };
 
@@ -559,13 +562,11 @@ inline size_t smem_bytes(int BN, int stages, bool split = false, bool x3 = false
 // resident CTA per SM (grid <= #SM) gets the deep ring, denser grids 4 stages.
 template <int EB, bool A_MN, int ST, bool SPLIT, bool X3 = false>
 inline cudaError_t launch_one(const TcMaps& maps, const TcParams& p, dim3 grid, cudaStream_t st) {
-  static bool attr_done = false;
-  if (!attr_done) {
+  static std::atomic<uint64_t> attr_done{0};
+  {
     const size_t mx = std::min<size_t>(227 * 1024, smem_bytes(128, ST, SPLIT, X3));
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<EB, A_MN, ST, SPLIT, X3>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mx);
+    cudaError_t e = set_smem_attr_once(attr_done, (const void*)tc_gemm_kernel<EB, A_MN, ST, SPLIT, X3>, (int)mx);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
@@ -730,7 +731,7 @@ inline geig_status products_cca(TcPlan& t, const void* X, const void* Y, int64_t
     p.idesc = make_idesc(eb, false, t.BN, TC_BM);
     const int mt = (rows + TC_BM - 1) / TC_BM;
     p.splits = std::min(TC_MAX_SPLITS, choose_splits_deep(2 * mt, std::min(p.kblocks[0][0], p.kblocks[1][0]), t.nsm));
-    if (const char* e = getenv("GEIG_FWD_SPLITS")) p.splits = std::max(1, std::min(TC_MAX_SPLITS, atoi(e)));
+    if (const char* e = dev_knob("GEIG_FWD_SPLITS")) p.splits = std::max(1, std::min(TC_MAX_SPLITS, atoi(e)));
     fsplits = p.splits;
     dim3 grid(mt, p.splits, 2);
     geig_status s = eb == 2 ? launch<2, false>(maps, p, grid, st, t.nsm, t.splitb)
@@ -855,7 +856,7 @@ inline geig_status products_dense(TcPlan& t, const void* A, const void* B, int64
     for (int s = 2; t.x3 && s <= 8 && s <= p.kblocks[0][0]; ++s)
       if (eff(s) > eff(best) + 0.05) best = s;
     p.splits = best;
-    if (const char* e = getenv("GEIG_DENSE_SPLITS")) p.splits = std::max(1, atoi(e));   // developer A/B
+    if (const char* e = dev_knob("GEIG_DENSE_SPLITS")) p.splits = std::max(1, atoi(e));   // developer A/B
   } else {
     p.splits = choose_splits(2 * mt, p.kblocks[0][0], t.nsm);
   }

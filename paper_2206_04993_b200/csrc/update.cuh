@@ -578,9 +578,6 @@ update_kernel(UpdateArgs p) {
 constexpr int UPD_RES_WMAX = 168;   // max columns per CTA (smem: 4 x 64 x 172 x 4 B + tables)
 constexpr int UPD_GT = 72;          // 8x4 lower-triangle Gram tiles of a 64 x 64 table
 constexpr int UPD_GS = 3;           // column slices of the Gram phase (UPD_GT * UPD_GS <= UPD_THREADS)
-#ifndef GEIG_DEV_KNOBS
-#define GEIG_DEV_KNOBS 0
-#endif
 // developer timing knobs (GEIG_DBG_MODE / GEIG_DBG_NOSTORE: skip work, wrong
 // results) are compiled in only with -DGEIG_DEV_KNOBS=1 (GEIG_NVCC_EXTRA)
 constexpr bool kDevKnobs = GEIG_DEV_KNOBS;

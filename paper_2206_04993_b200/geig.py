@@ -19,6 +19,7 @@ GEIG_OK, GEIG_ERR_ARG, GEIG_ERR_CUDA, GEIG_ERR_UNSUPPORTED, GEIG_ERR_STATE = ran
 GEIG_DENSE, GEIG_CCA = 0, 1
 GEIG_MATH_F32, GEIG_MATH_BF16, GEIG_MATH_TF32, GEIG_MATH_3XTF32, GEIG_MATH_BF16X2 = 0, 1, 2, 3, 4
 GEIG_DATA_F32, GEIG_DATA_BF16 = 0, 1
+GEIG_OPT_FUSED_M_TILES, GEIG_OPT_STAGED_PRODUCTS = 1, 2
 
 MATH_NAMES = {"f32": GEIG_MATH_F32, "bf16": GEIG_MATH_BF16, "tf32": GEIG_MATH_TF32,
               "3xtf32": GEIG_MATH_3XTF32, "bf16x2": GEIG_MATH_BF16X2}
@@ -59,6 +60,7 @@ _SIGS = {
                            ctypes.POINTER(_i64)],
     "geig_get_gram": [_vp, _vp, _vp, _vp],
     "geig_update_phase_ns": [_vp, ctypes.POINTER(_i64)],
+    "geig_set_option": [_vp, ctypes.c_int, _i64],
 }
 for _name, _args in _SIGS.items():
     _fn = getattr(_lib, _name)
@@ -76,7 +78,7 @@ EXPORTED = ["geig_create", "geig_destroy", "geig_set_stream", "geig_sync", "geig
             "geig_step_cca", "geig_step_dense", "geig_run_cca", "geig_step_cca_host", "geig_get_gram",
             "geig_set_smooth", "geig_smooth_state", "geig_set_adam",
             "geig_launch_count", "geig_last_error", "geig_version", "geig_update_phase_ns",
-            "geig_table_floats", "geig_products_cca_tables", "geig_update_tables"]
+            "geig_table_floats", "geig_products_cca_tables", "geig_update_tables", "geig_set_option"]
 
 
 def _check(st: int):
@@ -218,6 +220,10 @@ def geig_step_cca_host(h, X_host, Y_host, b: int, eta: float, gamma: float, ga_h
 
 def geig_get_gram(h, GA=None, GB=None, GC=None):
     _check(_lib.geig_get_gram(h, _ptr(GA, torch.float32), _ptr(GB, torch.float32), _ptr(GC, torch.float32)))
+
+
+def geig_set_option(h, option: int, value: int):
+    _check(_lib.geig_set_option(h, option, value))
 
 
 def geig_update_phase_ns(h):

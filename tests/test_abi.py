@@ -58,3 +58,18 @@ def test_no_gpu_fails_loudly(lib_path):
     from paper_2206_04993_b200 import geig
     with pytest.raises(geig.GeigError):
         geig.geig_create(geig.GEIG_CCA, 8, 8, 2, geig.GEIG_MATH_F32, geig.GEIG_DATA_F32, 0.1, 16, 0)
+
+
+def test_default_build_reads_no_environment():
+    """No environment variable changes the library's schedule or numerics:
+    getenv appears only inside common.cuh's dev_knob, compiled in only with
+    -DGEIG_DEV_KNOBS=1 (developer A/B builds)."""
+    csrc = os.path.join(ROOT, "paper_2206_04993_b200", "csrc")
+    hits = []
+    for f in sorted(os.listdir(csrc)):
+        for i, line in enumerate(open(os.path.join(csrc, f)), 1):
+            if "getenv" in line:
+                hits.append((f, i, line.strip()))
+    assert hits == [("common.cuh", 21, "return std::getenv(name);")], hits
+    src = open(os.path.join(csrc, "common.cuh")).read()
+    assert "#if GEIG_DEV_KNOBS\n  return std::getenv(name);" in src

@@ -324,9 +324,8 @@ def test_dense_config4_full_size_3xtf32_split_k(geig):
                                                   (3, 1024, 64, 2048, 1024), (3, 512, 48, 256, 384)])
 def test_fused_step_bf16(geig, cfg_idx, rows, k, dx, dy):
     """geig_step_cca runs forward GEMM, split-K reduction, backward GEMM, Gram
-    tables and the update in ONE cooperative kernel (the dataflow schedule
-    when h % 128 == 0 and d_view % 128 == 0, else the phase-ordered one); the
-    step must match the oracle like the staged path."""
+    tables and the update in ONE cooperative kernel; the step must match the
+    oracle like the staged path."""
     errs, _ = check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math="bf16", use_step=True)
     _assert(errs, 1e-2)
 
@@ -335,12 +334,12 @@ def test_fused_step_bf16(geig, cfg_idx, rows, k, dx, dy):
                                                        (2, 1200, 64, 400, 272, "bf16x2"),
                                                        (3, 4096, 16, 8192, 8192, "bf16x2")])
 @pytest.mark.parametrize("tm", ["1", "2"])
-def test_fused_step_forced_m_tiles(geig, monkeypatch, cfg_idx, rows, k, dx, dy, math, tm):
+def test_fused_step_forced_m_tiles(geig, cfg_idx, rows, k, dx, dy, math, tm):
     """Work items of two 128-row M tiles sharing each B-operand tile (the
     default at full size) and of one, forced on ragged shapes: a last item
     with a partial second M tile, a last item with a single M tile."""
-    monkeypatch.setenv("GEIG_TM", tm)
-    errs, _ = check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math=math, use_step=True)
+    errs, _ = check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math=math, use_step=True,
+                             options={geig.GEIG_OPT_FUSED_M_TILES: int(tm)})
     if math == "bf16":
         _assert(errs, 1e-2)
     else:
@@ -356,14 +355,6 @@ def test_fused_step_matches_staged_path(geig):
     e2, g2 = check_cca_step(geig, 2, 1024, math="bf16", use_step=False)
     assert rel_err(g1["V"] - g2["V"] + 1.0, np.ones_like(g2["V"])) < 1e-3
     assert rel_err(g1["aux"], g2["aux"]) < 1e-3
-
-
-def test_dataflow_step_bf16(geig, monkeypatch):
-    """The opt-in dataflow schedule (GEIG_DATAFLOW=1) matches the oracle too."""
-    monkeypatch.setenv("GEIG_DATAFLOW", "1")
-    for cfg_idx, rows, k, dx, dy in [(3, 4096, None, None, None), (3, 1024, 64, 2048, 1024)]:
-        errs, _ = check_cca_step(geig, cfg_idx, rows, k=k, dx=dx, dy=dy, math="bf16", use_step=True)
-        _assert(errs, 1e-2)
 
 
 # --- bf16x2: V and Z split into hi + lo bf16 operands (exact bf16 data) ------
@@ -437,13 +428,14 @@ def test_run_cca_matches_single_steps_and_oracle(geig, math, cfg_idx, rows, k, d
     assert rel_err(states[0][1], Ao) < tol
 
 
-def test_staged_tensor_core_products_still_match(geig, monkeypatch):
+def test_staged_tensor_core_products_still_match(geig):
     """geig_products_cca uses phases F, S, B of the fused kernel; the staged
     three-launch products (tc_gemm forward, zshuffle, tc_gemm backward — the
-    path for k > 64 or d % 4 != 0) stay covered here."""
-    monkeypatch.setenv("GEIG_STAGED_PRODUCTS", "1")
+    path for k > 64 or d % 4 != 0, selected here with GEIG_OPT_STAGED_PRODUCTS)
+    stay covered here."""
     for math, tol in (("bf16", 1e-2), ("bf16x2", 1e-3)):
-        errs, _ = check_cca_step(geig, 3, 1024, k=64, dx=2048, dy=1024, math=math)
+        errs, _ = check_cca_step(geig, 3, 1024, k=64, dx=2048, dy=1024, math=math,
+                                 options={geig.GEIG_OPT_STAGED_PRODUCTS: 1})
         _assert(errs, tol)
 
 
