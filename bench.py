@@ -250,7 +250,12 @@ def run_gpu(args, cfg, rank, world, local_rank):
     math = args.math
     data_bf16 = cfg.dtype == "bf16"
     dtype = torch.bfloat16 if data_bf16 else torch.float32
-    b = cfg.batch
+    # config 3 reads "batch 4096; rows sharded over 8 GPUs": --scaling weak
+    # (default) gives every rank its own 4096-row batch (global N x 4096),
+    # --scaling strong shards ONE 4096-row batch over the N ranks
+    b = cfg.batch if args.scaling == "weak" else cfg.batch // world
+    if b < 2:
+        raise SystemExit("bench: --scaling strong leaves fewer than 2 rows per rank")
     esz = 2 if data_bf16 else 4
     batch_bytes = b * cfg.d * esz
     # ring of P distinct batches in HBM, larger than the 126 MB L2
@@ -471,10 +476,17 @@ def run_gpu(args, cfg, rank, world, local_rank):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
                 "dtype": "bf16" if math in ("bf16", "bf16x2") else ("f32" if math == "f32" else math),
                 "data": "synthetic",
-                "config": dict(_workload(cfg, math), parallelism=f"dp{world}", global_batch=world * b, update=variant,
+                "config": dict(_workload(cfg, math), batch_per_gpu=b, parallelism=f"dp{world}", global_batch=world * b,
+                               batch_reading=("weak: every rank streams its own batch of %d rows (global N x %d); "
+                                              "--scaling strong shards one %d-row batch over the N ranks"
+                                              % (cfg.batch, cfg.batch, cfg.batch)) if args.scaling == "weak" else
+                                             ("strong: one %d-row batch sharded over the N ranks (%d rows each); "
+                                              "--scaling weak gives every rank its own %d-row batch"
+                                              % (cfg.batch, b, cfg.batch)),
+                               update=variant,
                                step=("fused single launch (geig_run_cca)" if multi else
                                      "fused single launch per step" if fused else
                                      "products+tables launch, all-reduce, update_tables" if tables else
@@ -485,6 +497,15 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     s.close()
+
+
+def _free_port():
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    return port
 
 
 def main():
@@ -499,6 +520,8 @@ def main():
     ap.add_argument("--per-step-launch", action="store_true",
                     help="fused path: one geig_step_cca launch per step instead of geig_run_cca")
     ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="weak: cfg.batch rows per rank; strong: cfg.batch rows sharded over the ranks")
     ap.add_argument("--math", default=None)
     ap.add_argument("--impl", default="b200")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -517,9 +540,18 @@ def main():
         # bf16 data: tensor cores with hi+lo bf16 operands (bf16x2) — same speed as
         # plain bf16 on this HBM-bound step, products ~fp32-accurate
         args.math = "bf16x2" if cfg.dtype == "bf16" else "f32"
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # `python bench.py --gpus N` without a launcher: re-exec under
+        # torch.distributed.run, one rank per GPU (rank 0 prints the line)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.stderr.write("bench: launching " + " ".join(cmd) + "\n")
+        raise SystemExit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world} (launch one rank per GPU)")
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return

@@ -123,3 +123,54 @@ def test_gloo_world2_allreduce_matches_global_batch():
     for r in range(world):
         got, ref, _ = res[100 + r]
         assert np.allclose(got, ref, atol=1e-12)
+
+
+def _tables_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2206_04993_b200.parallel import allreduce_products
+        k, d, nt = 3, 7, 12
+        g = torch.Generator().manual_seed(100 + rank)
+        # adjacent [AV | BV | T] in one buffer: ONE in-place all-reduce
+        AV, BV, T = product_buffers(k, d, nt, dtype=torch.float64)
+        AV.copy_(torch.randn(k, d, generator=g, dtype=torch.float64))
+        BV.copy_(torch.randn(k, d, generator=g, dtype=torch.float64))
+        T.copy_(torch.randn(nt, generator=g, dtype=torch.float64))
+        mine = (AV.clone(), BV.clone(), T.clone())
+        allreduce_products(AV, BV, T=T)
+        # separate tensors: the stacked fallback
+        AV2, BV2, T2 = mine[0].clone(), mine[1].clone(), mine[2].clone()
+        allreduce_products(AV2, BV2, T=T2)
+        out_q.put((rank, [t.numpy().copy() for t in mine], [t.numpy().copy() for t in (AV, BV, T)],
+                   [t.numpy().copy() for t in (AV2, BV2, T2)]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_tables_buffer_allreduce():
+    """The multi-GPU step's [AV | BV | T] buffer (product_buffers with
+    n_tables > 0, T = the Gram-table partials of geig_products_cca_tables) is
+    summed over ranks by allreduce_products — in place when adjacent, through
+    a stacked copy otherwise — and every rank ends with the same sums
+    (Appendix F)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tables_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, mine, inplace, stacked = q.get(timeout=120)
+        res[r] = (mine, inplace, stacked)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [res[0][0][i] + res[1][0][i] for i in range(3)]
+    for r in range(world):
+        for i in range(3):
+            np.testing.assert_allclose(res[r][1][i], want[i], rtol=0, atol=1e-14)
+            np.testing.assert_allclose(res[r][2][i], want[i], rtol=0, atol=1e-14)
