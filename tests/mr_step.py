@@ -46,7 +46,7 @@ def main():
         geig.geig_sync(s.h)
         allreduce_products(AV, BV, T=Tt)
         geig.geig_update_tables(s.h, AV, BV, Tt, eta, cfg.gamma)
-    Vg, Ag = s.state()
+    Vg, Ag = (t_.cpu() for t_ in s.state())
     s.close()
     Vs = [torch.empty_like(Vg) for _ in range(world)]
     dist.all_gather(Vs, Vg)
