@@ -77,6 +77,9 @@ struct geig_solver {
   int64_t launches = 0;
   tc::TcPlan tc;                                      // tcgen05 plans (tensor maps, scratch)
   int opt_staged = 0;                                 // geig_set_option(GEIG_OPT_STAGED_PRODUCTS)
+  int nsm = 148;
+  float* splitk = nullptr;                            // SIMT split-K partials (lazily sized)
+  size_t splitk_floats = 0;
 };
 
 extern "C" const char* geig_last_error(void) { return g_err.c_str(); }
@@ -151,6 +154,7 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
   {
     int nsm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    s->nsm = std::max(1, nsm);
     int64_t G = std::min<int64_t>(nsm, (s->d + UPD_XC - 1) / UPD_XC);
     G = std::max<int64_t>(G, 1);
     int64_t segw = (s->d + G - 1) / G;
@@ -197,7 +201,7 @@ extern "C" geig_status geig_destroy(geig_solver* s) {
   for (void* p : {(void*)s->arena,
                   (void*)s->gram, (void*)s->raw, (void*)s->partial,
                   (void*)s->Wx, (void*)s->Wy, (void*)s->ts, (void*)s->Wxb, (void*)s->Wyb, s->hX, s->hY,
-                  (void*)s->zbuf, (void*)s->am, (void*)s->as})
+                  (void*)s->zbuf, (void*)s->am, (void*)s->as, (void*)s->splitk})
     if (p) cudaFree(p);
   tc::plan_destroy(s->tc);
   delete s;
@@ -299,11 +303,40 @@ extern "C" geig_status geig_get_gram(geig_solver* s, float* GA, float* GB, float
 // products
 // ---------------------------------------------------------------------------
 
+// SIMT (FFMA) product launch.  When the M x N tile grid leaves most SMs idle
+// and K is long (the backward X^T Z of small d with a large batch), K is
+// split over gridDim.z slices into s->splitk partials and reduced in fixed
+// order by simt_splitk_reduce (two launches, deterministic).
 template <typename TA, bool A_K, bool B_K, class Epi>
 static geig_status launch_simt(geig_solver* s, const TA* A, int64_t lda, const float* B, int64_t ldb,
                                int M, int N, int64_t kbeg, int64_t kend, Epi epi) {
   if (M <= 0 || N <= 0) return GEIG_OK;
   dim3 grid((M + SG_BM - 1) / SG_BM, (N + SG_BN - 1) / SG_BN);
+  const int tiles = (int)(grid.x * grid.y);
+  const int64_t K = kend - kbeg;
+  int splits = 1;
+  while (tiles * splits * 2 <= 2 * s->nsm && K / (splits * 2) >= 512) splits *= 2;
+  if (splits > 1) {
+    const size_t need = (size_t)splits * M * N;
+    if (need > s->splitk_floats) {
+      if (s->splitk) cudaFree(s->splitk);
+      s->splitk = nullptr;
+      s->splitk_floats = 0;
+      CU(cudaMalloc((void**)&s->splitk, need * sizeof(float)));
+      s->splitk_floats = need;
+    }
+    int64_t kchunk = (K + splits - 1) / splits;
+    kchunk = (kchunk + SG_BK - 1) / SG_BK * SG_BK;
+    grid.z = (unsigned)splits;
+    simt_gemm_kernel<TA, float, A_K, B_K, Epi><<<grid, 256, 0, s->stream>>>(A, lda, B, ldb, M, N, kbeg, kend, epi,
+                                                                           s->splitk, kchunk);
+    CHECK_LAUNCH();
+    const int rb = (int)std::min<int64_t>(2 * s->nsm, ((int64_t)M * N + 255) / 256);
+    simt_splitk_reduce<Epi><<<rb, 256, 0, s->stream>>>(s->splitk, M, N, splits, epi);
+    CHECK_LAUNCH();
+    s->launches += 2;
+    return GEIG_OK;
+  }
   simt_gemm_kernel<TA, float, A_K, B_K, Epi><<<grid, 256, 0, s->stream>>>(A, lda, B, ldb, M, N, kbeg, kend, epi);
   CHECK_LAUNCH();
   s->launches++;

@@ -5,6 +5,11 @@
 //   B_K: B(n,kk) = B[n*ldb + kk]   (K-major)   else B[kk*ldb + n] (N-major)
 // 64x64 output tile per 256-thread CTA, BK = 16, 4x4 outputs per thread.
 // The epilogue functor receives (m, n, value) for in-range outputs.
+// Split-K (gridDim.z > 1, for the tall-skinny products whose M x N grid is
+// a handful of tiles, e.g. the backward X^T Z with M = d_view, N = k, K = h):
+// slice z sums kk in its K chunk and writes the raw partial to
+// part[(z * N + n) * M + m]; simt_splitk_reduce then adds the slices in
+// fixed order (deterministic) and applies the epilogue.
 #pragma once
 #include "common.cuh"
 
@@ -15,7 +20,12 @@ constexpr int SG_BM = 64, SG_BN = 64, SG_BK = 16;
 template <typename TA, typename TB, bool A_K, bool B_K, class Epi>
 __global__ void __launch_bounds__(256)
 simt_gemm_kernel(const TA* __restrict__ A, int64_t lda, const TB* __restrict__ B, int64_t ldb,
-                 int M, int N, int64_t kbeg, int64_t kend, Epi epi) {
+                 int M, int N, int64_t kbeg, int64_t kend, Epi epi, float* __restrict__ part = nullptr,
+                 int64_t kchunk = 0) {
+  if (gridDim.z > 1) {   // split-K slice
+    kbeg += (int64_t)blockIdx.z * kchunk;
+    kend = min(kend, kbeg + kchunk);
+  }
   __shared__ float As[SG_BK][SG_BM + 4];
   __shared__ float Bs[SG_BK][SG_BN + 4];
   const int tid = threadIdx.x;
@@ -68,8 +78,23 @@ simt_gemm_kernel(const TA* __restrict__ A, int64_t lda, const TB* __restrict__ B
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
-      if (m < M && n < N) epi(m, n, acc[i][j]);
+      if (m < M && n < N) {
+        if (gridDim.z > 1) part[((int64_t)blockIdx.z * N + n) * M + m] = acc[i][j];
+        else epi(m, n, acc[i][j]);
+      }
     }
+}
+
+template <class Epi>
+__global__ void __launch_bounds__(256)
+simt_splitk_reduce(const float* __restrict__ part, int M, int N, int splits, Epi epi) {
+  const int64_t MN = (int64_t)M * N;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < MN; e += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += part[z * MN + e];
+    const int n = (int)(e / M), m = (int)(e - (int64_t)n * M);
+    epi(m, n, s);
+  }
 }
 
 // Epilogue of the CCA forward product Z_v = X_v V_v^T (rows r, player n):

@@ -55,16 +55,19 @@ def test_converges_fp32_variant(geig):
     assert ang.mean() < 1e-3 and se < 1e-6
 
 
-def test_converges_bf16_variant(geig):
-    """bf16 tensor-core variant (fused single-launch step): V is rounded to
-    bf16 for the products, so the fixed point moves by O(bf16 eps / gap)."""
+def test_converges_plain_bf16_operands(geig):
+    """Plain bf16 operands (GEIG_MATH_BF16, not one of the north star's two
+    variants — the bf16 variant is bf16x2, below): V is rounded to bf16 for
+    the products, so the fixed point moves by O(bf16 eps / gap); held to
+    1e-2 rad."""
     ang, se = _run_cca(geig, "bf16", torch.bfloat16)
     print("bf16 tcgen05 variant: angles", ang, "mean", ang.mean(), "subspace error", se)
     assert ang.mean() < 1e-2 and se < 1e-3
 
 
 def test_converges_bf16x2_variant(geig):
-    """bf16 data, tensor cores, hi+lo bf16 operands: meets the 1e-3 rad bar."""
+    """The bf16 variant (bf16 data, bf16 tensor-core operands carried as
+    hi + lo halves, fp32 accumulate): meets the 1e-3 rad bar."""
     ang, se = _run_cca(geig, "bf16x2", torch.bfloat16)
     print("bf16x2 tcgen05 variant: angles", ang, "mean", ang.mean(), "subspace error", se)
     assert ang.mean() < 1e-3 and se < 1e-6
@@ -93,7 +96,13 @@ def test_converges_3xtf32_cca_variant(geig):
     assert ang.mean() < 1e-3 and se < 1e-6
 
 
-def test_converges_tf32_dense_config0(geig):
+@pytest.mark.parametrize("math,bar", [("tf32", 1e-2), ("3xtf32", 1e-3)])
+def test_converges_dense_config0_tensor_cores(geig, math, bar):
+    """Config 0 on the tensor cores.  3xTF32 (fp32-accurate products, the
+    tensor-core fp32 variant) meets the 1e-3 rad bar; plain tf32 rounds V to
+    10 mantissa bits for the products, which moves the fixed point by
+    O(tf32 eps / eigengap) — it is not one of the north star's two
+    variants and is held to 1e-2."""
     from oracle import linalg, metrics
     from synth import CONFIGS, dense_gep_small, gaussian_init
     cfg = CONFIGS[0]
@@ -102,7 +111,7 @@ def test_converges_tf32_dense_config0(geig):
     A = torch.tensor(a, dtype=torch.float32, device=dev)
     B = torch.tensor(b, dtype=torch.float32, device=dev)
     w, Vt = linalg.generalized_eigh(A.double().cpu().numpy(), B.double().cpu().numpy(), cfg.k)
-    s = geig.Solver(geig.GEIG_DENSE, cfg.d, 0, cfg.k, math="tf32", rho=cfg.rho)
+    s = geig.Solver(geig.GEIG_DENSE, cfg.d, 0, cfg.k, math=math, rho=cfg.rho)
     try:
         s.init_state(torch.tensor(gaussian_init(cfg.k, cfg.d, 0), dtype=torch.float32, device=dev))
         for _ in range(cfg.steps):
@@ -111,5 +120,5 @@ def test_converges_tf32_dense_config0(geig):
     finally:
         s.close()
     ang = metrics.per_vector_angles(V.double().cpu().numpy(), Vt)
-    print("tf32 dense config 0: angles", ang)
-    assert ang.mean() < 1e-2
+    print(f"{math} dense config 0: angles", ang, "mean", ang.mean())
+    assert ang.mean() < bar
