@@ -165,10 +165,15 @@ def oracle_sample(cfg, seconds: float, max_steps: int | None = None, seed: int =
                 return rows / el, n, rows, el
     a, b = dense_gep_small(seed, cfg.d) if cfg.d <= 64 else (None, None)
     if a is None:
+        # config 4's matrices at full size, drawn on the GPU when there is one
+        # (the draw is input preparation, not timed); on a CPU-only host a
+        # reduced d
         import torch
         from synth import dense_gep_large
-        at, bt = dense_gep_large(min(cfg.d, 2048), seed)
-        a, b = at.double().numpy(), bt.double().numpy()
+        on_gpu = torch.cuda.is_available()
+        at, bt = dense_gep_large(cfg.d if on_gpu else min(cfg.d, 2048), seed, device="cuda:0" if on_gpu else "cpu")
+        a, b = at.double().cpu().numpy(), bt.double().cpu().numpy()
+        del at, bt
     V, aux = game.init_state(gaussian_init(cfg.k, a.shape[0], seed))
     n, t0 = 0, time.perf_counter()
     while True:
@@ -223,6 +228,140 @@ def _box_copy_gbs(dev, n=1 << 28, reps=5):
     except Exception:
         return None
 
+def run_gpu_dense(args, cfg, rank, world, dev, stream, peaks, peaks_src):
+    """Dense full-batch GEP step (configs 0, 4; Alg. 2 with exact A, B =
+    Alg. 1's direction): A and B row-sharded over the
+    ranks (shard_rows), each rank's geig_products_dense forms its columns of
+    AV, BV, one all-gather of the column blocks (dense_allgather_rows)
+    assembles them, every rank applies geig_update to its replica of V and
+    [Bv].  The unit is steps/s; the problem size is fixed as N grows
+    (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2206_04993_b200 import geig
+    from paper_2206_04993_b200.parallel import dense_allgather_rows, dense_wire_bytes, shard_rows
+    from synth import dense_gep_large, dense_gep_small, gaussian_init
+    math = args.math
+    d, k = cfg.d, cfg.k
+    if d <= 64:
+        a64, b64 = dense_gep_small(0, d)
+        A = torch.tensor(a64, dtype=torch.float32, device=dev)
+        B = torch.tensor(b64, dtype=torch.float32, device=dev)
+    else:
+        A, B = dense_gep_large(d, seed=0, device=dev)
+    r0, r1 = shard_rows(d, world, rank)
+    Ar, Br = A[r0:r1].contiguous(), B[r0:r1].contiguous()
+    if world > 1:
+        del A, B
+        torch.cuda.empty_cache()
+    s = geig.Solver(geig.GEIG_DENSE, d, 0, k, math=math, rho=cfg.rho, device=dev.index, stream=stream.cuda_stream)
+    s.init_state(torch.tensor(gaussian_init(k, d, 0), dtype=torch.float32, device=dev))
+    AV = torch.empty(k, d, device=dev)
+    BV = torch.empty_like(AV)
+    ev = []
+
+    def step(timed):
+        if timed:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        geig.geig_products_dense(s.h, Ar, Br, r0, r1, AV, BV)
+        if timed:
+            e1.record(stream)
+            ev.append((e0, e1))
+        if world > 1:
+            dense_allgather_rows(AV, BV, d, world)
+        geig.geig_update(s.h, AV, BV, cfg.eta, cfg.gamma)
+
+    t_spin = time.perf_counter()
+    while time.perf_counter() - t_spin < args.spinup:
+        step(False)
+        torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = s.launches()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t_start.record(stream)
+        for _ in range(args.steps):
+            step(True)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = s.launches() - l0
+    elapsed_ms = t_start.elapsed_time(t_end)
+    prod_ms = statistics.mean(a.elapsed_time(b_) for a, b_ in ev)
+    if world > 1:
+        t = torch.tensor([elapsed_ms, prod_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms, prod_ms = t.tolist()
+    value = args.steps / (elapsed_ms / 1e3)
+    # roofline of the products launch (the dominant kernel): this rank's rows
+    # of A and B read once, V read, its columns of AV, BV written
+    esz = 4
+    rows = r1 - r0
+    alg_bytes = 2 * rows * d * esz + k * d * esz + 2 * k * rows * 4
+    achieved = alg_bytes / (prod_ms / 1e3) / 1e9
+    box_copy = _box_copy_gbs(dev)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
+            "frac": achieved / peaks.get("hbm_gbs", 6650.0), "box_copy_gbs": box_copy,
+            "frac_of_box_copy": (achieved / box_copy) if box_copy else None, "traffic": None,
+            "algorithmic_bytes": alg_bytes, "peak_source": peaks_src,
+            "kernel": f"tc_gemm products of the rank's rows of A and B ({math})", "ms_per_launch": prod_ms,
+            "step_ms": elapsed_ms / args.steps, "products_share": prod_ms / (elapsed_ms / args.steps),
+            "tensor_tflops": 4.0 * k * rows * d / (prod_ms / 1e3) / 1e12}
+    e2e = None
+    if not args.no_e2e:
+        # end to end through the C ABI from pinned host memory: every step
+        # copies this rank's rows of A and B host -> device, runs the step and
+        # reads the k x k Gram table back
+        hA, hB = Ar.cpu().pin_memory(), Br.cpu().pin_memory()
+        ga = torch.empty(k, k).pin_memory()
+        gd = torch.empty(3, k, k, device=dev)
+        n_e2e = 3
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            Ar.copy_(hA, non_blocking=True)
+            Br.copy_(hB, non_blocking=True)
+            step(False)
+            geig.geig_get_gram(s.h, gd[0], gd[1], gd[2])
+            ga.copy_(gd[0])
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": n_e2e / el, "unit": "steps/s", "h2d_bytes_per_step": 2 * rows * d * esz,
+               "d2h_bytes_per_step": k * k * 4, "steps": n_e2e, "timer": "host wall clock (synchronised)"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, n, _, el = oracle_sample(cfg, args.cpu_seconds, seed=0)
+        cpu = {"value": v, "unit": "steps/s", "cores": _blas_threads(), "kind": "oracle",
+               "sample": f"{n} full fp64 oracle steps at d={d}, k={k} ({el:.1f} s)"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32" if math == "f32" else math,
+                "data": "synthetic",
+                "config": {"workload": cfg.name, "problem": "dense", "d": d, "k": k, "math": math,
+                           "data_dtype": "f32", "recipe": cfg.recipe, "parallelism": f"rows{world}",
+                           "rows_per_gpu": rows,
+                           "collective": "all-gather of the column blocks of AV, BV" if world > 1 else None,
+                           "wire_bytes_per_rank": dense_wire_bytes(k, d, world) if world > 1 else None,
+                           "l2_policy": "A and B (2 x %.1f GiB) exceed the 126 MB L2; read once per step"
+                                        % (rows * d * 4 / 2**30)},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    s.close()
+
 
 def run_gpu(args, cfg, rank, world, local_rank):
     import torch
@@ -245,8 +384,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     peaks, peaks_src = _peaks()
 
     if cfg.problem != "cca":
-        raise SystemExit("bench: only the CCA workloads are benchmarked as the headline; "
-                         "use --config 1|2|3")
+        return run_gpu_dense(args, cfg, rank, world, dev, stream, peaks, peaks_src)
     math = args.math
     data_bf16 = cfg.dtype == "bf16"
     dtype = torch.bfloat16 if data_bf16 else torch.float32
@@ -539,7 +677,7 @@ def main():
     if args.math is None:
         # bf16 data: tensor cores with hi+lo bf16 operands (bf16x2) — same speed as
         # plain bf16 on this HBM-bound step, products ~fp32-accurate
-        args.math = "bf16x2" if cfg.dtype == "bf16" else "f32"
+        args.math = "bf16x2" if cfg.dtype == "bf16" else ("tf32" if cfg.problem == "dense" and cfg.d > 64 else "f32")
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         # `python bench.py --gpus N` without a launcher: re-exec under
         # torch.distributed.run, one rank per GPU (rank 0 prints the line)

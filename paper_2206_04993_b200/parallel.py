@@ -87,7 +87,34 @@ def cca_scale(b_local: int, world: int) -> float:
 
 
 def dense_allgather_rows(AV: torch.Tensor, BV: torch.Tensor, d: int, world: int, group=None):
-    """Dense row sharding: rank r wrote columns [r0, r1) of AV, BV (zeros
-    elsewhere); a SUM all-reduce assembles the full products."""
-    if world > 1:
-        allreduce_products(AV, BV, group)
+    """Dense row sharding (configs 0, 4: A, B row-sharded across ranks):
+    rank r wrote columns [r0, r1) = shard_rows(d, world, r) of AV, BV (the
+    products of its rows of A, B with every v_j, geig_products_dense).  One
+    all-gather of the ranks' column blocks (packed contiguous, padded to
+    ceil(d / world) columns) assembles the full k x d products on every rank:
+    each rank sends 2 k (d / world) floats and receives the rest — half the
+    wire bytes of a SUM all-reduce of zero-padded k x d buffers."""
+    if world <= 1:
+        return
+    rank = dist.get_rank(group)
+    k = AV.shape[0]
+    w = (d + world - 1) // world
+    r0, r1 = shard_rows(d, world, rank)
+    send = torch.zeros(2, k, w, dtype=AV.dtype, device=AV.device)
+    send[0, :, :r1 - r0] = AV[:, r0:r1]
+    send[1, :, :r1 - r0] = BV[:, r0:r1]
+    recv = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(recv, send, group=group)
+    for q in range(world):
+        q0, q1 = shard_rows(d, world, q)
+        if q != rank:
+            AV[:, q0:q1] = recv[q][0, :, :q1 - q0]
+            BV[:, q0:q1] = recv[q][1, :, :q1 - q0]
+
+
+def dense_wire_bytes(k: int, d: int, world: int, elem: int = 4) -> dict:
+    """Bytes each rank sends per dense step: all-gather of its column block
+    of AV, BV vs the (ring) all-reduce of the full buffers it replaces."""
+    w = (d + world - 1) // world
+    return {"allgather_send": 2 * k * w * elem * (world - 1),
+            "allreduce_ring_send": 2 * 2 * k * d * elem * (world - 1) // world}

@@ -58,17 +58,17 @@ def _worker(rank, world, port, x, y, V, aux, out_q):
         step(AV, BV)
         out_q.put((rank, AV.numpy().copy(), state["V"], state["aux"]))
         # dense row sharding: each rank writes its columns, all-reduce assembles
-        d = 10
+        d = 11                               # ragged: shards of 6 and 5 rows
         rng = np.random.default_rng(0)
         A = rng.standard_normal((d, d)); A = A + A.T
         W = rng.standard_normal((3, d))
         r0, r1 = shard_rows(d, world, rank)
-        AVd = torch.zeros(3, d, dtype=torch.float64)
-        BVd = torch.zeros_like(AVd)
+        AVd = torch.full((3, d), float("nan"), dtype=torch.float64)   # other ranks' columns are filled by the gather
+        BVd = torch.full_like(AVd, float("nan"))
         AVd[:, r0:r1] = torch.from_numpy((A[r0:r1] @ W.T).T)
         BVd[:, r0:r1] = torch.from_numpy((2 * A[r0:r1] @ W.T).T)
         dense_allgather_rows(AVd, BVd, d, world)
-        out_q.put((rank + 100, AVd.numpy(), (A @ W.T).T, None))
+        out_q.put((rank + 100, AVd.numpy(), (A @ W.T).T, BVd.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -121,8 +121,9 @@ def test_gloo_world2_allreduce_matches_global_batch():
         assert np.allclose(Vr, V2, atol=1e-12) and np.allclose(auxr, aux2, atol=1e-12)
     assert np.array_equal(res[0][1], res[1][1])        # replicas identical
     for r in range(world):
-        got, ref, _ = res[100 + r]
+        got, ref, gotb = res[100 + r]
         assert np.allclose(got, ref, atol=1e-12)
+        assert np.allclose(gotb, 2 * ref, atol=1e-12)
 
 
 def _tables_worker(rank, world, port, out_q):
