@@ -420,6 +420,19 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # from the aggregated tables (geig_products_cca_tables / geig_update_tables)
     tables = (world > 1 or args.split_step) and math in ("bf16", "bf16x2") and cfg.k <= 64 and not args.staged \
         and not args.no_tables
+    # column-owned step (default at N > 1 where the partition fits): the
+    # products launch writes per-owner chunks, ONE reduce-scatter, the update
+    # of the rank's d / N columns, ONE all-gather of the bf16 shadow blocks
+    owned = None
+    if world > 1 and tables and args.multi == "owned":
+        from paper_2206_04993_b200.parallel import (ColumnOwnedStep, allgather_blocks, owned_wire_bytes,
+                                                    reduce_scatter_chunks)
+        try:
+            geig.geig_set_partition(s.h, world, rank)
+            owned = ColumnOwnedStep(geig, s, world, rank)
+        except geig.GeigError as e:
+            if rank == 0:
+                sys.stderr.write(f"bench: column-owned step unavailable ({e}); replicated all-reduce step\n")
     if tables:
         AV, BV, T = product_buffers(cfg.k, cfg.d, geig.geig_table_floats(s.h), device=dev)
     else:
@@ -439,6 +452,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
             geig.geig_step_cca(s.h, Xs[i % P], Ys[i % P], b, cfg.eta, cfg.gamma)
             if timed:
                 e1.record(stream)
+        elif owned is not None:
+            geig.geig_products_cca_owned(s.h, Xs[i % P], Ys[i % P], b, scale, owned.buf)
+            if timed:
+                e1.record(stream)
+            reduce_scatter_chunks(owned.buf, owned.mine)
+            geig.geig_update_owned(s.h, owned.mine, cfg.eta, cfg.gamma)
+            allgather_blocks(owned.shadow)
         elif tables:
             geig.geig_products_cca_tables(s.h, Xs[i % P], Ys[i % P], b, scale, AV, BV, T)
             if timed:
@@ -579,7 +599,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
             def e2e_step():
                 xd.copy_(hx, non_blocking=True)
                 yd.copy_(hy, non_blocking=True)
-                if tables:
+                if owned is not None:
+                    owned(xd, yd, b, cfg.eta, cfg.gamma)
+                elif tables:
                     geig.geig_products_cca_tables(s.h, xd, yd, b, scale, AV, BV, T)
                     allreduce_products(AV, BV, T=T)
                     geig.geig_update_tables(s.h, AV, BV, T, cfg.eta, cfg.gamma)
@@ -625,8 +647,12 @@ def run_gpu(args, cfg, rank, world, local_rank):
                                               "--scaling weak gives every rank its own %d-row batch"
                                               % (cfg.batch, b, cfg.batch)),
                                update=variant,
+                               wire_bytes_per_rank=(owned_wire_bytes(cfg.k, cfg.d, world, geig.geig_table_floats(s.h))
+                                                    if owned is not None else None),
                                step=("fused single launch (geig_run_cca)" if multi else
                                      "fused single launch per step" if fused else
+                                     "column-owned: products launch (per-owner chunks), reduce-scatter, update of "
+                                     "the rank's d/N columns, all-gather of the bf16 shadow" if owned is not None else
                                      "products+tables launch, all-reduce, update_tables" if tables else
                                      "products launch, all-reduce, update"),
                                l2_policy=f"ring of {P} distinct batches ({P * batch_bytes / 2**20:.0f} MiB) "
@@ -658,6 +684,8 @@ def main():
     ap.add_argument("--per-step-launch", action="store_true",
                     help="fused path: one geig_step_cca launch per step instead of geig_run_cca")
     ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--multi", choices=("owned", "replicated"), default="owned",
+                    help="N > 1: column-owned reduce-scatter / all-gather step, or the replicated all-reduce step")
     ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
                     help="weak: cfg.batch rows per rank; strong: cfg.batch rows sharded over the ranks")
     ap.add_argument("--math", default=None)

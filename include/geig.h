@@ -175,6 +175,41 @@ geig_status geig_products_cca_tables(geig_solver* s, const void* X, const void* 
 geig_status geig_update_tables(geig_solver* s, const float* AV, const float* BV,
                                const float* T, double eta, double gamma);
 
+/* Column-owned multi-GPU step (the products reduce-scattered instead of
+ * all-reduced; Appendix F, "parallelized the estimation of the
+ * matrix-vector products ... then aggregated this information across
+ * machines"; Alg. 2 lines 8-19 are separable over feature columns once the
+ * k x k tables are summed).  Rank `rank` of `world` owns the columns
+ * [rank W, (rank + 1) W), W = d / world, and keeps V, [Bv] current on them
+ * only.  Per step:
+ *   geig_products_cca_owned  one launch (forward, split-K sums, backward):
+ *                            buf = world chunks of geig_owned_chunk_floats
+ *                            floats, chunk r = [AV | BV (k x W each, columns
+ *                            of rank r, row stride W) | tables (the rank's
+ *                            partial G^A, G^B from its rows and G^C,
+ *                            ||v''||^2 from its own columns)];
+ *   reduce-scatter (sum) of buf -> the rank's chunk (caller, e.g. NCCL);
+ *   geig_update_owned        the update of the own columns from the summed
+ *                            chunk; writes the rank's block of the gathered
+ *                            bf16 shadow;
+ *   all-gather of the shadow blocks (caller): geig_shadow_buffer gives the
+ *                            device buffer [world][hi|lo][k][W] bf16 and the
+ *                            bytes per rank (rank r's block at r * bytes).
+ * geig_set_partition(s, 1, 0) switches back.  Needs CCA, bf16 / bf16x2 math,
+ * k <= 64, d % (64 world) == 0 and dx % 64 == 0 (GEIG_ERR_UNSUPPORTED).  While
+ * partitioned, geig_get returns the raw (unretracted) v'' — only the own
+ * columns are current and the retraction needs every rank's columns; the
+ * caller gathers the blocks and divides by the row norms.  Errors:
+ * GEIG_ERR_STATE without a partition; GEIG_ERR_ARG for bad sizes, NULL or
+ * unaligned (16-byte) buffers. */
+geig_status geig_set_partition(geig_solver* s, int world, int rank);
+int64_t geig_owned_chunk_floats(const geig_solver* s);
+geig_status geig_shadow_buffer(geig_solver* s, void** ptr, int64_t* bytes_per_rank);
+geig_status geig_products_cca_owned(geig_solver* s, const void* X, const void* Y,
+                                    int64_t b, float scale, float* buf);
+geig_status geig_update_owned(geig_solver* s, const float* chunk, double eta,
+                              double gamma);
+
 /* One full step = products + update on the solver's scratch.  On the bf16
  * tensor-core path with k <= 64 the whole step is ONE persistent cooperative
  * kernel (forward GEMM, split-K reduction, backward GEMM, Gram tables and

@@ -78,6 +78,12 @@ struct FusedParams {
                                    // columns): tm tiles share one B-operand tile per K step, so the ring
                                    // holds tm x more batch bytes in flight per byte of V / Z re-read
   int nsteps;                      // steps of Alg. 2 run by this launch (one batch each)
+  // column-owned products (geig_products_cca_owned): 0 = off, else the block
+  // width W — the forward's V operand is the gathered shadow [rank][hi|lo][k][W]
+  // (3D maps), the backward epilogue writes AV | BV of column c into rank
+  // c / W's chunk of `chunk` floats ([AV k x W | BV k x W | tables])
+  int ownW;
+  int64_t chunk;
   int products_only;               // 1: phases F, S, B only (AV, BV to global; multi-GPU: all-reduce, then geig_update)
   int update_only;                 // phase U only (multi-GPU: from the all-reduced products and tables)
   int tables;                      // products-only launch that also forms the Gram tables (G^A, G^B of the
@@ -96,6 +102,7 @@ struct FusedParams {
 };
 
 struct Item {
+  int64_t coff;       // global column offset of the item's view
   int nseg, m0, mbound;
   int view;           // backward item: view of the feature columns
   int mt;             // M tiles of this item (<= tm of the phase; fewer at the ragged end)
@@ -128,6 +135,8 @@ __device__ __forceinline__ void decode_forward(const FusedMaps& M, const CUtenso
   it.mb[1] = it.mb[0];
   it.mblo[0] = it.mblo[1] = v == 0 ? &M.bFlo[0] : &M.bFlo[1];
   it.keep_a = p.l2_keep && v == 1;    // view Y is streamed last in F and first in B
+  it.view = v;
+  it.coff = v == 0 ? 0 : p.dv[0];
   it.out[0] = p.Zt + ((int64_t)(2 * sp + v) * p.k) * p.ldz;
   it.out[1] = nullptr;
   it.ldo = p.ldz;
@@ -157,9 +166,10 @@ __device__ __forceinline__ void decode_backward(const FusedMaps& M, const CUtens
   it.mblo[0] = it.mblo[1] = &M.bBlo[2 * v + seg];
   const int64_t off = v == 0 ? 0 : p.dv[0];
   it.keep_a = false;
-  it.out[0] = (seg == 0 ? p.AV : p.BV) + off;
+  it.coff = off;
+  it.out[0] = (seg == 0 ? p.AV : p.BV) + (p.ownW ? 0 : off);
   it.out[1] = nullptr;
-  it.ldo = p.d;
+  it.ldo = p.ownW ? p.ownW : p.d;
   it.scale = p.scale;
 }
 
@@ -214,8 +224,16 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
             }
           }
           if (!nob) {   // V / Z tiles: small, re-read by every CTA
-            tma_load_2d_hint(sb, it.mb[s], &full_bar[st], k0, 0, pol_keep);
-            if (split) tma_load_2d_hint(sb + B_BYTES, it.mblo[s], &full_bar[st], k0, 0, pol_keep);
+            if (!A_MN && p.ownW) {
+              // column-owned: V from the gathered shadow, block g / W of rank g / W
+              const int64_t g = it.coff + k0;
+              const int gw = (int)(g % p.ownW), gr = (int)(g / p.ownW);
+              tma_load_3d_hint(sb, it.mb[s], &full_bar[st], gw, 0, gr, pol_keep);
+              if (split) tma_load_3d_hint(sb + B_BYTES, it.mblo[s], &full_bar[st], gw, 0, gr, pol_keep);
+            } else {
+              tma_load_2d_hint(sb, it.mb[s], &full_bar[st], k0, 0, pol_keep);
+              if (split) tma_load_2d_hint(sb + B_BYTES, it.mblo[s], &full_bar[st], k0, 0, pol_keep);
+            }
           }
         }
       }
@@ -296,6 +314,11 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
               if (n < p.k) {
                 const float4 v = *reinterpret_cast<const float4*>(ws + jn * 32 + 4 * q);
                 float* o = outw + (int64_t)n * it.ldo + 4 * q;
+                if (A_MN && p.ownW) {   // rank-blocked chunk of column gc's owner
+                  const int64_t gc = it.coff + mw + 4 * q;
+                  const int64_t r = gc / p.ownW;
+                  o = it.out[seg] + r * p.chunk + (int64_t)n * p.ownW + (gc - r * p.ownW);
+                }
                 if (full_m || q_ok) {
                   __stcg(reinterpret_cast<float4*>(o), v);
                 } else {
@@ -750,6 +773,19 @@ inline bool make_batch_maps(CUtensorMap* a, const TcPlan& t, const void* X, cons
   return true;
 }
 
+// Column-owned multi-GPU step (geig_set_partition): rank `rank` of `world`
+// owns columns [rank W, (rank + 1) W) of d.  products launch: the forward's
+// V operand is the gathered bf16 shadow `gathered` ([world][hi|lo][k][W]),
+// AV | BV | tables go to `buf` (world chunks of `chunk` floats, one per
+// owner, for the reduce-scatter); update launch: AV, BV and the tables come
+// from the rank's summed chunk `buf` and the update covers the own columns.
+struct OwnedCfg {
+  int W, world, rank;
+  int64_t chunk;
+  float* buf;
+  __nv_bfloat16* gathered;
+};
+
 // Whole CCA step(s) in one cooperative launch (bf16 tensor cores, k <= 64):
 // nsteps consecutive steps of Alg. 2, step i on batch (X[i], Y[i]) (device
 // pointers, b rows each).  `upd` carries the update arguments (state, AV/BV
@@ -758,7 +794,7 @@ inline bool make_batch_maps(CUtensorMap* a, const TcPlan& t, const void* X, cons
 inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* const* Y, int nsteps, int64_t b,
                                   float scale, const __nv_bfloat16* Vbf, float* AV, float* BV, UpdateArgs upd,
                                   int grid_ctas, size_t upd_bytes, cudaStream_t st, bool products_only = false,
-                                  bool tables = false, bool update_only = false) {
+                                  bool tables = false, bool update_only = false, const OwnedCfg* own = nullptr) {
   if (!t.ready || t.math != GEIG_MATH_BF16) return tc_fail(GEIG_ERR_STATE, "fused step needs the bf16 plan");
   if (nsteps < 1) return tc_fail(GEIG_ERR_ARG, "nsteps < 1");
   // (t.math is BF16 for both GEIG_MATH_BF16 and GEIG_MATH_BF16X2; t.splitb selects hi+lo operands)
@@ -831,10 +867,18 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   }
   for (int v = 0; v < 2; ++v) {
     const char* vb = (const char*)Vbf + (v == 0 ? 0 : t.dx * eb);
-    if (!make_map(&maps.bF[v], vb, eb, dv[v], k, t.d, ATOM, t.BN))
-      return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused forward) failed");
-    if (t.splitb && !make_map(&maps.bFlo[v], vb + (int64_t)k * t.d * eb, eb, dv[v], k, t.d, ATOM, t.BN))
-      return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused forward lo) failed");
+    if (own && !update_only) {   // the gathered shadow [world][hi|lo][k][W]
+      const int64_t W = own->W;
+      if (!make_map3(&maps.bF[v], own->gathered, W, k, own->world, W, 2 * (int64_t)k * W, ATOM, t.BN) ||
+          (t.splitb && !make_map3(&maps.bFlo[v], own->gathered + (int64_t)k * W, W, k, own->world, W, 2 * (int64_t)k * W,
+                                  ATOM, t.BN)))
+        return tc_fail(GEIG_ERR_CUDA, "tensor map encode (owned forward) failed");
+    } else {
+      if (!make_map(&maps.bF[v], vb, eb, dv[v], k, t.d, ATOM, t.BN))
+        return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused forward) failed");
+      if (t.splitb && !make_map(&maps.bFlo[v], vb + (int64_t)k * t.d * eb, eb, dv[v], k, t.d, ATOM, t.BN))
+        return tc_fail(GEIG_ERR_CUDA, "tensor map encode (fused forward lo) failed");
+    }
     for (int s = 0; s < 2 && !update_only; ++s) {
       const char* zb = (const char*)t.Zb + (int64_t)(v * 2 + s) * k * t.hpad * eb;
       if (!make_map(&maps.bB[v * 2 + s], zb, eb, h, k, t.hpad, ATOM, t.BN))
@@ -858,9 +902,14 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
     for (int v = 0; v < 2; ++v) p.mtB[v] = (int)((dv[v] + p.tmB * TC_BM - 1) / (p.tmB * TC_BM));
   }
   {
+    // phase U tiles: V'', AV, [Bv], BV over upd.d columns (the own block when
+    // column-owned: V, [Bv] pre-offset with row stride upd.ld, AV / BV from
+    // the rank's chunk with row stride W)
     const float* src[4] = {upd.V, AV, upd.AUX, BV};
+    const int64_t lds = upd.ld ? upd.ld : upd.d, ldp = (own && update_only) ? own->W : upd.d;
+    const int64_t lda[4] = {lds, ldp, lds, ldp};
     for (int a = 0; a < 4; ++a)
-      if (!make_map(&maps.um.t[a], src[a], 4, t.d, k, t.d, (int)upd.segw + 4, 64, false))
+      if (!make_map(&maps.um.t[a], src[a], 4, upd.d, k, lda[a], (int)upd.segw + 4, 64, false))
         return tc_fail(GEIG_ERR_CUDA, "tensor map encode (update tiles) failed");
   }
   p.rows = rows; p.h = h; p.k = k; p.BN = t.BN; p.d = t.d; p.ldz = t.ldz; p.hpad = t.hpad;
@@ -876,6 +925,19 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.AV = AV;
   p.BV = BV;
   p.upd = upd;
+  p.ownW = 0;
+  p.chunk = 0;
+  if (own && !update_only) {
+    p.ownW = own->W;
+    p.chunk = own->chunk;
+    p.AV = own->buf;
+    p.BV = own->buf + (int64_t)k * own->W;
+    p.upd.tout = own->buf + 2 * (int64_t)k * own->W;
+    p.upd.tN = own->world;
+    p.upd.tstride = own->chunk;
+    p.upd.own0 = (int64_t)own->rank * own->W;
+    p.upd.own1 = p.upd.own0 + own->W;
+  }
   p.upd.dbg = dbg_ptr();
   p.upd.dbg_mode = dev_knob("GEIG_DBG_MODE") ? atoi(dev_knob("GEIG_DBG_MODE")) : 0;
   p.upd.ga_done = 1;       // phase S forms G^A, G^B from z

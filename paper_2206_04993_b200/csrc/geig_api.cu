@@ -78,6 +78,12 @@ struct geig_solver {
   tc::TcPlan tc;                                      // tcgen05 plans (tensor maps, scratch)
   int opt_staged = 0;                                 // geig_set_option(GEIG_OPT_STAGED_PRODUCTS)
   int nsm = 148;
+  // column-owned multi-GPU step (geig_set_partition)
+  int part_world = 1, part_rank = 0;
+  int64_t part_W = 0;
+  __nv_bfloat16* gshadow = nullptr;                   // [world][hi|lo][k][W] gathered bf16 shadow of V
+  int own_grid = 1;
+  int64_t own_segw = 0;
   float* splitk = nullptr;                            // SIMT split-K partials (lazily sized)
   size_t splitk_floats = 0;
 };
@@ -201,7 +207,7 @@ extern "C" geig_status geig_destroy(geig_solver* s) {
   for (void* p : {(void*)s->arena,
                   (void*)s->gram, (void*)s->raw, (void*)s->partial,
                   (void*)s->Wx, (void*)s->Wy, (void*)s->ts, (void*)s->Wxb, (void*)s->Wyb, s->hX, s->hY,
-                  (void*)s->zbuf, (void*)s->am, (void*)s->as, (void*)s->splitk})
+                  (void*)s->zbuf, (void*)s->am, (void*)s->as, (void*)s->splitk, (void*)s->gshadow})
     if (p) cudaFree(p);
   tc::plan_destroy(s->tc);
   delete s;
@@ -254,13 +260,37 @@ extern "C" geig_status geig_sync(geig_solver* s) {
   return GEIG_OK;
 }
 
+// Column-owned mode: the gathered bf16 shadow [rank][hi|lo][k][W] of the
+// whole state V (rank r's block = columns [r W, (r + 1) W)).
+__global__ void pack_shadow_kernel(const float* __restrict__ V, __nv_bfloat16* __restrict__ g, int k, int64_t d,
+                                   int64_t W) {
+  const int64_t n = (int64_t)k * d;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / d);
+    const int64_t c = e - (int64_t)i * d, r = c / W, x = c - r * W;
+    const float v = V[e];
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    __nv_bfloat16* blk = g + r * 2 * (int64_t)k * W;
+    blk[(int64_t)i * W + x] = h;
+    blk[(int64_t)k * W + (int64_t)i * W + x] = __float2bfloat16_rn(v - __bfloat162float(h));
+  }
+}
+
+static geig_status refresh_gathered_shadow(geig_solver* s) {
+  if (!s->gshadow) return GEIG_OK;
+  pack_shadow_kernel<<<2 * s->nsm, 256, 0, s->stream>>>(s->V, s->gshadow, s->k, s->d, s->part_W);
+  CHECK_LAUNCH();
+  s->launches++;
+  return GEIG_OK;
+}
+
 extern "C" geig_status geig_init_state(geig_solver* s, const float* G) {
   if (!s || !G) return fail(GEIG_ERR_ARG, "NULL argument");
   CU(cudaSetDevice(s->device));
   init_state_kernel<<<s->k, 256, 0, s->stream>>>(G, s->V, s->AUX, s->Vbf, s->d);
   CHECK_LAUNCH();
   s->launches++;
-  return GEIG_OK;
+  return refresh_gathered_shadow(s);
 }
 
 extern "C" geig_status geig_set_state(geig_solver* s, const float* V, const float* AUX) {
@@ -272,14 +302,18 @@ extern "C" geig_status geig_set_state(geig_solver* s, const float* V, const floa
   f32_to_bf16_kernel<<<256, 256, 0, s->stream>>>(s->V, s->Vbf, (int64_t)kd);   // hi + lo planes
   CHECK_LAUNCH();
   s->launches++;
-  return GEIG_OK;
+  return refresh_gathered_shadow(s);
 }
 
 extern "C" geig_status geig_get(geig_solver* s, float* V, float* AUX) {
   if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
   CU(cudaSetDevice(s->device));
   const size_t kd = (size_t)s->k * s->d;
-  if (V) {
+  if (V && s->part_world > 1) {
+    // column-owned: only the own block is current and the retraction needs
+    // the row norms over every rank's columns — return the raw v''
+    CU(cudaMemcpyAsync(V, s->V, kd * 4, cudaMemcpyDeviceToDevice, s->stream));
+  } else if (V) {
     // the state holds v'' (retraction folded into the next update): return v''/||v''||
     normalize_rows_kernel<<<s->k, 256, 0, s->stream>>>(s->V, V, s->d);
     CHECK_LAUNCH();
@@ -660,6 +694,99 @@ extern "C" geig_status geig_set_adam(geig_solver* s, double b1, double b2, doubl
   s->adam_t = 0;
   s->b1 = (float)b1; s->b2 = (float)b2; s->eps = (float)eps;
   s->adam = 1;
+  return GEIG_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// column-owned multi-GPU step (reduce-scatter of the products, update of the
+// own columns, all-gather of the bf16 shadow)
+// ---------------------------------------------------------------------------
+
+extern "C" geig_status geig_set_partition(geig_solver* s, int world, int rank) {
+  if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  if (world < 1 || rank < 0 || rank >= world) return fail(GEIG_ERR_ARG, "bad partition world=%d rank=%d", world, rank);
+  CU(cudaSetDevice(s->device));
+  if (s->gshadow) { CU(cudaStreamSynchronize(s->stream)); cudaFree(s->gshadow); s->gshadow = nullptr; }
+  s->part_world = 1; s->part_rank = 0; s->part_W = 0;
+  if (world == 1) return GEIG_OK;
+  if (s->problem != GEIG_CCA || !(s->math == GEIG_MATH_BF16 || s->math == GEIG_MATH_BF16X2) || !s->upd_res)
+    return fail(GEIG_ERR_UNSUPPORTED, "column-owned step needs CCA, bf16 / bf16x2 math and k <= 64");
+  if (s->d % ((int64_t)world * 64) != 0 || s->dx % 64 != 0)
+    return fail(GEIG_ERR_UNSUPPORTED, "column-owned step needs d %% (64 world) == 0 and dx %% 64 == 0");
+  const int64_t W = s->d / world;
+  CU(cudaMalloc((void**)&s->gshadow, (size_t)2 * s->k * s->d * sizeof(__nv_bfloat16)));
+  s->part_world = world; s->part_rank = rank; s->part_W = W;
+  // update grid over the W own columns (segment width a multiple of 8, <= UPD_RES_WMAX)
+  int64_t G = std::max<int64_t>(1, std::min<int64_t>(s->nsm, (W + 7) / 8));
+  int64_t segw = ((W + G - 1) / G + 7) / 8 * 8;
+  if (segw > UPD_RES_WMAX) return fail(GEIG_ERR_UNSUPPORTED, "own block too wide for the resident update");
+  s->own_segw = segw;
+  s->own_grid = (int)((W + segw - 1) / segw);
+  return refresh_gathered_shadow(s);
+}
+
+extern "C" int64_t geig_owned_chunk_floats(const geig_solver* s) {
+  if (!s || s->part_world <= 1) return 0;
+  const int64_t ntri = (int64_t)s->k * (s->k + 1) / 2, hA = (ntri + s->k + 3) & ~(int64_t)3;
+  return 2 * (int64_t)s->k * s->part_W + 2 * hA;
+}
+
+extern "C" geig_status geig_shadow_buffer(geig_solver* s, void** ptr, int64_t* bytes_per_rank) {
+  if (!s || !ptr) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (!s->gshadow) return fail(GEIG_ERR_STATE, "no partition (geig_set_partition)");
+  *ptr = s->gshadow;
+  if (bytes_per_rank) *bytes_per_rank = 2 * (int64_t)s->k * s->part_W * (int64_t)sizeof(__nv_bfloat16);
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_products_cca_owned(geig_solver* s, const void* X, const void* Y, int64_t b, float scale,
+                                               float* buf) {
+  if (!s || !X || !Y || !buf) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (!s->gshadow) return fail(GEIG_ERR_STATE, "no partition (geig_set_partition)");
+  if (b < 2 || b > s->max_rows) return fail(GEIG_ERR_ARG, "b=%lld outside [2, max_rows]", (long long)b);
+  if (!fused_ok(s, X, Y) || ((uintptr_t)buf % 16)) return fail(GEIG_ERR_ARG, "unaligned views or buffer");
+  CU(cudaSetDevice(s->device));
+  tc::OwnedCfg own{(int)s->part_W, s->part_world, s->part_rank, geig_owned_chunk_floats(s), buf, s->gshadow};
+  UpdateArgs a = update_args(s, 0.0, 0.0);
+  geig_status st = tc::fused_cca_step(s->tc, &X, &Y, 1, b, scale, s->Vbf, s->AV, s->BV, a, s->upd_grid, s->upd_smem,
+                                      s->stream, /*products_only=*/true, /*tables=*/true, false, &own);
+  if (st) return fail(st, "%s", tc::last_error());
+  s->launches++;
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_update_owned(geig_solver* s, const float* chunk, double eta, double gamma) {
+  if (!s || !chunk) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (!s->gshadow) return fail(GEIG_ERR_STATE, "no partition (geig_set_partition)");
+  if ((uintptr_t)chunk % 16) return fail(GEIG_ERR_ARG, "chunk must be 16-byte aligned");
+  CU(cudaSetDevice(s->device));
+  const int64_t W = s->part_W, c0 = (int64_t)s->part_rank * W, k = s->k;
+  UpdateArgs a = update_args(s, eta, gamma);
+  a.V = s->V + c0;
+  a.AUX = s->AUX + c0;
+  a.d = W;
+  a.ld = s->d;
+  a.segw = s->own_segw;
+  a.Vbf = s->gshadow + (int64_t)s->part_rank * 2 * k * W;   // this rank's block of the gathered shadow
+  a.vbf_ld = W;
+  a.vbf_lo = k * W;
+  if (a.am) { a.am += c0; a.as += c0; }
+  float* AV = const_cast<float*>(chunk);
+  float* BV = AV + k * W;
+  a.AV = AV; a.BV = BV;
+  a.raw_a = AV + 2 * k * W;
+  a.raw = a.raw_a;
+  a.pre_reduced = 1;
+  tc::OwnedCfg own{(int)W, s->part_world, s->part_rank, geig_owned_chunk_floats(s), AV, s->gshadow};
+  const void* none[1] = {nullptr};
+  geig_status st = tc::fused_cca_step(s->tc, none, none, 1, 0, 1.f, s->Vbf, AV, BV, a, s->own_grid,
+                                      upd_res_smem_floats((int)s->own_segw) * 4, s->stream,
+                                      /*products_only=*/false, /*tables=*/false, /*update_only=*/true, &own);
+  if (st) return fail(st, "%s", tc::last_error());
+  s->launches++;
+  s->fused_last = false;
+  advance_variant_state(s, 1);
   return GEIG_OK;
 }
 

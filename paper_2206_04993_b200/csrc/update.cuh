@@ -54,6 +54,18 @@ struct UpdateArgs {
   float* raw_a;          // nullable: the first half of the resident raw row (tri(G^A) | diag G^B)
                          // lives here instead of raw (multi-GPU: summed over ranks with AV, BV)
   float* gram;           // 3 x k x k out: normalised GA, GB, GC of the step
+  // Column-owned multi-GPU step (geig_set_partition): 0 = off.
+  //  ld: row stride of V, AUX (and the Adam moments) when the update covers
+  //      a column block [c0, c0 + d) of a wider state (V, AUX pre-offset);
+  //  vbf_ld / vbf_lo: row stride / lo-plane offset of the bf16 shadow written
+  //      by the update (the rank's block of the gathered shadow);
+  //  own0, own1: the rank's columns — G^C and ||v''||^2 partials are formed
+  //      over them only (the rest of the replicated state is stale);
+  //  tout, tN, tstride: the reduced table row is written into tN chunks of
+  //      tstride floats (one per rank, for the reduce-scatter)
+  int64_t ld, vbf_ld, vbf_lo, own0, own1, tstride;
+  float* tout;
+  int tN;
   int k;
   int64_t d;
   int64_t segw;          // columns per CTA (multiple of 4)
@@ -607,8 +619,9 @@ __device__ __forceinline__ void gram_c_side(const UpdateArgs& p, int t) {
   const int k = p.k;
   const int64_t d = p.d;
   const int W = (int)p.segw;
-  const int64_t c0 = (int64_t)blockIdx.x * W;
-  const int64_t c1 = min(d, c0 + W);
+  int64_t c0 = (int64_t)blockIdx.x * W;
+  int64_t c1 = min(d, c0 + W);
+  if (p.own1 > p.own0) { c0 = max(c0, p.own0); c1 = min(c1, p.own1); }   // column-owned: own columns only
   const int ntri = k * (k + 1) / 2, hA = (ntri + k + 3) & ~3;
   float* out = p.partial + (size_t)blockIdx.x * (2 * hA) + hA;
   const int nq = c1 > c0 ? (int)((c1 - c0) / 4) : 0;      // d % 4 == 0 on the fused path
@@ -682,8 +695,14 @@ __device__ __forceinline__ void reduce_side(const UpdateArgs& p, int t, float* s
     scratch[t] = s;
     asm volatile("bar.sync 1, 64;" ::: "memory");
     if (half == 0 && e < e1) {
-      if (p.raw_a && e < hA) p.raw_a[e] = s + scratch[t + 32];
-      else p.raw[e] = s + scratch[t + 32];
+      const float v = s + scratch[t + 32];
+      if (p.tN > 0) {
+        for (int r = 0; r < p.tN; ++r) p.tout[(int64_t)r * p.tstride + e] = v;   // every rank's chunk
+      } else if (p.raw_a && e < hA) {
+        p.raw_a[e] = v;
+      } else {
+        p.raw[e] = v;
+      }
     }
     asm volatile("bar.sync 1, 64;" ::: "memory");
   }
@@ -792,7 +811,10 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int k = p.k;
-  const int64_t d = p.d;
+  const int64_t d = p.d;                         // columns covered (the block's width when column-owned)
+  const int64_t lds = p.ld ? p.ld : d;           // row stride of V, AUX, Adam moments
+  const int64_t bld = p.vbf_ld ? p.vbf_ld : lds; // row stride of the bf16 shadow
+  const int64_t blo = p.vbf_lo ? p.vbf_lo : (int64_t)k * bld;   // its lo-plane offset
   const int W = (int)p.segw;                     // multiple of 8
   const int S = W + 4;                           // S/4 odd: conflict-free LDS.128 below
   const int64_t c0 = (int64_t)blockIdx.x * W;
@@ -1283,7 +1305,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
       float4 vn, an;
       if (ADAM && p.adam) {
         // Appendix H: Adam ascent on v_i with the Alg. 2 direction as the gradient
-        const size_t o0 = (size_t)i * d + gx;
+        const size_t o0 = (size_t)i * lds + gx;
         float4 m4 = *reinterpret_cast<const float4*>(p.am + o0);
         float4 s4 = *reinterpret_cast<const float4*>(p.as + o0);
         const float tt = (float)(p.adam_t0 + step + 1);
@@ -1315,20 +1337,21 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
       an.y = xa.y + p.gamma * (ni * bv.y - xa.y);
       an.z = xa.z + p.gamma * (ni * bv.z - xa.z);
       an.w = xa.w + p.gamma * (ni * bv.w - xa.w);
-      const size_t o = (size_t)i * d + gx;
+      const size_t o = (size_t)i * lds + gx;
+      const size_t ob = (size_t)i * bld + gx;
       if (kDevKnobs && (p.dbg_mode & 256)) {   // developer: no state write-back (timing only)
         if (vn.x == 12345.f && an.x == 12345.f) p.V[o] = 0.f;
       } else if (VEC && gx + 3 < c1) {
         *reinterpret_cast<float4*>(p.V + o) = vn;
         *reinterpret_cast<float4*>(p.AUX + o) = an;
-        if (p.Vbf) store_vbf4(p.Vbf, (int64_t)k * d, o, vn);
+        if (p.Vbf) store_vbf4(p.Vbf, blo, ob, vn);
       } else {
         const float vs[4] = {vn.x, vn.y, vn.z, vn.w}, as[4] = {an.x, an.y, an.z, an.w};
         for (int tq = 0; tq < 4; ++tq)
           if (gx + tq < c1) {
             p.V[o + tq] = vs[tq];
             p.AUX[o + tq] = as[tq];
-            if (p.Vbf) store_vbf1(p.Vbf, (int64_t)k * d, o + tq, vs[tq]);
+            if (p.Vbf) store_vbf1(p.Vbf, blo, ob + tq, vs[tq]);
           }
       }
     }

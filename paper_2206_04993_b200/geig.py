@@ -61,6 +61,10 @@ _SIGS = {
     "geig_get_gram": [_vp, _vp, _vp, _vp],
     "geig_update_phase_ns": [_vp, ctypes.POINTER(_i64)],
     "geig_set_option": [_vp, ctypes.c_int, _i64],
+    "geig_set_partition": [_vp, ctypes.c_int, ctypes.c_int],
+    "geig_shadow_buffer": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64)],
+    "geig_products_cca_owned": [_vp, _vp, _vp, _i64, _f32, _vp],
+    "geig_update_owned": [_vp, _vp, _f64, _f64],
 }
 for _name, _args in _SIGS.items():
     _fn = getattr(_lib, _name)
@@ -68,6 +72,8 @@ for _name, _args in _SIGS.items():
     _fn.restype = ctypes.c_int
 _lib.geig_table_floats.argtypes = [_vp]
 _lib.geig_table_floats.restype = _i64
+_lib.geig_owned_chunk_floats.argtypes = [_vp]
+_lib.geig_owned_chunk_floats.restype = _i64
 _lib.geig_launch_count.argtypes = [_vp]
 _lib.geig_launch_count.restype = _i64
 _lib.geig_last_error.restype = ctypes.c_char_p
@@ -78,7 +84,9 @@ EXPORTED = ["geig_create", "geig_destroy", "geig_set_stream", "geig_sync", "geig
             "geig_step_cca", "geig_step_dense", "geig_run_cca", "geig_step_cca_host", "geig_get_gram",
             "geig_set_smooth", "geig_smooth_state", "geig_set_adam",
             "geig_launch_count", "geig_last_error", "geig_version", "geig_update_phase_ns",
-            "geig_table_floats", "geig_products_cca_tables", "geig_update_tables", "geig_set_option"]
+            "geig_table_floats", "geig_products_cca_tables", "geig_update_tables", "geig_set_option",
+            "geig_set_partition", "geig_owned_chunk_floats", "geig_shadow_buffer", "geig_products_cca_owned",
+            "geig_update_owned"]
 
 
 def _check(st: int):
@@ -226,6 +234,29 @@ def geig_set_option(h, option: int, value: int):
     _check(_lib.geig_set_option(h, option, value))
 
 
+def geig_set_partition(h, world: int, rank: int):
+    _check(_lib.geig_set_partition(h, world, rank))
+
+
+def geig_owned_chunk_floats(h) -> int:
+    return int(_lib.geig_owned_chunk_floats(h))
+
+
+def geig_shadow_buffer(h):
+    """(device pointer, bytes per rank) of the gathered bf16 shadow."""
+    p, n = _vp(), _i64(0)
+    _check(_lib.geig_shadow_buffer(h, ctypes.byref(p), ctypes.byref(n)))
+    return p.value, n.value
+
+
+def geig_products_cca_owned(h, X, Y, b: int, scale: float, buf):
+    _check(_lib.geig_products_cca_owned(h, _ptr(X), _ptr(Y), b, scale, _ptr(buf, torch.float32)))
+
+
+def geig_update_owned(h, chunk, eta: float, gamma: float):
+    _check(_lib.geig_update_owned(h, _ptr(chunk, torch.float32), eta, gamma))
+
+
 def geig_update_phase_ns(h):
     out = (_i64 * 5)()
     _check(_lib.geig_update_phase_ns(h, out))
@@ -282,3 +313,21 @@ class Solver:
 
     def launches(self):
         return geig_launch_count(self.h)
+
+
+class _DevArray:
+    """__cuda_array_interface__ wrapper (zero-copy torch view of a device
+    buffer the library owns)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"data": (ptr, False), "shape": tuple(shape), "typestr": typestr,
+                                         "version": 3, "strides": None}
+
+
+def shadow_tensor(h, world: int, k: int, W: int, device: int = 0):
+    """The gathered bf16 shadow of a partitioned solver as a torch int16 view
+    [world, 2, k, W] (the bytes the all-gather moves; bf16 hi | lo planes)."""
+    ptr, nbytes = geig_shadow_buffer(h)
+    if nbytes != 2 * k * W * 2:
+        raise GeigError(f"shadow block is {nbytes} bytes, expected {2 * k * W * 2}")
+    return torch.as_tensor(_DevArray(ptr, (world, 2, k, W), "<i2"), device=f"cuda:{device}")

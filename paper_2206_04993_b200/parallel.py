@@ -118,3 +118,88 @@ def dense_wire_bytes(k: int, d: int, world: int, elem: int = 4) -> dict:
     w = (d + world - 1) // world
     return {"allgather_send": 2 * k * w * elem * (world - 1),
             "allreduce_ring_send": 2 * 2 * k * d * elem * (world - 1) // world}
+
+
+# ---------------------------------------------------------------------------
+# Column-owned step (geig_set_partition): reduce-scatter + all-gather
+# ---------------------------------------------------------------------------
+
+def reduce_scatter_chunks(buf: torch.Tensor, out: torch.Tensor, group=None):
+    """Sum buf (world chunks, chunk r for rank r) over the ranks into `out`
+    (this rank's summed chunk).  NCCL: one reduce-scatter; backends without
+    it (gloo): an all-reduce of the buffer and a copy of the own chunk."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    chunks = buf.view(world, -1)
+    if dist.get_backend(group) == "nccl":
+        dist.reduce_scatter_tensor(out, buf, op=dist.ReduceOp.SUM, group=group)
+    else:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        out.copy_(chunks[rank])
+
+
+def allgather_blocks(blocks: torch.Tensor, group=None):
+    """blocks: [world, ...] with this rank's block current; afterwards every
+    block is the owner's.  NCCL: one in-place all-gather; gloo: through
+    host copies."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(blocks.view(-1), blocks[rank].reshape(-1), group=group)
+    else:
+        # host copies as raw bytes (gloo has no int16 / bf16 all-gather)
+        raw = blocks.view(torch.uint8) if blocks.element_size() == 2 else blocks
+        mine = raw[rank].cpu()
+        got = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(got, mine, group=group)
+        for q in range(world):
+            if q != rank:
+                raw[q].copy_(got[q])
+
+
+def owned_wire_bytes(k: int, d: int, world: int, n_tables: int) -> dict:
+    """Bytes each rank sends per step: reduce-scatter of [AV | BV | tables]
+    chunks (fp32) + all-gather of the bf16 hi / lo shadow blocks, vs the
+    ring all-reduce of [AV | BV | tables] of the replicated step."""
+    W = d // world
+    chunk = 2 * k * W + n_tables
+    return {"reduce_scatter_send": 4 * chunk * (world - 1),
+            "allgather_send": 2 * 2 * k * W * (world - 1),
+            "allreduce_ring_send": 2 * 4 * (2 * k * d + n_tables) * (world - 1) // world}
+
+
+class ColumnOwnedStep:
+    """One column-owned multi-GPU step of Alg. 2 for a partitioned solver
+    (geig_set_partition(world, rank)): products of the rank's rows (one
+    launch) -> reduce-scatter of the per-owner chunks -> update of the own
+    columns -> all-gather of the bf16 shadow blocks that the next forward
+    reads (Appendix F)."""
+
+    def __init__(self, geig, solver, world: int, rank: int, group=None):
+        self.g, self.s, self.world, self.rank, self.group = geig, solver, world, rank, group
+        self.k, self.d = solver.k, solver.d
+        self.W = self.d // world
+        self.chunk = geig.geig_owned_chunk_floats(solver.h)
+        dev = f"cuda:{solver.device}"
+        self.buf = torch.empty(world * self.chunk, device=dev)
+        self.mine = torch.empty(self.chunk, device=dev)
+        self.shadow = geig.shadow_tensor(solver.h, world, self.k, self.W, solver.device)
+
+    def __call__(self, X, Y, b: int, eta: float, gamma: float):
+        g = self.g
+        g.geig_products_cca_owned(self.s.h, X, Y, b, cca_scale(b, self.world), self.buf)
+        reduce_scatter_chunks(self.buf, self.mine, self.group)
+        g.geig_update_owned(self.s.h, self.mine, eta, gamma)
+        allgather_blocks(self.shadow, self.group)
+
+    def gather_state(self):
+        """The retracted V (unit rows) and [Bv] assembled from every rank's
+        own columns (not on the hot path)."""
+        V, AUX = self.s.state()
+        Vb = V.view(self.k, self.world, self.W).permute(1, 0, 2).contiguous()
+        Ab = AUX.view(self.k, self.world, self.W).permute(1, 0, 2).contiguous()
+        allgather_blocks(Vb, self.group)
+        allgather_blocks(Ab, self.group)
+        V = Vb.permute(1, 0, 2).reshape(self.k, self.d)
+        AUX = Ab.permute(1, 0, 2).reshape(self.k, self.d)
+        return V / V.norm(dim=1, keepdim=True), AUX

@@ -23,12 +23,13 @@ def _port():
     return p
 
 
-def test_two_ranks_appendix_f_step_matches_oracle():
+@pytest.mark.parametrize("mode", ["replicated", "owned"])
+def test_two_ranks_appendix_f_step_matches_oracle(mode):
     assert torch.cuda.is_available()
     from paper_2206_04993_b200 import build
     build.build()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "mr_step.py")]
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "mr_step.py"), mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     line = next(l for l in r.stdout.splitlines() if l.startswith("MR_RESULT "))

@@ -175,3 +175,50 @@ def test_gloo_world2_tables_buffer_allreduce():
         for i in range(3):
             np.testing.assert_allclose(res[r][1][i], want[i], rtol=0, atol=1e-14)
             np.testing.assert_allclose(res[r][2][i], want[i], rtol=0, atol=1e-14)
+
+
+def _owned_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2206_04993_b200.parallel import allgather_blocks, reduce_scatter_chunks
+        chunk = 7
+        g = torch.Generator().manual_seed(200 + rank)
+        buf = torch.randn(world * chunk, generator=g, dtype=torch.float64)
+        mine = buf.clone()
+        out = torch.empty(chunk, dtype=torch.float64)
+        reduce_scatter_chunks(buf, out)
+        blocks = torch.full((world, 2, 3, 5), -1.0, dtype=torch.float64)
+        blocks[rank] = rank + torch.arange(30, dtype=torch.float64).view(2, 3, 5)
+        allgather_blocks(blocks)
+        out_q.put((rank, mine.numpy(), out.numpy(), blocks.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world3_column_owned_collectives():
+    """Host plumbing of the column-owned step (parallel.ColumnOwnedStep):
+    the reduce-scatter of per-owner chunks gives rank r the sum of every
+    rank's chunk r; the all-gather of shadow blocks gives every rank every
+    owner's block."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_owned_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, mine, out, blocks = q.get(timeout=120)
+        res[r] = (mine, out, blocks)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    chunk = 7
+    total = sum(res[r][0] for r in range(world))
+    for r in range(world):
+        np.testing.assert_allclose(res[r][1], total[r * chunk:(r + 1) * chunk], rtol=0, atol=1e-12)
+        for q_ in range(world):
+            np.testing.assert_array_equal(res[r][2][q_], q_ + np.arange(30.0).reshape(2, 3, 5))
