@@ -173,6 +173,18 @@ __device__ __forceinline__ void decode_backward(const FusedMaps& M, const CUtens
   it.scale = p.scale;
 }
 
+// developer NaN tracing (dev-knob builds with the stamp buffer set): slot
+// 56 + what of this CTA records step + 1 of the first non-finite value
+__device__ __forceinline__ void nan_rec(const FusedParams& p, int what, int, float v) {
+  // records after the G x 64 stamp slots: 8 per CTA, [7] = the current step
+  if (kDevKnobs && p.upd.dbg && !isfinite(v)) {
+    unsigned long long* r = p.upd.dbg + (size_t)gridDim.x * 64 + (size_t)blockIdx.x * 8;
+    atomicCAS(&r[what], 0ull, *(volatile unsigned long long*)&r[7] + 1ull);
+  }
+}
+
+__device__ __forceinline__ bool dev_tbar_in_ring(const FusedParams& p) { return kDevKnobs && (p.dbg_mode & 8192); }
+
 struct RingState {
   int it_prod = 0, it_mma = 0, items = 0;   // per-role running counters (persist across phases)
 };
@@ -319,6 +331,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
                   const int64_t r = gc / p.ownW;
                   o = it.out[seg] + r * p.chunk + (int64_t)n * p.ownW + (gc - r * p.ownW);
                 }
+                if (kDevKnobs) nan_rec(p, A_MN ? 0 : 1, 0, v.x + v.y + v.z + v.w);
                 if (full_m || q_ok) {
                   __stcg(reinterpret_cast<float4*>(o), v);
                 } else {
@@ -408,11 +421,17 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   // Alg. 2's loop over t: one batch per step, the state stays in HBM/L2, the
   // TMEM allocation, mbarrier ring and its phase counters persist.
   for (int t = 0; t < p.nsteps; ++t) {
+  if (kDevKnobs && p.upd.dbg && threadIdx.x == 0) p.upd.dbg[(size_t)gridDim.x * 64 + (size_t)blockIdx.x * 8 + 7] = t;
   const CUtensorMap* A = p.xmaps ? p.xmaps + 6 * t : maps.a;
   if (t > 0) stamp(p.upd, 4);
   if (!p.update_only) {   // (update-only launch: phase U alone, from given products and tables)
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
+    // consumer-side proxy fence: the V shadow read by this step's TMA was
+    // written with generic stores by every CTA's phase U of the previous step
+    // (ordered by the grid barrier); the async proxy must see them
+    asm volatile("fence.proxy.async.global;" ::: "memory");
     for (int v = 0; v < 2; ++v) tma_prefetch_desc(&A[v]);
+  }
 
   // ---- phase F: forward split-K partials; warps 2-3: G^C, ||v''||^2 partials ----
   if (warp == 2 || warp == 3) {
@@ -536,6 +555,8 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
         }
         // Zb planes: 0 = y1 (-> AV_x), 1 = x2 (-> BV_x), 2 = x1 (-> AV_y), 3 = y2 (-> BV_y)
         const int64_t o = (int64_t)n * p.hpad + r;
+        if (kDevKnobs)
+          nan_rec(p, 2, 0, z[0][0] + z[1][0] + z[2][0] + z[3][0] + z[0][3] + z[1][3] + z[2][3] + z[3][3]);
         if (vec) {
           store4<__nv_bfloat16>(p.Zb + 0 * plane + o, z[2][0], z[2][1], z[2][2], z[2][3]);
           store4<__nv_bfloat16>(p.Zb + 1 * plane + o, z[1][0], z[1][1], z[1][2], z[1][3]);
@@ -616,8 +637,10 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   dstamp(p.upd, 5);
 
   // ---- phase B: backward products into AV, BV ----
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");   // Zb of every CTA's phase S, read by TMA below
     for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&A[2 + v]); tma_prefetch_desc(&maps.bB[v]); }
+  }
   if (warp == 2 || warp == 3) {    // warps 2-3: reduce the (now complete) Gram partial rows
     if (!p.products_only || p.tables) {
       reduce_side(p.upd, threadIdx.x - 64, side_scratch);
@@ -693,7 +716,8 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   // ---- phase U: Gram tables + fused update ----
   if (!p.products_only && !(kDevKnobs && (p.dbg_mode & 64)))
     update_res_phases<true, 1, ADAM>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um, t,
-                                     p.early_coef ? coef_smem : nullptr);
+                                     p.early_coef ? coef_smem : nullptr,
+                                     dev_tbar_in_ring(p) ? nullptr : acce_bar + 2);
   if (t + 1 < p.nsteps) {
     // next step: its forward TMA reads the new bf16 shadow of V (generic
     // stores above) and refills the smem ring the update phase used
@@ -838,7 +862,10 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   }
   if (products_only && nsteps != 1) return tc_fail(GEIG_ERR_ARG, "products-only launch runs one step");
   p.xmaps = nullptr;
-  if (nsteps > 1) {
+  bool same_batch = true;   // every step on one batch: the param-space maps serve all steps
+  for (int i = 1; i < nsteps && same_batch; ++i) same_batch = X[i] == X[0] && Y[i] == Y[0];
+  if (dev_knob("GEIG_XMAPS_ALWAYS")) same_batch = false;
+  if (nsteps > 1 && !same_batch) {
     // per-step A maps in global memory (distinct batches encoded once)
     if (nsteps > TC_RUN_CHUNK) return tc_fail(GEIG_ERR_ARG, "fused run: more than TC_RUN_CHUNK steps per launch");
     if (!t.xm_dev) {   // fixed capacity, allocated once (never inside a timed loop of later calls)

@@ -805,7 +805,7 @@ __device__ __forceinline__ void coef_early(const UpdateArgs& p, float* cf, int s
 template <bool VEC, int PRE = -1, bool ADAM = true>
 __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* smem, cg::grid_group& grid,
                                                   const UpdMaps* um = nullptr, int step = 0,
-                                                  float* coef = nullptr) {
+                                                  float* coef = nullptr, uint64_t* tbar_ext = nullptr) {
   // coef: coefficients already formed (coef_early, fused kernel) — no table
   // staging, phase 3a skipped
   const int tid = threadIdx.x;
@@ -831,7 +831,10 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   float* red = D2s + 64;                         // [8][32]
   float* rs = red + 8 * 32;                      // staged raw tables
   float* gred = Lt;                              // phase 1 only: Gram slice partials
-  uint64_t* tbar = reinterpret_cast<uint64_t*>(Bt + 64 * S + (UPD_AUXF > UPD_GREDF ? UPD_AUXF : UPD_GREDF));
+  // the tile barrier: outside the arena when the caller provides one (the
+  // fused kernel: its barrier region, never a TMA destination)
+  uint64_t* tbar = tbar_ext ? tbar_ext
+                            : reinterpret_cast<uint64_t*>(Bt + 64 * S + (UPD_AUXF > UPD_GREDF ? UPD_AUXF : UPD_GREDF));
   const int ntri = k * (k + 1) / 2;
   const int hA = (ntri + k + 3) & ~3;            // half row: [tri | diag | pad]
   const int pstride = 2 * hA;                    // per-CTA partial row (16-byte multiple)
@@ -848,6 +851,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
   }
   if (um) {
     if (tid == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");   // state / products written by generic stores
       tc::mbar_init(tbar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       // smem last written through the async proxy (GEMM ring) or generic
@@ -1333,6 +1337,12 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
         vn.z = ni * vv.z + p.eta * gr.z;
         vn.w = ni * vv.w + p.eta * gr.w;
       }
+      if (kDevKnobs && p.dbg && !isfinite(vn.x + vn.y + vn.z + vn.w))
+        atomicCAS(&p.dbg[(size_t)gridDim.x * 64 + (size_t)blockIdx.x * 8 + 3], 0ull, (unsigned long long)(step + 1));
+      if (kDevKnobs && p.dbg && !isfinite(gr.x + gr.y + gr.z + gr.w))
+        atomicCAS(&p.dbg[(size_t)gridDim.x * 64 + (size_t)blockIdx.x * 8 + 4], 0ull, (unsigned long long)(step + 1));
+      if (kDevKnobs && p.dbg && !isfinite(bv.x + bv.y + bv.z + bv.w + vv.x + vv.y + vv.z + vv.w))
+        atomicCAS(&p.dbg[(size_t)gridDim.x * 64 + (size_t)blockIdx.x * 8 + 5], 0ull, (unsigned long long)(step + 1));
       an.x = xa.x + p.gamma * (ni * bv.x - xa.x);
       an.y = xa.y + p.gamma * (ni * bv.y - xa.y);
       an.z = xa.z + p.gamma * (ni * bv.z - xa.z);

@@ -656,3 +656,29 @@ def test_fused_step_random_shapes(geig, k, dx, dy, rows, math):
         step = errs.pop("step")
         _assert(errs, 1e-4)
         assert step < 1e-3, errs
+
+
+def test_run_cca_large_batch_long_run_is_deterministic(geig):
+    """Regression: the multi-step launch's phase-U tile barrier used to live
+    in the smem ring (a TMA destination of phases F and B); re-initialising it
+    there let phase U read partially landed tiles about once per 10^4 steps
+    (non-finite v'' at b = 100k, config 1).  Two identical runs of 2000 steps
+    in launches of 100 must stay finite and bit-identical."""
+    from synth import CONFIGS, cca_views, gaussian_init
+    cfg = CONFIGS[1]
+    n, dx, k = 100_000, 64, 8
+    x, y = cca_views(cfg, n, seed=3)
+    x, y = x.to(torch.bfloat16).contiguous().cuda(), y.to(torch.bfloat16).contiguous().cuda()
+    out = []
+    for _ in range(2):
+        s = geig.Solver(geig.GEIG_CCA, dx, dx, k, math="bf16x2", data_dtype=geig.GEIG_DATA_BF16, rho=cfg.rho,
+                        max_rows=n)
+        try:
+            s.init_state(torch.tensor(gaussian_init(k, 2 * dx, 0), dtype=torch.float32, device="cuda:0"))
+            for _ in range(20):
+                geig.geig_run_cca(s.h, [x] * 100, [y] * 100, n, 0.0086, 1.0)
+            out.append([t_.cpu() for t_ in s.state()])
+        finally:
+            s.close()
+    assert all(torch.isfinite(t_).all() for t_ in out[0] + out[1])
+    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
