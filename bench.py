@@ -442,6 +442,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
     ev = []
 
     fused = world == 1 and math in ("bf16", "bf16x2") and cfg.k <= 64 and not args.staged and not args.split_step
+    # fp32 small problems (config 1): the one-CTA step kernel, state resident
+    # in shared memory (small_step.cuh; k <= 16, KP d <= 8192, KP = 8 or 16)
+    small = (world == 1 and math == "f32" and cfg.k <= 16 and (8 if cfg.k <= 8 else 16) * cfg.d <= 8192 and not args.staged
+             and not args.split_step)
+    fused = fused or small
 
     def step(i, timed):
         if timed:
@@ -545,12 +550,18 @@ def run_gpu(args, cfg, rank, world, local_rank):
     kd = cfg.k * cfg.d
     if fused:
         alg_bytes = b * cfg.d * esz + 2 * kd * 4 + 2 * kd * 4 + kd * 2
-        kernel = ("cca_step_kernel (fused: forward GEMM, reshuffle, backward GEMM, Gram, update; "
-                  + ("K steps in one persistent launch via geig_run_cca)" if multi else "one launch per step)"))
+        if small:
+            kernel = ("small_step_kernel (one CTA: forward, backward, Gram, update, state in shared memory; "
+                      + ("K steps in one launch via geig_run_cca)" if multi else "one launch per step)"))
+            phases = {}
+        else:
+            kernel = ("cca_step_kernel (fused: forward GEMM, reshuffle, backward GEMM, Gram, update; "
+                      + ("K steps in one persistent launch via geig_run_cca)" if multi else "one launch per step)"))
+            ph = geig.geig_update_phase_ns(s.h)
+            phases = {"forward_us": ph[3] / 1e3, "reshuffle_backward_us": ph[4] / 1e3, "gram_us": ph[0] / 1e3,
+                      "reduce_us": ph[1] / 1e3, "coef_update_us": ph[2] / 1e3,
+                      "source": "%globaltimer, CTA 0, last step"}
         k_ms = prod_ms
-        ph = geig.geig_update_phase_ns(s.h)
-        phases = {"forward_us": ph[3] / 1e3, "reshuffle_backward_us": ph[4] / 1e3, "gram_us": ph[0] / 1e3,
-                  "reduce_us": ph[1] / 1e3, "coef_update_us": ph[2] / 1e3, "source": "%globaltimer, CTA 0, last step"}
     else:
         alg_bytes = b * cfg.d * esz + kd * (2 if math in ("bf16", "bf16x2") else 4) + 2 * kd * 4
         kernel = ("cca_step_kernel products-only launch (phases F, S, B; multi-GPU: then all-reduce + update)"

@@ -219,6 +219,17 @@ geig_status geig_step_cca(geig_solver* s, const void* X, const void* Y,
 geig_status geig_step_dense(geig_solver* s, const void* A, const void* B,
                             double eta, double gamma);
 
+/* Alg. 1's loop (deterministic full-batch game): nsteps
+ * consecutive dense steps on the same d x d matrices A, B (device, row-major,
+ * the solver's data dtype).  Equivalent to nsteps calls of geig_step_dense.
+ * With fp32 math, k <= 16 and A, B small enough to sit in one SM's shared
+ * memory (d <= ~100 at fp32), the steps run in ONE launch of the one-CTA
+ * small-problem kernel with A, B resident (GEIG_OPT_SMALL_STEP); otherwise
+ * products + update per step.  Errors: GEIG_ERR_ARG for NULL pointers or
+ * nsteps outside [0, 2^30]; GEIG_ERR_STATE for a CCA solver. */
+geig_status geig_run_dense(geig_solver* s, const void* A, const void* B,
+                           int64_t nsteps, double eta, double gamma);
+
 /* Alg. 2's loop over t ("for t = 1 : T"): nsteps
  * consecutive CCA steps, step i on the minibatch (X[i], Y[i]) — host arrays
  * of nsteps DEVICE pointers, each view b x d_view row-major in the solver's
@@ -285,12 +296,23 @@ geig_status geig_get_gram(geig_solver* s, float* GA, float* GB, float* GC);
  *  GEIG_OPT_FUSED_M_TILES   : 128-row M tiles per work item of the fused
  *                             step's GEMM phases (0 = auto: 2 where the grid
  *                             stays busy, else 1; 1; 2)
+ *  GEIG_OPT_SMALL_STEP      : 1 = (default) fp32 (GEIG_MATH_F32) steps of
+ *                             small problems — k <= 16, KP d <= 8192 (KP = k rounded up to 8 or 16) and
+ *                             the state plus a chunk of rows (CCA) or A and
+ *                             B (dense) within one SM's 227 KB of shared
+ *                             memory, 16-byte aligned rows — run as ONE
+ *                             launch of a one-CTA kernel per call
+ *                             (geig_step_cca / geig_run_cca /
+ *                             geig_step_dense / geig_run_dense: the whole
+ *                             run in one launch, state resident in shared
+ *                             memory, each batch byte read once); 0 = the
+ *                             staged products + update kernels
  *  GEIG_OPT_STAGED_PRODUCTS : 1 = geig_products_cca runs the three-launch
  *                             staged tcgen05 products (forward GEMM, z
  *                             reshuffle, backward GEMM) instead of phases
  *                             F, S, B of the fused kernel; 0 = fused (default)
  * Errors: GEIG_ERR_ARG for an unknown option or a value out of range. */
-typedef enum { GEIG_OPT_FUSED_M_TILES = 1, GEIG_OPT_STAGED_PRODUCTS = 2 } geig_option;
+typedef enum { GEIG_OPT_FUSED_M_TILES = 1, GEIG_OPT_STAGED_PRODUCTS = 2, GEIG_OPT_SMALL_STEP = 3 } geig_option;
 geig_status geig_set_option(geig_solver* s, int option, int64_t value);
 
 /* Phase durations (ns, %globaltimer of CTA 0) of the last update:

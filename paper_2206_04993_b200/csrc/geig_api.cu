@@ -16,6 +16,7 @@
 #include "update.cuh"
 #include "tc_gemm.cuh"
 #include "fused_step.cuh"
+#include "small_step.cuh"
 
 using namespace geig;
 
@@ -86,6 +87,11 @@ struct geig_solver {
   int64_t own_segw = 0;
   float* splitk = nullptr;                            // SIMT split-K partials (lazily sized)
   size_t splitk_floats = 0;
+  // one-CTA small-problem step (small_step.cuh)
+  int opt_small = 1;                                  // geig_set_option(GEIG_OPT_SMALL_STEP)
+  const void** ptab_dev = nullptr;                    // per-step batch pointers of a run (device, pinned staging)
+  const void** ptab_host = nullptr;
+  cudaEvent_t ptab_ev = nullptr;
 };
 
 extern "C" const char* geig_last_error(void) { return g_err.c_str(); }
@@ -209,6 +215,9 @@ extern "C" geig_status geig_destroy(geig_solver* s) {
                   (void*)s->Wx, (void*)s->Wy, (void*)s->ts, (void*)s->Wxb, (void*)s->Wyb, s->hX, s->hY,
                   (void*)s->zbuf, (void*)s->am, (void*)s->as, (void*)s->splitk, (void*)s->gshadow})
     if (p) cudaFree(p);
+  if (s->ptab_dev) cudaFree((void*)s->ptab_dev);
+  if (s->ptab_host) cudaFreeHost((void*)s->ptab_host);
+  if (s->ptab_ev) cudaEventDestroy(s->ptab_ev);
   tc::plan_destroy(s->tc);
   delete s;
   return GEIG_OK;
@@ -571,9 +580,107 @@ static void advance_variant_state(geig_solver* s, int64_t n) {
   s->adam_t += n;
 }
 
+// ---------------------------------------------------------------------------
+// one-CTA small-problem step (small_step.cuh): fp32 FFMA math, k <= 16, the
+// state (4 k x d fp32 arrays) and a chunk of rows (CCA) or A and B (dense)
+// resident in one SM's shared memory.  Otherwise the staged path runs.
+// ---------------------------------------------------------------------------
+struct SmallPlan {
+  bool ok = false;
+  int KP = 8, rc = 0, dpad = 0, RG = 1;
+  size_t smem = 0;
+};
+
+static SmallPlan small_plan(const geig_solver* s, int64_t b) {
+  SmallPlan pl;
+  if (!s->opt_small || s->math != GEIG_MATH_F32 || s->k > 16 || s->adam) return pl;
+  const size_t es = s->dtype == GEIG_DATA_BF16 ? 2 : 4;
+  const int E = (int)(16 / es);
+  const int64_t d = s->d;
+  pl.KP = s->k <= 8 ? 8 : 16;
+  if (d % E != 0 || s->dx % E != 0 || (pl.KP / 4) * ((d / 4 + 7) / 8) * 8 > SM_THREADS) return pl;
+  pl.dpad = (int)d;
+  // backward tiles: (KP / 4) player quads x 8-quad column groups, RG row groups
+  const int tiles = (pl.KP / 4) * (int)((d / 4 + 7) / 8) * 8;
+  pl.RG = 1;
+  while (pl.RG < 4 && tiles * pl.RG * 2 <= SM_THREADS) pl.RG *= 2;
+  if (s->problem == GEIG_DENSE) {
+    pl.rc = (int)((d + 3) / 4 * 4);                    // A, B resident: d rows each (rounded to 4)
+    pl.smem = small_smem_bytes(true, pl.KP, (int)d, s->k, pl.rc, pl.dpad, es);
+    pl.ok = pl.smem <= (size_t)SM_SMEM_MAX;
+    return pl;
+  }
+  const int b4 = (int)((b + 3) / 4 * 4);
+  for (int rc = std::min(b4, 1024); rc >= 4; rc -= 4) {
+    const size_t need = small_smem_bytes(false, pl.KP, (int)d, s->k, rc, pl.dpad, es);
+    if (need <= (size_t)SM_SMEM_MAX) { pl.rc = rc; pl.smem = need; pl.ok = true; break; }
+  }
+  return pl;
+}
+
+// nsteps steps of the small path; batches: X[i], Y[i] (CCA) or A, B (dense, X[0], Y[0])
+static geig_status small_launch(geig_solver* s, const SmallPlan& pl, const void* const* X, const void* const* Y,
+                                int64_t nsteps, int64_t b, double eta, double gamma) {
+  SmallParams p{};
+  const bool dense = s->problem == GEIG_DENSE;
+  p.dense = dense ? 1 : 0;
+  p.k = s->k; p.KPr = pl.KP;
+  p.dx = (int)s->dx; p.dy = (int)s->dy; p.d = (int)s->d;
+  p.b = dense ? 0 : (int)b;
+  p.h = (int)(b / 2);
+  p.nsteps = (int)nsteps;
+  p.x0 = X[0]; p.y0 = Y[0];
+  p.xs = nullptr;
+  bool same = true;
+  for (int64_t i = 1; i < nsteps && same && !dense; ++i) same = X[i] == X[0] && Y[i] == Y[0];
+  if (!same) {
+    if (!s->ptab_dev) {
+      CU(cudaMalloc((void**)&s->ptab_dev, (size_t)tc::TC_RUN_CHUNK * 2 * sizeof(void*)));
+      CU(cudaMallocHost((void**)&s->ptab_host, (size_t)tc::TC_RUN_CHUNK * 2 * sizeof(void*)));
+      CU(cudaEventCreateWithFlags(&s->ptab_ev, cudaEventDisableTiming));
+    }
+    CU(cudaEventSynchronize(s->ptab_ev));               // the previous run's copy out of the staging buffer is done
+    for (int64_t i = 0; i < nsteps; ++i) { s->ptab_host[2 * i] = X[i]; s->ptab_host[2 * i + 1] = Y[i]; }
+    CU(cudaMemcpyAsync((void*)s->ptab_dev, (const void*)s->ptab_host, (size_t)nsteps * 2 * sizeof(void*),
+                       cudaMemcpyHostToDevice, s->stream));
+    CU(cudaEventRecord(s->ptab_ev, s->stream));
+    p.xs = s->ptab_dev;
+  }
+  p.scale = dense ? 1.f : 1.0f / (float)(b / 2);
+  p.eta = (float)eta; p.gamma = (float)gamma; p.rho = s->rho;
+  p.V = s->V; p.AUX = s->AUX; p.AV = s->AV; p.BV = s->BV; p.Vbf = s->Vbf; p.gram = s->gram;
+  p.smooth = s->smooth; p.zbuf = s->zbuf; p.zpar = s->zpar;
+  p.lnrho = logf(std::max(s->rho, 1e-30f)); p.lnnu = logf(std::max(s->nu, 1e-30f));
+  p.rc = pl.rc; p.dpad = pl.dpad; p.RG = pl.RG;
+  p.ts = nullptr;
+  p.prof = tc::dbg_ptr();   // developer hook (geig_debug_set_tc_stamps): per-phase cycles
+  const bool bf = s->dtype == GEIG_DATA_BF16;
+  const void* fn = bf ? (pl.KP == 8 ? (const void*)small_step_kernel<__nv_bfloat16, 8>
+                                    : (const void*)small_step_kernel<__nv_bfloat16, 16>)
+                      : (pl.KP == 8 ? (const void*)small_step_kernel<float, 8> : (const void*)small_step_kernel<float, 16>);
+  static std::atomic<uint64_t> attr[4];
+  const int ai = (bf ? 2 : 0) + (pl.KP == 8 ? 0 : 1);
+  CU(set_smem_attr_once(attr[ai], fn, SM_SMEM_MAX));
+  void* args[] = {&p};
+  CU(cudaLaunchKernel(fn, dim3(1), dim3(SM_THREADS), args, pl.smem, s->stream));
+  s->launches++;
+  s->fused_last = false;
+  advance_variant_state(s, nsteps);
+  return GEIG_OK;
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p % 16) == 0; }
+
 extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* Y, int64_t b, double eta,
                                      double gamma) {
   if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
+  if (s->problem == GEIG_CCA && b >= 2 && b <= s->max_rows && X && Y && aligned16(X) && aligned16(Y)) {
+    const SmallPlan pl = small_plan(s, b);
+    if (pl.ok) {
+      CU(cudaSetDevice(s->device));
+      return small_launch(s, pl, &X, &Y, 1, b, eta, gamma);
+    }
+  }
   if (s->problem == GEIG_CCA && b >= 2 && b <= s->max_rows && X && Y && fused_ok(s, X, Y)) {
     // whole step in one persistent cooperative launch (fused_step.cuh)
     CU(cudaSetDevice(s->device));
@@ -598,6 +705,21 @@ extern "C" geig_status geig_run_cca(geig_solver* s, const void* const* X, const 
   if (nsteps < 0 || nsteps > (1 << 20)) return fail(GEIG_ERR_ARG, "nsteps = %lld out of range", (long long)nsteps);
   if (nsteps == 0) return GEIG_OK;
   bool fused = s->problem == GEIG_CCA && b >= 2 && b <= s->max_rows;
+  {
+    // one-CTA small path: up to TC_RUN_CHUNK steps per launch
+    const SmallPlan pl = fused ? small_plan(s, b) : SmallPlan{};
+    bool small = pl.ok;
+    for (int64_t i = 0; small && i < nsteps; ++i) small = X[i] && Y[i] && aligned16(X[i]) && aligned16(Y[i]);
+    if (small) {
+      CU(cudaSetDevice(s->device));
+      for (int64_t i0 = 0; i0 < nsteps; i0 += tc::TC_RUN_CHUNK) {
+        const int64_t n = std::min<int64_t>(tc::TC_RUN_CHUNK, nsteps - i0);
+        geig_status st = small_launch(s, pl, X + i0, Y + i0, n, b, eta, gamma);
+        if (st) return st;
+      }
+      return GEIG_OK;
+    }
+  }
   for (int64_t i = 0; fused && i < nsteps; ++i) fused = X[i] && Y[i] && fused_ok(s, X[i], Y[i]);
   if (!fused) {
     for (int64_t i = 0; i < nsteps; ++i) {
@@ -624,9 +746,33 @@ extern "C" geig_status geig_run_cca(geig_solver* s, const void* const* X, const 
 extern "C" geig_status geig_step_dense(geig_solver* s, const void* A, const void* B, double eta,
                                        double gamma) {
   if (!s) return fail(GEIG_ERR_ARG, "solver is NULL");
-  geig_status st = geig_products_dense(s, A, B, 0, s->d, s->AV, s->BV);
-  if (st) return st;
-  return geig_update(s, s->AV, s->BV, eta, gamma);
+  return geig_run_dense(s, A, B, 1, eta, gamma);
+}
+
+extern "C" geig_status geig_run_dense(geig_solver* s, const void* A, const void* B, int64_t nsteps, double eta,
+                                      double gamma) {
+  if (!s || !A || !B) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (s->problem != GEIG_DENSE) return fail(GEIG_ERR_STATE, "solver is not a dense solver");
+  if (nsteps < 0 || nsteps > (1 << 30)) return fail(GEIG_ERR_ARG, "nsteps = %lld out of range", (long long)nsteps);
+  if (nsteps == 0) return GEIG_OK;
+  const SmallPlan pl = small_plan(s, 0);
+  if (pl.ok && aligned16(A) && aligned16(B)) {
+    // A, B resident in one SM's shared memory for the whole launch
+    CU(cudaSetDevice(s->device));
+    for (int64_t i0 = 0; i0 < nsteps; i0 += tc::TC_RUN_CHUNK) {
+      const int64_t n = std::min<int64_t>(tc::TC_RUN_CHUNK, nsteps - i0);
+      geig_status st = small_launch(s, pl, &A, &B, n, 0, eta, gamma);
+      if (st) return st;
+    }
+    return GEIG_OK;
+  }
+  for (int64_t i = 0; i < nsteps; ++i) {
+    geig_status st = geig_products_dense(s, A, B, 0, s->d, s->AV, s->BV);
+    if (st) return st;
+    st = geig_update(s, s->AV, s->BV, eta, gamma);
+    if (st) return st;
+  }
+  return GEIG_OK;
 }
 
 extern "C" geig_status geig_step_cca_host(geig_solver* s, const void* X_host, const void* Y_host, int64_t b,
@@ -796,6 +942,10 @@ extern "C" geig_status geig_set_option(geig_solver* s, int option, int64_t value
     case GEIG_OPT_FUSED_M_TILES:
       if (value < 0 || value > 2) return fail(GEIG_ERR_ARG, "GEIG_OPT_FUSED_M_TILES must be 0, 1 or 2");
       s->tc.opt_m_tiles = (int)value;
+      return GEIG_OK;
+    case GEIG_OPT_SMALL_STEP:
+      if (value != 0 && value != 1) return fail(GEIG_ERR_ARG, "GEIG_OPT_SMALL_STEP must be 0 or 1");
+      s->opt_small = (int)value;
       return GEIG_OK;
     case GEIG_OPT_STAGED_PRODUCTS:
       if (value != 0 && value != 1) return fail(GEIG_ERR_ARG, "GEIG_OPT_STAGED_PRODUCTS must be 0 or 1");

@@ -19,7 +19,7 @@ GEIG_OK, GEIG_ERR_ARG, GEIG_ERR_CUDA, GEIG_ERR_UNSUPPORTED, GEIG_ERR_STATE = ran
 GEIG_DENSE, GEIG_CCA = 0, 1
 GEIG_MATH_F32, GEIG_MATH_BF16, GEIG_MATH_TF32, GEIG_MATH_3XTF32, GEIG_MATH_BF16X2 = 0, 1, 2, 3, 4
 GEIG_DATA_F32, GEIG_DATA_BF16 = 0, 1
-GEIG_OPT_FUSED_M_TILES, GEIG_OPT_STAGED_PRODUCTS = 1, 2
+GEIG_OPT_FUSED_M_TILES, GEIG_OPT_STAGED_PRODUCTS, GEIG_OPT_SMALL_STEP = 1, 2, 3
 
 MATH_NAMES = {"f32": GEIG_MATH_F32, "bf16": GEIG_MATH_BF16, "tf32": GEIG_MATH_TF32,
               "3xtf32": GEIG_MATH_3XTF32, "bf16x2": GEIG_MATH_BF16X2}
@@ -52,6 +52,7 @@ _SIGS = {
     "geig_update_tables": [_vp, _vp, _vp, _vp, _f64, _f64],
     "geig_step_cca": [_vp, _vp, _vp, _i64, _f64, _f64],
     "geig_step_dense": [_vp, _vp, _vp, _f64, _f64],
+    "geig_run_dense": [_vp, _vp, _vp, _i64, _f64, _f64],
     "geig_run_cca": [_vp, _vp, _vp, _i64, _i64, _f64, _f64],
     "geig_set_smooth": [_vp, _f64],
     "geig_smooth_state": [_vp, _vp, _vp],
@@ -81,7 +82,7 @@ _lib.geig_version.restype = ctypes.c_char_p
 
 EXPORTED = ["geig_create", "geig_destroy", "geig_set_stream", "geig_sync", "geig_init_state",
             "geig_set_state", "geig_get", "geig_products_cca", "geig_products_dense", "geig_update",
-            "geig_step_cca", "geig_step_dense", "geig_run_cca", "geig_step_cca_host", "geig_get_gram",
+            "geig_step_cca", "geig_step_dense", "geig_run_dense", "geig_run_cca", "geig_step_cca_host", "geig_get_gram",
             "geig_set_smooth", "geig_smooth_state", "geig_set_adam",
             "geig_launch_count", "geig_last_error", "geig_version", "geig_update_phase_ns",
             "geig_table_floats", "geig_products_cca_tables", "geig_update_tables", "geig_set_option",
@@ -216,6 +217,10 @@ def geig_run_cca(h, Xs, Ys, b: int, eta: float, gamma: float, batches=None):
 
 def geig_step_dense(h, A, B, eta: float, gamma: float):
     _check(_lib.geig_step_dense(h, _ptr(A), _ptr(B), eta, gamma))
+
+
+def geig_run_dense(h, A, B, nsteps: int, eta: float, gamma: float):
+    _check(_lib.geig_run_dense(h, _ptr(A), _ptr(B), nsteps, eta, gamma))
 
 
 def geig_step_cca_host(h, X_host, Y_host, b: int, eta: float, gamma: float, ga_host=None):
