@@ -307,12 +307,21 @@ geig_status geig_get_gram(geig_solver* s, float* GA, float* GB, float* GC);
  *                             run in one launch, state resident in shared
  *                             memory, each batch byte read once); 0 = the
  *                             staged products + update kernels
+ *  GEIG_OPT_FUSED_PAIRS     : 1 = (default) full fused steps (geig_step_cca,
+ *                             geig_run_cca; bf16 / bf16x2, views a multiple of
+ *                             256 wide) run on CTA pairs (thread-block
+ *                             clusters of 2): the two halves of each
+ *                             256-column backward tile are one pair's work and
+ *                             the backward accumulators move into the update
+ *                             through distributed shared memory instead of
+ *                             global memory; 0 = one CTA per item
  *  GEIG_OPT_STAGED_PRODUCTS : 1 = geig_products_cca runs the three-launch
  *                             staged tcgen05 products (forward GEMM, z
  *                             reshuffle, backward GEMM) instead of phases
  *                             F, S, B of the fused kernel; 0 = fused (default)
  * Errors: GEIG_ERR_ARG for an unknown option or a value out of range. */
-typedef enum { GEIG_OPT_FUSED_M_TILES = 1, GEIG_OPT_STAGED_PRODUCTS = 2, GEIG_OPT_SMALL_STEP = 3 } geig_option;
+typedef enum { GEIG_OPT_FUSED_M_TILES = 1, GEIG_OPT_STAGED_PRODUCTS = 2, GEIG_OPT_SMALL_STEP = 3,
+               GEIG_OPT_FUSED_PAIRS = 4 } geig_option;
 geig_status geig_set_option(geig_solver* s, int option, int64_t value);
 
 /* Phase durations (ns, %globaltimer of CTA 0) of the last update:

@@ -91,6 +91,13 @@ struct FusedParams {
   uint32_t bar_off;                // smem offset of the ring mbarriers (past the ring AND the update arena)
   const CUtensorMap* xmaps;        // nsteps x 6 A-operand maps in global memory (nullptr: maps.a, one step)
   int kbF[2], kbB;                 // K blocks: forward per view, backward per half
+  // CTA pairs (thread-block clusters of 2; 0 = off): the backward items of
+  // CTAs 2m, 2m + 1 are the two halves of one 256-column tile (AV, BV), and
+  // each CTA updates 128 of those columns: the backward accumulators go
+  // straight from TMEM into the update's shared-memory tiles — own columns
+  // locally, the partner's through distributed shared memory — instead of
+  // through AV / BV in global memory and the B -> U tile counters
+  int pair;
   int64_t dv[2], d, ldz, hpad;
   float scale;
   uint32_t idescF, idescB;
@@ -287,7 +294,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
       }
       umma_commit(accf_bar);
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && !(A_MN && p.pair)) {   // (CTA pairs: the backward drain is pair_exchange)
     // ---------------- epilogue warps: TMEM -> registers -> smem -> global ----------------
     // Each warp drains its 32 TMEM lanes (32 consecutive m) 16 columns (n) at
     // a time, transposes the 32 x 16 block through its 2 KB of smem and
@@ -373,6 +380,119 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
   __syncwarp();
 }
 
+// CTA pairs: after phase B, the backward accumulators of this CTA (half
+// `rank` of the pair's 256-column tile: rank 0 AV, rank 1 BV; M tile 0 =
+// the columns of rank 0, M tile 1 those of rank 1) go into the update tiles
+// [64 players][W + 4] of the CTA that owns the columns:
+//  * own columns: TMEM -> registers -> this CTA's tile (generic stores);
+//  * the partner's columns: TMEM -> a staging tile in this CTA's free ring
+//    space, then ONE bulk copy (TMA engine, shared::cta -> the partner's
+//    shared::cluster tile) that completes on the partner's tile barrier,
+//    issued once the partner has announced (remote arrive on this CTA's
+//    `freebar`) that its ring is free and its tile barrier is armed.
+// No cluster-wide barrier: each CTA waits only for its own MMAs, the
+// announcement of its partner and, in the update, its tile barrier (V'' and
+// [Bv] by TMA from global memory + the partner's pushed tile).
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ uint32_t cluster_map(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void pair_exchange(const FusedParams& p, const UpdMaps& um, uint8_t* smem,
+                                              uint64_t* accf_bar, uint64_t* acce_bar, uint64_t* tbar,
+                                              uint64_t* freebar, uint32_t tmem_base, RingState& rs, int t,
+                                              int nitemsB) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool has = (int)blockIdx.x < nitemsB;      // both CTAs of a pair have an item or neither
+  const uint32_t rank = blockIdx.x & 1u, peer = rank ^ 1u;   // cluster (2, 1, 1)
+  const int W = (int)p.upd.segw, S = W + 4;
+  float* Vt = reinterpret_cast<float*>(smem);
+  float* At = Vt + 64 * S;
+  float* Ct = At + 64 * S;
+  float* Bt = Ct + 64 * S;
+  float* stage = Bt + 64 * S;                       // the partner's columns (inside the free ring)
+  float* tile = rank == 0 ? At : Bt;                // the half this CTA computed (AV or BV)
+  const uint32_t push_bytes = (uint32_t)(p.k * S * 4);
+  if (warp >= 4 && has) {
+    mbar_wait(accf_bar, rs.items & 1);   // this CTA's MMAs are complete: its ring is free
+    __syncwarp();
+    tc_fence_after();
+    if (threadIdx.x == 128) tstamp(p.upd, 11);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // this step's tile barrier: V'' and [Bv] of the own columns (TMA) and the
+    // partner's pushed tile; then announce to the partner that it may push
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    mbar_init(tbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(tbar, (uint32_t)(2 * 64 * S * 4) + (has ? push_bytes : 0u));
+    const int c0 = (int)((int64_t)blockIdx.x * W);
+    tma_load_2d(Vt, &um.t[0], tbar, c0, 0);
+    tma_load_2d(Ct, &um.t[2], tbar, c0, 0);
+    if (has)
+      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_map(freebar, peer))
+                   : "memory");
+  }
+  if (warp >= 4 && has) {
+    const int ew = warp - 4;
+    const int acols = p.BN * (p.splitB ? 2 : 1);
+    const int m = ew * 32 + lane;                   // this thread's column within the M tile (TMEM lane)
+    for (int mtile = 0; mtile < 2; ++mtile) {
+      float* dst = ((uint32_t)mtile == rank ? tile : stage) + m;
+      const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(mtile * acols);
+      for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        uint32_t r0[16], r1[16], l0[16], l1[16];
+        tmem_ld16_nw(tb + (uint32_t)c0, r0);
+        tmem_ld16_nw(tb + (uint32_t)(c0 + 16), r1);
+        if (p.splitB) {
+          tmem_ld16_nw(tb + (uint32_t)(p.BN + c0), l0);
+          tmem_ld16_nw(tb + (uint32_t)(p.BN + c0 + 16), l1);
+        }
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        // lanes = 32 consecutive columns: each store is one 128-byte row segment
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int n0 = c0 + j, n1 = c0 + 16 + j;
+          const float a0 = p.splitB ? __uint_as_float(r0[j]) + __uint_as_float(l0[j]) : __uint_as_float(r0[j]);
+          const float a1 = p.splitB ? __uint_as_float(r1[j]) + __uint_as_float(l1[j]) : __uint_as_float(r1[j]);
+          if (n0 < p.k) dst[n0 * S] = p.scale * a0;
+          if (n1 < p.k) dst[n1 * S] = p.scale * a1;
+        }
+      }
+    }
+    tc_fence_before();
+    mbar_arrive(acce_bar);
+    ++rs.items;
+    // the staged tile is read by the bulk copy (async proxy)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 3, 128;" ::: "memory");
+    if (threadIdx.x == 128) {
+      tstamp(p.upd, 17);
+      mbar_wait(freebar, (uint32_t)(t & 1));        // the partner's ring is free, its tile barrier armed
+      asm volatile(
+          "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              cluster_map(tile, peer)),
+          "r"(smem_u32(stage)), "r"(push_bytes), "r"(cluster_map(tbar, peer))
+          : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      // without early coefficients the update stages its tables right after
+      // the four tiles, i.e. over the staging tile: the push must have read it
+      if (!p.early_coef) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+  }
+  __syncthreads();                                   // the own-column tile (generic stores) is complete
+}
+
 template <int EB, bool ADAM>
 __global__ void __launch_bounds__(FS_THREADS, 1)
 cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
@@ -390,6 +510,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   uint64_t* acce_bar = accf_bar + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce_bar + 1);
   float* side_scratch = reinterpret_cast<float*>(acce_bar + 3);   // 64 floats for warps 2-3
+  uint64_t* freebar = reinterpret_cast<uint64_t*>(side_scratch + 64);   // CTA pairs: "the partner's ring is free"
   float* epi_stage = reinterpret_cast<float*>(smem + p.bar_off + 512);   // 4 x 2 KB epilogue transpose tiles
   float* coef_smem = epi_stage + 4 * 16 * 32;                              // early coefficients (GEIG_COEF_FLOATS)
   const int warp = threadIdx.x >> 5;
@@ -402,6 +523,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     }
     mbar_init(accf_bar, 1);
     mbar_init(acce_bar, 128);
+    if (p.pair) mbar_init(freebar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int v = 0; v < 2; ++v) tma_prefetch_desc(&maps.bF[v]);
   }
@@ -686,7 +808,25 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     p.upd.dbg[(size_t)blockIdx.x * 64 + 18] = *(volatile unsigned long long*)&p.upd.dbg[(size_t)blockIdx.x * 64 + 17];
     __threadfence(); dstamp(p.upd, 15);
   }
-  if (p.bcnt && !p.products_only) {
+  if (p.pair) {
+    // the update needs the Gram reduction of every CTA (coefficients) and the
+    // backward accumulators of the pair (exchanged through DSMEM)
+    if (threadIdx.x == 0 && p.rcnt) spin_geq_trap(p.rcnt, (t + 1) * (int)gridDim.x);
+    pair_exchange(p, maps.um, smem, accf_bar, acce_bar, acce_bar + 2, freebar, tmem_base, rs, t,
+                  2 * (p.mtB[0] + p.mtB[1]));
+    if (kDevKnobs && (p.dbg_mode & 16384)) {   // developer: the exchanged tiles to AV / BV (global)
+      mbar_wait(acce_bar + 2, 0);
+      const int W = (int)p.upd.segw, S = W + 4;
+      const float* At = reinterpret_cast<const float*>(smem) + 64 * S;
+      const float* Bt = At + 2 * 64 * S;
+      const int64_t c0 = (int64_t)blockIdx.x * W;
+      for (int e = threadIdx.x; e < p.k * W; e += FS_THREADS) {
+        const int i = e / W, c = e - i * W;
+        if (c0 + c < p.d) { p.AV[i * p.d + c0 + c] = At[i * S + c]; p.BV[i * p.d + c0 + c] = Bt[i * S + c]; }
+      }
+      __syncthreads();
+    }
+  } else if (p.bcnt && !p.products_only) {
     // the update phase of this CTA needs the Gram reduction of every CTA and
     // the backward items of its own columns [c W, (c + 1) W) only
     if (threadIdx.x == 0) {
@@ -718,6 +858,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     update_res_phases<true, 1, ADAM>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um, t,
                                      p.early_coef ? coef_smem : nullptr,
                                      dev_tbar_in_ring(p) ? nullptr : acce_bar + 2);
+  if (p.pair && threadIdx.x == 128) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging reusable
   if (t + 1 < p.nsteps) {
     // next step: its forward TMA reads the new bf16 shadow of V (generic
     // stores above) and refills the smem ring the update phase used
@@ -764,16 +905,22 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
 // launch only (no stream attribute is changed, so the caller's later kernels
 // on the same stream do not inherit it).
 inline cudaError_t launch_coop(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st,
-                               const cudaAccessPolicyWindow& win) {
+                               const cudaAccessPolicyWindow& win, int cluster = 0) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   int n = 0;
   attr[n].id = cudaLaunchAttributeCooperative;
   attr[n++].val.cooperative = 1;
+  if (cluster > 1) {   // thread-block clusters (CTA pairs of the fused step)
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = (unsigned)cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n++].val.clusterDim.z = 1;
+  }
   if (win.num_bytes > 0) {
     attr[n].id = cudaLaunchAttributeAccessPolicyWindow;
     attr[n++].val.accessPolicyWindow = win;
@@ -818,7 +965,8 @@ struct OwnedCfg {
 inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* const* Y, int nsteps, int64_t b,
                                   float scale, const __nv_bfloat16* Vbf, float* AV, float* BV, UpdateArgs upd,
                                   int grid_ctas, size_t upd_bytes, cudaStream_t st, bool products_only = false,
-                                  bool tables = false, bool update_only = false, const OwnedCfg* own = nullptr) {
+                                  bool tables = false, bool update_only = false, const OwnedCfg* own = nullptr,
+                                  int pair_grid = 0) {
   if (!t.ready || t.math != GEIG_MATH_BF16) return tc_fail(GEIG_ERR_STATE, "fused step needs the bf16 plan");
   if (nsteps < 1) return tc_fail(GEIG_ERR_ARG, "nsteps < 1");
   // (t.math is BF16 for both GEIG_MATH_BF16 and GEIG_MATH_BF16X2; t.splitb selects hi+lo operands)
@@ -828,6 +976,19 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   FusedMaps maps;
   FusedParams p{};
   if (update_only && (products_only || nsteps != 1)) return tc_fail(GEIG_ERR_ARG, "update-only launch: one step");
+  // CTA pairs (full steps): every 256-column backward tile of both views is
+  // one pair's item and each CTA of the pair updates 128 of its columns
+  // (the update then covers d / 128 CTAs: used where that is most of the grid)
+  const int64_t pair_ctas = (t.dx + t.dy) / 128;
+  const bool pair = pair_grid > 0 && t.opt_pairs && !products_only && !update_only && !own && t.dx % 256 == 0 &&
+                    t.dy % 256 == 0 && pair_ctas <= pair_grid && 4 * pair_ctas >= 3 * (int64_t)pair_grid &&
+                    (pair_grid & 1) == 0 && t.opt_m_tiles != 1 && 128 <= UPD_RES_WMAX;
+  if (pair) {
+    grid_ctas = pair_grid;
+    upd.segw = 128;
+    upd.pair_tiles = 1;
+    upd_bytes = upd_res_smem_floats(128) * 4;
+  }
   if (!update_only && !make_batch_maps(maps.a, t, X[0], Y[0], h))
     return tc_fail(GEIG_ERR_CUDA, "tensor map encode (batch) failed");
   p.nsteps = nsteps;
@@ -858,7 +1019,7 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
     }
     if (!dev_knob("GEIG_F_BARRIER")) p.fcnt = t.dep + 32;   // GEIG_F_BARRIER: developer A/B (grid barrier after F)
     p.btiles = btiles;
-    if (!products_only && !dev_knob("GEIG_BU_BARRIER")) p.bcnt = t.dep + 32 + ntiles;   // (grid barrier after B)
+    if (!products_only && !pair && !dev_knob("GEIG_BU_BARRIER")) p.bcnt = t.dep + 32 + ntiles;   // (grid barrier after B)
   }
   if (products_only && nsteps != 1) return tc_fail(GEIG_ERR_ARG, "products-only launch runs one step");
   p.xmaps = nullptr;
@@ -973,6 +1134,11 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.splitB = t.splitb;   // bf16x2: the backward B operand (z) as hi + lo too
   p.idescB = make_idesc(eb, true, t.BN * (p.splitB ? 2 : 1), TC_BM);
   p.bwd_y_first = dev_knob("GEIG_BWD_X_FIRST") ? 0 : 1;
+  p.pair = pair ? 1 : 0;
+  if (pair) {
+    p.bwd_y_first = 0;   // CTA c <-> columns [128 c, 128 c + 128)
+    if (p.tmB != 2) return tc_fail(GEIG_ERR_STATE, "CTA pairs need 2 M tiles per backward item");
+  }
   p.l2_keep = dev_knob("GEIG_L2_KEEP") ? 1 : 0;   // measured: evict-last on a whole view thrashes the state arrays (slower)
   p.dbg_nostore = dev_knob("GEIG_DBG_NOSTORE") ? 1 : 0;   // developer: drop GEMM epilogue stores (timing only)
   p.dbg_mode = dev_knob("GEIG_DBG_MODE") ? atoi(dev_knob("GEIG_DBG_MODE")) : 0;   // developer timing knobs (wrong results)
@@ -981,7 +1147,9 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
     return tc_fail(GEIG_ERR_UNSUPPORTED, "fused step: accumulators exceed the TMEM allocation");
   p.stages = (int)std::min<size_t>(TC_MAX_STAGES, (200 * 1024) / stage_bytes);
   p.bar_off = (uint32_t)((std::max((size_t)p.stages * stage_bytes, upd_bytes) + 15) & ~(size_t)15);
-  static_assert((2 * TC_MAX_STAGES + 4) * 8 + 64 * 4 <= 512, "barrier + scratch area");
+  if (pair && (size_t)5 * 64 * (128 + 4) * 4 > p.bar_off)   // 4 update tiles + the staging tile
+    return tc_fail(GEIG_ERR_STATE, "CTA pairs: the staging tile does not fit below the barrier region");
+  static_assert((2 * TC_MAX_STAGES + 4) * 8 + 64 * 4 + 8 <= 512, "barrier + scratch area + freebar");
   size_t smem = 1024 + p.bar_off + 512 + 4 * 16 * 32 * 4;
   if (smem > 227 * 1024) return tc_fail(GEIG_ERR_UNSUPPORTED, "fused step: shared memory budget exceeded");
   if (p.early_coef) {   // the coefficient region follows the epilogue tiles when it fits
@@ -994,7 +1162,7 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
     return tc_fail(GEIG_ERR_CUDA, "cudaFuncSetAttribute(cca_step_kernel) failed");
   void* args[] = {(void*)&maps, (void*)&p};
   void* kfn = p.upd.adam ? (void*)cca_step_kernel<2, true> : (void*)cca_step_kernel<2, false>;
-  cudaError_t e = launch_coop(kfn, dim3(grid_ctas), dim3(FS_THREADS), args, smem, st, t.l2win);
+  cudaError_t e = launch_coop(kfn, dim3(grid_ctas), dim3(FS_THREADS), args, smem, st, t.l2win, pair ? 2 : 0);
   if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("cca_step_kernel launch: ") + cudaGetErrorString(e));
 
   return GEIG_OK;

@@ -192,7 +192,8 @@ extern "C" geig_status geig_create(geig_solver** out, int problem, int64_t dx, i
         return cleanup(fail(GEIG_ERR_CUDA, "update kernel cannot be co-resident"));
     }
     const size_t pfl = res ? (size_t)upd_raw_floats_res(k) : upd_partial_floats(NB);
-    if (cudaMalloc((void**)&s->partial, (size_t)G * pfl * 4) != cudaSuccess ||
+    // one partial row per CTA of any grid the fused step launches (<= #SM)
+    if (cudaMalloc((void**)&s->partial, (size_t)std::max<int64_t>(G, s->nsm) * pfl * 4) != cudaSuccess ||
         cudaMalloc((void**)&s->raw, pfl * 4) != cudaSuccess)
       return cleanup(fail(GEIG_ERR_CUDA, "cudaMalloc gram partials"));
   }
@@ -686,7 +687,8 @@ extern "C" geig_status geig_step_cca(geig_solver* s, const void* X, const void* 
     CU(cudaSetDevice(s->device));
     const UpdateArgs a = update_args(s, eta, gamma);
     geig_status st = tc::fused_cca_step(s->tc, &X, &Y, 1, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV, a,
-                                        s->upd_grid, s->upd_smem, s->stream);
+                                        s->upd_grid, s->upd_smem, s->stream, false, false, false, nullptr,
+                                        s->nsm & ~1);
     if (st) return fail(st, "%s", tc::last_error());
     s->launches++;
     s->fused_last = true;
@@ -734,7 +736,8 @@ extern "C" geig_status geig_run_cca(geig_solver* s, const void* const* X, const 
   for (int64_t i0 = 0; i0 < nsteps; i0 += tc::TC_RUN_CHUNK) {
     const int n = (int)std::min<int64_t>(tc::TC_RUN_CHUNK, nsteps - i0);
     geig_status st = tc::fused_cca_step(s->tc, X + i0, Y + i0, n, b, 1.0f / (float)(b / 2), s->Vbf, s->AV, s->BV,
-                                        update_args(s, eta, gamma), s->upd_grid, s->upd_smem, s->stream);
+                                        update_args(s, eta, gamma), s->upd_grid, s->upd_smem, s->stream, false,
+                                        false, false, nullptr, s->nsm & ~1);
     if (st) return fail(st, "%s", tc::last_error());
     s->launches++;
     advance_variant_state(s, n);
@@ -943,6 +946,10 @@ extern "C" geig_status geig_set_option(geig_solver* s, int option, int64_t value
       if (value < 0 || value > 2) return fail(GEIG_ERR_ARG, "GEIG_OPT_FUSED_M_TILES must be 0, 1 or 2");
       s->tc.opt_m_tiles = (int)value;
       return GEIG_OK;
+    case GEIG_OPT_FUSED_PAIRS:
+      if (value != 0 && value != 1) return fail(GEIG_ERR_ARG, "GEIG_OPT_FUSED_PAIRS must be 0 or 1");
+      s->tc.opt_pairs = (int)value;
+      return GEIG_OK;
     case GEIG_OPT_SMALL_STEP:
       if (value != 0 && value != 1) return fail(GEIG_ERR_ARG, "GEIG_OPT_SMALL_STEP must be 0 or 1");
       s->opt_small = (int)value;
@@ -972,3 +979,10 @@ extern "C" geig_status geig_update_phase_ns(geig_solver* s, int64_t* out) {
 // of the tensor-core product kernels are written to `buf` (4 x uint64 per CTA,
 // launch after launch overwrite), NULL disables.
 extern "C" void geig_debug_set_tc_stamps(void* buf) { tc::dbg_ptr() = (unsigned long long*)buf; }
+
+// Developer hook (not part of the documented ABI): device pointers of the
+// solver's internal AV / BV scratch (k x d fp32 each).
+extern "C" void geig_debug_products(geig_solver* s, float** av, float** bv) {
+  if (av) *av = s ? s->AV : nullptr;
+  if (bv) *bv = s ? s->BV : nullptr;
+}

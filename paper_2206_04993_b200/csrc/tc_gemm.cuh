@@ -507,6 +507,7 @@ struct TcPlan {
   int* dep = nullptr;               // fused step: Gram-reduction counter (monotonic, zeroed once)
   int x3 = 0;                       // 3xTF32 products (tf32 plan with hi/lo operands)
   int opt_m_tiles = 0;              // geig_set_option(GEIG_OPT_FUSED_M_TILES): 0 = auto, 1 or 2
+  int opt_pairs = 1;                // geig_set_option(GEIG_OPT_FUSED_PAIRS): CTA pairs in the fused step
   cudaAccessPolicyWindow l2win{};   // persisting-L2 window over the solver's state arena (num_bytes 0: none)
   float* Vx3 = nullptr;             // 3xTF32: [hi plane | lo plane] of V (2 x k x d fp32)
 };

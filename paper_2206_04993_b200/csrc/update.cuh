@@ -84,6 +84,7 @@ struct UpdateArgs {
   float lnrho, lnnu;
   // Adam ascent on v_i (Appendix H): moments am, as (k x d);
   // step t of a launch uses bias corrections of the global count adam_t0 + t + 1
+  int pair_tiles;          // fused CTA pairs: AV, BV tiles already in smem, V'' / [Bv] staged on the tile barrier
   int adam;
   float* am;
   float* as;
@@ -850,6 +851,10 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
     cp_async_commit();
   }
   if (um) {
+    if (p.pair_tiles) {
+      // fused CTA pairs: AV, BV tiles written by pair_exchange, V'' and [Bv]
+      // in flight on the tile barrier (waited below)
+    } else {
     if (tid == 0) {
       asm volatile("fence.proxy.async.global;" ::: "memory");   // state / products written by generic stores
       tc::mbar_init(tbar, 1);
@@ -866,6 +871,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
     // pre-reduced tables (fused step): the coefficients do not read the
     // tiles, so their staging overlaps the coefficient phase (wait below)
     if (!(PRE == 1 || (PRE < 0 && p.pre_reduced))) tc::mbar_wait(tbar, 0);
+    }
   } else {
     auto stage = [&](float* dst, const float* src) {
       if (VEC) {

@@ -558,6 +558,9 @@ def test_products_tables_single_shard_equals_fused_step(geig, variant):
         s = geig.Solver(geig.GEIG_CCA, cfg.dx, cfg.dy, cfg.k, math="bf16x2", data_dtype=geig.GEIG_DATA_BF16,
                         rho=cfg.rho, max_rows=rows)
         try:
+            # one CTA per item: the tables path's column partition (CTA pairs
+            # re-partition the update's columns: test_fused_pairs_match_single_ctas)
+            geig.geig_set_option(s.h, geig.GEIG_OPT_FUSED_PAIRS, 0)
             s.set_state(torch.tensor(V, dtype=torch.float32, device=dev),
                         torch.tensor(aux, dtype=torch.float32, device=dev))
             if variant == "alg3":
@@ -682,3 +685,44 @@ def test_run_cca_large_batch_long_run_is_deterministic(geig):
             s.close()
     assert all(torch.isfinite(t_).all() for t_ in out[0] + out[1])
     assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("variant", ["alg2", "alg3", "adam", "run"])
+def test_fused_pairs_match_single_ctas(geig, variant):
+    """The fused step on CTA pairs (thread-block clusters of 2: backward
+    accumulators exchanged through distributed shared memory into the
+    update's tiles, 128 update columns per CTA) against one CTA per item
+    (AV, BV through global memory, 112 columns per CTA) over 3 steps at
+    config 3: the same arithmetic up to the order of the Gram partial sums."""
+    from synth import CONFIGS, cca_views
+    cfg = CONFIGS[3]
+    rows = 4096
+    x, y = cca_views(cfg, 2 * rows, seed=17)
+    V, aux = random_state(cfg.k, cfg.d, 12)
+    dev = "cuda:0"
+    xs = [x[:rows].to(dev), x[rows:].to(dev), x[:rows].to(dev)]
+    ys = [y[:rows].to(dev), y[rows:].to(dev), y[:rows].to(dev)]
+    eta = 0.02
+    out = []
+    for pairs in (1, 0):
+        s = geig.Solver(geig.GEIG_CCA, cfg.dx, cfg.dy, cfg.k, math="bf16x2", data_dtype=geig.GEIG_DATA_BF16,
+                        rho=cfg.rho, max_rows=rows)
+        try:
+            geig.geig_set_option(s.h, geig.GEIG_OPT_FUSED_PAIRS, pairs)
+            s.set_state(torch.tensor(V, dtype=torch.float32, device=dev),
+                        torch.tensor(aux, dtype=torch.float32, device=dev))
+            if variant == "alg3":
+                geig.geig_set_smooth(s.h, 10.0)
+            if variant == "adam":
+                geig.geig_set_adam(s.h, 0.9, 0.999, 1e-8)
+            if variant == "run":
+                geig.geig_run_cca(s.h, xs, ys, rows, eta, cfg.gamma)
+            else:
+                for t in range(3):
+                    geig.geig_step_cca(s.h, xs[t], ys[t], rows, eta, cfg.gamma)
+            out.append([t.double().cpu().numpy() for t in s.state()])
+        finally:
+            s.close()
+    (Vp, ap), (Vs, as_) = out
+    step, aux_e = rel_err(Vp - V, Vs - V), rel_err(ap, as_)
+    assert step < 1e-5 and aux_e < 1e-5, (step, aux_e)
