@@ -428,10 +428,13 @@ __device__ __forceinline__ void pair_exchange(const FusedParams& p, const UpdMap
     if (threadIdx.x == 128) tstamp(p.upd, 11);
   }
   __syncthreads();
+  if (threadIdx.x == 128) tstamp(p.upd, 15);
   if (threadIdx.x == 0) {
     // this step's tile barrier: V'' and [Bv] of the own columns (TMA) and the
-    // partner's pushed tile; then announce to the partner that it may push
-    asm volatile("fence.proxy.async.global;" ::: "memory");
+    // partner's pushed tile; then announce to the partner that it may push.
+    // (V'' and [Bv] were last written by the previous step's update with
+    // generic stores: ordered for the async proxy by this thread's
+    // fence.proxy.async.global at the start of this step's phase F)
     mbar_init(tbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -442,12 +445,18 @@ __device__ __forceinline__ void pair_exchange(const FusedParams& p, const UpdMap
     if (has)
       asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_map(freebar, peer))
                    : "memory");
+    tstamp(p.upd, 16);
   }
-  if (warp >= 4 && has) {
-    const int ew = warp - 4;
+  if (has) {
+    // all 8 warps drain: warps 0-3 M tile 0, warps 4-7 M tile 1 (a warp
+    // reaches TMEM lanes 32 (warp % 4) .. + 31)
+    __syncwarp();                                   // (thread 0 ran the tile-barrier block alone)
+    if (warp < 4) tc_fence_after();
+    const int ew = warp & 3;
     const int acols = p.BN * (p.splitB ? 2 : 1);
     const int m = ew * 32 + lane;                   // this thread's column within the M tile (TMEM lane)
-    for (int mtile = 0; mtile < 2; ++mtile) {
+    {
+      const int mtile = warp >> 2;
       float* dst = ((uint32_t)mtile == rank ? tile : stage) + m;
       const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(mtile * acols);
       for (int c0 = 0; c0 < p.BN; c0 += 32) {
@@ -470,12 +479,15 @@ __device__ __forceinline__ void pair_exchange(const FusedParams& p, const UpdMap
         }
       }
     }
+    if (threadIdx.x == 128) tstamp(p.upd, 18);
     tc_fence_before();
-    mbar_arrive(acce_bar);
-    ++rs.items;
+    if (warp >= 4) {
+      mbar_arrive(acce_bar);
+      ++rs.items;
+    }
     // the staged tile is read by the bulk copy (async proxy)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("bar.sync 3, 128;" ::: "memory");
+    asm volatile("bar.sync 3, 256;" ::: "memory");
     if (threadIdx.x == 128) {
       tstamp(p.upd, 17);
       mbar_wait(freebar, (uint32_t)(t & 1));        // the partner's ring is free, its tile barrier armed

@@ -20,7 +20,7 @@ lib = geig._lib
 lib.geig_debug_set_tc_stamps.argtypes = [ctypes.c_void_p]
 names = {0: "launch", 1: "setup", 2: "F done", 3: "F sync", 4: "S done", 5: "S sync", 6: "B done", 7: "B sync",
          8: "U staged", 9: "F accf", 10: "B coef end", 11: "B accf", 12: "B red all", 13: "U coef", 14: "U update",
-         15: "B fence0", 16: "B epi fence", 17: "B epi end", 19: "coef raw", 20: "coef N", 21: "U tiles", 22: "U penalty", 23: "S zinit", 24: "S zsum", 25: "S gram", 26: "S tri", 27: "B red own", 28: "Uc pst", 29: "F mma end", 30: "F epi end", 31: "F side end"}
+         15: "B fence0", 16: "B epi fence", 17: "B epi end", 18: "pair drained", 19: "coef raw", 20: "coef N", 21: "U tiles", 22: "U penalty", 23: "S zinit", 24: "S zsum", 25: "S gram", 26: "S tri", 27: "B red own", 28: "Uc pst", 29: "F mma end", 30: "F epi end", 31: "F side end"}
 for it in range(50):
     geig.geig_step_cca(s.h, X[:b], Y[:b], b, cfg.eta, cfg.gamma)
 torch.cuda.synchronize()
