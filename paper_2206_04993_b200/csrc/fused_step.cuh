@@ -54,6 +54,28 @@ __device__ __forceinline__ void spin_geq_trap(const int* c, int target) {
   } while (v - target < 0);
 }
 
+// Grid barrier of the CTA-pair launches, which are NOT cooperative launches
+// (the profiler cannot replay a cooperative launch with thread-block
+// clusters; co-residency of the grid is checked on the host with
+// cudaOccupancyMaxActiveClusters instead): the cooperative-groups algorithm —
+// CTA 0 adds 2^31 - (n - 1), every other CTA 1, so the counter's top bit
+// flips exactly once per barrier and the counter never needs a reset.
+__device__ __forceinline__ void grid_bar(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned n = gridDim.x;
+    const unsigned add = blockIdx.x == 0 ? 0x80000000u - (n - 1) : 1u;
+    unsigned old, cur;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(add) : "memory");
+    long long polls = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+      if (++polls > (1ll << 26)) __trap();   // a CTA that never arrives: fail instead of hanging
+    } while (((old ^ cur) & 0x80000000u) == 0);
+  }
+  __syncthreads();
+}
+
 struct FusedParams {
   int rows, h, k, BN, stages, splitsF, mtF, mtB[2], split, bwd_y_first, dbg_nostore, dbg_mode, l2_keep;
   // Dependency counters (zero at launch start; CTA 0 zeroes them again after
@@ -98,6 +120,7 @@ struct FusedParams {
   // locally, the partner's through distributed shared memory — instead of
   // through AV / BV in global memory and the B -> U tile counters
   int pair;
+  unsigned* gbar;                  // non-null: grid barriers by grid_bar (non-cooperative cluster launch)
   int64_t dv[2], d, ldz, hpad;
   float scale;
   uint32_t idescF, idescB;
@@ -509,6 +532,9 @@ template <int EB, bool ADAM>
 __global__ void __launch_bounds__(FS_THREADS, 1)
 cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   cg::grid_group grid = cg::this_grid();
+  auto gsync = [&]() {
+    if (p.gbar) grid_bar(p.gbar); else grid.sync();
+  };
   dstamp(p.upd, 0);
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned view of the dynamic smem that stays in the shared
@@ -596,7 +622,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     }
     __syncthreads();
   } else {
-    grid.sync();
+    gsync();
   }
   stamp(p.upd, 5);
   dstamp(p.upd, 3);
@@ -766,7 +792,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   }
   __syncthreads();
   dstamp(p.upd, 4);
-  grid.sync();
+  gsync();
   stamp(p.upd, 6);
   dstamp(p.upd, 5);
 
@@ -856,7 +882,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     }
     __syncthreads();
   } else {
-    grid.sync();
+    gsync();
   }
   stamp(p.upd, 7);
   dstamp(p.upd, 7);
@@ -877,14 +903,14 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     asm volatile("fence.proxy.async.global;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
-    grid.sync();
+    gsync();
     tc_fence_after();
   }
   }  // steps
 
   if (p.rcnt || p.fcnt || p.bcnt) {
     // every CTA is past its last counter read: back to zero for the next launch
-    grid.sync();
+    gsync();
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       if (p.rcnt) *p.rcnt = 0;
       if (p.fcnt)
@@ -917,7 +943,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
 // launch only (no stream attribute is changed, so the caller's later kernels
 // on the same stream do not inherit it).
 inline cudaError_t launch_coop(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st,
-                               const cudaAccessPolicyWindow& win, int cluster = 0) {
+                               const cudaAccessPolicyWindow& win, int cluster = 0, bool coop = true) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -925,8 +951,10 @@ inline cudaError_t launch_coop(const void* fn, dim3 grid, dim3 block, void** arg
   cfg.stream = st;
   cudaLaunchAttribute attr[3];
   int n = 0;
-  attr[n].id = cudaLaunchAttributeCooperative;
-  attr[n++].val.cooperative = 1;
+  if (coop) {
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n++].val.cooperative = 1;
+  }
   if (cluster > 1) {   // thread-block clusters (CTA pairs of the fused step)
     attr[n].id = cudaLaunchAttributeClusterDimension;
     attr[n].val.clusterDim.x = (unsigned)cluster;
@@ -1018,8 +1046,9 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   if (!update_only) {
     const int ntiles = (int)((t.max_rows + TC_BM - 1) / TC_BM);
     const int btiles = (int)((std::max(t.dx, t.dy) + TC_BM - 1) / TC_BM);
-    if (!t.dep) {   // [rcnt | pad | fcnt per 128-row tile | bcnt per view x 128-column tile], zero between launches
-      const size_t words = 32 + (size_t)ntiles + 2 * (size_t)btiles;
+    if (!t.dep) {   // [rcnt | pad][grid barrier | pad][fcnt per 128-row tile | bcnt per view x 128-column tile]
+                    // (128-byte lines; the counts are zero between launches, the barrier word persists)
+      const size_t words = 64 + (size_t)ntiles + 2 * (size_t)btiles;
       if (cudaMalloc((void**)&t.dep, words * sizeof(int)) != cudaSuccess ||
           cudaMemsetAsync(t.dep, 0, words * sizeof(int), st) != cudaSuccess)
         return tc_fail(GEIG_ERR_CUDA, "allocating the dependency counters failed");
@@ -1029,9 +1058,9 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
       p.rcnt = t.dep;
       p.early_coef = products_only ? 0 : 1;
     }
-    if (!dev_knob("GEIG_F_BARRIER")) p.fcnt = t.dep + 32;   // GEIG_F_BARRIER: developer A/B (grid barrier after F)
+    if (!dev_knob("GEIG_F_BARRIER")) p.fcnt = t.dep + 64;   // GEIG_F_BARRIER: developer A/B (grid barrier after F)
     p.btiles = btiles;
-    if (!products_only && !pair && !dev_knob("GEIG_BU_BARRIER")) p.bcnt = t.dep + 32 + ntiles;   // (grid barrier after B)
+    if (!products_only && !pair && !dev_knob("GEIG_BU_BARRIER")) p.bcnt = t.dep + 64 + ntiles;   // (grid barrier after B)
   }
   if (products_only && nsteps != 1) return tc_fail(GEIG_ERR_ARG, "products-only launch runs one step");
   p.xmaps = nullptr;
@@ -1147,6 +1176,11 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.idescB = make_idesc(eb, true, t.BN * (p.splitB ? 2 : 1), TC_BM);
   p.bwd_y_first = dev_knob("GEIG_BWD_X_FIRST") ? 0 : 1;
   p.pair = pair ? 1 : 0;
+  // GEIG_OPT_FUSED_PAIRS 1: non-cooperative cluster launch, grid barriers by
+  // grid_bar (the profiler can replay it); 2: cooperative cluster launch
+  // (grid.sync of cooperative groups)
+  const bool pair_coop = pair && t.opt_pairs == 2;
+  p.gbar = (pair && !pair_coop) ? reinterpret_cast<unsigned*>(t.dep + 32) : nullptr;   // own 128-byte line; never reset
   if (pair) {
     p.bwd_y_first = 0;   // CTA c <-> columns [128 c, 128 c + 128)
     if (p.tmB != 2) return tc_fail(GEIG_ERR_STATE, "CTA pairs need 2 M tiles per backward item");
@@ -1174,7 +1208,23 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
     return tc_fail(GEIG_ERR_CUDA, "cudaFuncSetAttribute(cca_step_kernel) failed");
   void* args[] = {(void*)&maps, (void*)&p};
   void* kfn = p.upd.adam ? (void*)cca_step_kernel<2, true> : (void*)cca_step_kernel<2, false>;
-  cudaError_t e = launch_coop(kfn, dim3(grid_ctas), dim3(FS_THREADS), args, smem, st, t.l2win, pair ? 2 : 0);
+  if (pair && !pair_coop) {
+    // the pair launch is not cooperative: every CTA pair of the grid must be
+    // co-resident (one CTA per SM) for its grid barriers
+    int ncl = 0;
+    cudaLaunchConfig_t oc = {};
+    oc.gridDim = dim3(grid_ctas);
+    oc.blockDim = dim3(FS_THREADS);
+    oc.dynamicSmemBytes = smem;
+    cudaLaunchAttribute ca;
+    ca.id = cudaLaunchAttributeClusterDimension;
+    ca.val.clusterDim.x = 2; ca.val.clusterDim.y = 1; ca.val.clusterDim.z = 1;
+    oc.attrs = &ca;
+    oc.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&ncl, kfn, &oc) != cudaSuccess || 2 * ncl < grid_ctas)
+      return tc_fail(GEIG_ERR_UNSUPPORTED, "CTA pairs: the grid's clusters are not co-resident");
+  }
+  cudaError_t e = launch_coop(kfn, dim3(grid_ctas), dim3(FS_THREADS), args, smem, st, t.l2win, pair ? 2 : 0, !pair || pair_coop);
   if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("cca_step_kernel launch: ") + cudaGetErrorString(e));
 
   return GEIG_OK;

@@ -947,7 +947,7 @@ extern "C" geig_status geig_set_option(geig_solver* s, int option, int64_t value
       s->tc.opt_m_tiles = (int)value;
       return GEIG_OK;
     case GEIG_OPT_FUSED_PAIRS:
-      if (value != 0 && value != 1) return fail(GEIG_ERR_ARG, "GEIG_OPT_FUSED_PAIRS must be 0 or 1");
+      if (value < 0 || value > 2) return fail(GEIG_ERR_ARG, "GEIG_OPT_FUSED_PAIRS must be 0, 1 or 2");
       s->tc.opt_pairs = (int)value;
       return GEIG_OK;
     case GEIG_OPT_SMALL_STEP:

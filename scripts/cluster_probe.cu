@@ -4,10 +4,29 @@
 // does a DSMEM store into the peer CTA's smem land.
 #include <cooperative_groups.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 namespace cg = cooperative_groups;
 
-__global__ void probe(int* out, int iters) {
+// grid barrier without a cooperative launch (the cooperative-groups
+// algorithm: block 0 adds 2^31 - (n - 1), the others 1, so the top bit of
+// the counter flips once per barrier); needs all CTAs co-resident
+__device__ __forceinline__ void grid_bar(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned n = gridDim.x;
+    const unsigned add = blockIdx.x == 0 ? 0x80000000u - (n - 1) : 1u;
+    __threadfence();
+    const unsigned old = atomicAdd(bar, add);
+    unsigned cur;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+    } while (((old ^ cur) & 0x80000000u) == 0);
+  }
+  __syncthreads();
+}
+
+__global__ void probe(int* out, int iters, unsigned* gbar, int coop) {
   extern __shared__ int sm[];
   cg::grid_group grid = cg::this_grid();
   cg::cluster_group cl = cg::this_cluster();
@@ -20,12 +39,14 @@ __global__ void probe(int* out, int iters) {
     cl.sync();
     const int expect = (int)((blockIdx.x ^ 1) * 1000 + threadIdx.x + it);
     if (sm[threadIdx.x] != expect) atomicAdd(out, 1);
-    grid.sync();
+    if (coop) grid.sync(); else grid_bar(gbar);
   }
   if (threadIdx.x == 0) atomicAdd(out + 1, 1);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const int force_ctas = argc > 1 ? atoi(argv[1]) : 0;   // cap the cooperative grid (e.g. under a profiler)
+  int coop = argc > 2 ? atoi(argv[2]) : 1;                  // 0: no cooperative attribute, hand-rolled grid barrier
   int dev = 0, nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = 227 * 1024;
@@ -49,12 +70,14 @@ int main() {
            ncl * csz, nsm);
     if (ncl <= 0) continue;
     int* out;
-    cudaMalloc(&out, 8);
-    cudaMemset(out, 0, 8);
+    cudaMalloc(&out, 16);
+    cudaMemset(out, 0, 16);
+    unsigned* gbar = reinterpret_cast<unsigned*>(out + 2);
+    if (force_ctas > 0 && force_ctas / csz < ncl) ncl = force_ctas / csz;
     cfg.gridDim = dim3(ncl * csz);
-    cfg.numAttrs = 2;
+    cfg.numAttrs = coop ? 2 : 1;
     int iters = 100;
-    void* args[] = {&out, &iters};
+    void* args[] = {&out, &iters, &gbar, &coop};
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
     cudaEventRecord(a);
