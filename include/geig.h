@@ -210,6 +210,51 @@ geig_status geig_products_cca_owned(geig_solver* s, const void* X, const void* Y
 geig_status geig_update_owned(geig_solver* s, const float* chunk, double eta,
                               double gamma);
 
+/* Peer-memory form of the column-owned step (one process per GPU over
+ * NVLink peer memory; Appendix F, with the reduce-scatter and
+ * the all-gather folded into the kernels): instead of NCCL collectives,
+ *  - the products launch stores every column's AV | BV and the rank's table
+ *    row straight into the OWNER's receive buffer (slot = this rank) from
+ *    the backward epilogue, and then raises this rank's receive flag at
+ *    every owner;
+ *  - the update launch waits for the flags of all senders, sums the slots in
+ *    rank order (deterministic: the same sum as a reduce-scatter of rank
+ *    order), updates the own columns, writes its bf16 shadow block into
+ *    EVERY rank's gathered shadow, and raises its shadow flag at every rank;
+ *  - the next products launch waits for every rank's shadow flag.
+ * Flags are 32-bit step epochs (monotonic, never reset) at system scope.
+ * Setup: after geig_set_partition, geig_peer_buffers gives this rank's
+ * receive buffer (world x geig_owned_chunk_floats floats) and flag words
+ * (device memory, for CUDA IPC export with geig_ipc_handle); with
+ * geig_shadow_buffer's gathered shadow these three are exchanged among the
+ * ranks (geig_ipc_open maps another process's buffer) and passed to
+ * geig_set_peers as arrays of `world` device pointers (entry `rank` = this
+ * rank's own buffers).  geig_step_cca_peer then runs one step (two
+ * launches); the ranks must call it in lockstep (the kernels wait on each
+ * other's flags: a rank that never calls traps the others' kernels after
+ * seconds).  Up to 8 ranks.  Errors: GEIG_ERR_STATE without a partition /
+ * peers; GEIG_ERR_ARG for NULL, unaligned or inconsistent pointers. */
+geig_status geig_peer_buffers(geig_solver* s, void** recv, int64_t* recv_bytes,
+                              void** flags, int64_t* flags_bytes);
+geig_status geig_set_peers(geig_solver* s, void* const* recv, void* const* shadow,
+                           void* const* flags);
+geig_status geig_step_cca_peer(geig_solver* s, const void* X, const void* Y,
+                               int64_t b, float scale, double eta, double gamma);
+/* The two launches of geig_step_cca_peer separately (e.g. several ranks
+ * emulated in one process: every rank's products, then every rank's
+ * update); GEIG_ERR_STATE when called out of order. */
+geig_status geig_products_cca_peer(geig_solver* s, const void* X, const void* Y,
+                                   int64_t b, float scale);
+geig_status geig_update_peer(geig_solver* s, double eta, double gamma);
+
+/* CUDA IPC of device allocations between the processes of one node:
+ * geig_ipc_handle writes the 64-byte handle of dev_ptr (the base of a
+ * device allocation of this process); geig_ipc_open maps another process's
+ * handle (peer access enabled lazily); geig_ipc_close unmaps it. */
+geig_status geig_ipc_handle(const void* dev_ptr, void* handle64);
+geig_status geig_ipc_open(const void* handle64, void** dev_ptr);
+geig_status geig_ipc_close(void* dev_ptr);
+
 /* One full step = products + update on the solver's scratch.  On the bf16
  * tensor-core path with k <= 64 the whole step is ONE persistent cooperative
  * kernel (forward GEMM, split-K reduction, backward GEMM, Gram tables and

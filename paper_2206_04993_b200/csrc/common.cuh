@@ -12,6 +12,8 @@
 
 namespace geig {
 
+constexpr int GEIG_MAX_PEERS = 8;   // ranks of the peer-memory exchange (one NVLink domain of the box)
+
 // Developer A/B and timing knobs read from the environment exist only in a
 // build with -DGEIG_DEV_KNOBS=1 (GEIG_NVCC_EXTRA); the default library reads
 // no environment variable, so nothing outside the ABI changes its schedule

@@ -54,6 +54,19 @@ __device__ __forceinline__ void spin_geq_trap(const int* c, int target) {
   } while (v - target < 0);
 }
 
+// Peer-exchange flags (system scope: the writers are kernels on other GPUs)
+__device__ __forceinline__ void peer_flag_wait(const unsigned* f, unsigned epoch) {
+  unsigned v;
+  long long polls = 0;
+  do {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    if (++polls > (1ll << 26)) __trap();   // a peer that never signals: fail instead of hanging
+  } while ((int)(v - epoch) < 0);
+}
+__device__ __forceinline__ void peer_flag_set(unsigned* f, unsigned epoch) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+}
+
 // Grid barrier of the CTA-pair launches, which are NOT cooperative launches
 // (the profiler cannot replay a cooperative launch with thread-block
 // clusters; co-residency of the grid is checked on the host with
@@ -121,6 +134,20 @@ struct FusedParams {
   // through AV / BV in global memory and the B -> U tile counters
   int pair;
   unsigned* gbar;                  // non-null: grid barriers by grid_bar (non-cooperative cluster launch)
+  // Peer exchange of the column-owned step (geig_set_peers): the products
+  // launch stores each column's AV | BV and the table row straight into the
+  // owner's receive buffer (slot = this rank) over peer memory and then
+  // raises this rank's flag at every owner; the update launch waits for the
+  // flags of all senders, sums the slots in rank order, updates the own
+  // columns, writes its shadow block into every rank's gathered shadow and
+  // raises its shadow flag at every rank; the next products launch waits for
+  // the shadow flags.  Flags carry the step epoch (monotonic, never reset):
+  // flag words [q * 32] (receive, from sender q) and [(GEIG_MAX_PEERS + q) * 32]
+  // (shadow, from owner q), one 128-byte line each.
+  int peer, prank, pworld;
+  unsigned epoch;
+  float* precv[GEIG_MAX_PEERS];    // owner r's receive buffer (peer-mapped; this rank's own: local)
+  unsigned* pflags[GEIG_MAX_PEERS];// rank q's flag words (peer-mapped; this rank's own: local)
   int64_t dv[2], d, ldz, hpad;
   float scale;
   uint32_t idescF, idescB;
@@ -359,7 +386,9 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
                 if (A_MN && p.ownW) {   // rank-blocked chunk of column gc's owner
                   const int64_t gc = it.coff + mw + 4 * q;
                   const int64_t r = gc / p.ownW;
-                  o = it.out[seg] + r * p.chunk + (int64_t)n * p.ownW + (gc - r * p.ownW);
+                  o = (p.peer ? p.precv[r] + (int64_t)p.prank * p.chunk + (it.out[seg] - p.AV)   // owner r's slot
+                              : it.out[seg] + r * p.chunk) +
+                      (int64_t)n * p.ownW + (gc - r * p.ownW);
                 }
                 if (kDevKnobs) nan_rec(p, A_MN ? 0 : 1, 0, v.x + v.y + v.z + v.w);
                 if (full_m || q_ok) {
@@ -585,6 +614,8 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   const CUtensorMap* A = p.xmaps ? p.xmaps + 6 * t : maps.a;
   if (t > 0) stamp(p.upd, 4);
   if (!p.update_only) {   // (update-only launch: phase U alone, from given products and tables)
+  if (p.peer && threadIdx.x == 0)   // every rank's shadow block of the previous update has landed here
+    for (int q = 0; q < p.pworld; ++q) peer_flag_wait(p.pflags[p.prank] + (GEIG_MAX_PEERS + q) * 32, p.epoch - 1);
   if (threadIdx.x == 0) {
     // consumer-side proxy fence: the V shadow read by this step's TMA was
     // written with generic stores by every CTA's phase U of the previous step
@@ -882,11 +913,43 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     }
     __syncthreads();
   } else {
+    if (p.peer) __threadfence_system();   // this thread's peer stores performed before the flags below
     gsync();
+    if (p.peer && blockIdx.x == 0 && threadIdx.x == 0)   // this rank's slot is complete at every owner
+      for (int r = 0; r < p.pworld; ++r) peer_flag_set(p.pflags[r] + p.prank * 32, p.epoch);
   }
   stamp(p.upd, 7);
   dstamp(p.upd, 7);
   }  // !update_only
+
+  if (p.peer && p.update_only) {
+    // the senders' slots of this step have landed: sum them in rank order
+    // into slot 0 (the own columns of this CTA; CTA 0 also the table row)
+    if (threadIdx.x == 0)
+      for (int q = 0; q < p.pworld; ++q) peer_flag_wait(p.pflags[p.prank] + q * 32, p.epoch);
+    __syncthreads();
+    float* rb = p.precv[p.prank];
+    const int64_t W = p.ownW, kW = (int64_t)p.k * W;
+    const int64_t c0 = (int64_t)blockIdx.x * p.upd.segw, c1 = min(W, c0 + p.upd.segw);
+    const int nc = c1 > c0 ? (int)(c1 - c0) : 0;
+    for (int e = threadIdx.x; e < 2 * p.k * nc; e += FS_THREADS) {
+      const int h = e / (p.k * nc), r = e - h * p.k * nc, i = r / nc, c = r - i * nc;
+      const int64_t o = h * kW + (int64_t)i * W + c0 + c;
+      float v = rb[o];
+      for (int q = 1; q < p.pworld; ++q) v += rb[(int64_t)q * p.chunk + o];
+      rb[o] = v;
+    }
+    if (blockIdx.x == 0) {
+      const int ntri = p.k * (p.k + 1) / 2, hA = (ntri + p.k + 3) & ~3;
+      for (int e = threadIdx.x; e < 2 * hA; e += FS_THREADS) {
+        float v = rb[2 * kW + e];
+        for (int q = 1; q < p.pworld; ++q) v += rb[(int64_t)q * p.chunk + 2 * kW + e];
+        rb[2 * kW + e] = v;
+      }
+    }
+    __threadfence();
+    gsync();
+  }
 
   if (t + 1 < p.nsteps && p.xmaps && threadIdx.x == 0)   // the next step's batch descriptors, ahead of its phase F
     for (int v = 0; v < 2; ++v) tma_prefetch_desc(p.xmaps + 6 * (t + 1) + v);
@@ -908,6 +971,12 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   }
   }  // steps
 
+  if (p.peer && p.update_only) {
+    __threadfence_system();               // this thread's shadow stores into the peers performed
+    gsync();
+    if (blockIdx.x == 0 && threadIdx.x == 0)   // this rank's shadow block is in every rank's copy
+      for (int q = 0; q < p.pworld; ++q) peer_flag_set(p.pflags[q] + (GEIG_MAX_PEERS + p.prank) * 32, p.epoch);
+  }
   if (p.rcnt || p.fcnt || p.bcnt) {
     // every CTA is past its last counter read: back to zero for the next launch
     gsync();
@@ -995,6 +1064,11 @@ struct OwnedCfg {
   int64_t chunk;
   float* buf;
   __nv_bfloat16* gathered;
+  // peer exchange (geig_set_peers): nullptr = NCCL-style buffers
+  float* const* recv = nullptr;              // [world] receive buffers (peer-mapped)
+  __nv_bfloat16* const* shadows = nullptr;   // [world] gathered shadows (peer-mapped)
+  unsigned* const* flags = nullptr;          // [world] flag words (peer-mapped)
+  unsigned epoch = 0;
 };
 
 // Whole CCA step(s) in one cooperative launch (bf16 tensor cores, k <= 64):
@@ -1156,6 +1230,26 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   p.upd = upd;
   p.ownW = 0;
   p.chunk = 0;
+  p.peer = 0;
+  if (own && own->recv) {
+    if (own->world > GEIG_MAX_PEERS) return tc_fail(GEIG_ERR_UNSUPPORTED, "peer exchange: more than 8 ranks");
+    p.peer = 1;
+    p.prank = own->rank;
+    p.pworld = own->world;
+    p.epoch = own->epoch;
+    for (int q = 0; q < own->world; ++q) { p.precv[q] = own->recv[q]; p.pflags[q] = own->flags[q]; }
+    if (update_only) {
+      p.ownW = own->W;   // the slot sum reads these
+      p.chunk = own->chunk;
+      int n = 0;
+      for (int q = 0; q < own->world; ++q)
+        if (q != own->rank) p.upd.vpeer[n++] = own->shadows[q] + (int64_t)own->rank * 2 * k * own->W;
+      p.upd.vpeer_n = n;
+    } else {
+      for (int q = 0; q < own->world; ++q) p.upd.tpeer[q] = own->recv[q];
+      p.upd.tpeer_off = (int64_t)own->rank * own->chunk + 2 * (int64_t)k * own->W;
+    }
+  }
   if (own && !update_only) {
     p.ownW = own->W;
     p.chunk = own->chunk;

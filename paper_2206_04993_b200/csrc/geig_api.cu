@@ -87,6 +87,15 @@ struct geig_solver {
   int64_t own_segw = 0;
   float* splitk = nullptr;                            // SIMT split-K partials (lazily sized)
   size_t splitk_floats = 0;
+  // peer exchange of the column-owned step (geig_set_peers)
+  float* precv = nullptr;                             // [world][chunk] receive slots (local)
+  unsigned* pflags = nullptr;                         // flag words (local): 2 x GEIG_MAX_PEERS lines of 32
+  float* peer_recv[GEIG_MAX_PEERS] = {};
+  __nv_bfloat16* peer_shadow[GEIG_MAX_PEERS] = {};
+  unsigned* peer_flags[GEIG_MAX_PEERS] = {};
+  bool peer_on = false;
+  unsigned peer_epoch = 0;                            // last completed step
+  unsigned peer_pending = 0;                          // products launched, update not yet
   // one-CTA small-problem step (small_step.cuh)
   int opt_small = 1;                                  // geig_set_option(GEIG_OPT_SMALL_STEP)
   const void** ptab_dev = nullptr;                    // per-step batch pointers of a run (device, pinned staging)
@@ -211,7 +220,7 @@ extern "C" geig_status geig_destroy(geig_solver* s) {
   if (!s) return GEIG_OK;
   cudaSetDevice(s->device);
   if (s->tc.l2win.num_bytes > 0) cudaCtxResetPersistingL2Cache();   // no persisting lines outlive the arena
-  for (void* p : {(void*)s->arena,
+  for (void* p : {(void*)s->arena, (void*)s->precv, (void*)s->pflags,
                   (void*)s->gram, (void*)s->raw, (void*)s->partial,
                   (void*)s->Wx, (void*)s->Wy, (void*)s->ts, (void*)s->Wxb, (void*)s->Wyb, s->hX, s->hY,
                   (void*)s->zbuf, (void*)s->am, (void*)s->as, (void*)s->splitk, (void*)s->gshadow})
@@ -857,6 +866,11 @@ extern "C" geig_status geig_set_partition(geig_solver* s, int world, int rank) {
   if (world < 1 || rank < 0 || rank >= world) return fail(GEIG_ERR_ARG, "bad partition world=%d rank=%d", world, rank);
   CU(cudaSetDevice(s->device));
   if (s->gshadow) { CU(cudaStreamSynchronize(s->stream)); cudaFree(s->gshadow); s->gshadow = nullptr; }
+  if (s->precv) { cudaFree(s->precv); s->precv = nullptr; }
+  if (s->pflags) { cudaFree(s->pflags); s->pflags = nullptr; }
+  s->peer_on = false;
+  s->peer_epoch = 0;
+  s->peer_pending = 0;
   s->part_world = 1; s->part_rank = 0; s->part_W = 0;
   if (world == 1) return GEIG_OK;
   if (s->problem != GEIG_CCA || !(s->math == GEIG_MATH_BF16 || s->math == GEIG_MATH_BF16X2) || !s->upd_res)
@@ -872,7 +886,150 @@ extern "C" geig_status geig_set_partition(geig_solver* s, int world, int rank) {
   if (segw > UPD_RES_WMAX) return fail(GEIG_ERR_UNSUPPORTED, "own block too wide for the resident update");
   s->own_segw = segw;
   s->own_grid = (int)((W + segw - 1) / segw);
+  // receive slots and flag words of the peer exchange (used after geig_set_peers)
+  const int64_t chunk = geig_owned_chunk_floats(s);
+  CU(cudaMalloc((void**)&s->precv, (size_t)world * chunk * sizeof(float)));
+  CU(cudaMalloc((void**)&s->pflags, (size_t)2 * GEIG_MAX_PEERS * 32 * sizeof(unsigned)));
+  CU(cudaMemsetAsync(s->pflags, 0, (size_t)2 * GEIG_MAX_PEERS * 32 * sizeof(unsigned), s->stream));
   return refresh_gathered_shadow(s);
+}
+
+extern "C" geig_status geig_peer_buffers(geig_solver* s, void** recv, int64_t* recv_bytes, void** flags,
+                                         int64_t* flags_bytes) {
+  if (!s || !recv || !flags) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (!s->precv) return fail(GEIG_ERR_STATE, "no partition (geig_set_partition)");
+  *recv = s->precv;
+  *flags = s->pflags;
+  if (recv_bytes) *recv_bytes = (int64_t)s->part_world * geig_owned_chunk_floats(s) * (int64_t)sizeof(float);
+  if (flags_bytes) *flags_bytes = (int64_t)2 * GEIG_MAX_PEERS * 32 * (int64_t)sizeof(unsigned);
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_set_peers(geig_solver* s, void* const* recv, void* const* shadow, void* const* flags) {
+  if (!s || !recv || !shadow || !flags) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (!s->precv) return fail(GEIG_ERR_STATE, "no partition (geig_set_partition)");
+  if (s->part_world > GEIG_MAX_PEERS) return fail(GEIG_ERR_UNSUPPORTED, "peer exchange: at most %d ranks", GEIG_MAX_PEERS);
+  for (int q = 0; q < s->part_world; ++q) {
+    if (!recv[q] || !shadow[q] || !flags[q]) return fail(GEIG_ERR_ARG, "NULL peer pointer for rank %d", q);
+    if (((uintptr_t)recv[q] | (uintptr_t)shadow[q] | (uintptr_t)flags[q]) % 16) return fail(GEIG_ERR_ARG, "unaligned peer pointer");
+  }
+  if (recv[s->part_rank] != s->precv || shadow[s->part_rank] != s->gshadow || flags[s->part_rank] != s->pflags)
+    return fail(GEIG_ERR_ARG, "the entries of this rank must be its own buffers (geig_peer_buffers, geig_shadow_buffer)");
+  CU(cudaSetDevice(s->device));
+  for (int q = 0; q < s->part_world; ++q) {
+    s->peer_recv[q] = (float*)recv[q];
+    s->peer_shadow[q] = (__nv_bfloat16*)shadow[q];
+    s->peer_flags[q] = (unsigned*)flags[q];
+  }
+  s->peer_on = true;
+  s->peer_epoch = 0;   // every rank starts here (its flags are zero after geig_set_partition)
+  s->peer_pending = 0;
+  return GEIG_OK;
+}
+
+static tc::OwnedCfg peer_cfg(geig_solver* s, unsigned epoch) {
+  tc::OwnedCfg own{(int)s->part_W, s->part_world, s->part_rank, geig_owned_chunk_floats(s), s->precv, s->gshadow};
+  own.recv = s->peer_recv;
+  own.shadows = s->peer_shadow;
+  own.flags = s->peer_flags;
+  own.epoch = epoch;
+  return own;
+}
+
+extern "C" geig_status geig_products_cca_peer(geig_solver* s, const void* X, const void* Y, int64_t b, float scale) {
+  if (!s || !X || !Y) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (!s->peer_on) return fail(GEIG_ERR_STATE, "no peers (geig_set_peers)");
+  if (s->peer_pending) return fail(GEIG_ERR_STATE, "geig_products_cca_peer twice without geig_update_peer");
+  if (b < 2 || b > s->max_rows) return fail(GEIG_ERR_ARG, "b=%lld outside [2, max_rows]", (long long)b);
+  if (!fused_ok(s, X, Y)) return fail(GEIG_ERR_ARG, "unaligned views");
+  CU(cudaSetDevice(s->device));
+  const unsigned epoch = s->peer_epoch + 1;
+  tc::OwnedCfg own = peer_cfg(s, epoch);
+  // forward from the gathered shadow (after every rank's shadow flag of the
+  // previous step), backward AV | BV and the table row straight into the
+  // owners' receive slots, then this rank's flag at every owner
+  UpdateArgs a = update_args(s, 0.0, 0.0);
+  geig_status st = tc::fused_cca_step(s->tc, &X, &Y, 1, b, scale, s->Vbf, s->AV, s->BV, a, s->upd_grid, s->upd_smem,
+                                      s->stream, /*products_only=*/true, /*tables=*/true, false, &own);
+  if (st) return fail(st, "%s", tc::last_error());
+  s->launches++;
+  s->peer_pending = epoch;
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_update_peer(geig_solver* s, double eta, double gamma) {
+  if (!s) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (!s->peer_on) return fail(GEIG_ERR_STATE, "no peers (geig_set_peers)");
+  if (!s->peer_pending) return fail(GEIG_ERR_STATE, "geig_update_peer without geig_products_cca_peer");
+  CU(cudaSetDevice(s->device));
+  const unsigned epoch = s->peer_pending;
+  const int64_t W = s->part_W, k = s->k;
+  tc::OwnedCfg own = peer_cfg(s, epoch);
+  geig_status st;
+  // update: waits for every sender's slot, sums them, updates the own columns,
+  // writes the shadow block into every rank's gathered shadow, flags there
+  const int64_t c0 = (int64_t)s->part_rank * W;
+  UpdateArgs u = update_args(s, eta, gamma);
+  u.V = s->V + c0;
+  u.AUX = s->AUX + c0;
+  u.d = W;
+  u.ld = s->d;
+  u.segw = s->own_segw;
+  u.Vbf = s->gshadow + (int64_t)s->part_rank * 2 * k * W;
+  u.vbf_ld = W;
+  u.vbf_lo = k * W;
+  if (u.am) { u.am += c0; u.as += c0; }
+  float* AV = s->precv;   // slot 0 holds the sum after the slot pass
+  float* BV = AV + k * W;
+  u.AV = AV; u.BV = BV;
+  u.raw_a = AV + 2 * k * W;
+  u.raw = u.raw_a;
+  u.pre_reduced = 1;
+  own.buf = AV;
+  const void* none[1] = {nullptr};
+  st = tc::fused_cca_step(s->tc, none, none, 1, 0, 1.f, s->Vbf, AV, BV, u, s->own_grid,
+                          upd_res_smem_floats((int)s->own_segw) * 4, s->stream, /*products_only=*/false,
+                          /*tables=*/false, /*update_only=*/true, &own);
+  if (st) return fail(st, "%s", tc::last_error());
+  s->launches++;
+  s->fused_last = false;
+  s->peer_epoch = epoch;
+  s->peer_pending = 0;
+  advance_variant_state(s, 1);
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_step_cca_peer(geig_solver* s, const void* X, const void* Y, int64_t b, float scale,
+                                          double eta, double gamma) {
+  geig_status st = geig_products_cca_peer(s, X, Y, b, scale);
+  if (st) return st;
+  return geig_update_peer(s, eta, gamma);
+}
+
+// CUDA IPC of the peer buffers (one process per GPU): the handle of a
+// device allocation of this process, and the mapping of another process's
+// handle into this one (peer access enabled lazily).
+extern "C" geig_status geig_ipc_handle(const void* dev_ptr, void* handle64) {
+  if (!dev_ptr || !handle64) return fail(GEIG_ERR_ARG, "NULL argument");
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle64, &h, 64);
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_ipc_open(const void* handle64, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return fail(GEIG_ERR_ARG, "NULL argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  CU(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return fail(GEIG_ERR_ARG, "NULL argument");
+  CU(cudaIpcCloseMemHandle(dev_ptr));
+  return GEIG_OK;
 }
 
 extern "C" int64_t geig_owned_chunk_floats(const geig_solver* s) {

@@ -66,6 +66,15 @@ struct UpdateArgs {
   int64_t ld, vbf_ld, vbf_lo, own0, own1, tstride;
   float* tout;
   int tN;
+  // Peer exchange of the column-owned step (geig_set_peers; nullptr = off):
+  //  tpeer[r]: owner r's receive buffer (peer-mapped); the table row goes to
+  //      tpeer[r] + tpeer_off (this rank's slot) instead of tout + r tstride;
+  //  vpeer[0 .. vpeer_n): the other ranks' gathered shadows (peer-mapped):
+  //      the update writes its shadow block into every peer's copy too
+  float* tpeer[GEIG_MAX_PEERS];
+  int64_t tpeer_off;
+  __nv_bfloat16* vpeer[GEIG_MAX_PEERS];
+  int vpeer_n;
   int k;
   int64_t d;
   int64_t segw;          // columns per CTA (multiple of 4)
@@ -698,7 +707,10 @@ __device__ __forceinline__ void reduce_side(const UpdateArgs& p, int t, float* s
     if (half == 0 && e < e1) {
       const float v = s + scratch[t + 32];
       if (p.tN > 0) {
-        for (int r = 0; r < p.tN; ++r) p.tout[(int64_t)r * p.tstride + e] = v;   // every rank's chunk
+        for (int r = 0; r < p.tN; ++r) {   // every rank's chunk (peer exchange: this rank's slot at owner r)
+          if (p.tpeer[0]) p.tpeer[r][p.tpeer_off + e] = v;
+          else p.tout[(int64_t)r * p.tstride + e] = v;
+        }
       } else if (p.raw_a && e < hA) {
         p.raw_a[e] = v;
       } else {
@@ -1361,6 +1373,8 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
         *reinterpret_cast<float4*>(p.V + o) = vn;
         *reinterpret_cast<float4*>(p.AUX + o) = an;
         if (p.Vbf) store_vbf4(p.Vbf, blo, ob, vn);
+        for (int q = 0; q < p.vpeer_n; ++q)   // peer exchange: the block into every peer's gathered shadow
+          store_vbf4(p.vpeer[q], blo, ob, vn);
       } else {
         const float vs[4] = {vn.x, vn.y, vn.z, vn.w}, as[4] = {an.x, an.y, an.z, an.w};
         for (int tq = 0; tq < 4; ++tq)
@@ -1368,6 +1382,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
             p.V[o + tq] = vs[tq];
             p.AUX[o + tq] = as[tq];
             if (p.Vbf) store_vbf1(p.Vbf, blo, ob + tq, vs[tq]);
+            for (int q = 0; q < p.vpeer_n; ++q) store_vbf1(p.vpeer[q], blo, ob + tq, vs[tq]);
           }
       }
     }

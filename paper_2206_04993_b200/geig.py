@@ -66,6 +66,14 @@ _SIGS = {
     "geig_shadow_buffer": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64)],
     "geig_products_cca_owned": [_vp, _vp, _vp, _i64, _f32, _vp],
     "geig_update_owned": [_vp, _vp, _f64, _f64],
+    "geig_peer_buffers": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_i64), ctypes.POINTER(_vp), ctypes.POINTER(_i64)],
+    "geig_set_peers": [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp)],
+    "geig_step_cca_peer": [_vp, _vp, _vp, _i64, _f32, _f64, _f64],
+    "geig_products_cca_peer": [_vp, _vp, _vp, _i64, _f32],
+    "geig_update_peer": [_vp, _f64, _f64],
+    "geig_ipc_handle": [_vp, _vp],
+    "geig_ipc_open": [_vp, ctypes.POINTER(_vp)],
+    "geig_ipc_close": [_vp],
 }
 for _name, _args in _SIGS.items():
     _fn = getattr(_lib, _name)
@@ -87,7 +95,8 @@ EXPORTED = ["geig_create", "geig_destroy", "geig_set_stream", "geig_sync", "geig
             "geig_launch_count", "geig_last_error", "geig_version", "geig_update_phase_ns",
             "geig_table_floats", "geig_products_cca_tables", "geig_update_tables", "geig_set_option",
             "geig_set_partition", "geig_owned_chunk_floats", "geig_shadow_buffer", "geig_products_cca_owned",
-            "geig_update_owned"]
+            "geig_update_owned", "geig_peer_buffers", "geig_set_peers", "geig_step_cca_peer", "geig_products_cca_peer", "geig_update_peer", "geig_ipc_handle",
+            "geig_ipc_open", "geig_ipc_close"]
 
 
 def _check(st: int):
@@ -260,6 +269,49 @@ def geig_products_cca_owned(h, X, Y, b: int, scale: float, buf):
 
 def geig_update_owned(h, chunk, eta: float, gamma: float):
     _check(_lib.geig_update_owned(h, _ptr(chunk, torch.float32), eta, gamma))
+
+
+def geig_peer_buffers(h):
+    """(recv_ptr, recv_bytes, flags_ptr, flags_bytes) of this rank (device)."""
+    r, f = _vp(), _vp()
+    rb, fb = _i64(), _i64()
+    _check(_lib.geig_peer_buffers(h, ctypes.byref(r), ctypes.byref(rb), ctypes.byref(f), ctypes.byref(fb)))
+    return r.value, rb.value, f.value, fb.value
+
+
+def geig_set_peers(h, recv_ptrs, shadow_ptrs, flag_ptrs):
+    """Arrays of `world` device pointers (ints), entry `rank` = own buffers."""
+    n = len(recv_ptrs)
+    arr = lambda xs: (_vp * n)(*[_vp(int(x)) for x in xs])
+    _check(_lib.geig_set_peers(h, arr(recv_ptrs), arr(shadow_ptrs), arr(flag_ptrs)))
+
+
+def geig_step_cca_peer(h, X, Y, b: int, scale: float, eta: float, gamma: float):
+    _check(_lib.geig_step_cca_peer(h, _ptr(X), _ptr(Y), b, scale, eta, gamma))
+
+
+def geig_products_cca_peer(h, X, Y, b: int, scale: float):
+    _check(_lib.geig_products_cca_peer(h, _ptr(X), _ptr(Y), b, scale))
+
+
+def geig_update_peer(h, eta: float, gamma: float):
+    _check(_lib.geig_update_peer(h, eta, gamma))
+
+
+def geig_ipc_handle(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _check(_lib.geig_ipc_handle(_vp(int(ptr)), buf))
+    return buf.raw
+
+
+def geig_ipc_open(handle: bytes) -> int:
+    out = _vp()
+    _check(_lib.geig_ipc_open(ctypes.create_string_buffer(bytes(handle), 64), ctypes.byref(out)))
+    return out.value
+
+
+def geig_ipc_close(ptr: int):
+    _check(_lib.geig_ipc_close(_vp(int(ptr))))
 
 
 def geig_update_phase_ns(h):
