@@ -424,6 +424,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
     # products launch writes per-owner chunks, ONE reduce-scatter, the update
     # of the rank's d / N columns, ONE all-gather of the bf16 shadow blocks
     owned = None
+    peer = None
+    if world > 1 and tables and args.multi == "peer":
+        # the column-owned step over NVLink peer memory: no NCCL call on the
+        # data path (buffers mapped by CUDA IPC, epoch flags)
+        from paper_2206_04993_b200.parallel import PeerColumnOwnedStep, owned_wire_bytes
+        geig.geig_set_partition(s.h, world, rank)
+        peer = PeerColumnOwnedStep(geig, s, world, rank)
     if world > 1 and tables and args.multi == "owned":
         from paper_2206_04993_b200.parallel import (ColumnOwnedStep, allgather_blocks, owned_wire_bytes,
                                                     reduce_scatter_chunks)
@@ -457,6 +464,11 @@ def run_gpu(args, cfg, rank, world, local_rank):
             geig.geig_step_cca(s.h, Xs[i % P], Ys[i % P], b, cfg.eta, cfg.gamma)
             if timed:
                 e1.record(stream)
+        elif peer is not None:
+            geig.geig_products_cca_peer(s.h, Xs[i % P], Ys[i % P], b, scale)
+            if timed:
+                e1.record(stream)
+            geig.geig_update_peer(s.h, cfg.eta, cfg.gamma)
         elif owned is not None:
             geig.geig_products_cca_owned(s.h, Xs[i % P], Ys[i % P], b, scale, owned.buf)
             if timed:
@@ -610,7 +622,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
             def e2e_step():
                 xd.copy_(hx, non_blocking=True)
                 yd.copy_(hy, non_blocking=True)
-                if owned is not None:
+                if peer is not None:
+                    peer(xd, yd, b, cfg.eta, cfg.gamma)
+                elif owned is not None:
                     owned(xd, yd, b, cfg.eta, cfg.gamma)
                 elif tables:
                     geig.geig_products_cca_tables(s.h, xd, yd, b, scale, AV, BV, T)
@@ -659,9 +673,12 @@ def run_gpu(args, cfg, rank, world, local_rank):
                                               % (cfg.batch, b, cfg.batch)),
                                update=variant,
                                wire_bytes_per_rank=(owned_wire_bytes(cfg.k, cfg.d, world, geig.geig_table_floats(s.h))
-                                                    if owned is not None else None),
+                                                    if (owned is not None or peer is not None) else None),
                                step=("fused single launch (geig_run_cca)" if multi else
                                      "fused single launch per step" if fused else
+                                     "column-owned over NVLink peer memory: products launch stores every column's "
+                                     "AV|BV into its owner's slot, update sums the slots and stores its shadow block "
+                                     "into every rank (epoch flags, no NCCL on the data path)" if peer is not None else
                                      "column-owned: products launch (per-owner chunks), reduce-scatter, update of "
                                      "the rank's d/N columns, all-gather of the bf16 shadow" if owned is not None else
                                      "products+tables launch, all-reduce, update_tables" if tables else
@@ -695,8 +712,9 @@ def main():
     ap.add_argument("--per-step-launch", action="store_true",
                     help="fused path: one geig_step_cca launch per step instead of geig_run_cca")
     ap.add_argument("--config", type=int, default=3)
-    ap.add_argument("--multi", choices=("owned", "replicated"), default="owned",
-                    help="N > 1: column-owned reduce-scatter / all-gather step, or the replicated all-reduce step")
+    ap.add_argument("--multi", choices=("owned", "peer", "replicated"), default="owned",
+                    help="N > 1: column-owned reduce-scatter / all-gather step (NCCL), the column-owned step over "
+                         "NVLink peer memory (CUDA IPC, no NCCL on the data path), or the replicated all-reduce step")
     ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
                     help="weak: cfg.batch rows per rank; strong: cfg.batch rows sharded over the ranks")
     ap.add_argument("--math", default=None)

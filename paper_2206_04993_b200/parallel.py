@@ -203,3 +203,50 @@ class ColumnOwnedStep:
         V = Vb.permute(1, 0, 2).reshape(self.k, self.d)
         AUX = Ab.permute(1, 0, 2).reshape(self.k, self.d)
         return V / V.norm(dim=1, keepdim=True), AUX
+
+
+def exchange_peer_pointers(local: list[int], world: int, rank: int, handle_fn, open_fn, group=None):
+    """CUDA IPC handshake of the peer exchange: `local` holds this rank's
+    device pointers (receive slots, gathered shadow, flag words); every
+    rank's handles are all-gathered and every OTHER rank's are mapped into
+    this process.  Returns (per buffer kind, a list of `world` pointers in
+    rank order; this rank's entries are its own pointers) and the list of
+    mapped pointers to unmap at the end."""
+    mine = [handle_fn(p) for p in local]
+    got = [None] * world
+    dist.all_gather_object(got, mine, group=group)
+    opened = []
+    table = [[0] * world for _ in local]
+    for q in range(world):
+        for j in range(len(local)):
+            if q == rank:
+                table[j][q] = local[j]
+            else:
+                ptr = open_fn(got[q][j])
+                table[j][q] = ptr
+                opened.append(ptr)
+    return table, opened
+
+
+class PeerColumnOwnedStep:
+    """The column-owned step over NVLink peer memory (geig_set_peers): one
+    process per GPU; the products launch stores every column's AV | BV and
+    the table row into the owner's receive slot, the update launch sums the
+    slots and writes its shadow block into every rank's gathered shadow —
+    no NCCL call on the data path (Appendix F)."""
+
+    def __init__(self, geig, solver, world: int, rank: int, group=None):
+        self.g, self.s, self.world, self.rank = geig, solver, world, rank
+        recv, _, flags, _ = geig.geig_peer_buffers(solver.h)
+        shadow, _ = geig.geig_shadow_buffer(solver.h)
+        (self.recv, self.shadow, self.flags), self.opened = exchange_peer_pointers(
+            [recv, shadow, flags], world, rank, geig.geig_ipc_handle, geig.geig_ipc_open, group)
+        geig.geig_set_peers(solver.h, self.recv, self.shadow, self.flags)
+
+    def __call__(self, X, Y, b: int, eta: float, gamma: float):
+        self.g.geig_step_cca_peer(self.s.h, X, Y, b, cca_scale(b, self.world), eta, gamma)
+
+    def close(self):
+        for p in self.opened:
+            self.g.geig_ipc_close(p)
+        self.opened = []

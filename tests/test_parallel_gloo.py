@@ -222,3 +222,54 @@ def test_gloo_world3_column_owned_collectives():
         np.testing.assert_allclose(res[r][1], total[r * chunk:(r + 1) * chunk], rtol=0, atol=1e-12)
         for q_ in range(world):
             np.testing.assert_array_equal(res[r][2][q_], q_ + np.arange(30.0).reshape(2, 3, 5))
+
+
+def _peer_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2206_04993_b200.parallel import exchange_peer_pointers
+        # stand-ins for CUDA IPC: a "handle" names (rank, pointer); opening it
+        # maps to a distinct address so the assembled table is checkable
+        local = [1000 * rank + 1, 1000 * rank + 2, 1000 * rank + 3]
+        handle = lambda p: ("h", rank, p)
+        opened_log = []
+
+        def open_fn(h):
+            opened_log.append(h)
+            return 10 ** 6 + h[2]
+
+        table, opened = exchange_peer_pointers(local, world, rank, handle, open_fn)
+        out_q.put((rank, table, opened, opened_log))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world3_peer_pointer_exchange():
+    """Host plumbing of the peer exchange (parallel.exchange_peer_pointers):
+    every rank ends with, per buffer kind, `world` pointers in rank order —
+    its own pointers in its own slot, every other rank's handle opened once
+    (the CUDA IPC calls are injected, exactly where PeerColumnOwnedStep
+    passes geig_ipc_handle / geig_ipc_open)."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, table, opened, log = q.get(timeout=120)
+        res[r] = (table, opened, log)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        table, opened, log = res[r]
+        for j in range(3):
+            for q_ in range(world):
+                want = 1000 * r + j + 1 if q_ == r else 10 ** 6 + 1000 * q_ + j + 1
+                assert table[j][q_] == want
+        assert len(opened) == 3 * (world - 1) and all(h[1] != r for h in log)
