@@ -360,13 +360,18 @@ geig_status geig_get_gram(geig_solver* s, float* GA, float* GB, float* GC);
  *                             the backward accumulators move into the update
  *                             through distributed shared memory instead of
  *                             global memory; 0 = one CTA per item
+ *  GEIG_OPT_GRAM_TC         : 1 = (default) the streamed update (k > 64) of a
+ *                             tf32 / 3xTF32 solver forms its Gram tables
+ *                             G^A, G^C on the tensor cores (one launch of
+ *                             split-K partial rows before the update); 0 =
+ *                             FFMA in the update kernel
  *  GEIG_OPT_STAGED_PRODUCTS : 1 = geig_products_cca runs the three-launch
  *                             staged tcgen05 products (forward GEMM, z
  *                             reshuffle, backward GEMM) instead of phases
  *                             F, S, B of the fused kernel; 0 = fused (default)
  * Errors: GEIG_ERR_ARG for an unknown option or a value out of range. */
 typedef enum { GEIG_OPT_FUSED_M_TILES = 1, GEIG_OPT_STAGED_PRODUCTS = 2, GEIG_OPT_SMALL_STEP = 3,
-               GEIG_OPT_FUSED_PAIRS = 4 } geig_option;
+               GEIG_OPT_FUSED_PAIRS = 4, GEIG_OPT_GRAM_TC = 5 } geig_option;
 geig_status geig_set_option(geig_solver* s, int option, int64_t value);
 
 /* Phase durations (ns, %globaltimer of CTA 0) of the last update:

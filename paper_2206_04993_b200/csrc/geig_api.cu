@@ -98,6 +98,7 @@ struct geig_solver {
   unsigned peer_pending = 0;                          // products launched, update not yet
   // one-CTA small-problem step (small_step.cuh)
   int opt_small = 1;                                  // geig_set_option(GEIG_OPT_SMALL_STEP)
+  int opt_gram_tc = 1;                                // geig_set_option(GEIG_OPT_GRAM_TC)
   const void** ptab_dev = nullptr;                    // per-step batch pointers of a run (device, pinned staging)
   const void** ptab_host = nullptr;
   cudaEvent_t ptab_ev = nullptr;
@@ -553,8 +554,20 @@ extern "C" geig_status geig_update(geig_solver* s, const float* AV, const float*
   CU(cudaSetDevice(s->device));
   UpdateArgs a = update_args(s, eta, gamma);
   a.AV = AV; a.BV = BV;
-  void* args[] = {&a};
   const bool vec = (s->d % 4 == 0) && (((uintptr_t)AV | (uintptr_t)BV) % 16 == 0);
+  if (!s->upd_res && s->opt_gram_tc && s->tc.ready && (s->math == GEIG_MATH_TF32 || s->math == GEIG_MATH_3XTF32) &&
+      vec && (s->d + 31) / 32 >= s->upd_grid) {
+    // k > 64: the G'^A, G'^C partial rows on the tensor cores (one split per
+    // update CTA), the update's phase 1 only forms the diagonals
+    int64_t nl = 0;
+    const int KP = 128;
+    geig_status st = tc::gram_dense_tc(s->tc, s->V, AV, s->AUX, s->partial, (int64_t)upd_partial_floats(2), KP,
+                                       s->upd_grid, s->stream, &nl);
+    s->launches += nl;
+    if (st) return fail(st, "%s", tc::last_error());
+    a.gram_tc = 1;
+  }
+  void* args[] = {&a};
   void* fn;
   if (s->upd_res) fn = vec ? (void*)update_res_kernel<true> : (void*)update_res_kernel<false>;
   else if (s->k <= 64) fn = vec ? (void*)update_kernel<1, true> : (void*)update_kernel<1, false>;
@@ -1106,6 +1119,10 @@ extern "C" geig_status geig_set_option(geig_solver* s, int option, int64_t value
     case GEIG_OPT_FUSED_PAIRS:
       if (value < 0 || value > 2) return fail(GEIG_ERR_ARG, "GEIG_OPT_FUSED_PAIRS must be 0, 1 or 2");
       s->tc.opt_pairs = (int)value;
+      return GEIG_OK;
+    case GEIG_OPT_GRAM_TC:
+      if (value != 0 && value != 1) return fail(GEIG_ERR_ARG, "GEIG_OPT_GRAM_TC must be 0 or 1");
+      s->opt_gram_tc = (int)value;
       return GEIG_OK;
     case GEIG_OPT_SMALL_STEP:
       if (value != 0 && value != 1) return fail(GEIG_ERR_ARG, "GEIG_OPT_SMALL_STEP must be 0 or 1");

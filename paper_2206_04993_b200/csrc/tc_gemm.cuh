@@ -902,4 +902,58 @@ inline geig_status products_dense(TcPlan& t, const void* A, const void* B, int64
   return GEIG_OK;
 }
 
+// Gram tables of the streamed (k > 64) update on the tensor cores (tf32 /
+// 3xTF32 plans): per split s of the d columns (one split per update CTA,
+// `splits` = the update grid), the partial rows
+//   partial[s][i KP + j]          = sum_{c in split s} V''[i][c] AV''[j][c]   (G'^A)
+//   partial[s][KP^2 + i KP + j]   = sum_{c in split s} V''[i][c] AUX[j][c]    (G'^C)
+// as two groups of one launch: A operand = AV (group 0) / AUX (group 1), k
+// rows, K-major over d (the split's K blocks); B operand = V'' (tf32, or its
+// hi / lo planes with the in-smem A split for 3xTF32); store mode at
+// split_stride = pstride (deterministic: the update's phase 2 sums the rows
+// in fixed order).  The update's phase 1 then forms only the diagonals.
+// Needs d / 32 >= splits (no empty split).
+inline geig_status gram_dense_tc(TcPlan& t, const float* V, const float* AV, const float* AUX, float* partial,
+                                 int64_t pstride, int KP, int splits, cudaStream_t st, int64_t* nl) {
+  if (!t.ready || (t.math != GEIG_MATH_TF32 && t.math != GEIG_MATH_3XTF32))
+    return tc_fail(GEIG_ERR_STATE, "tensor-core Gram needs a tf32 / 3xTF32 plan");
+  const int eb = 4, ATOM = 32;
+  const int k = t.k;
+  const int kb = (int)((t.d + ATOM - 1) / ATOM);
+  if (k > TC_BM || splits < 1 || kb < splits) return tc_fail(GEIG_ERR_UNSUPPORTED, "tensor-core Gram: shape");
+  if (t.x3) {   // V's hi / lo planes (V may have changed since the products' split)
+    geig_status e = split_v_x3(t, V, st, nl);
+    if (e) return e;
+  }
+  const void* Vop = t.x3 ? (const void*)t.Vx3 : (const void*)V;
+  TcMaps maps;
+  TcParams p{};
+  // one group, two segments (AV, then AUX against the same V): one CTA per
+  // split (one wave), two TMEM accumulators
+  const float* mats[2] = {AV, AUX};
+  for (int sg = 0; sg < 2; ++sg) {
+    if (!make_map(&maps.a[sg], mats[sg], eb, t.d, k, t.d, ATOM, TC_BM) ||
+        !make_map(&maps.b[sg], Vop, eb, t.d, k, t.d, ATOM, t.BN))
+      return tc_fail(GEIG_ERR_CUDA, "tensor map encode (Gram) failed");
+    if (t.x3 && !make_map(&maps.blo[sg], (const char*)Vop + (int64_t)k * t.d * eb, eb, t.d, k, t.d, ATOM, t.BN))
+      return tc_fail(GEIG_ERR_CUDA, "tensor map encode (Gram lo) failed");
+    p.kblocks[0][sg] = kb;
+    p.out[0][sg] = partial + (int64_t)sg * KP * KP;
+    maps.a[2 + sg] = maps.a[sg];
+    maps.b[2 + sg] = maps.b[sg];
+    maps.blo[2 + sg] = maps.blo[sg];
+  }
+  p.M[0] = p.M[1] = k;
+  p.N = k; p.BN = t.BN; p.nseg = 2; p.ldo = KP; p.scale = 1.f;
+  p.idesc = make_idesc(eb, false, t.BN, TC_BM);
+  p.splits = splits;
+  p.atomic = 0;
+  p.split_stride = pstride;
+  dim3 grid(1, splits, 1);
+  geig_status s = launch<4, false>(maps, p, grid, st, t.nsm, t.x3 != 0, t.x3 != 0);
+  if (s) return s;
+  ++*nl;
+  return GEIG_OK;
+}
+
 }}  // namespace geig::tc

@@ -94,6 +94,8 @@ struct UpdateArgs {
   // Adam ascent on v_i (Appendix H): moments am, as (k x d);
   // step t of a launch uses bias corrections of the global count adam_t0 + t + 1
   int pair_tiles;          // fused CTA pairs: AV, BV tiles already in smem, V'' / [Bv] staged on the tile barrier
+  int gram_tc;             // streamed update (k > 64): G'^A, G'^C partial rows written by the tensor-core Gram
+                           // launch (tc::gram_dense_tc); phase 1 forms only the diagonals
   int adam;
   float* am;
   float* as;
@@ -214,7 +216,42 @@ update_kernel(UpdateArgs p) {
   stamp(p, 0);
 
   // ---------------- phase 1: Gram partial sums of this CTA's columns ----------------
-  {
+  if (p.gram_tc) {
+    // G'^A, G'^C of this CTA's partial row came from the tensor cores: the
+    // diagonals <v''_i, BV''_i> and ||v''_i||^2 of its columns (warp per row)
+    // (thread pair per row, each half of the column quads, every load of a
+    // thread independent of the others: one L2 round trip, not one per row)
+    float* out = p.partial + (size_t)blockIdx.x * PSTRIDE;
+    static_assert(2 * KP <= UPD_THREADS || KP > 64, "thread pairs cover the rows");
+    for (int i0 = 0; i0 < KP; i0 += UPD_THREADS / 2) {
+      const int i = i0 + (tid >> 1), h = tid & 1;
+      float gb = 0.f, nn = 0.f;
+      if (i < k) {
+        const float* vr = p.V + (int64_t)i * d;
+        const float* br = p.BV + (int64_t)i * d;
+        if (VEC) {
+#pragma unroll 4
+          for (int64_t x = c0 + 4 * h; x < c1; x += 8) {
+            const float4 v = *reinterpret_cast<const float4*>(vr + x);
+            const float4 bb = *reinterpret_cast<const float4*>(br + x);
+            gb = fmaf(v.x, bb.x, fmaf(v.y, bb.y, fmaf(v.z, bb.z, fmaf(v.w, bb.w, gb))));
+            nn = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, nn))));
+          }
+        } else {
+          for (int64_t x = c0 + h; x < c1; x += 2) {
+            gb = fmaf(vr[x], br[x], gb);
+            nn = fmaf(vr[x], vr[x], nn);
+          }
+        }
+      }
+      gb += __shfl_xor_sync(0xffffffffu, gb, 1);
+      nn += __shfl_xor_sync(0xffffffffu, nn, 1);
+      if (h == 0 && i < KP) {
+        out[2 * KP * KP + i] = gb;
+        out[2 * KP * KP + KP + i] = nn;
+      }
+    }
+  } else {
     const int ti = tid & 15, tj = tid >> 4;
     float accA[NPAIR][4][4], accC[NPAIR][4][4];
 #pragma unroll
@@ -320,7 +357,7 @@ update_kernel(UpdateArgs p) {
         out[2 * KP * KP + KP + warp + 8 * q] = s2;
       }
     }
-  }
+  }   // (gram_tc else)
   grid.sync();
   stamp(p, 1);
 

@@ -726,3 +726,51 @@ def test_fused_pairs_match_single_ctas(geig, variant):
     (Vp, ap), (Vs, as_) = out
     step, aux_e = rel_err(Vp - V, Vs - V), rel_err(ap, as_)
     assert step < 1e-5 and aux_e < 1e-5, (step, aux_e)
+
+
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("d,k", [(4096, 128), (3000, 100), (16384, 128)])
+def test_gram_tensor_cores_match_ffma_gram(geig, math, d, k):
+    """The streamed (k > 64) update's Gram tables G^A, G^C on the tensor
+    cores (GEIG_OPT_GRAM_TC, split-K partial rows, one per update CTA)
+    against the FFMA Gram of the update kernel, from the same products: the
+    tables (geig_get_gram) and the step agree to the Gram arithmetic's
+    precision (3xTF32: fp32 level; tf32: 10-bit operands), and the
+    3xTF32 step matches the oracle at the fp32 bar (1e-4)."""
+    from oracle import estimators, game
+    from synth import dense_gep_large
+    dev = "cuda:0"
+    a, b = dense_gep_large(d, seed=3, device=dev)
+    V, aux = random_state(k, d, 5)
+    V = V.astype(np.float32).astype(np.float64)
+    aux = aux.astype(np.float32).astype(np.float64)
+    a64, b64 = a.double().cpu().numpy(), b.double().cpu().numpy()
+    av0, bv0 = estimators.dense_products(a64, b64, V)
+    rho = 5e-4
+    eta = 0.1 / max(np.linalg.norm(game.direction_alg2(i, V, aux, av0, bv0, rho)) for i in range(k))
+    out = {}
+    for tc in (1, 0):
+        s = geig.Solver(geig.GEIG_DENSE, d, 0, k, math=math, rho=rho)
+        try:
+            geig.geig_set_option(s.h, geig.GEIG_OPT_GRAM_TC, tc)
+            s.set_state(torch.tensor(V, dtype=torch.float32, device=dev), torch.tensor(aux, dtype=torch.float32, device=dev))
+            AV = torch.empty(k, d, device=dev)
+            BV = torch.empty_like(AV)
+            geig.geig_products_dense(s.h, a, b, 0, d, AV, BV)
+            l0 = s.launches()
+            geig.geig_update(s.h, AV, BV, eta, 1.0)
+            launches = s.launches() - l0
+            V2, A2 = [x.double().cpu().numpy() for x in s.state()]
+            ga, gb, gc = [x.double().cpu().numpy() for x in s.gram()]
+            out[tc] = (V2, A2, ga, gb, gc, launches)
+        finally:
+            s.close()
+    assert out[1][5] > out[0][5]            # the Gram launch (+ the 3xTF32 V split) ran
+    tol = 1e-5 if math == "3xtf32" else 3e-3
+    for j, name in ((2, "ga"), (4, "gc")):
+        assert rel_err(out[1][j], out[0][j]) < tol, name
+    assert rel_err(out[1][0] - V, out[0][0] - V) < 10 * tol
+    if math == "3xtf32":
+        V2, aux2 = game.step_alg2(V, aux, [(av0, bv0)], eta, 1.0, rho)
+        assert rel_err(out[1][0] - V, V2 - V) < 1e-4
+        assert rel_err(out[1][1], aux2) < 1e-4
