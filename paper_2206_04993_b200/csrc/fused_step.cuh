@@ -1102,6 +1102,15 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
     upd.segw = 128;
     upd.pair_tiles = 1;
     upd_bytes = upd_res_smem_floats(128) * 4;
+  } else if (pair_grid > 0 && !products_only && !update_only && !own && 2 * grid_ctas <= pair_grid) {
+    // small d (config 2: 49 CTAs of 32 columns): the update's column
+    // partition would leave most SMs idle in phases F, S and B — a finer
+    // partition (8-column multiples) widens the grid (98 CTAs of 16
+    // columns: 27.05 vs 27.55 us/step, same-box A/B)
+    int64_t segw = ((t.dx + t.dy + pair_grid - 1) / pair_grid + 7) / 8 * 8;
+    grid_ctas = (int)((t.dx + t.dy + segw - 1) / segw);
+    upd.segw = segw;
+    upd_bytes = upd_res_smem_floats((int)segw) * 4;
   }
   if (!update_only && !make_batch_maps(maps.a, t, X[0], Y[0], h))
     return tc_fail(GEIG_ERR_CUDA, "tensor map encode (batch) failed");
