@@ -52,7 +52,7 @@ int main(int argc, char** argv) {
   const size_t smem = 227 * 1024;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(probe, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  for (int csz : {2, 4, 8}) {
+  for (int csz : {2, 4, 8, 16}) {
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = smem;
