@@ -289,6 +289,20 @@ geig_status geig_run_cca(geig_solver* s, const void* const* X,
                          const void* const* Y, int64_t b, int64_t nsteps,
                          double eta, double gamma);
 
+/* nsteps CCA steps end to end from HOST buffers (X_host[t], Y_host[t]:
+ * pinned host memory, b x d_view rows each): the host->device copy of batch
+ * t + 1 (a copy stream, double-buffered device staging) overlaps step t on
+ * the solver's stream; after every step its k x k normalised G^A table is
+ * copied back into ga_host (nullable; pinned, k*k floats; the last step's
+ * table remains).  Synchronises before returning; *h2d / *d2h = bytes
+ * moved (nullable).  Same results as nsteps geig_step_cca calls on the
+ * device copies.  Errors: those of geig_step_cca; GEIG_ERR_ARG for NULL
+ * arrays. */
+geig_status geig_run_cca_host(geig_solver* s, const void* const* X_host,
+                              const void* const* Y_host, int64_t b, int64_t nsteps,
+                              double eta, double gamma, float* ga_host,
+                              int64_t* h2d, int64_t* d2h);
+
 /* Variants of the update, applied by every following step (geig_update,
  * geig_step_cca, geig_run_cca, geig_step_dense); resident update only
  * (k <= 64, otherwise GEIG_ERR_UNSUPPORTED).

@@ -60,6 +60,9 @@ struct geig_solver {
   float *Wx = nullptr, *Wy = nullptr;                 // fp32 backward operands k x max_rows
   __nv_bfloat16 *Wxb = nullptr, *Wyb = nullptr;       // bf16 backward operands
   void *hX = nullptr, *hY = nullptr;                  // device staging for *_host
+  void *hX2 = nullptr, *hY2 = nullptr;                // second staging pair (geig_run_cca_host double buffer)
+  cudaStream_t copy_stream = nullptr;                 // H2D copies of geig_run_cca_host
+  cudaEvent_t ev_loaded[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   int upd_grid = 1;
   bool upd_res = false;                               // resident (k <= 64) update kernel
   bool fused_last = false;                            // last step ran the fused cooperative kernel
@@ -227,6 +230,13 @@ extern "C" geig_status geig_destroy(geig_solver* s) {
                   (void*)s->zbuf, (void*)s->am, (void*)s->as, (void*)s->splitk, (void*)s->gshadow})
     if (p) cudaFree(p);
   if (s->ptab_dev) cudaFree((void*)s->ptab_dev);
+  if (s->hX2) cudaFree(s->hX2);
+  if (s->hY2) cudaFree(s->hY2);
+  for (int i = 0; i < 2; ++i) {
+    if (s->ev_loaded[i]) cudaEventDestroy(s->ev_loaded[i]);
+    if (s->ev_free[i]) cudaEventDestroy(s->ev_free[i]);
+  }
+  if (s->copy_stream) cudaStreamDestroy(s->copy_stream);
   if (s->ptab_host) cudaFreeHost((void*)s->ptab_host);
   if (s->ptab_ev) cudaEventDestroy(s->ptab_ev);
   tc::plan_destroy(s->tc);
@@ -822,6 +832,54 @@ extern "C" geig_status geig_step_cca_host(geig_solver* s, const void* X_host, co
   CU(cudaStreamSynchronize(s->stream));
   if (h2d) *h2d = (int64_t)(bx + by);
   if (d2h) *d2h = ga_host ? (int64_t)gb : 0;
+  return GEIG_OK;
+}
+
+extern "C" geig_status geig_run_cca_host(geig_solver* s, const void* const* X_host, const void* const* Y_host,
+                                         int64_t b, int64_t nsteps, double eta, double gamma, float* ga_host,
+                                         int64_t* h2d, int64_t* d2h) {
+  if (!s || !X_host || !Y_host) return fail(GEIG_ERR_ARG, "NULL argument");
+  if (s->problem != GEIG_CCA) return fail(GEIG_ERR_STATE, "solver is not a CCA solver");
+  if (b < 2 || b > s->max_rows) return fail(GEIG_ERR_ARG, "bad b");
+  if (nsteps < 0) return fail(GEIG_ERR_ARG, "nsteps < 0");
+  CU(cudaSetDevice(s->device));
+  const size_t es = s->dtype == GEIG_DATA_BF16 ? 2 : 4;
+  const size_t bx = (size_t)b * s->dx * es, by = (size_t)b * s->dy * es;
+  if (!s->hX) {
+    CU(cudaMalloc(&s->hX, (size_t)s->max_rows * s->dx * es));
+    CU(cudaMalloc(&s->hY, (size_t)s->max_rows * s->dy * es));
+  }
+  if (!s->hX2) {
+    CU(cudaMalloc(&s->hX2, (size_t)s->max_rows * s->dx * es));
+    CU(cudaMalloc(&s->hY2, (size_t)s->max_rows * s->dy * es));
+    CU(cudaStreamCreateWithFlags(&s->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CU(cudaEventCreateWithFlags(&s->ev_loaded[i], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&s->ev_free[i], cudaEventDisableTiming));
+    }
+  }
+  void* dX[2] = {s->hX, s->hX2};
+  void* dY[2] = {s->hY, s->hY2};
+  const size_t gb = (size_t)s->k * s->k * 4;
+  // the staging pairs are free when this call starts (previous work on the solver's stream)
+  for (int i = 0; i < 2; ++i) CU(cudaEventRecord(s->ev_free[i], s->stream));
+  for (int64_t t = 0; t < nsteps; ++t) {
+    const int q = (int)(t & 1);
+    // copy engine: batch t into pair q once step t - 2 has released it
+    CU(cudaStreamWaitEvent(s->copy_stream, s->ev_free[q], 0));
+    CU(cudaMemcpyAsync(dX[q], X_host[t], bx, cudaMemcpyHostToDevice, s->copy_stream));
+    CU(cudaMemcpyAsync(dY[q], Y_host[t], by, cudaMemcpyHostToDevice, s->copy_stream));
+    CU(cudaEventRecord(s->ev_loaded[q], s->copy_stream));
+    // compute: step t (overlaps the copy of batch t + 1), then its Gram table back
+    CU(cudaStreamWaitEvent(s->stream, s->ev_loaded[q], 0));
+    geig_status st = geig_step_cca(s, dX[q], dY[q], b, eta, gamma);
+    if (st) return st;
+    CU(cudaEventRecord(s->ev_free[q], s->stream));
+    if (ga_host) CU(cudaMemcpyAsync(ga_host, s->gram, gb, cudaMemcpyDeviceToHost, s->stream));
+  }
+  CU(cudaStreamSynchronize(s->stream));
+  if (h2d) *h2d = (int64_t)(bx + by) * nsteps;
+  if (d2h) *d2h = ga_host ? (int64_t)gb * nsteps : 0;
   return GEIG_OK;
 }
 

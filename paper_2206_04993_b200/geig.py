@@ -60,6 +60,7 @@ _SIGS = {
     "geig_step_cca_host": [_vp, _vp, _vp, _i64, _f64, _f64, _vp, ctypes.POINTER(_i64),
                            ctypes.POINTER(_i64)],
     "geig_get_gram": [_vp, _vp, _vp, _vp],
+    "geig_run_cca_host": [_vp, _vp, _vp, _i64, _i64, _f64, _f64, _vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
     "geig_update_phase_ns": [_vp, ctypes.POINTER(_i64)],
     "geig_set_option": [_vp, ctypes.c_int, _i64],
     "geig_set_partition": [_vp, ctypes.c_int, ctypes.c_int],
@@ -90,7 +91,7 @@ _lib.geig_version.restype = ctypes.c_char_p
 
 EXPORTED = ["geig_create", "geig_destroy", "geig_set_stream", "geig_sync", "geig_init_state",
             "geig_set_state", "geig_get", "geig_products_cca", "geig_products_dense", "geig_update",
-            "geig_step_cca", "geig_step_dense", "geig_run_dense", "geig_run_cca", "geig_step_cca_host", "geig_get_gram",
+            "geig_step_cca", "geig_step_dense", "geig_run_dense", "geig_run_cca", "geig_step_cca_host", "geig_run_cca_host", "geig_get_gram",
             "geig_set_smooth", "geig_smooth_state", "geig_set_adam",
             "geig_launch_count", "geig_last_error", "geig_version", "geig_update_phase_ns",
             "geig_table_floats", "geig_products_cca_tables", "geig_update_tables", "geig_set_option",
@@ -237,6 +238,19 @@ def geig_step_cca_host(h, X_host, Y_host, b: int, eta: float, gamma: float, ga_h
     _check(_lib.geig_step_cca_host(h, _ptr(X_host, device=False), _ptr(Y_host, device=False), b, eta,
                                    gamma, _ptr(ga_host, torch.float32, device=False),
                                    ctypes.byref(h2d), ctypes.byref(d2h)))
+    return h2d.value, d2h.value
+
+
+def geig_run_cca_host(h, Xs_host, Ys_host, b: int, eta: float, gamma: float, ga_host=None):
+    """T steps from pinned host batches (lists of tensors); returns (h2d, d2h) bytes."""
+    n = len(Xs_host)
+    if len(Ys_host) != n:
+        raise ValueError("Xs_host and Ys_host differ in length")
+    xs = (_vp * n)(*[_ptr(x, device=False) for x in Xs_host])
+    ys = (_vp * n)(*[_ptr(y, device=False) for y in Ys_host])
+    h2d, d2h = _i64(0), _i64(0)
+    _check(_lib.geig_run_cca_host(h, xs, ys, b, n, eta, gamma, _ptr(ga_host, torch.float32, device=False),
+                                  ctypes.byref(h2d), ctypes.byref(d2h)))
     return h2d.value, d2h.value
 
 

@@ -200,3 +200,39 @@ def test_small_path_declines_what_it_cannot_hold(geig):
             assert s.launches() - l0 > 1
         finally:
             s.close()
+
+
+@pytest.mark.parametrize("cfg_idx,math,rows", [(1, "f32", 256), (2, "bf16x2", 1024)])
+def test_run_cca_host_pipeline_equals_device_steps(geig, cfg_idx, math, rows):
+    """geig_run_cca_host (pinned host batches; the copy of batch t + 1 on a
+    copy stream overlaps step t) leaves exactly the state of the same steps
+    on device copies, and reports the bytes it moved."""
+    from synth import CONFIGS, cca_views
+    cfg = CONFIGS[cfg_idx]
+    T = 5
+    x, y = cca_views(cfg, 2 * rows, seed=41)
+    hx = [x[:rows].contiguous().pin_memory(), x[rows:].contiguous().pin_memory()]
+    hy = [y[:rows].contiguous().pin_memory(), y[rows:].contiguous().pin_memory()]
+    V, aux = random_state(cfg.k, cfg.d, 42)
+    dev = "cuda:0"
+    flag = 1 if x.dtype == torch.bfloat16 else 0
+    out = []
+    for host in (True, False):
+        s = geig.Solver(geig.GEIG_CCA, cfg.dx, cfg.dy, cfg.k, math=math, data_dtype=flag, rho=cfg.rho, max_rows=rows)
+        try:
+            s.set_state(torch.tensor(V, dtype=torch.float32, device=dev), torch.tensor(aux, dtype=torch.float32, device=dev))
+            if host:
+                ga = torch.empty(cfg.k, cfg.k).pin_memory()
+                h2d, d2h = geig.geig_run_cca_host(s.h, [hx[t % 2] for t in range(T)], [hy[t % 2] for t in range(T)],
+                                                  rows, cfg.eta, cfg.gamma, ga)
+                assert h2d == T * (hx[0].numel() * hx[0].element_size() + hy[0].numel() * hy[0].element_size())
+                assert d2h == T * cfg.k * cfg.k * 4
+            else:
+                for t in range(T):
+                    geig.geig_step_cca(s.h, hx[t % 2].to(dev), hy[t % 2].to(dev), rows, cfg.eta, cfg.gamma)
+            out.append([t_.cpu().numpy() for t_ in s.state()] + [s.gram()[0].cpu().numpy()])
+        finally:
+            s.close()
+    for a, b_ in zip(out[0], out[1]):
+        assert np.array_equal(a, b_)
+    assert np.array_equal(ga.numpy(), out[1][2])
