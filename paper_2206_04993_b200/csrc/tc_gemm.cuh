@@ -632,6 +632,12 @@ inline geig_status launch(const TcMaps& maps, const TcParams& p, dim3 grid, cuda
     else e = launch_one<EB, A_MN, 3, true>(maps, p, grid, st);
   } else {
     if (one_per_sm && smem_bytes(p.BN, 8) <= 227 * 1024) e = launch_one<EB, A_MN, 8, false>(maps, p, grid, st);
+    else if (ctas <= 2 * nsm && smem_bytes(p.BN, 3) <= 113 * 1024)
+      // up to two CTAs per SM: every CTA of the grid resident at once, so the
+      // HBM stream is shared by all tiles to the end instead of a ragged
+      // second wave (config 4: 256 tiles on 148 SMs); 3 stages per CTA keep
+      // 192 KB in flight per SM
+      e = launch_one<EB, A_MN, 3, false>(maps, p, grid, st);
     else e = launch_one<EB, A_MN, 4, false>(maps, p, grid, st);
   }
   if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("tc_gemm launch: ") + cudaGetErrorString(e));
