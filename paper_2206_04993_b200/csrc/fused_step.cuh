@@ -1090,6 +1090,9 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
   FusedMaps maps;
   FusedParams p{};
   if (update_only && (products_only || nsteps != 1)) return tc_fail(GEIG_ERR_ARG, "update-only launch: one step");
+  const UpdateArgs upd_in = upd;                     // (the fallback below relaunches with the caller's arguments)
+  const int grid_in = grid_ctas;
+  const size_t upd_bytes_in = upd_bytes;
   // CTA pairs (full steps): every 256-column backward tile of both views is
   // one pair's item and each CTA of the pair updates 128 of its columns
   // (the update then covers d / 128 CTAs: used where that is most of the grid)
@@ -1324,8 +1327,14 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
     ca.val.clusterDim.x = 2; ca.val.clusterDim.y = 1; ca.val.clusterDim.z = 1;
     oc.attrs = &ca;
     oc.numAttrs = 1;
-    if (cudaOccupancyMaxActiveClusters(&ncl, kfn, &oc) != cudaSuccess || 2 * ncl < grid_ctas)
-      return tc_fail(GEIG_ERR_UNSUPPORTED, "CTA pairs: the grid's clusters are not co-resident");
+    if (cudaOccupancyMaxActiveClusters(&ncl, kfn, &oc) != cudaSuccess || 2 * ncl < grid_ctas) {
+      // not every pair fits at once (another context holds SMs, MPS limits):
+      // this plan falls back to one CTA per item, cooperative launch
+      cudaGetLastError();
+      t.opt_pairs = 0;
+      return fused_cca_step(t, X, Y, nsteps, b, scale, Vbf, AV, BV, upd_in, grid_in, upd_bytes_in, st, products_only,
+                            tables, update_only, own, pair_grid);
+    }
   }
   cudaError_t e = launch_coop(kfn, dim3(grid_ctas), dim3(FS_THREADS), args, smem, st, t.l2win, pair ? 2 : 0, !pair || pair_coop);
   if (e != cudaSuccess) return tc_fail(GEIG_ERR_CUDA, std::string("cca_step_kernel launch: ") + cudaGetErrorString(e));
