@@ -125,6 +125,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+def _dense_traffic(math, world):
+    """DRAM bytes of one config-4 products launch from an ncu --set full
+    capture (profiles/roofline_traffic_dense.json), for the captured math at
+    N = 1; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic_dense.json")) as f:
+            tr = json.load(f)
+        return tr["dram_bytes_per_launch"] if tr.get("math") == math and world == 1 else None
+    except Exception:
+        return None
+
+
 def _workload(cfg, math):
     return {"workload": cfg.name, "problem": cfg.problem, "dx": cfg.dx, "dy": cfg.dy, "k": cfg.k,
             "batch_per_gpu": cfg.batch, "math": math, "data_dtype": cfg.dtype,
@@ -311,7 +323,7 @@ def run_gpu_dense(args, cfg, rank, world, dev, stream, peaks, peaks_src):
     box_copy = _box_copy_gbs(dev)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peaks.get("hbm_gbs", 6650.0), "unit": "GB/s",
             "frac": achieved / peaks.get("hbm_gbs", 6650.0), "box_copy_gbs": box_copy,
-            "frac_of_box_copy": (achieved / box_copy) if box_copy else None, "traffic": None,
+            "frac_of_box_copy": (achieved / box_copy) if box_copy else None, "traffic": _dense_traffic(math, world),
             "algorithmic_bytes": alg_bytes, "peak_source": peaks_src,
             "kernel": f"tc_gemm products of the rank's rows of A and B ({math})", "ms_per_launch": prod_ms,
             "step_ms": elapsed_ms / args.steps, "products_share": prod_ms / (elapsed_ms / args.steps),
