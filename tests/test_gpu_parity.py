@@ -774,3 +774,35 @@ def test_gram_tensor_cores_match_ffma_gram(geig, math, d, k):
         V2, aux2 = game.step_alg2(V, aux, [(av0, bv0)], eta, 1.0, rho)
         assert rel_err(out[1][0] - V, V2 - V) < 1e-4
         assert rel_err(out[1][1], aux2) < 1e-4
+
+
+@pytest.mark.parametrize("k,rows", [(40, 1000), (17, 2050), (64, 258)])
+def test_fused_pairs_other_k_and_ragged_batches(geig, k, rows):
+    """CTA pairs with k not a multiple of 32 (the drain reads TMEM columns
+    past k, which must not reach the tiles) and ragged batches (h not a
+    multiple of the 64-row K blocks): the pair step against one CTA per
+    item and against the oracle."""
+    from synth import CONFIGS, cca_views
+    cfg = CONFIGS[3]
+    x, y = cca_views(cfg, rows, seed=19)
+    V, aux = random_state(k, cfg.d, 13)
+    V32 = V.astype(np.float32).astype(np.float64)
+    aux32 = aux.astype(np.float32).astype(np.float64)
+    dev = "cuda:0"
+    out = []
+    for pairs in (1, 0):
+        s = geig.Solver(geig.GEIG_CCA, cfg.dx, cfg.dy, k, math="bf16x2", data_dtype=geig.GEIG_DATA_BF16,
+                        rho=cfg.rho, max_rows=rows)
+        try:
+            geig.geig_set_option(s.h, geig.GEIG_OPT_FUSED_PAIRS, pairs)
+            s.set_state(torch.tensor(V32, dtype=torch.float32, device=dev),
+                        torch.tensor(aux32, dtype=torch.float32, device=dev))
+            geig.geig_step_cca(s.h, x.to(dev), y.to(dev), rows, 0.02, cfg.gamma)
+            out.append([t.double().cpu().numpy() for t in s.state()])
+        finally:
+            s.close()
+    (Vp, ap), (Vs, as_) = out
+    assert rel_err(Vp - V32, Vs - V32) < 1e-5 and rel_err(ap, as_) < 1e-5
+    _, _, Vo, Ao = oracle_cca_step(x.double().numpy(), y.double().numpy(), V32, aux32, 0.02, cfg.gamma, cfg.rho)
+    assert rel_err(Vp - V32, Vo - V32) < 1e-3
+    assert rel_err(ap, Ao) < 1e-4
