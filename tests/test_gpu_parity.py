@@ -181,7 +181,11 @@ def test_cca_config2_bf16_tcgen05(geig):
 
 
 def test_cca_config3_full_size_bf16_tcgen05(geig):
-    """Config 3 at full size in the launch configuration bench.py times."""
+    """Config 3 at full size, plain bf16 operands, through the products
+    launch + update launch (AV, BV compared too).  The configuration
+    bench.py times — bf16x2, geig_run_cca, CTA pairs — is held to the oracle
+    by test_run_cca_matches_single_steps_and_oracle[bf16x2-3-4096-...] and
+    test_fused_pairs_match_single_ctas."""
     errs, _ = check_cca_step(geig, 3, 4096, math="bf16")
     _assert(errs, 1e-2)
 
