@@ -374,6 +374,14 @@ geig_status geig_get_gram(geig_solver* s, float* GA, float* GB, float* GC);
  *                             the backward accumulators move into the update
  *                             through distributed shared memory instead of
  *                             global memory; 0 = one CTA per item
+ *  GEIG_OPT_SMALL_CLUSTER   : CTAs (a thread-block cluster) of the small-problem
+ *                             CCA step: each takes a contiguous share of every
+ *                             batch's rows and owns a block of the update's
+ *                             columns; the products, Gram tables and v'' are
+ *                             combined through distributed shared memory in
+ *                             rank order (deterministic).  0 = (default) auto:
+ *                             the largest power of 2 <= 8 leaving >= 64 rows
+ *                             and >= 16 columns per CTA; 1, 2, 4, 8 = forced
  *  GEIG_OPT_GRAM_TC         : 1 = (default) the streamed update (k > 64) of a
  *                             tf32 / 3xTF32 solver forms its Gram tables
  *                             G^A, G^C on the tensor cores (one launch of
@@ -385,7 +393,8 @@ geig_status geig_get_gram(geig_solver* s, float* GA, float* GB, float* GC);
  *                             F, S, B of the fused kernel; 0 = fused (default)
  * Errors: GEIG_ERR_ARG for an unknown option or a value out of range. */
 typedef enum { GEIG_OPT_FUSED_M_TILES = 1, GEIG_OPT_STAGED_PRODUCTS = 2, GEIG_OPT_SMALL_STEP = 3,
-               GEIG_OPT_FUSED_PAIRS = 4, GEIG_OPT_GRAM_TC = 5 } geig_option;
+               GEIG_OPT_FUSED_PAIRS = 4, GEIG_OPT_GRAM_TC = 5,
+               GEIG_OPT_SMALL_CLUSTER = 6 } geig_option;
 geig_status geig_set_option(geig_solver* s, int option, int64_t value);
 
 /* Phase durations (ns, %globaltimer of CTA 0) of the last update:

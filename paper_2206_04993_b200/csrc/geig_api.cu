@@ -102,6 +102,7 @@ struct geig_solver {
   // one-CTA small-problem step (small_step.cuh)
   int opt_small = 1;                                  // geig_set_option(GEIG_OPT_SMALL_STEP)
   int opt_gram_tc = 1;                                // geig_set_option(GEIG_OPT_GRAM_TC)
+  int opt_small_cluster = 0;                          // geig_set_option(GEIG_OPT_SMALL_CLUSTER): 0 auto, else CTAs
   const void** ptab_dev = nullptr;                    // per-step batch pointers of a run (device, pinned staging)
   const void** ptab_host = nullptr;
   cudaEvent_t ptab_ev = nullptr;
@@ -621,6 +622,7 @@ static void advance_variant_state(geig_solver* s, int64_t n) {
 struct SmallPlan {
   bool ok = false;
   int KP = 8, rc = 0, dpad = 0, RG = 1;
+  int C = 1, bq = 0, dq = 0;                           // cluster CTAs, rows / columns per CTA
   size_t smem = 0;
 };
 
@@ -643,7 +645,16 @@ static SmallPlan small_plan(const geig_solver* s, int64_t b) {
     pl.ok = pl.smem <= (size_t)SM_SMEM_MAX;
     return pl;
   }
-  const int b4 = (int)((b + 3) / 4 * 4);
+  // a cluster of C CTAs splits the rows of every batch (and owns column
+  // blocks of the update): auto = the largest power of 2 <= 8 leaving >= 64
+  // rows and >= 16 columns per CTA
+  if (s->opt_small_cluster > 0) pl.C = s->opt_small_cluster;
+  else
+    while (pl.C < 8 && b / (2 * pl.C) >= 64 && d / (2 * pl.C) >= 16) pl.C *= 2;
+  pl.bq = (int)(((b + pl.C - 1) / pl.C + 3) / 4 * 4);
+  pl.dq = (int)(((d + pl.C - 1) / pl.C + 3) / 4 * 4);
+  if ((int64_t)(pl.C - 1) * pl.bq >= b || (int64_t)(pl.C - 1) * pl.dq >= d) { pl.C = 1; pl.bq = (int)b; pl.dq = (int)d; }
+  const int b4 = (int)((pl.bq + 3) / 4 * 4);
   for (int rc = std::min(b4, 1024); rc >= 4; rc -= 4) {
     const size_t need = small_smem_bytes(false, pl.KP, (int)d, s->k, rc, pl.dpad, es);
     if (need <= (size_t)SM_SMEM_MAX) { pl.rc = rc; pl.smem = need; pl.ok = true; break; }
@@ -685,6 +696,9 @@ static geig_status small_launch(geig_solver* s, const SmallPlan& pl, const void*
   p.smooth = s->smooth; p.zbuf = s->zbuf; p.zpar = s->zpar;
   p.lnrho = logf(std::max(s->rho, 1e-30f)); p.lnnu = logf(std::max(s->nu, 1e-30f));
   p.rc = pl.rc; p.dpad = pl.dpad; p.RG = pl.RG;
+  p.cl = dense ? 1 : pl.C;
+  p.bq = dense ? 0 : pl.bq;
+  p.dq = dense ? p.d : pl.dq;
   p.ts = nullptr;
   p.prof = tc::dbg_ptr();   // developer hook (geig_debug_set_tc_stamps): per-phase cycles
   const bool bf = s->dtype == GEIG_DATA_BF16;
@@ -695,7 +709,21 @@ static geig_status small_launch(geig_solver* s, const SmallPlan& pl, const void*
   const int ai = (bf ? 2 : 0) + (pl.KP == 8 ? 0 : 1);
   CU(set_smem_attr_once(attr[ai], fn, SM_SMEM_MAX));
   void* args[] = {&p};
-  CU(cudaLaunchKernel(fn, dim3(1), dim3(SM_THREADS), args, pl.smem, s->stream));
+  if (p.cl > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.cl);
+    cfg.blockDim = dim3(SM_THREADS);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = s->stream;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = (unsigned)p.cl; at.val.clusterDim.y = 1; at.val.clusterDim.z = 1;
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelExC(&cfg, fn, args));
+  } else {
+    CU(cudaLaunchKernel(fn, dim3(1), dim3(SM_THREADS), args, pl.smem, s->stream));
+  }
   s->launches++;
   s->fused_last = false;
   advance_variant_state(s, nsteps);
@@ -1177,6 +1205,10 @@ extern "C" geig_status geig_set_option(geig_solver* s, int option, int64_t value
     case GEIG_OPT_FUSED_PAIRS:
       if (value < 0 || value > 2) return fail(GEIG_ERR_ARG, "GEIG_OPT_FUSED_PAIRS must be 0, 1 or 2");
       s->tc.opt_pairs = (int)value;
+      return GEIG_OK;
+    case GEIG_OPT_SMALL_CLUSTER:
+      if (value < 0 || value > 8 || (value & (value - 1))) return fail(GEIG_ERR_ARG, "GEIG_OPT_SMALL_CLUSTER: 0 (auto), 1, 2, 4 or 8");
+      s->opt_small_cluster = (int)value;
       return GEIG_OK;
     case GEIG_OPT_GRAM_TC:
       if (value != 0 && value != 1) return fail(GEIG_ERR_ARG, "GEIG_OPT_GRAM_TC must be 0 or 1");

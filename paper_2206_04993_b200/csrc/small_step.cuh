@@ -39,11 +39,13 @@
 // into smem ONCE per launch and the products are the forward tile loop with
 // the rows of A (B) in place of the batch rows.
 #pragma once
+#include <cooperative_groups.h>
 #include "common.cuh"
 #include "tc_gemm.cuh"
 
 namespace geig {
 
+namespace cgs = cooperative_groups;
 constexpr int SM_THREADS = 512;
 constexpr int SM_SMEM_MAX = 227 * 1024;
 
@@ -72,6 +74,9 @@ struct SmallParams {
   int RG;                    // row groups of the backward (1, 2 or 4)
   unsigned long long* ts;    // %globaltimer at start / end (nullable, CTA 0)
   unsigned long long* prof;  // developer: clock64 cycles per phase summed over the launch (8 slots), nullable
+  int cl;                    // CTAs of the thread-block cluster running the step (1: one CTA): CTA r takes
+                             // rows [r bq, (r + 1) bq) of every batch and owns columns [r dq, (r + 1) dq)
+  int bq, dq;                // rows / columns per cluster rank (dq a multiple of 4)
 };
 
 // developer phase profile: thread 0 adds the cycles since the last mark to slot `ph`
@@ -226,7 +231,9 @@ small_step_kernel(const SmallParams p) {
   float* D1s = IS2 + KP;
   float* D2s = D1s + KP;
   float* Lt = D2s + KP;                             // [KP][KP] Lt[j][i] = L_ij
-  uint64_t* full = reinterpret_cast<uint64_t*>(Lt + KP * KP + ((KP * KP) & 1));   // 2 mbarriers (8-byte aligned)
+  float* pt = Lt + KP * KP;                         // cluster: this CTA's partial tables [tri A | tri C | B | N]
+  const int npt = 2 * ntri + 2 * KP;
+  uint64_t* full = reinterpret_cast<uint64_t*>(pt + npt + ((KP * KP + npt) & 1));   // 2 mbarriers (8-byte aligned)
   // chunk buffers, 16-byte aligned (the same offset as small_smem_bytes)
   const size_t ring_off = ((size_t)(reinterpret_cast<float*>(full + 2) - Vs) + 3) & ~(size_t)3;
   T* ring = reinterpret_cast<T*>(Vs + ring_off);
@@ -250,7 +257,14 @@ small_step_kernel(const SmallParams p) {
     Cs[i * ldv + c] = i < k ? p.AUX[e] : 0.f;
   }
   __syncthreads();
-  const int nchunks = p.dense ? 1 : (p.b + p.rc - 1) / p.rc;
+  // cluster rank: rows [rlo, rhi) of every batch, own columns [clo, chi)
+  cgs::cluster_group cluster = cgs::this_cluster();
+  const int C = p.cl;
+  const int rank = C > 1 ? (int)cluster.block_rank() : 0;
+  const int rlo = p.dense ? 0 : min(p.b, rank * p.bq), rhi = p.dense ? 0 : min(p.b, rlo + p.bq);
+  const int clo = C > 1 ? min(d, rank * p.dq) : 0, chi = C > 1 ? min(d, clo + p.dq) : d;
+  const int nrows = rhi - rlo;
+  const int nchunks = p.dense ? 1 : max(1, (nrows + p.rc - 1) / p.rc);
   auto batch = [&](int t, int v) -> const T* {
     return reinterpret_cast<const T*>(p.xs ? p.xs[2 * t + v] : (v == 0 ? p.x0 : p.y0));
   };
@@ -260,7 +274,7 @@ small_step_kernel(const SmallParams p) {
       sm_stage_rows<T>(buf0, batch(0, 0), batch(0, 0), d, 0, p.rc, 0, d, &full[0]);
       sm_stage_rows<T>(buf1, batch(0, 1), batch(0, 1), d, 0, p.rc, 0, d, &full[1]);
     } else {
-      sm_stage_rows<T>(buf0, batch(0, 0), batch(0, 1), dx, p.dy, p.rc, 0, min(p.rc, p.b), &full[0]);
+      sm_stage_rows<T>(buf0, batch(0, 0), batch(0, 1), dx, p.dy, p.rc, rlo, min(p.rc, nrows), &full[0]);
     }
   }
 
@@ -291,7 +305,7 @@ small_step_kernel(const SmallParams p) {
       if (t == 0) { tc::mbar_wait(&full[0], 0); tc::mbar_wait(&full[1], 0); }   // A, B resident
     } else {
       for (int c = 0; c < nchunks; ++c, ++q) {
-        const int r0 = c * p.rc, nr = min(p.rc, p.b - r0);
+        const int r0 = rlo + c * p.rc, nr = min(p.rc, rhi - r0);
         // next chunk (of this step or of the next one) into the other buffer:
         // its previous contents were last read before the barrier that ended
         // the previous chunk
@@ -299,8 +313,8 @@ small_step_kernel(const SmallParams p) {
           int tn = t, cn = c + 1;
           if (cn == nchunks) { tn = t + 1; cn = 0; }
           if (tn < p.nsteps)
-            sm_stage_rows<T>(((q & 1) ? buf0 : buf1), batch(tn, 0), batch(tn, 1), dx, p.dy, p.rc, cn * p.rc,
-                             min(p.rc, p.b - cn * p.rc), &full[(q + 1) & 1]);
+            sm_stage_rows<T>(((q & 1) ? buf0 : buf1), batch(tn, 0), batch(tn, 1), dx, p.dy, p.rc, rlo + cn * p.rc,
+                             min(p.rc, nrows - cn * p.rc), &full[(q + 1) & 1]);
         }
         tc::mbar_wait(&full[q & 1], (uint32_t)((q >> 1) & 1));
         pf.mark(prof, 0);
@@ -420,13 +434,55 @@ small_step_kernel(const SmallParams p) {
           const int i = e - 2 * ntri - k;
           a = Vs + i * ldv; b2 = a; dst = rN + i;
         }
+        // G'^A, G'^B are linear in the products: with a cluster each CTA sums
+        // its row partials over ALL columns (no reduce-scatter needed first);
+        // G'^C, ||v''||^2 need [Bv] / the state only where they are current:
+        // the own columns
+        const bool own_only = e >= ntri && (e < 2 * ntri || e >= 2 * ntri + k);
+        const int c_lo = own_only ? clo : 0, c_hi = own_only ? chi : d;
         float sum = 0.f;
         if (dst)
-          for (int c = l8; c < d; c += 8) sum = fmaf(a[c], b2[c], sum);
+          for (int c = c_lo + l8; c < c_hi; c += 8) sum = fmaf(a[c], b2[c], sum);
         sum += __shfl_xor_sync(0xffffffffu, sum, 4);
         sum += __shfl_xor_sync(0xffffffffu, sum, 2);
         sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-        if (dst && l8 == 0) *dst = sum;
+        if (dst && l8 == 0) {
+          if (C > 1) dst = pt + (dst - rA);   // the cluster sum below forms rA.. from every CTA's pt
+          *dst = sum;
+        }
+      }
+    }
+    if (C > 1) {
+      // ONE cluster barrier: every CTA's row-partial products and partial
+      // tables are complete.  The tables are summed over the ranks (rank
+      // order: identical in every CTA) and the products reduce-scattered:
+      // this CTA sums its own columns of every CTA's As / Bs in place (the
+      // others read only their own columns of these tiles)
+      cluster.sync();
+      {
+        const int nc = chi - clo;
+        for (int e = tid; e < 2 * k * nc; e += SM_THREADS) {
+          const int h = e / (k * nc), r = e - h * k * nc, i = r / nc, c = clo + (r - i * nc);
+          float* loc = (h ? Bs : As) + i * ldv + c;
+          float vq[8];
+#pragma unroll
+          for (int q2 = 0; q2 < 8; ++q2) vq[q2] = q2 < C ? *cluster.map_shared_rank(loc, q2) : 0.f;   // all in flight
+          float v = 0.f;
+#pragma unroll
+          for (int q2 = 0; q2 < 8; ++q2) v += vq[q2];   // rank order (the zeros past C are exact)
+          *loc = v;
+        }
+      }
+      for (int e = tid; e < 2 * ntri + 2 * k; e += SM_THREADS) {
+        // offsets of [tri A | tri C | B (k of KP) | N (k of KP)]
+        const int oo = e < 2 * ntri + k ? e : 2 * ntri + KP + (e - 2 * ntri - k);
+        float vq[8];
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2) vq[q2] = q2 < C ? *cluster.map_shared_rank(pt + oo, q2) : 0.f;
+        float v = 0.f;
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2) v += vq[q2];
+        rA[oo] = v;
       }
     }
     __syncthreads();
@@ -445,8 +501,10 @@ small_step_kernel(const SmallParams p) {
           const float sg = 1.f / (1.f + expf(-z));
           const float br = expf(p.lnrho + (p.lnnu - p.lnrho) * sg);
           is2 = 1.f / br;
-          float* zw = p.zbuf + ((p.zpar + t + 1) & 1) * 64;
-          zw[i] = z + p.gamma * (gcii - br) * br * (p.lnnu - p.lnrho) * sg * (1.f - sg);
+          if (rank == 0) {
+            float* zw = p.zbuf + ((p.zpar + t + 1) & 1) * 64;
+            zw[i] = z + p.gamma * (gcii - br) * br * (p.lnnu - p.lnrho) * sg * (1.f - sg);
+          }
         } else {
           is2 = 1.f / fmaxf(gcii, p.rho);
         }
@@ -470,16 +528,17 @@ small_step_kernel(const SmallParams p) {
       }
       D2s[i] = i < k ? Ns[i] * Ns[i] * rA[sm_tri(i, i)] - c : 0.f;
     }
+    const int nc = chi - clo;                       // this CTA's columns (all of them when C == 1)
     if (t + 1 == p.nsteps) {
       // the last step's products to global memory (before the update reuses Bs)
-      for (int e = tid; e < k * d; e += SM_THREADS) {
-        const int i = e / d, c = e - i * d;
-        p.AV[e] = As[i * ldv + c];
-        p.BV[e] = Bs[i * ldv + c];
+      for (int e = tid; e < k * nc; e += SM_THREADS) {
+        const int i = e / nc, c = clo + (e - i * nc);
+        p.AV[(int64_t)i * d + c] = As[i * ldv + c];
+        p.BV[(int64_t)i * d + c] = Bs[i * ldv + c];
       }
     }
     __syncthreads();
-    if (t + 1 == p.nsteps) {
+    if (t + 1 == p.nsteps && rank == 0) {
       // the last step's normalised tables (geig_get_gram)
       for (int e = tid; e < k * k; e += SM_THREADS) {
         const int i = e / k, j = e - (e / k) * k;
@@ -492,8 +551,8 @@ small_step_kernel(const SmallParams p) {
     }
     pf.mark(prof, 5);
     // ---- U: direction, ascent, aux moving average (new aux into Bs, then swap) ----
-    for (int e = tid; e < k * d; e += SM_THREADS) {
-      const int i = e / d, c = e - i * d;
+    for (int e = tid; e < k * nc; e += SM_THREADS) {
+      const int i = e / nc, c = clo + (e - i * nc);
       const int o = i * ldv + c;
       float pen = 0.f;
       for (int j = 0; j < i; ++j) pen = fmaf(Lt[j * KP + i], Cs[j * ldv + c], pen);
@@ -504,19 +563,34 @@ small_step_kernel(const SmallParams p) {
       Bs[o] = xa + p.gamma * (ni * bv - xa);
     }
     __syncthreads();
+    if (C > 1) {
+      // every CTA's next forward reads all of v'': the own columns into the
+      // other CTAs' copies (distributed shared memory), then a cluster barrier
+      for (int e = tid; e < k * nc; e += SM_THREADS) {
+        const int i = e / nc, c = clo + (e - i * nc);
+        const float v = Vs[i * ldv + c];
+        for (int q2 = 0; q2 < C; ++q2)
+          if (q2 != rank) *cluster.map_shared_rank(Vs + i * ldv + c, q2) = v;
+      }
+      cluster.sync();
+    }
     pf.mark(prof, 6);
     { float* tmp = Cs; Cs = Bs; Bs = tmp; }
   }
-  // ---- state back to global memory ----
-  for (int e = tid; e < k * d; e += SM_THREADS) {
-    const int i = e / d, c = e - i * d;
-    const float v = Vs[i * ldv + c];
-    p.V[e] = v;
-    p.AUX[e] = Cs[i * ldv + c];
-    if (p.Vbf) {
-      const __nv_bfloat16 hv = __float2bfloat16_rn(v);
-      p.Vbf[e] = hv;
-      p.Vbf[(int64_t)k * d + e] = __float2bfloat16_rn(v - __bfloat162float(hv));
+  // ---- state back to global memory (this CTA's columns) ----
+  {
+    const int nc = chi - clo;
+    for (int e2 = tid; e2 < k * nc; e2 += SM_THREADS) {
+      const int i = e2 / nc, c = clo + (e2 - i * nc);
+      const int64_t e = (int64_t)i * d + c;
+      const float v = Vs[i * ldv + c];
+      p.V[e] = v;
+      p.AUX[e] = Cs[i * ldv + c];
+      if (p.Vbf) {
+        const __nv_bfloat16 hv = __float2bfloat16_rn(v);
+        p.Vbf[e] = hv;
+        p.Vbf[(int64_t)k * d + e] = __float2bfloat16_rn(v - __bfloat162float(hv));
+      }
     }
   }
   if (prof) {
@@ -533,8 +607,9 @@ small_step_kernel(const SmallParams p) {
 // Host: smem bytes of a configuration (0 = does not fit).
 inline size_t small_smem_bytes(bool dense, int KP, int d, int k, int rc, int dpad, size_t es) {
   const int ntri = k * (k + 1) / 2;
-  size_t fl = (size_t)4 * KP * (d + 4) + (dense ? 0 : (size_t)rc * (2 * KP + 4)) + 2 * ntri + 6 * KP + KP * KP +
-              ((KP * KP) & 1) + 4;
+  const int npt = 2 * ntri + 2 * KP;
+  size_t fl = (size_t)4 * KP * (d + 4) + (dense ? 0 : (size_t)rc * (2 * KP + 4)) + 2 * ntri + 6 * KP + KP * KP + npt +
+              ((KP * KP + npt) & 1) + 4;
   fl = (fl + 3) & ~(size_t)3;   // ring 16-byte aligned
   (void)dpad;
   const size_t ring = 2 * (size_t)rc * d * es;   // dense: rc = d rounded up to 4

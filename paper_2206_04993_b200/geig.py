@@ -19,7 +19,8 @@ GEIG_OK, GEIG_ERR_ARG, GEIG_ERR_CUDA, GEIG_ERR_UNSUPPORTED, GEIG_ERR_STATE = ran
 GEIG_DENSE, GEIG_CCA = 0, 1
 GEIG_MATH_F32, GEIG_MATH_BF16, GEIG_MATH_TF32, GEIG_MATH_3XTF32, GEIG_MATH_BF16X2 = 0, 1, 2, 3, 4
 GEIG_DATA_F32, GEIG_DATA_BF16 = 0, 1
-GEIG_OPT_FUSED_M_TILES, GEIG_OPT_STAGED_PRODUCTS, GEIG_OPT_SMALL_STEP, GEIG_OPT_FUSED_PAIRS, GEIG_OPT_GRAM_TC = 1, 2, 3, 4, 5
+GEIG_OPT_FUSED_M_TILES, GEIG_OPT_STAGED_PRODUCTS, GEIG_OPT_SMALL_STEP, GEIG_OPT_FUSED_PAIRS, GEIG_OPT_GRAM_TC, \
+    GEIG_OPT_SMALL_CLUSTER = 1, 2, 3, 4, 5, 6
 
 MATH_NAMES = {"f32": GEIG_MATH_F32, "bf16": GEIG_MATH_BF16, "tf32": GEIG_MATH_TF32,
               "3xtf32": GEIG_MATH_3XTF32, "bf16x2": GEIG_MATH_BF16X2}

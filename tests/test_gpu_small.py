@@ -236,3 +236,51 @@ def test_run_cca_host_pipeline_equals_device_steps(geig, cfg_idx, math, rows):
     for a, b_ in zip(out[0], out[1]):
         assert np.array_equal(a, b_)
     assert np.array_equal(ga.numpy(), out[1][2])
+
+
+@pytest.mark.parametrize("cl", [1, 2, 4, 8])
+@pytest.mark.parametrize("rows,k,dx,dy", [(256, None, None, None), (3001, 13, 60, 52)])
+def test_small_cluster_sizes_match_oracle_and_runs(geig, cl, rows, k, dx, dy):
+    """The small-problem step on a thread-block cluster of cl CTAs (rows split
+    over the CTAs, the products reduce-scattered, the Gram tables summed and
+    v'' all-gathered through distributed shared memory in rank order): each
+    cluster size matches the oracle's Alg. 2 over 3 steps at the fp32 bar,
+    and a 3-step geig_run_cca equals 3 geig_step_cca calls bit for bit."""
+    from synth import CONFIGS, cca_views
+    cfg = CONFIGS[1]
+    k = k or cfg.k
+    dx, dy = dx or cfg.dx, dy or cfg.dy
+    T = 3
+    x, y = cca_views(cfg, T * rows, seed=51)
+    x, y = x[:, :dx].contiguous(), y[:, :dy].contiguous()
+    batches = [(x[t * rows:(t + 1) * rows], y[t * rows:(t + 1) * rows]) for t in range(T)]
+    V, aux = random_state(k, dx + dy, 52)
+    V32 = V.astype(np.float32).astype(np.float64)
+    aux32 = aux.astype(np.float32).astype(np.float64)
+    dev = "cuda:0"
+    Xd = [b_[0].to(dev).contiguous() for b_ in batches]
+    Yd = [b_[1].to(dev).contiguous() for b_ in batches]
+    states = []
+    for run in (True, False):
+        s = geig.Solver(geig.GEIG_CCA, dx, dy, k, math="f32", rho=cfg.rho, max_rows=rows)
+        try:
+            geig.geig_set_option(s.h, geig.GEIG_OPT_SMALL_CLUSTER, cl)
+            s.set_state(torch.tensor(V32, dtype=torch.float32, device=dev),
+                        torch.tensor(aux32, dtype=torch.float32, device=dev))
+            l0 = s.launches()
+            if run:
+                geig.geig_run_cca(s.h, Xd, Yd, rows, cfg.eta, cfg.gamma)
+            else:
+                for t in range(T):
+                    geig.geig_step_cca(s.h, Xd[t], Yd[t], rows, cfg.eta, cfg.gamma)
+                assert s.launches() - l0 == T
+            Vg, Ag = s.state()
+            states.append((Vg.cpu().numpy(), Ag.cpu().numpy()))
+        finally:
+            s.close()
+    assert np.array_equal(states[0][0], states[1][0]) and np.array_equal(states[0][1], states[1][1])
+    Vo, Ao = V32, aux32
+    for xb, yb in batches:
+        _, _, Vo, Ao = oracle_cca_step(xb.double().numpy(), yb.double().numpy(), Vo, Ao, cfg.eta, cfg.gamma, cfg.rho)
+    assert rel_err(states[0][0] - V32, Vo - V32) < 1e-4
+    assert rel_err(states[0][1], Ao) < 1e-4
