@@ -150,8 +150,8 @@ __device__ __forceinline__ void stamp(const UpdateArgs& p, int slot) {
 }
 
 __host__ __device__ constexpr size_t upd_smem_floats(int NB) {
-  // double buffer of 4 tiles + phase-3 Lt + n, s^2, D1, D2
-  return (size_t)2 * 4 * (NB * 64) * UPD_S + (size_t)(NB * 64) * (NB * 64) + 4 * (NB * 64);
+  // double buffer of 4 tiles + phase-3 Lt (row stride KP + 4) + n, s^2, D1, D2
+  return (size_t)2 * 4 * (NB * 64) * UPD_S + (size_t)(NB * 64) * (NB * 64 + 4) + 4 * (NB * 64);
 }
 __host__ __device__ constexpr size_t upd_partial_floats(int NB) { return 2 * (NB * 64) * (NB * 64) + 2 * (NB * 64); }
 
@@ -172,15 +172,18 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // Stage rows [0, KP) x columns [x0, x0+32) of the four k x d arrays into
 // tiles[4][KP][UPD_S]; rows >= k and columns >= xend are zero-filled.
 template <int KP, bool VEC>
-__device__ __forceinline__ void stage_tiles(float* tiles, const float* const* src, int k, int64_t d, int64_t x0,
-                                            int64_t xend) {
+__device__ __forceinline__ void stage_tiles(float* tiles, const float* s0, const float* s1, const float* s2,
+                                            const float* s3, int k, int64_t d, int64_t x0, int64_t xend) {
   if (VEC) {
     constexpr int Q = UPD_XC / 4;                 // float4 per row
     for (int e = threadIdx.x; e < 4 * KP * Q; e += UPD_THREADS) {
       const int a = e / (KP * Q), rem = e % (KP * Q), r = rem / Q, q = rem % Q;
       const int64_t gx = x0 + 4 * q;
       const bool ok = r < k && gx < xend;
-      const float* s = ok ? src[a] + (int64_t)r * d + gx : src[a];
+      // (four pointer arguments: a runtime-indexed pointer array lived in
+      // local memory — ncu: 7% of the k > 64 update's stall samples)
+      const float* base = a == 0 ? s0 : a == 1 ? s1 : a == 2 ? s2 : s3;
+      const float* s = ok ? base + (int64_t)r * d + gx : base;
       cp_async16(tiles + ((size_t)a * KP + r) * UPD_S + 4 * q, s, ok ? 16 : 0);
     }
   } else {
@@ -188,7 +191,8 @@ __device__ __forceinline__ void stage_tiles(float* tiles, const float* const* sr
       const int a = e / (KP * UPD_XC), rem = e % (KP * UPD_XC), r = rem / UPD_XC, x = rem % UPD_XC;
       const int64_t gx = x0 + x;
       const bool ok = r < k && gx < xend;
-      const float* s = ok ? src[a] + (int64_t)r * d + gx : src[a];
+      const float* base = a == 0 ? s0 : a == 1 ? s1 : a == 2 ? s2 : s3;
+      const float* s = ok ? base + (int64_t)r * d + gx : base;
       cp_async4(tiles + ((size_t)a * KP + r) * UPD_S + x, s, ok ? 4 : 0);
     }
   }
@@ -212,7 +216,7 @@ update_kernel(UpdateArgs p) {
   const int64_t c0 = (int64_t)blockIdx.x * p.segw;
   const int64_t c1 = min(d, c0 + p.segw);
   const int nsub = c1 > c0 ? (int)((c1 - c0 + UPD_XC - 1) / UPD_XC) : 0;
-  const float* src[4] = {p.V, p.AV, p.AUX, p.BV};   // tile order: 0 V', 1 AV', 2 AUX, 3 BV'
+  // tile order (stage_tiles): 0 V', 1 AV', 2 AUX, 3 BV'
   stamp(p, 0);
 
   // ---------------- phase 1: Gram partial sums of this CTA's columns ----------------
@@ -230,7 +234,7 @@ update_kernel(UpdateArgs p) {
         const float* vr = p.V + (int64_t)i * d;
         const float* br = p.BV + (int64_t)i * d;
         if (VEC) {
-#pragma unroll 4
+#pragma unroll 8
           for (int64_t x = c0 + 4 * h; x < c1; x += 8) {
             const float4 v = *reinterpret_cast<const float4*>(vr + x);
             const float4 bb = *reinterpret_cast<const float4*>(br + x);
@@ -264,12 +268,12 @@ update_kernel(UpdateArgs p) {
 #pragma unroll
     for (int q = 0; q < KP / 8; ++q) gb[q] = nn[q] = 0.f;
 
-    if (nsub > 0) stage_tiles<KP, VEC>(buf0, src, k, d, c0, c1);
+    if (nsub > 0) stage_tiles<KP, VEC>(buf0, p.V, p.AV, p.AUX, p.BV, k, d, c0, c1);
     cp_async_commit();
     for (int sc = 0; sc < nsub; ++sc) {
       float* cur = (sc & 1) ? buf1 : buf0;
       float* nxt = (sc & 1) ? buf0 : buf1;
-      if (sc + 1 < nsub) stage_tiles<KP, VEC>(nxt, src, k, d, c0 + (int64_t)(sc + 1) * UPD_XC, c1);
+      if (sc + 1 < nsub) stage_tiles<KP, VEC>(nxt, p.V, p.AV, p.AUX, p.BV, k, d, c0 + (int64_t)(sc + 1) * UPD_XC, c1);
       cp_async_commit();
       cp_async_wait<1>();
       __syncthreads();
@@ -362,12 +366,15 @@ update_kernel(UpdateArgs p) {
   stamp(p, 1);
 
   // ---------------- phase 2: reduce the per-CTA partials -> raw tables ----------------
-  // lanes over 32 consecutive entries, warps over the partial index (fixed order).
+  // Warp w of CTA c reduces the 32-entry groups c + G w, c + G (w + 8), ...:
+  // each lane sums one entry over all G partial rows in a fixed order (8
+  // interleaved accumulators, 32 loads in flight per lane), so a CTA's groups
+  // proceed in parallel instead of one group per pair of CTA barriers (ncu:
+  // the group-at-a-time loop was a chain of L2 round trips, ~10 us).
   {
-    float* red = smem;                            // [8][32]
     const int ngroups = (PSTRIDE + 31) / 32;
     const int G = gridDim.x;
-    for (int grp = blockIdx.x; grp < ngroups; grp += G) {
+    for (int grp = blockIdx.x + G * warp; grp < ngroups; grp += G * (UPD_THREADS / 32)) {
       const int e = grp * 32 + lane;
       bool ok = e < PSTRIDE;
       if (ok && e < 2 * KP * KP) {
@@ -376,27 +383,21 @@ update_kernel(UpdateArgs p) {
       } else if (ok) {
         ok = (e - 2 * KP * KP) % KP < k;
       }
-      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
       if (ok) {
         const float* srcp = p.partial + e;
-        int b = warp;
-        for (; b + 24 < G; b += 32) {
-          s0 += srcp[(size_t)b * PSTRIDE];
-          s1 += srcp[(size_t)(b + 8) * PSTRIDE];
-          s2 += srcp[(size_t)(b + 16) * PSTRIDE];
-          s3 += srcp[(size_t)(b + 24) * PSTRIDE];
-        }
-        for (; b < G; b += 8) s0 += srcp[(size_t)b * PSTRIDE];
-      }
-      red[warp * 32 + lane] = (s0 + s1) + (s2 + s3);
-      __syncthreads();
-      if (warp == 0 && ok) {
-        float s = 0.f;
+        float s[8];
 #pragma unroll
-        for (int w = 0; w < 8; ++w) s += red[w * 32 + lane];
-        p.raw[e] = s;
+        for (int u = 0; u < 8; ++u) s[u] = 0.f;
+        int b = 0;
+#pragma unroll 4
+        for (; b + 8 <= G; b += 8)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) s[u] += __ldcg(srcp + (size_t)(b + u) * PSTRIDE);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (b + u < G) s[u] += __ldcg(srcp + (size_t)(b + u) * PSTRIDE);
+        p.raw[e] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
       }
-      __syncthreads();
     }
   }
   dstamp(p, 11);
@@ -408,8 +409,12 @@ update_kernel(UpdateArgs p) {
   // Normalisation folded in (retraction of the previous step, Alg. 2 line 17):
   // n_i = 1/||v'_i||, v_i = n_i v'_i, AV_i = n_i AV'_i, BV_i = n_i BV'_i, so
   // G^A_ij = n_i n_j G'^A_ij, G^C_ij = n_i G'^C_ij, G^B_ii = n_i^2 G'^B_ii.
-  float* Lt = smem + 8 * TILE;                   // [KP][KP]  Lt[j][i]
-  float* Ns = Lt + KP * KP;                      // n_i
+  // Lt[j][i] = L_ij, row stride KP + 4: the coefficient loop stores it with
+  // lanes over j (stride KP was a 32-way bank conflict, ncu: 32x the ideal
+  // wavefronts), the penalty loop reads float4 rows of 4 consecutive i
+  constexpr int LTS = KP + 4;
+  float* Lt = smem + 8 * TILE;                   // [KP][LTS]
+  float* Ns = Lt + KP * LTS;                      // n_i
   float* S2 = Ns + KP;                           // s_j^2 = max(G^C_jj, rho)
   float* D1s = S2 + KP;                          // G^B_ii
   float* D2s = D1s + KP;                         // G^A_ii - c_i
@@ -445,18 +450,24 @@ update_kernel(UpdateArgs p) {
       Ns[i] = n; S2[i] = s2; D1s[i] = gb;
     }
     __syncthreads();
+    // 1 / s_j^2 once per j (the loop below divided k^2 times per CTA)
+    float rs2[KP / 32];
+#pragma unroll
+    for (int m = 0; m < KP / 32; ++m) rs2[m] = 1.f / S2[lane + 32 * m];
     for (int i = warp; i < KP; i += UPD_THREADS / 32) {
       const float ni = Ns[i];
       float c = 0.f;
-      for (int j = lane; j < KP; j += 32) {
+#pragma unroll
+      for (int m = 0; m < KP / 32; ++m) {
+        const int j = lane + 32 * m;
         float l = 0.f;
         if (i < k && j < i) {
           const float ga = ni * Ns[j] * sA[i * KP + j];
           const float gc = ni * sC[i * KP + j];
-          l = D1s[i] * ga / S2[j];
-          c = fmaf(ga, gc / S2[j], c);
+          l = D1s[i] * ga * rs2[m];
+          c = fmaf(ga, gc * rs2[m], c);
         }
-        Lt[j * KP + i] = l;
+        Lt[j * LTS + i] = l;
       }
       c = warp_sum(c);
       if (lane == 0) D2s[i] = i < k ? ni * ni * sA[i * KP + i] - c : 0.f;
@@ -490,12 +501,12 @@ update_kernel(UpdateArgs p) {
     const int hh = (tid >> 3) & 1;
     const int q = tid >> 4;
     const int i0 = NB == 2 ? 4 * (hh ? 31 - q : q) : 4 * (tid >> 3);
-    if (nsub > 0) stage_tiles<KP, VEC>(buf0, src, k, d, c0, c1);
+    if (nsub > 0) stage_tiles<KP, VEC>(buf0, p.V, p.AV, p.AUX, p.BV, k, d, c0, c1);
     cp_async_commit();
     for (int sc = 0; sc < nsub; ++sc) {
       float* cur = (sc & 1) ? buf1 : buf0;
       float* nxt = (sc & 1) ? buf0 : buf1;
-      if (sc + 1 < nsub) stage_tiles<KP, VEC>(nxt, src, k, d, c0 + (int64_t)(sc + 1) * UPD_XC, c1);
+      if (sc + 1 < nsub) stage_tiles<KP, VEC>(nxt, p.V, p.AV, p.AUX, p.BV, k, d, c0 + (int64_t)(sc + 1) * UPD_XC, c1);
       cp_async_commit();
       cp_async_wait<1>();
       __syncthreads();
@@ -524,8 +535,8 @@ update_kernel(UpdateArgs p) {
         for (; j0 < jm1; j0 += 8) {      // both groups
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const float4 l1 = *reinterpret_cast<const float4*>(Lt + (j0 + u) * KP + r1);
-            const float4 l2 = *reinterpret_cast<const float4*>(Lt + (j0 + u) * KP + r2);
+            const float4 l1 = *reinterpret_cast<const float4*>(Lt + (j0 + u) * LTS + r1);
+            const float4 l2 = *reinterpret_cast<const float4*>(Lt + (j0 + u) * LTS + r2);
             const float4 x = *reinterpret_cast<const float4*>(Ct + (j0 + u) * UPD_S + 4 * tx);
             const float lv1[4] = {l1.x, l1.y, l1.z, l1.w}, lv2[4] = {l2.x, l2.y, l2.z, l2.w};
             const float xv[4] = {x.x, x.y, x.z, x.w};
@@ -543,7 +554,7 @@ update_kernel(UpdateArgs p) {
           float4 l[4], x[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            l[u] = *reinterpret_cast<const float4*>(Lt + (j0 + u) * KP + r2);
+            l[u] = *reinterpret_cast<const float4*>(Lt + (j0 + u) * LTS + r2);
             x[u] = *reinterpret_cast<const float4*>(Ct + (j0 + u) * UPD_S + 4 * tx);
           }
 #pragma unroll
@@ -571,7 +582,7 @@ update_kernel(UpdateArgs p) {
           float4 l[4], x[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            l[u] = *reinterpret_cast<const float4*>(Lt + (j0 + u) * KP + i0);
+            l[u] = *reinterpret_cast<const float4*>(Lt + (j0 + u) * LTS + i0);
             x[u] = *reinterpret_cast<const float4*>(Ct + (j0 + u) * UPD_S + 4 * tx);
           }
 #pragma unroll
