@@ -145,7 +145,11 @@ def allgather_blocks(blocks: torch.Tensor, group=None):
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(blocks.view(-1), blocks[rank].reshape(-1), group=group)
+        # raw bytes: the shadow is an int16 view, a dtype torch's NCCL binding
+        # does not map; the in-place form (input = this rank's slice of the
+        # output) moves no local copy
+        raw = blocks.view(torch.uint8) if blocks.element_size() == 2 else blocks
+        dist.all_gather_into_tensor(raw.view(-1), raw[rank].reshape(-1), group=group)
     else:
         # host copies as raw bytes (gloo has no int16 / bf16 all-gather)
         raw = blocks.view(torch.uint8) if blocks.element_size() == 2 else blocks

@@ -54,3 +54,10 @@ print("phase durations (clock64 us, medians):", " ".join(out), f"| total {prev:.
 dg = (t[:, 14] - t[:, 0]).double()
 dc = (t[:, 46] - t[:, 32]).double()
 print("effective SM clock over the kernel (clock64 / globaltimer): median %.0f MHz" % statistics.median((dc / dg * 1e3).tolist()))
+# stragglers: the CTAs that reach a stamp last (CTA id: us after the median)
+ids = torch.nonzero(buf.view(-1, 64)[:, 0].cpu() > 0).flatten().tolist()
+for j in (2, 30, 3, 24, 25, 4, 5, 17, 18, 7, 8, 21, 22, 14):
+    col = ((t[:, j] - t0).double() / 1e3)
+    med = col.median().item()
+    top = torch.argsort(col, descending=True)[:8].tolist()
+    print(f"late at {names[j]:12s} (median {med:6.2f}):", " ".join(f"{ids[i]}:+{col[i].item() - med:.2f}" for i in top))
