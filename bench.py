@@ -156,14 +156,16 @@ def _blas_threads():
         return os.cpu_count()
 
 
-def oracle_sample(cfg, seconds: float, max_steps: int | None = None, seed: int = 0):
+def oracle_sample(cfg, seconds: float, max_steps: int | None = None, seed: int = 0, rows_per_step: int | None = None):
     """Time the oracle (as it stands) on real steps of the workload until
-    `seconds` of CPU work or `max_steps`; returns (rows/s, steps, rows)."""
+    `seconds` of CPU work or `max_steps`; returns (rows/s, steps, rows).
+    rows_per_step: a bounded sample of the batch (the first rows) per step."""
     import numpy as np
     from oracle import estimators, game
     from synth import cca_views, dense_gep_small, gaussian_init
     if cfg.problem == "cca":
-        x, y = cca_views(cfg, cfg.batch, seed=seed)
+        b = rows_per_step or cfg.batch
+        x, y = cca_views(cfg, b, seed=seed)
         x64, y64 = x.double().numpy(), y.double().numpy()
         V, aux = game.init_state(gaussian_init(cfg.k, cfg.d, seed))
         n, rows, t0 = 0, 0, time.perf_counter()
@@ -171,7 +173,7 @@ def oracle_sample(cfg, seconds: float, max_steps: int | None = None, seed: int =
             av, bv = estimators.cca_products(x64, y64, V)
             V, aux = game.step_alg2(V, aux, [(av, bv)], cfg.eta, cfg.gamma, cfg.rho)
             n += 1
-            rows += cfg.batch
+            rows += b
             el = time.perf_counter() - t0
             if el >= seconds or (max_steps and n >= max_steps):
                 return rows / el, n, rows, el
@@ -200,10 +202,20 @@ def oracle_sample(cfg, seconds: float, max_steps: int | None = None, seed: int =
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
-    # warmup steps (untimed), then K timed steps, each a full oracle step
-    oracle_sample(cfg, 0.0, max_steps=max(1, args.warmup))
-    # K full oracle steps, bounded to ~150 s of host time (the line reports the steps run)
-    v, n, rows, el = oracle_sample(cfg, 150.0, max_steps=args.steps)
+    # one untimed full step warms the BLAS threads up and sizes the run: the
+    # K timed steps are full oracle steps when they fit ~120 s of host time,
+    # else each step runs on a bounded sample of the batch (its first rows,
+    # the oracle's cost being linear in the rows) so that EXACTLY K steps are
+    # timed.  A dense step (full batch by definition) cannot be sampled: its
+    # run is bounded in time and the line reports the steps run.
+    _, _, _, t1 = oracle_sample(cfg, 0.0, max_steps=1)
+    _, _, _, t1 = oracle_sample(cfg, 0.0, max_steps=1)
+    rows_step = None
+    sample = f"full oracle steps of {cfg.batch if cfg.problem == 'cca' else 'full-batch'} rows"
+    if cfg.problem == "cca" and args.steps * t1 > 120.0:
+        rows_step = max(64, int(cfg.batch * 120.0 / (args.steps * t1)) // 2 * 2)
+        sample = f"oracle steps on the first {rows_step} of {cfg.batch} rows of the batch"
+    v, n, rows, el = oracle_sample(cfg, 300.0 if rows_step else 150.0, max_steps=args.steps, rows_per_step=rows_step)
     unit = "samples/s" if cfg.problem == "cca" else "steps/s"
     cores = _blas_threads()
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": unit, "n_gpus": world,
@@ -211,7 +223,7 @@ def run_reference(args, cfg, rank, world):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _workload(cfg, "f64-oracle"),
             "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "oracle",
-                             "sample": f"{n} full oracle steps of {cfg.batch if cfg.problem == 'cca' else 'full-batch'} rows"},
+                             "sample": f"{n} {sample}"},
             "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
