@@ -482,36 +482,43 @@ __device__ __forceinline__ void pair_exchange(const FusedParams& p, const UpdMap
   __syncthreads();
   if (threadIdx.x == 128) tstamp(p.upd, 15);
   if (threadIdx.x == 0) {
-    // this step's tile barrier: V'' and [Bv] of the own columns (TMA) and the
-    // partner's pushed tile; then announce to the partner that it may push.
+    // this step's tile barrier (initialised, with its fences, by this thread
+    // at the start of phase B — off this critical path): V'' and [Bv] of the
+    // own columns (TMA) and the partner's pushed tile; then announce to the
+    // partner that it may push.
     // (V'' and [Bv] were last written by the previous step's update with
     // generic stores: ordered for the async proxy by this thread's
     // fence.proxy.async.global at the start of this step's phase F)
-    mbar_init(tbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(tbar, (uint32_t)(2 * 64 * S * 4) + (has ? push_bytes : 0u));
     const int c0 = (int)((int64_t)blockIdx.x * W);
     tma_load_2d(Vt, &um.t[0], tbar, c0, 0);
     tma_load_2d(Ct, &um.t[2], tbar, c0, 0);
+    // relaxed: the announcement publishes no data of this CTA — the partner's
+    // push writes this CTA's tile through the async proxy, the MMAs that read
+    // that smem have completed (accf), and the tile barrier's init was released
+    // to the cluster by the fence.mbarrier_init at the start of phase B (a
+    // release fence followed by this strong relaxed arrive is a release
+    // pattern).  A release here cost ~0.7 us/step on the B -> U hand-off.
     if (has)
-      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_map(freebar, peer))
+      asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_map(freebar, peer))
                    : "memory");
     tstamp(p.upd, 16);
   }
   if (has) {
-    // all 8 warps drain: warps 0-3 M tile 0, warps 4-7 M tile 1 (a warp
-    // reaches TMEM lanes 32 (warp % 4) .. + 31)
+    // all 8 warps drain, the partner's M tile first (its push then crosses
+    // DSMEM while the own tile is drained): warps w and w + 4 reach TMEM lanes
+    // 32 (w % 4) .. + 31 and split the players in blocks of 32
     __syncwarp();                                   // (thread 0 ran the tile-barrier block alone)
     if (warp < 4) tc_fence_after();
     const int ew = warp & 3;
     const int acols = p.BN * (p.splitB ? 2 : 1);
     const int m = ew * 32 + lane;                   // this thread's column within the M tile (TMEM lane)
-    {
-      const int mtile = warp >> 2;
-      float* dst = ((uint32_t)mtile == rank ? tile : stage) + m;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      const int mtile = (int)(pass == 0 ? peer : rank);
+      float* dst = (pass == 0 ? stage : tile) + m;
       const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(mtile * acols);
-      for (int c0 = 0; c0 < p.BN; c0 += 32) {
+      for (int c0 = (warp >> 2) * 32; c0 < p.BN; c0 += 64) {
         uint32_t r0[16], r1[16], l0[16], l1[16];
         tmem_ld16_nw(tb + (uint32_t)c0, r0);
         tmem_ld16_nw(tb + (uint32_t)(c0 + 16), r1);
@@ -530,6 +537,22 @@ __device__ __forceinline__ void pair_exchange(const FusedParams& p, const UpdMap
           if (n1 < p.k) dst[n1 * S] = p.scale * a1;
         }
       }
+      if (pass == 0) {
+        // the staged tile is read by the bulk copy (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 3, 256;" ::: "memory");
+        if (threadIdx.x == 128) {
+          tstamp(p.upd, 17);
+          mbar_wait(freebar, (uint32_t)(t & 1));    // the partner's ring is free, its tile barrier armed
+          asm volatile(
+              "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  cluster_map(tile, peer)),
+              "r"(smem_u32(stage)), "r"(push_bytes), "r"(cluster_map(tbar, peer))
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        __syncwarp();
+      }
     }
     if (threadIdx.x == 128) tstamp(p.upd, 18);
     tc_fence_before();
@@ -537,22 +560,9 @@ __device__ __forceinline__ void pair_exchange(const FusedParams& p, const UpdMap
       mbar_arrive(acce_bar);
       ++rs.items;
     }
-    // the staged tile is read by the bulk copy (async proxy)
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("bar.sync 3, 256;" ::: "memory");
-    if (threadIdx.x == 128) {
-      tstamp(p.upd, 17);
-      mbar_wait(freebar, (uint32_t)(t & 1));        // the partner's ring is free, its tile barrier armed
-      asm volatile(
-          "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              cluster_map(tile, peer)),
-          "r"(smem_u32(stage)), "r"(push_bytes), "r"(cluster_map(tbar, peer))
-          : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      // without early coefficients the update stages its tables right after
-      // the four tiles, i.e. over the staging tile: the push must have read it
-      if (!p.early_coef) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    }
+    // without early coefficients the update stages its tables right after
+    // the four tiles, i.e. over the staging tile: the push must have read it
+    if (threadIdx.x == 128 && !p.early_coef) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
   __syncthreads();                                   // the own-column tile (generic stores) is complete
 }
@@ -831,6 +841,16 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   if (threadIdx.x == 0) {
     asm volatile("fence.proxy.async.global;" ::: "memory");   // Zb of every CTA's phase S, read by TMA below
     for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&A[2 + v]); tma_prefetch_desc(&maps.bB[v]); }
+    if (p.pair) {
+      // CTA pairs: this step's update-tile barrier, initialised here so that
+      // the init and its fences are off the B -> U hand-off (pair_exchange
+      // arms it; nothing arrives on it before this CTA's announcement there)
+      mbar_init(acce_bar + 2, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tma_prefetch_desc(&maps.um.t[0]);
+      tma_prefetch_desc(&maps.um.t[2]);
+    }
   }
   if (warp == 2 || warp == 3) {    // warps 2-3: reduce the (now complete) Gram partial rows
     if (!p.products_only || p.tables) {
@@ -880,7 +900,8 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   if (p.pair) {
     // the update needs the Gram reduction of every CTA (coefficients) and the
     // backward accumulators of the pair (exchanged through DSMEM)
-    if (threadIdx.x == 0 && p.rcnt) spin_geq_trap(p.rcnt, (t + 1) * (int)gridDim.x);
+    // (with early coefficients warps 2-3 have waited for it in phase B)
+    if (threadIdx.x == 0 && p.rcnt && !p.early_coef) spin_geq_trap(p.rcnt, (t + 1) * (int)gridDim.x);
     pair_exchange(p, maps.um, smem, accf_bar, acce_bar, acce_bar + 2, freebar, tmem_base, rs, t,
                   2 * (p.mtB[0] + p.mtB[1]));
     if (kDevKnobs && (p.dbg_mode & 16384)) {   // developer: the exchanged tiles to AV / BV (global)

@@ -39,7 +39,7 @@ for j, nm in names.items():
     col = ((t[:, j] - t0).double() / 1e3).tolist()
     ck = ((t[:, 32 + j] - t[:, 32]).double() / MHZ).tolist() if j != 15 else [0]
     print(f"  {j:2d} {nm:12s} {min(col):7.2f} {statistics.median(col):7.2f} {max(col):7.2f} | {statistics.median(ck):7.2f}")
-order = [0, 1, 2, 3, 23, 24, 25, 26, 4, 5, 17, 6, 7, 8, 27, 28, 9, 10, 11, 12, 19, 20, 13, 21, 22, 14]
+order = [0, 1, 2, 3, 23, 24, 25, 26, 4, 5, 17, 6, 7, 8, 27, 28, 9, 10, 11, 12, 13, 21, 22, 14]
 prev = None
 out = []
 for j in order:
