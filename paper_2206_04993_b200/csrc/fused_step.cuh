@@ -1232,7 +1232,12 @@ inline geig_status fused_cca_step(TcPlan& t, const void* const* X, const void* c
     int nB2 = 0;
     for (int v = 0; v < 2; ++v) nB2 += 2 * (int)((dv[v] + 2 * TC_BM - 1) / (2 * TC_BM));
     p.tmB = fixed ? fixed : (2 * nB2 >= grid_ctas ? 2 : 1);
-    p.tmF = fixed ? fixed : (rows >= 8 * TC_BM ? 2 : 1);
+    // forward: 2 tiles only beside a 2-tile backward or for a long batch — with
+    // a 1-tile backward the smaller stage of 1-tile items gives the ring up to
+    // 8 stages (config 2: all 8 K blocks of a backward item in flight at once)
+    // and halves the forward's split-K partials (same-box A/B over 7 shapes,
+    // scripts/mtiles_time.py: 1.5-10 % faster except b = 8192)
+    p.tmF = fixed ? fixed : ((rows >= 8 * TC_BM && (p.tmB == 2 || rows >= 64 * TC_BM)) ? 2 : 1);
     if (dev_knob("GEIG_TMF")) p.tmF = std::max(1, std::min(2, atoi(dev_knob("GEIG_TMF"))));   // developer A/B knobs
     if (dev_knob("GEIG_TMB")) p.tmB = std::max(1, std::min(2, atoi(dev_knob("GEIG_TMB"))));
     for (int v = 0; v < 2; ++v) p.mtB[v] = (int)((dv[v] + p.tmB * TC_BM - 1) / (p.tmB * TC_BM));
