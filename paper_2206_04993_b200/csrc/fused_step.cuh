@@ -920,7 +920,8 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     // the update phase of this CTA needs the Gram reduction of every CTA and
     // the backward items of its own columns [c W, (c + 1) W) only
     if (threadIdx.x == 0) {
-      if (p.rcnt) spin_geq_trap(p.rcnt, (t + 1) * (int)gridDim.x);
+      // (with early coefficients warps 2-3 have waited for the reduction in phase B)
+      if (p.rcnt && !p.early_coef) spin_geq_trap(p.rcnt, (t + 1) * (int)gridDim.x);
       const int64_t W = p.upd.segw;
       const int64_t c0 = (int64_t)blockIdx.x * W, c1 = min(p.d, c0 + W);
       for (int v = 0; v < 2; ++v) {
