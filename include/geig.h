@@ -353,8 +353,10 @@ geig_status geig_get_gram(geig_solver* s, float* GA, float* GB, float* GC);
  * floating-point summation order).  No environment variable is read by the
  * library.
  *  GEIG_OPT_FUSED_M_TILES   : 128-row M tiles per work item of the fused
- *                             step's GEMM phases (0 = auto: 2 where the grid
- *                             stays busy, else 1; 1; 2)
+ *                             step's GEMM phases (0 = auto: backward 2 where
+ *                             the 256-column tiles keep the grid busy, else 1;
+ *                             forward 2 beside a 2-tile backward or for
+ *                             batches of >= 8192 rows, else 1; 1; 2)
  *  GEIG_OPT_SMALL_STEP      : 1 = (default) fp32 (GEIG_MATH_F32) steps of
  *                             small problems — k <= 16, KP d <= 8192 (KP = k rounded up to 8 or 16) and
  *                             the state plus a chunk of rows (CCA) or A and
