@@ -266,7 +266,7 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
   const uint32_t idesc = A_MN ? p.idescB : p.idescF;
   Item it;
   if (threadIdx.x == 0) {
-    // ---------------- TMA producer ----------------
+    // ---------------- TMA producer (lane 0 of the converged warp 0) ----------------
     const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
     for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x) {
       if (A_MN) decode_backward(M, A, p, idx, it); else decode_forward(M, A, p, idx, it);
@@ -307,8 +307,8 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
         }
       }
     }
-  } else if (threadIdx.x == 32) {
-    // ---------------- MMA issuer ----------------
+  } else if (warp == 1 && elect_one()) {
+    // ---------------- MMA issuer (lane 0 of the converged warp 1) ----------------
     for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++rs.items) {
       if (A_MN) decode_backward(M, A, p, idx, it); else decode_forward(M, A, p, idx, it);
       if (rs.items > 0) mbar_wait(acce_bar, (rs.items - 1) & 1);   // epilogue drained the accumulator

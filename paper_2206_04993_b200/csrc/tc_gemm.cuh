@@ -50,6 +50,20 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// one elected lane of a converged warp (elect.sync): unlike a threadIdx test,
+// the compiler then treats the lane's operands of the uniform-datapath
+// instructions (UTMALDG, UTCHMMA) as uniform instead of wrapping every issue
+// in an elect / broadcast loop
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -283,8 +297,8 @@ tc_gemm_kernel(const __grid_constant__ TcMaps maps, const TcParams p) {
           if constexpr (SPLIT) tma_load_2d(sb + B_BYTES, &maps.blo[g * 2 + s], &full_bar[st], k0, 0);
         }
       }
-    } else if (threadIdx.x == 32) {
-      // ---------------- MMA issuer ----------------
+    } else if ((threadIdx.x >> 5) == 1 && elect_one()) {
+      // ---------------- MMA issuer (lane 0 of the converged warp 1) ----------------
       int it = 0;
       for (int s = 0; s < p.nseg; ++s) {
         const uint32_t d_tmem = tmem_base + (uint32_t)(s * BN);
