@@ -307,6 +307,17 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
         }
       }
     }
+    if (!A_MN) {
+      // off the critical path (this thread now only waits for the phase to
+      // end): the descriptors of phase B and of the update tiles
+      for (int v = 0; v < 4; ++v) {
+        tma_prefetch_desc(&A[2 + v]);
+        tma_prefetch_desc(&M.bB[v]);
+        if (split) tma_prefetch_desc(&M.bBlo[v]);
+      }
+      tma_prefetch_desc(&M.um.t[0]);
+      tma_prefetch_desc(&M.um.t[2]);
+    }
   } else if (warp == 1 && elect_one()) {
     // ---------------- MMA issuer (lane 0 of the converged warp 1) ----------------
     for (int idx = blockIdx.x; idx < nitems; idx += gridDim.x, ++rs.items) {
@@ -668,9 +679,6 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   stamp(p.upd, 5);
   dstamp(p.upd, 3);
 
-  if (threadIdx.x == 0)   // the backward's descriptors, ahead of phase B
-    for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&A[2 + v]); tma_prefetch_desc(&maps.bB[v]); }
-
   // ---- phase S: sum partials, route halves, cast to bf16; Gram tables G^A, G^B ----
   // CTA c owns a contiguous range of sample rows of each half.  For every
   // row it sums the split-K partials of z = X_v v''^T (both views, both
@@ -840,7 +848,8 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   // ---- phase B: backward products into AV, BV ----
   if (threadIdx.x == 0) {
     asm volatile("fence.proxy.async.global;" ::: "memory");   // Zb of every CTA's phase S, read by TMA below
-    for (int v = 0; v < 4; ++v) { tma_prefetch_desc(&A[2 + v]); tma_prefetch_desc(&maps.bB[v]); }
+    // (the backward's descriptors were prefetched by this thread at the end
+    // of its forward producer loop, where it only waits for the epilogue)
     if (p.pair) {
       // CTA pairs: this step's update-tile barrier, initialised here so that
       // the init and its fences are off the B -> U hand-off (pair_exchange
@@ -848,8 +857,6 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
       mbar_init(acce_bar + 2, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tma_prefetch_desc(&maps.um.t[0]);
-      tma_prefetch_desc(&maps.um.t[2]);
     }
   }
   if (warp == 2 || warp == 3) {    // warps 2-3: reduce the (now complete) Gram partial rows
