@@ -661,16 +661,18 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     // phase S of this CTA reads the split-K partials of its own rows only:
     // wait for the forward items of those 128-row tiles (both halves)
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 || threadIdx.x == 32) {
+      // thread 0 polls the tiles of the rows in half 0, thread 32 those in
+      // half 1: the two L2 round trips overlap (the CTA barrier below joins them)
       const int U = (((p.h & 3) == 0) && ((p.ldz & 3) == 0) && ((p.hpad & 3) == 0)) ? 4 : 1;   // as phase S
       const int nu = p.h / U;
       const int ua = (int)((int64_t)nu * blockIdx.x / gridDim.x), ub = (int)((int64_t)nu * (blockIdx.x + 1) / gridDim.x);
       const int target = (t + 1) * p.fper;
-      if (ub > ua)
-        for (int half = 0; half < 2; ++half) {
-          const int r0 = half * p.h + ua * U, r1 = half * p.h + ub * U - 1;
-          for (int tile = r0 / TC_BM; tile <= r1 / TC_BM; ++tile) spin_geq_trap(p.fcnt + tile, target);
-        }
+      if (ub > ua) {
+        const int half = threadIdx.x >> 5;
+        const int r0 = half * p.h + ua * U, r1 = half * p.h + ub * U - 1;
+        for (int tile = r0 / TC_BM; tile <= r1 / TC_BM; ++tile) spin_geq_trap(p.fcnt + tile, target);
+      }
     }
     __syncthreads();
   } else {
