@@ -852,10 +852,11 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     asm volatile("fence.proxy.async.global;" ::: "memory");   // Zb of every CTA's phase S, read by TMA below
     // (the backward's descriptors were prefetched by this thread at the end
     // of its forward producer loop, where it only waits for the epilogue)
-    if (p.pair) {
-      // CTA pairs: this step's update-tile barrier, initialised here so that
-      // the init and its fences are off the B -> U hand-off (pair_exchange
-      // arms it; nothing arrives on it before this CTA's announcement there)
+    if (!p.products_only && !dev_tbar_in_ring(p)) {
+      // this step's update-tile barrier, initialised here so that the init
+      // and its fences are off the B -> U hand-off (CTA pairs: pair_exchange
+      // arms it and nothing arrives on it before this CTA's announcement
+      // there; else the update phase arms it)
       mbar_init(acce_bar + 2, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -989,7 +990,8 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
   if (!p.products_only && !(kDevKnobs && (p.dbg_mode & 64)))
     update_res_phases<true, 1, ADAM>(p.upd, reinterpret_cast<float*>(smem), grid, &maps.um, t,
                                      p.early_coef ? coef_smem : nullptr,
-                                     dev_tbar_in_ring(p) ? nullptr : acce_bar + 2);
+                                     dev_tbar_in_ring(p) ? nullptr : acce_bar + 2,
+                                     !p.update_only && !dev_tbar_in_ring(p));
   if (p.pair && threadIdx.x == 128) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging reusable
   if (t + 1 < p.nsteps) {
     // next step: its forward TMA reads the new bf16 shadow of V (generic

@@ -866,7 +866,10 @@ __device__ __forceinline__ void coef_early(const UpdateArgs& p, float* cf, int s
 template <bool VEC, int PRE = -1, bool ADAM = true>
 __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* smem, cg::grid_group& grid,
                                                   const UpdMaps* um = nullptr, int step = 0,
-                                                  float* coef = nullptr, uint64_t* tbar_ext = nullptr) {
+                                                  float* coef = nullptr, uint64_t* tbar_ext = nullptr,
+                                                  bool tbar_ready = false) {
+  // tbar_ready: the caller initialised tbar_ext (with the init and shared-memory
+  // proxy fences) earlier, off this critical path (fused kernel: start of phase B)
   // coef: coefficients already formed (coef_early, fused kernel) — no table
   // staging, phase 3a skipped
   const int tid = threadIdx.x;
@@ -915,13 +918,15 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
       // fused CTA pairs: AV, BV tiles written by pair_exchange, V'' and [Bv]
       // in flight on the tile barrier (waited below)
     } else {
-    if (tid == 0) {
+    if (warp == 0 && tc::elect_one()) {   // (elected lane: no elect / broadcast loop around the TMA issues)
       asm volatile("fence.proxy.async.global;" ::: "memory");   // state / products written by generic stores
-      tc::mbar_init(tbar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      // smem last written through the async proxy (GEMM ring) or generic
-      // stores of a previous use: order them before the TMA writes below
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (!tbar_ready) {
+        tc::mbar_init(tbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // smem last written through the async proxy (GEMM ring) or generic
+        // stores of a previous use: order them before the TMA writes below
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
       tc::mbar_expect_tx(tbar, (uint32_t)(4 * 64 * S * 4));
       float* dst[4] = {Vt, At, Ct, Bt};
 #pragma unroll
