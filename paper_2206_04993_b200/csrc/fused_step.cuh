@@ -251,7 +251,8 @@ template <int EB, bool A_MN>
 __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap* A, const FusedParams& p, int nitems,
                                            uint8_t* ring,
                                            uint64_t* full_bar, uint64_t* empty_bar, uint64_t* accf_bar,
-                                           uint64_t* acce_bar, uint32_t tmem_base, RingState& rs, float* epi) {
+                                           uint64_t* acce_bar, uint32_t tmem_base, RingState& rs, float* epi,
+                                           uint64_t* tbar_init = nullptr, const CUtensorMap* Anext = nullptr) {
   constexpr int ATOM = 128 / EB;
   constexpr int BK = ATOM;
   constexpr int UK = 32 / EB;
@@ -317,6 +318,10 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
       }
       tma_prefetch_desc(&M.um.t[0]);
       tma_prefetch_desc(&M.um.t[2]);
+    } else if (Anext) {
+      // the next step's forward descriptors, while this thread waits for the
+      // backward to end
+      for (int v = 0; v < 2; ++v) tma_prefetch_desc(Anext + v);
     }
   } else if (warp == 1 && elect_one()) {
     // ---------------- MMA issuer (lane 0 of the converged warp 1) ----------------
@@ -354,6 +359,17 @@ __device__ __forceinline__ void gemm_phase(const FusedMaps& M, const CUtensorMap
         }
       }
       umma_commit(accf_bar);
+    }
+    if (!A_MN && tbar_init) {
+      // this step's update-tile barrier, with its init and shared-memory proxy
+      // fences, by the MMA thread once its forward issues are done (it only
+      // waits for the phase to end): off the B -> U hand-off and off the start
+      // of the backward's stream (CTA pairs: pair_exchange arms it and nothing
+      // arrives on it before this CTA's announcement there; else the update
+      // phase arms it)
+      mbar_init(tbar_init, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
   } else if (warp >= 4 && !(A_MN && p.pair)) {   // (CTA pairs: the backward drain is pair_exchange)
     // ---------------- epilogue warps: TMEM -> registers -> smem -> global ----------------
@@ -642,7 +658,9 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     // written with generic stores by every CTA's phase U of the previous step
     // (ordered by the grid barrier); the async proxy must see them
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    for (int v = 0; v < 2; ++v) tma_prefetch_desc(&A[v]);
+    // (later steps: prefetched at the end of the previous backward, or the
+    // same descriptors as before)
+    if (t == 0) for (int v = 0; v < 2; ++v) tma_prefetch_desc(&A[v]);
   }
 
   // ---- phase F: forward split-K partials; warps 2-3: G^C, ||v''||^2 partials ----
@@ -651,7 +669,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     if (threadIdx.x == 64) tstamp(p.upd, 31);
   } else if (!(kDevKnobs && (p.dbg_mode & 8))) {
     gemm_phase<EB, false>(maps, A, p, 2 * p.mtF * p.splitsF, ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs,
-                          epi_stage);
+                          epi_stage, (!p.products_only && !dev_tbar_in_ring(p)) ? acce_bar + 2 : nullptr);
     if (threadIdx.x == 32) tstamp(p.upd, 29);
     if (threadIdx.x == 128) tstamp(p.upd, 30);
   }
@@ -852,15 +870,6 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     asm volatile("fence.proxy.async.global;" ::: "memory");   // Zb of every CTA's phase S, read by TMA below
     // (the backward's descriptors were prefetched by this thread at the end
     // of its forward producer loop, where it only waits for the epilogue)
-    if (!p.products_only && !dev_tbar_in_ring(p)) {
-      // this step's update-tile barrier, initialised here so that the init
-      // and its fences are off the B -> U hand-off (CTA pairs: pair_exchange
-      // arms it and nothing arrives on it before this CTA's announcement
-      // there; else the update phase arms it)
-      mbar_init(acce_bar + 2, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
   }
   if (warp == 2 || warp == 3) {    // warps 2-3: reduce the (now complete) Gram partial rows
     if (!p.products_only || p.tables) {
@@ -883,7 +892,7 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     }
   } else if (!(kDevKnobs && (p.dbg_mode & 32))) {
     gemm_phase<EB, true>(maps, A, p, 2 * (p.mtB[0] + p.mtB[1]), ring, full_bar, empty_bar, accf_bar, acce_bar, tmem_base, rs,
-                         epi_stage);
+                         epi_stage, nullptr, (p.xmaps && t + 1 < p.nsteps) ? p.xmaps + 6 * (t + 1) : nullptr);
   }
   tc_fence_before();
   if (p.upd.dbg && threadIdx.x >= 128) {
@@ -982,9 +991,6 @@ cca_step_kernel(const __grid_constant__ FusedMaps maps, const FusedParams p) {
     __threadfence();
     gsync();
   }
-
-  if (t + 1 < p.nsteps && p.xmaps && threadIdx.x == 0)   // the next step's batch descriptors, ahead of its phase F
-    for (int v = 0; v < 2; ++v) tma_prefetch_desc(p.xmaps + 6 * (t + 1) + v);
 
   // ---- phase U: Gram tables + fused update ----
   if (!p.products_only && !(kDevKnobs && (p.dbg_mode & 64)))
