@@ -510,7 +510,7 @@ __device__ __forceinline__ void pair_exchange(const FusedParams& p, const UpdMap
   if (threadIdx.x == 128) tstamp(p.upd, 15);
   if (threadIdx.x == 0) {
     // this step's tile barrier (initialised, with its fences, by this thread
-    // at the start of phase B — off this critical path): V'' and [Bv] of the
+    // by the MMA thread at the end of phase F — off this critical path): V'' and [Bv] of the
     // own columns (TMA) and the partner's pushed tile; then announce to the
     // partner that it may push.
     // (V'' and [Bv] were last written by the previous step's update with
@@ -523,7 +523,7 @@ __device__ __forceinline__ void pair_exchange(const FusedParams& p, const UpdMap
     // relaxed: the announcement publishes no data of this CTA — the partner's
     // push writes this CTA's tile through the async proxy, the MMAs that read
     // that smem have completed (accf), and the tile barrier's init was released
-    // to the cluster by the fence.mbarrier_init at the start of phase B (a
+    // to the cluster by the fence.mbarrier_init at the end of phase F (a
     // release fence followed by this strong relaxed arrive is a release
     // pattern).  A release here cost ~0.7 us/step on the B -> U hand-off.
     if (has)

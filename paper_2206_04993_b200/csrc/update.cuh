@@ -869,7 +869,7 @@ __device__ __forceinline__ void update_res_phases(const UpdateArgs& p, float* sm
                                                   float* coef = nullptr, uint64_t* tbar_ext = nullptr,
                                                   bool tbar_ready = false) {
   // tbar_ready: the caller initialised tbar_ext (with the init and shared-memory
-  // proxy fences) earlier, off this critical path (fused kernel: start of phase B)
+  // proxy fences) earlier, off this critical path (fused kernel: end of phase F)
   // coef: coefficients already formed (coef_early, fused kernel) — no table
   // staging, phase 3a skipped
   const int tid = threadIdx.x;
