@@ -509,10 +509,10 @@ __device__ __forceinline__ void pair_exchange(const FusedParams& p, const UpdMap
   __syncthreads();
   if (threadIdx.x == 128) tstamp(p.upd, 15);
   if (threadIdx.x == 0) {
-    // this step's tile barrier (initialised, with its fences, by this thread
-    // by the MMA thread at the end of phase F — off this critical path): V'' and [Bv] of the
-    // own columns (TMA) and the partner's pushed tile; then announce to the
-    // partner that it may push.
+    // this step's tile barrier (initialised, with its fences, by the MMA
+    // thread at the end of phase F — off this critical path): V'' and [Bv]
+    // of the own columns (TMA) and the partner's pushed tile; then announce
+    // to the partner that it may push.
     // (V'' and [Bv] were last written by the previous step's update with
     // generic stores: ordered for the async proxy by this thread's
     // fence.proxy.async.global at the start of this step's phase F)
